@@ -1,0 +1,234 @@
+/*
+ * pdx_b200.h — C-ABI of libpdx_b200.so, the B200 (sm_100a) pruned PDX scan.
+ *
+ * The reference (`dimscan`, /root/reference/pkg/src/dimscan) is pure
+ * Python/numpy and has no FFI or plugin ABI of its own: its boundary is the
+ * Python API.  Each entry point below replaces one
+ * reference function on the hot path; the reference file:line is cited on
+ * each.  The package's Python layer (paper_2503_04422_b200/) binds these
+ * with ctypes exactly as INTEGRATION.md shows.
+ *
+ * Conventions
+ *  - Every pointer argument named d_* is DEVICE memory; plain scalars are
+ *    host values.  `stream` is a cudaStream_t passed as void* (NULL = the
+ *    legacy default stream).  Calls are stream-ordered and asynchronous
+ *    unless stated otherwise; the handle-free design means any number of
+ *    threads may call concurrently on different streams.
+ *  - Return value: PDX_OK (0) or an error code; pdx_last_error() returns
+ *    the calling thread's last message.  PDX_EINVAL maps to Python
+ *    ValueError (the reference raises ValueError for the same cases,
+ *    search.py:70-85, index.py:115-116, kernels.py:35-37).
+ *  - Distances are float32 computed with the reference's per-op rounding
+ *    (kernels.py:55-61: t = q - x; acc += t*t, no FMA), summed in visit
+ *    order, so they are bit-identical to the reference's.
+ */
+#ifndef PDX_B200_H
+#define PDX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDX_ABI_VERSION 1
+
+#define PDX_OK 0
+#define PDX_EINVAL 1    /* bad argument (Python: ValueError) */
+#define PDX_ECUDA 2     /* CUDA runtime / launch failure */
+#define PDX_ENOSUPPORT 3 /* size outside what this build supports */
+
+/* Metric (kernels.py:22-25) */
+#define PDX_METRIC_L2 0
+#define PDX_METRIC_L1 1
+#define PDX_METRIC_IP 2
+
+/* SearchParams.pruner (search.py:65, :78-79) */
+#define PDX_PRUNER_NONE 0
+#define PDX_PRUNER_ADS 1
+#define PDX_PRUNER_BOND 2
+
+/* OrderCriteria (pruning.py:91-95) */
+#define PDX_ORDER_SEQUENTIAL 0
+#define PDX_ORDER_DECREASING 1
+#define PDX_ORDER_DMEANS 2
+#define PDX_ORDER_ZONES 3
+
+/* Number of vectors per HBM tile.  A reference Block (layout.py:53-83) of m
+ * vectors occupies ceil(m/64) consecutive tiles. */
+#define PDX_TILE 64
+
+/*
+ * A device-resident PDX store: the reference's list[Block]
+ * (layout.py:93-110) or IvfIndex bucket chains (index.py:75-108) in HBM.
+ *
+ * tiles  : float32 [ntiles][d_pad/group][64][group].  group = 1 is the
+ *          plain PDX block (one 256-byte row per dimension); group = 8 keeps
+ *          8 consecutive dimensions of a vector in one 32-byte sector so a
+ *          pruned survivor costs one sector per 8 dims.  Padding slots and
+ *          padding dims (d..d_pad) are zero.
+ * tile_ids : int64 [ntiles][64]  external id per slot, -1 for padding.
+ * Logical block b (a reference Block) = tiles block_tile[b] ..
+ *          block_tile[b] + ceil(block_m[b]/64) - 1, holding block_m[b] vectors.
+ * bucket_block : int64 [nbuckets+1]; bucket c owns logical blocks
+ *          [bucket_block[c], bucket_block[c+1]).  A flat store has
+ *          nbuckets = 1 covering every block (exact_search, index.py:182-191).
+ */
+typedef struct pdx_store {
+  int32_t d;
+  int32_t d_pad;
+  int32_t group;
+  int32_t nbuckets;
+  int64_t ntiles;
+  int64_t nblocks;
+  const float* d_tiles;
+  const int64_t* d_tile_ids;
+  const int64_t* d_block_tile;
+  const int32_t* d_block_m;
+  const int64_t* d_bucket_block;
+  int32_t max_bucket_blocks; /* max over buckets of (#blocks) */
+  int32_t _reserved;
+} pdx_store;
+
+/* SearchParams (search.py:61-85) + AdsPruner (pruning.py:56-65). */
+typedef struct pdx_search_params {
+  int32_t k;
+  int32_t metric;
+  int32_t pruner;
+  int32_t initial_step;
+  double selection_fraction;
+  int32_t ads_d;    /* AdsPruner.d (the reference defaults it to the data d) */
+  int32_t warps;    /* warps per query CTA (0 = auto) */
+  double ads_epsilon0;
+} pdx_search_params;
+
+/* Outputs of pdx_search.  Per query q (row q of each array):
+ *  d_dist/d_ids [nq][k]: TopK.items() (search.py:53-55) ascending by
+ *      (distance, id); IP distances are negated (search.py:120-122);
+ *      unused rows are +inf / -1 (estimators.py:24-31).
+ *  d_count [nq]      : len(TopK)                       (optional)
+ *  d_touched/d_total : SearchStats.values_touched / values_total
+ *                      (search.py:132, :169, :198)      (optional)
+ *  d_trace [nq][trace_cap], d_trace_len [nq]: SearchStats.survivors as
+ *      records [len, v1..vlen] per visited block (search.py:133, :170-172);
+ *      trace_len = -1 on overflow                     (optional) */
+typedef struct pdx_search_out {
+  float* d_dist;
+  int64_t* d_ids;
+  int32_t* d_count;
+  int64_t* d_touched;
+  int64_t* d_total;
+  int32_t* d_trace;
+  int64_t trace_cap;
+  int64_t* d_trace_len;
+} pdx_search_out;
+
+int pdx_abi_version(void);
+/* Copies the calling thread's last error message; returns its length. */
+int pdx_last_error(char* buf, size_t cap);
+/* Number of SMs and max opt-in shared memory per block of the current device. */
+int pdx_device_info(int32_t* sm_count, int32_t* smem_optin, int32_t* cc_major, int32_t* cc_minor);
+
+/*
+ * K1 — PDX transposition / IVF bucket packing.
+ * Replaces to_blocks (layout.py:93-110, the transpose at :107-108) and the
+ * per-bucket packing of ivf_build (index.py:98-106).
+ * d_x: float32 [n][d] row-major; d_slot_src: int64 [ntiles*64] source row of
+ * each slot (-1 = padding); d_ids_in: int64 [n] external ids (NULL = row
+ * index).  Writes d_tiles (layout above) and d_tile_ids.
+ */
+int pdx_pack_tiles(const float* d_x, int64_t n, int32_t d, const int64_t* d_slot_src,
+                   int64_t ntiles, int32_t group, const int64_t* d_ids_in, float* d_tiles,
+                   int64_t* d_tile_ids, void* stream);
+
+/*
+ * K3 — query / data projection y = x @ M^T (float32).
+ * Replaces apply_transform (pruning.py:48-53) as used per query batch at
+ * estimators.py:116-117 and at fit time (estimators.py:102-105).  Not
+ * bit-identical to numpy's sgemm (neither is any other BLAS); parity tests
+ * feed both sides identical rotated floats.
+ */
+int pdx_project(const float* d_x, int64_t n, int32_t d, const float* d_matrix, float* d_y,
+                void* stream);
+
+/*
+ * K2 — bucket selection.
+ * Replaces ivf_select_buckets (index.py:111-127): float32 centroid
+ * distances with the vertical kernel's per-op rounding in natural dim order,
+ * then the nprobe smallest (key, bucket) pairs (key = -dist for IP), i.e.
+ * numpy's stable argsort.  d_centroids: float32 [nlist][d] row-major.
+ * d_scratch: float32 [nq][nlist].  d_sel: int32 [nq][nprobe].
+ */
+int pdx_select_buckets(const float* d_queries, int64_t nq, int32_t d, const float* d_centroids,
+                       int32_t nlist, int32_t metric, int32_t nprobe, float* d_scratch,
+                       int32_t* d_sel, void* stream);
+
+/*
+ * K4 — query-aware dimension orders.
+ * Replaces bond_dimension_order (pruning.py:107-140) with default_zone_width
+ * (:98-99): stable float64 sorts, numpy's pairwise float64 sum for zone
+ * scores.  d_queries: [nq][d], float32 (queries_f64 = 0, what the scan
+ * uses) or float64 (queries_f64 = 1; the reference takes float64 queries,
+ * pruning.py:117).  d_means: float64 [nmeans][d].  For output row
+ * r = q*nsets + s the means row is d_mean_index[r] (NULL: row 0).
+ * d_out: uint16 [nq*nsets][d].  zone_width <= 0 selects the default.
+ */
+int pdx_dimension_orders(const void* d_queries, int32_t queries_f64, int64_t nq, int32_t d,
+                         const double* d_means, const int32_t* d_mean_index, int32_t nsets,
+                         int32_t criteria, int32_t zone_width, uint16_t* d_out, void* stream);
+
+/*
+ * K5+K6 — the pruned PDX scan with top-k (PDXearch).
+ * Replaces search / _linear_block / _search_block (search.py:125-205) with
+ * vertical_accumulate(_selected) (kernels.py:41-91), ads_bound
+ * (pruning.py:83-88), the BOND test (search.py:165) and TopK (search.py:27-58).
+ * The visit order for query q is: for s in 0..nseg-1, every logical block
+ * of bucket d_seg_bucket[q*nseg+s] (NULL: bucket s) in stored order — the
+ * block list ivf_search builds (index.py:140-149) or exact_search's
+ * partition list.  d_orders: NULL (natural order) or uint16 permutations,
+ * the one for (q, s) at d_orders + (q*order_qstride + s*order_sstride)*d.
+ * Results, the threshold chain, every prune decision and the stats are the
+ * reference's (block-synchronous thresholds, search.py:159).
+ * d_work/work_bytes: scratch of at least pdx_search_workspace() bytes.
+ */
+int64_t pdx_search_workspace(const pdx_store* store, int64_t nq, int32_t nseg);
+int pdx_search(const pdx_store* store, const pdx_search_params* params, const float* d_queries,
+               int64_t nq, const int32_t* d_seg_bucket, int32_t nseg, const uint16_t* d_orders,
+               int64_t order_qstride, int64_t order_sstride, const pdx_search_out* out,
+               void* d_work, int64_t work_bytes, void* stream);
+
+/*
+ * K7 — merge of per-shard top-k lists (multi-GPU; no reference counterpart:
+ * the reference is single-process).  d_dist/d_ids: [nparts][nq][k] sorted
+ * lists (+inf/-1 padded) → the k smallest (dist, id) pairs per query, the
+ * TopK tie rule (search.py:45-51).
+ */
+int pdx_merge_topk(const float* d_dist, const int64_t* d_ids, int32_t nparts, int64_t nq, int32_t k,
+                   float* d_out_dist, int64_t* d_out_ids, void* stream);
+
+/*
+ * Per-segment float64 means: for segment s, rows d_rows[seg_off[s] ..
+ * seg_off[s+1]) of d_x summed in that order in float64, divided by the
+ * count.  Replaces compute_means (layout.py:126-138: values.sum(axis=0)/n,
+ * numpy's axis-0 reduction adds rows sequentially) for the global / bucket
+ * means (index.py:103-104, :178) and the k-means centroid update
+ * (index.py:46-48).  Empty segments are left untouched.
+ * d_rows NULL = identity (segments of consecutive rows).
+ */
+int pdx_segment_means(const float* d_x, int32_t d, const int64_t* d_rows, const int64_t* d_seg_off,
+                      int32_t nseg, double* d_means, void* stream);
+
+/*
+ * Float64 brute-force ground truth (next #3): compute_ground_truth
+ * (bench.py:53-67) — horizontal float64 distances (kernels.py:108-119) and
+ * the k smallest (key, row) with the lower row on ties.  d_x [n][d] f32,
+ * d_queries [nq][d] f32 → d_ids [nq][k] (row indices), d_dist [nq][k] f64.
+ */
+int pdx_ground_truth(const float* d_x, int64_t n, int32_t d, const float* d_queries, int64_t nq,
+                     int32_t k, int32_t metric, int64_t* d_ids, double* d_dist, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDX_B200_H */

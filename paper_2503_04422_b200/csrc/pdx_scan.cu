@@ -1,0 +1,712 @@
+// K5 + K6: the pruned PDX scan with in-CTA top-k (PDXearch on sm_100a).
+//
+// Reference semantics (search.py:125-205, kernels.py:41-91, pruning.py:83-88):
+// blocks are visited in a fixed order; block 0 and every block met while
+// the heap is not full are scanned linearly; every other block runs the
+// exponential step schedule, after each step pruning against T_b, the k-th
+// best distance when the block STARTED (the heap only changes when the
+// block's survivors are pushed at its end).
+//
+// B200 mapping.  One CTA per query.  Its W warps each take one 64-vector
+// tile per round and run it SPECULATIVELY with a threshold T' >= T_b (the
+// live threshold at round start, or T_b itself for a block already open),
+// recording every slot's partial sum at every schedule step in shared
+// memory.  Because the partial sums do not depend on the threshold and both
+// bounds are monotone in T, the speculative survivor set is a superset of
+// the reference's at every step.  Warp 0 then COMMITS the round's tiles in
+// visit order with the exact T_b: it replays the decisions from the
+// recorded partials, pushes the exact survivors into the top-k and keeps
+// the reference's survivor counts and values_touched.  Results, threshold
+// chain, decisions and stats are therefore the reference's, while the data
+// reads (the only HBM traffic) proceed W tiles at a time per query.
+//
+// HBM layout (pdx_b200.h): tiles [d_pad/G][64][G].  G = 8 puts one slot's 8
+// consecutive dims in one 32-byte sector: the dense early steps read whole
+// 2 KB groups (coalesced float4 loads), and a pruned survivor later costs
+// one sector per 8 dims instead of one per dim.
+#include <cub/block/block_scan.cuh>
+
+#include "pdx_common.cuh"
+
+namespace pdx {
+
+struct VisitEntry {
+  int64_t tile0;
+  int32_t m;
+  int32_t seg;
+};
+static_assert(sizeof(VisitEntry) == 16, "visit entry is 16 bytes");
+
+struct TileDesc {
+  int64_t tile;
+  int32_t m_tile;
+  int32_t seg;
+  int32_t block_m;
+  int32_t vis;
+  float tspec;
+  int32_t flags;  // bit0 valid, bit1 first tile of block, bit2 last tile of block
+};
+
+struct ScanArgs {
+  const float* tiles;
+  const int64_t* tile_ids;
+  int32_t d, d_pad;
+  int64_t tile_stride;
+  const VisitEntry* vis;
+  int64_t vis_qstride;
+  const int32_t* vis_count;
+  int32_t vis_count_qstride;
+  const float* queries;
+  const uint16_t* orders;
+  int64_t oqs, oss;
+  int32_t k, pruner, initial_step, nsteps;
+  double sf;
+  int32_t ads_d;
+  double eps0;
+  float* out_dist;
+  int64_t* out_ids;
+  int32_t* out_count;
+  int64_t* out_touched;
+  int64_t* out_total;
+  int32_t* trace;
+  int64_t trace_cap;
+  int64_t* trace_len;
+};
+
+struct Control {
+  int32_t n;         // entries in the top-k
+  int32_t cur_t;     // next tile within the current visit entry
+  int64_t cur_v;     // next visit entry
+  int64_t open_vis;  // visit index of a block begun but not finished (-1: none)
+  float tblk;        // T_b of the open block
+  int32_t linear;    // open block is linear
+  int32_t nvalid;    // tiles scheduled this round
+  int64_t touched, total, tlen;
+};
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float ads_or_bond_bound(int pruner, float T, int dims_seen, int ads_d,
+                                                   double ratio, double band) {
+  if (pruner != PDX_PRUNER_ADS || dims_seen >= ads_d) return T;  // bond: acc < T
+  // pruning.py:88: threshold * (dims_seen / d) * band * band, in float64,
+  // left to right; the comparison then happens in float32 (numpy casts the
+  // Python float to the array's float32).
+  const double t = __dmul_rn(__dmul_rn(__dmul_rn((double)T, ratio), band), band);
+  return __double2float_rn(t);
+}
+
+// ----------------------------------------------------------- speculation
+// One warp scans one tile with threshold tspec.  Lane l owns slots 2l, 2l+1.
+// part[s*64 + slot] receives the slot's partial after step s (+inf once the
+// slot is pruned speculatively); ids of slots alive at the end go to sid.
+template <int G, bool ORD, int METRIC>
+__device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
+                                          const uint16_t* __restrict__ ord,
+                                          const float* __restrict__ s_q,
+                                          const int32_t* __restrict__ s_ends,
+                                          const double* __restrict__ s_ratio,
+                                          const double* __restrict__ s_band,
+                                          float* __restrict__ part, int64_t* __restrict__ sid,
+                                          int lane) {
+  const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
+  const int s0 = 2 * lane, s1 = s0 + 1;
+  bool al0 = s0 < t.m_tile, al1 = s1 < t.m_tile;
+  float acc0 = 0.f, acc1 = 0.f;
+  const float tspec = t.tspec;
+  const bool prune = tspec != INFINITY;
+  const int nsteps = A.nsteps;
+  float mybnd = INFINITY;
+  if (prune && lane < nsteps)
+    mybnd = ads_or_bond_bound(A.pruner, tspec, s_ends[lane], A.ads_d, s_ratio[lane], s_band[lane]);
+
+  // G = 8 sequential: cached last group (two slots x 8 dims).
+  float4 ca0 = make_float4(0.f, 0.f, 0.f, 0.f), cb0 = ca0, ca1 = ca0, cb1 = ca0;
+  int cg = -1;
+
+  int a = 0;
+  int s = 0;
+  for (; s < nsteps; ++s) {
+    const int b = s_ends[s];
+    if (!__any_sync(kFull, al0 || al1)) break;
+    if (G == 8 && !ORD) {
+      const int glast = (b - 1) >> 3;
+      for (int g0 = a >> 3; g0 <= glast; g0 += 4) {
+        float4 r[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = g0 + u;
+          r[u][0] = r[u][1] = r[u][2] = r[u][3] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (g <= glast) {
+            if (g == cg) {
+              r[u][0] = ca0; r[u][1] = cb0; r[u][2] = ca1; r[u][3] = cb1;
+            } else {
+              const float* p = tb + ((int64_t)g * kTile + s0) * 8;
+              if (al0) { r[u][0] = ldg4(p); r[u][1] = ldg4(p + 4); }
+              if (al1) { r[u][2] = ldg4(p + 8); r[u][3] = ldg4(p + 12); }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = g0 + u;
+          if (g <= glast) {
+            const float x0[8] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w,
+                                 r[u][1].x, r[u][1].y, r[u][1].z, r[u][1].w};
+            const float x1[8] = {r[u][2].x, r[u][2].y, r[u][2].z, r[u][2].w,
+                                 r[u][3].x, r[u][3].y, r[u][3].z, r[u][3].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int j = g * 8 + e;
+              if (j >= a && j < b) {
+                const float qj = s_q[j];
+                acc0 = upd<METRIC>(acc0, qj, x0[e]);
+                acc1 = upd<METRIC>(acc1, qj, x1[e]);
+              }
+            }
+            cg = g; ca0 = r[u][0]; cb0 = r[u][1]; ca1 = r[u][2]; cb1 = r[u][3];
+          }
+        }
+      }
+    } else {
+      for (int j0 = a; j0 < b; j0 += 8) {
+        int dim[8];
+        float x0[8], x1[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = j0 + e;
+          dim[e] = 0;
+          x0[e] = x1[e] = 0.f;
+          if (j < b) dim[e] = ORD ? (int)__ldg(ord + j) : j;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (j0 + e < b) {
+            const int dm = dim[e];
+            if (G == 1) {
+              if (al0 && al1) {
+                const float2 v = ldg2(tb + (int64_t)dm * kTile + s0);
+                x0[e] = v.x; x1[e] = v.y;
+              } else if (al0) {
+                x0[e] = __ldg(tb + (int64_t)dm * kTile + s0);
+              } else if (al1) {
+                x1[e] = __ldg(tb + (int64_t)dm * kTile + s1);
+              }
+            } else {
+              const float* p = tb + ((int64_t)(dm >> 3) * kTile + s0) * 8 + (dm & 7);
+              if (al0) x0[e] = __ldg(p);
+              if (al1) x1[e] = __ldg(p + 8);
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (j0 + e < b) {
+            const float qj = s_q[dim[e]];
+            acc0 = upd<METRIC>(acc0, qj, x0[e]);
+            acc1 = upd<METRIC>(acc1, qj, x1[e]);
+          }
+        }
+      }
+    }
+    float2 pv;
+    pv.x = al0 ? acc0 : INFINITY;
+    pv.y = al1 ? acc1 : INFINITY;
+    *reinterpret_cast<float2*>(part + s * kTile + s0) = pv;
+    if (prune) {
+      const float bs = __shfl_sync(kFull, mybnd, s);
+      al0 = al0 && (acc0 < bs);
+      al1 = al1 && (acc1 < bs);
+    }
+    a = b;
+  }
+  for (; s < nsteps; ++s)
+    *reinterpret_cast<float2*>(part + s * kTile + s0) = make_float2(INFINITY, INFINITY);
+  const int64_t* ids = A.tile_ids + t.tile * kTile;
+  if (al0) sid[s0] = __ldg(ids + s0);
+  if (al1) sid[s1] = __ldg(ids + s1);
+}
+
+// ------------------------------------------------------------------ top-k
+__device__ __forceinline__ float topk_threshold(const Control& c, int k, const float* tkd) {
+  return c.n < k ? INFINITY : tkd[k - 1];
+}
+
+// Warp-cooperative insertion of one (warp-uniform) candidate into the
+// ascending (dist, id) array; TopK.push (search.py:44-51).
+__device__ __forceinline__ void topk_insert(Control& c, int k, float* tkd, int64_t* tki, float dv,
+                                            int64_t iv, int lane) {
+  const int n = c.n;
+  if (n == k && !pair_less(dv, iv, tkd[k - 1], tki[k - 1])) return;
+  int pos = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int j = base + lane;
+    const bool lt = j < n && pair_less(tkd[j], tki[j], dv, iv);
+    pos += __popc(__ballot_sync(kFull, lt));
+  }
+  const int last = n < k ? n : k - 1;
+  for (int hi = last; hi > pos; hi -= 32) {
+    const int j = hi - 1 - lane;
+    const bool act = j >= pos;
+    float dd = 0.f;
+    int64_t ii = 0;
+    if (act) { dd = tkd[j]; ii = tki[j]; }
+    __syncwarp();
+    if (act) { tkd[j + 1] = dd; tki[j + 1] = ii; }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    tkd[pos] = dv;
+    tki[pos] = iv;
+    c.n = n < k ? n + 1 : k;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void topk_push_lanes(Control& c, int k, float* tkd, int64_t* tki,
+                                                bool cand, float dv, int64_t iv, int lane) {
+  // pre-filter against the current worst (it only improves as we insert)
+  if (cand && c.n == k && !pair_less(dv, iv, tkd[k - 1], tki[k - 1])) cand = false;
+  unsigned mask = __ballot_sync(kFull, cand);
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const float d = __shfl_sync(kFull, dv, src);
+    const int64_t i = __shfl_sync(kFull, iv, src);
+    topk_insert(c, k, tkd, tki, d, i, lane);
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+template <int G, bool ORD, int METRIC>
+__global__ void __launch_bounds__(512) pdx_scan_kernel(const ScanArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int q = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int W = blockDim.x >> 5;
+  const int nsteps = A.nsteps, k = A.k;
+
+  // shared-memory carve-up (must match scan_smem_bytes)
+  unsigned char* p = smem;
+  Control& ctl = *reinterpret_cast<Control*>(p); p += 128;
+  double* s_ratio = reinterpret_cast<double*>(p); p += sizeof(double) * kMaxSteps;
+  double* s_band = reinterpret_cast<double*>(p); p += sizeof(double) * kMaxSteps;
+  int32_t* s_ends = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kMaxSteps;
+  float* s_bnd = reinterpret_cast<float*>(p); p += sizeof(float) * kMaxSteps;
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kMaxSteps;
+  TileDesc* s_desc = reinterpret_cast<TileDesc*>(p); p += sizeof(TileDesc) * 32;
+  int64_t* s_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * kTile * W;
+  int64_t* tki = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * ((k + 1) & ~1);
+  float* s_part = reinterpret_cast<float*>(p); p += sizeof(float) * kTile * nsteps * W;
+  float* tkd = reinterpret_cast<float*>(p); p += sizeof(float) * ((k + 3) & ~3);
+  float* s_q = reinterpret_cast<float*>(p);
+
+  // ---- setup
+  const float* qg = A.queries + (int64_t)q * A.d;
+  for (int j = threadIdx.x; j < A.d_pad; j += blockDim.x) s_q[j] = j < A.d ? qg[j] : 0.f;
+  if (threadIdx.x == 0) {
+    int64_t start = 0, width = A.initial_step;  // step_schedule (search.py:106-117)
+    for (int s = 0; s < nsteps; ++s) {
+      const int64_t end = start + width < A.d ? start + width : A.d;
+      s_ends[s] = (int32_t)end;
+      start = end;
+      width *= 2;
+    }
+    ctl.n = 0;
+    ctl.cur_t = 0;
+    ctl.cur_v = 0;
+    ctl.open_vis = -1;
+    ctl.tblk = INFINITY;
+    ctl.linear = 1;
+    ctl.touched = ctl.total = ctl.tlen = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < nsteps) {
+    const double ds = (double)s_ends[threadIdx.x];
+    s_ratio[threadIdx.x] = __ddiv_rn(ds, (double)A.ads_d);
+    s_band[threadIdx.x] = __dadd_rn(1.0, __ddiv_rn(A.eps0, __dsqrt_rn(ds)));
+  }
+  const VisitEntry* vis = A.vis + (int64_t)q * A.vis_qstride;
+  const int64_t nvis = A.vis_count[(int64_t)q * A.vis_count_qstride];
+  const int64_t* trace = nullptr;
+  (void)trace;
+  int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
+
+  // warp 0's register windows of visit entries: lane l holds entry base+l
+  int64_t wbase = 0;
+  VisitEntry cur = {0, 0, 0}, nxt = {0, 0, 0};
+  if (warp == 0) {
+    if (lane < nvis) cur = vis[lane];
+    if (32 + lane < nvis) nxt = vis[32 + lane];
+  }
+  __syncthreads();
+
+  bool have_round = false;  // a round's speculation results await commit
+  for (;;) {
+    if (warp == 0) {
+      // ---------------- commit the previous round in visit order
+      if (have_round) {
+        for (int w = 0; w < ctl.nvalid; ++w) {
+          const TileDesc t = s_desc[w];
+          const float* part = s_part + (size_t)w * nsteps * kTile;
+          if (t.flags & 2) {  // first tile of its block: T_b is fixed now
+            const float T = topk_threshold(ctl, k, tkd);
+            const int lin = (t.vis == 0 || A.pruner == PDX_PRUNER_NONE || T == INFINITY);
+            if (lane < nsteps) {
+              s_cnt[lane] = 0;
+              if (!lin)
+                s_bnd[lane] = ads_or_bond_bound(A.pruner, T, s_ends[lane], A.ads_d,
+                                                s_ratio[lane], s_band[lane]);
+            }
+            if (lane == 0) {
+              ctl.tblk = T;
+              ctl.linear = lin;
+            }
+            __syncwarp();
+          }
+          const int s0 = 2 * lane, s1 = s0 + 1;
+          bool c0 = s0 < t.m_tile, c1 = s1 < t.m_tile;
+          if (!ctl.linear) {
+            for (int s = 0; s < nsteps; ++s) {
+              const float bs = s_bnd[s];
+              const float2 pv = *reinterpret_cast<const float2*>(part + s * kTile + s0);
+              c0 = c0 && (pv.x < bs);
+              c1 = c1 && (pv.y < bs);
+              const int cnt = __popc(__ballot_sync(kFull, c0)) + __popc(__ballot_sync(kFull, c1));
+              if (lane == 0) s_cnt[s] += cnt;
+            }
+          }
+          const float2 fin = *reinterpret_cast<const float2*>(part + (nsteps - 1) * kTile + s0);
+          const int64_t* sid = s_ids + (size_t)w * kTile;
+          const float key0 = METRIC == PDX_METRIC_IP ? -fin.x : fin.x;
+          const float key1 = METRIC == PDX_METRIC_IP ? -fin.y : fin.y;
+          topk_push_lanes(ctl, k, tkd, tki, c0, key0, c0 ? sid[s0] : 0, lane);
+          topk_push_lanes(ctl, k, tkd, tki, c1, key1, c1 ? sid[s1] : 0, lane);
+          if (t.flags & 4) {  // last tile: the block's stats (search.py:132, :169)
+            if (lane == 0) {
+              const int64_t m = t.block_m;
+              ctl.total += m * A.d;
+              if (ctl.linear) {
+                ctl.touched += m * A.d;
+                if (tr) {
+                  if (ctl.tlen >= 0 && ctl.tlen + 2 <= A.trace_cap) {
+                    tr[ctl.tlen] = 1;
+                    tr[ctl.tlen + 1] = (int32_t)m;
+                    ctl.tlen += 2;
+                  } else {
+                    ctl.tlen = -1;
+                  }
+                }
+              } else {
+                bool warm = true;
+                int64_t prev = m;
+                int a = 0;
+                for (int s = 0; s < nsteps; ++s) {
+                  const int w_s = s_ends[s] - a;
+                  a = s_ends[s];
+                  if (warm && ((double)prev / (double)m) >= A.sf) {
+                    ctl.touched += m * w_s;
+                  } else {
+                    warm = false;
+                    ctl.touched += prev * w_s;
+                  }
+                  prev = s_cnt[s];
+                }
+                if (tr) {
+                  if (ctl.tlen >= 0 && ctl.tlen + 1 + nsteps <= A.trace_cap) {
+                    tr[ctl.tlen] = nsteps;
+                    for (int s = 0; s < nsteps; ++s) tr[ctl.tlen + 1 + s] = s_cnt[s];
+                    ctl.tlen += 1 + nsteps;
+                  } else {
+                    ctl.tlen = -1;
+                  }
+                }
+              }
+              ctl.open_vis = -1;
+            }
+          } else if (lane == 0) {
+            ctl.open_vis = t.vis;
+          }
+          __syncwarp();
+        }
+      }
+      // ---------------- schedule the next round: W tiles in visit order
+      const float tlive = topk_threshold(ctl, k, tkd);
+      int nvalid = 0;
+      int64_t cv = ctl.cur_v;
+      int ct = ctl.cur_t;
+      for (int w = 0; w < W; ++w) {
+        if (cv >= nvis) break;
+        if (cv >= wbase + 32) {  // slide the window; prefetch the one after
+          wbase += 32;
+          cur = nxt;
+          nxt = VisitEntry{0, 0, 0};
+          if (wbase + 32 + lane < nvis) nxt = vis[wbase + 32 + lane];
+        }
+        const int src = (int)(cv - wbase);
+        const int64_t tile0 = __shfl_sync(kFull, cur.tile0, src);
+        const int m = __shfl_sync(kFull, cur.m, src);
+        const int seg = __shfl_sync(kFull, cur.seg, src);
+        const int ntl = (m + kTile - 1) / kTile;
+        if (lane == 0) {
+          TileDesc t;
+          t.tile = tile0 + ct;
+          t.m_tile = min(kTile, m - kTile * ct);
+          t.seg = seg;
+          t.block_m = m;
+          t.vis = (int32_t)cv;
+          t.flags = 1 | (ct == 0 ? 2 : 0) | (ct == ntl - 1 ? 4 : 0);
+          if (A.pruner == PDX_PRUNER_NONE) t.tspec = INFINITY;
+          else t.tspec = (cv == ctl.open_vis) ? ctl.tblk : tlive;
+          s_desc[w] = t;
+        }
+        ++nvalid;
+        if (++ct == ntl) {
+          ct = 0;
+          ++cv;
+        }
+      }
+      if (lane == 0) {
+        ctl.cur_v = cv;
+        ctl.cur_t = ct;
+        ctl.nvalid = nvalid;
+      }
+    }
+    __syncthreads();
+    const int nvalid = ctl.nvalid;
+    if (nvalid == 0) break;
+    have_round = true;
+    if (warp < nvalid) {
+      const TileDesc t = s_desc[warp];
+      const uint16_t* ord =
+          ORD ? A.orders + ((int64_t)q * A.oqs + (int64_t)t.seg * A.oss) * A.d : nullptr;
+      speculate<G, ORD, METRIC>(A, t, ord, s_q, s_ends, s_ratio, s_band,
+                                s_part + (size_t)warp * nsteps * kTile, s_ids + (size_t)warp * kTile,
+                                lane);
+    }
+    __syncthreads();
+  }
+
+  // ---- outputs
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool v = i < ctl.n;
+    A.out_dist[(int64_t)q * k + i] = v ? tkd[i] : INFINITY;
+    A.out_ids[(int64_t)q * k + i] = v ? tki[i] : -1;
+  }
+  if (threadIdx.x == 0) {
+    if (A.out_count) A.out_count[q] = ctl.n;
+    if (A.out_touched) A.out_touched[q] = ctl.touched;
+    if (A.out_total) A.out_total[q] = ctl.total;
+    if (A.trace_len) A.trace_len[q] = ctl.tlen;
+  }
+}
+
+size_t scan_smem_bytes(int W, int k, int nsteps, int d_pad) {
+  size_t b = 128 + sizeof(double) * kMaxSteps * 2 + sizeof(int32_t) * kMaxSteps * 3 +
+             sizeof(TileDesc) * 32 + sizeof(int64_t) * kTile * W + sizeof(int64_t) * ((k + 1) & ~1) +
+             sizeof(float) * kTile * nsteps * W + sizeof(float) * ((k + 3) & ~3) +
+             sizeof(float) * d_pad;
+  return (b + 15) & ~(size_t)15;
+}
+
+// ------------------------------------------------------------ visit lists
+// Flattens, per query, the block sequence ivf_search hands to search()
+// (index.py:140-149): selected buckets in selection order, each bucket's
+// chain in stored order.
+__global__ void __launch_bounds__(256) build_visits_kernel(
+    const int32_t* __restrict__ seg_bucket, int nseg, const int64_t* __restrict__ bucket_block,
+    const int64_t* __restrict__ block_tile, const int32_t* __restrict__ block_m,
+    VisitEntry* __restrict__ out, int64_t maxvis, int32_t* __restrict__ counts,
+    int32_t* __restrict__ overflow) {
+  using Scan = cub::BlockScan<int64_t, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t s_b0[256], s_off[256], s_nb[256];
+  __shared__ int64_t running;
+  const int q = blockIdx.x;
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  for (int base = 0; base < nseg; base += 256) {
+    const int pseg = base + threadIdx.x;
+    int64_t b0 = 0, nb = 0;
+    if (pseg < nseg) {
+      const int bucket = seg_bucket ? seg_bucket[(int64_t)q * nseg + pseg] : pseg;
+      b0 = bucket_block[bucket];
+      nb = bucket_block[bucket + 1] - b0;
+    }
+    int64_t off, tot;
+    Scan(tmp).ExclusiveSum(nb, off, tot);
+    s_b0[threadIdx.x] = b0;
+    s_nb[threadIdx.x] = nb;
+    s_off[threadIdx.x] = off;
+    __syncthreads();
+    const int cnt = min(256, nseg - base);
+    for (int i = 0; i < cnt; ++i) {
+      for (int64_t j = threadIdx.x; j < s_nb[i]; j += 256) {
+        const int64_t v = running + s_off[i] + j;
+        if (v < maxvis) {
+          const int64_t blk = s_b0[i] + j;
+          VisitEntry e;
+          e.tile0 = block_tile[blk];
+          e.m = block_m[blk];
+          e.seg = base + i;
+          out[(int64_t)q * maxvis + v] = e;
+        } else {
+          *overflow = 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) counts[q] = (int32_t)(running < maxvis ? running : maxvis);
+}
+
+template <int G, bool ORD, int METRIC>
+static cudaError_t launch_scan(const ScanArgs& A, int nq, int W, size_t smem, cudaStream_t st) {
+  auto fn = pdx_scan_kernel<G, ORD, METRIC>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<nq, W * 32, smem, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <int G, bool ORD>
+static cudaError_t launch_metric(int metric, const ScanArgs& A, int nq, int W, size_t smem,
+                                 cudaStream_t st) {
+  switch (metric) {
+    case PDX_METRIC_L2: return launch_scan<G, ORD, PDX_METRIC_L2>(A, nq, W, smem, st);
+    case PDX_METRIC_L1: return launch_scan<G, ORD, PDX_METRIC_L1>(A, nq, W, smem, st);
+    default: return launch_scan<G, ORD, PDX_METRIC_IP>(A, nq, W, smem, st);
+  }
+}
+
+}  // namespace pdx
+
+using namespace pdx;
+
+static int schedule_steps(int d, int initial_step) {
+  int n = 0;
+  int64_t start = 0, width = initial_step;
+  while (start < d) {
+    start = start + width < d ? start + width : d;
+    width *= 2;
+    ++n;
+  }
+  return n;
+}
+
+extern "C" int64_t pdx_search_workspace(const pdx_store* store, int64_t nq, int32_t nseg) {
+  if (!store || nq < 0 || nseg < 0) return -1;
+  const int64_t maxvis = (int64_t)nseg * store->max_bucket_blocks;
+  return 256 + nq * (int64_t)sizeof(int32_t) + 256 + nq * maxvis * (int64_t)sizeof(VisitEntry) + 256;
+}
+
+extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
+                          const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
+                          int32_t nseg, const uint16_t* d_orders, int64_t order_qstride,
+                          int64_t order_sstride, const pdx_search_out* out, void* d_work,
+                          int64_t work_bytes, void* stream) {
+  PDX_REQUIRE(store && prm && out, "pdx_search: null argument");
+  PDX_REQUIRE(prm->k >= 1, "k must be >= 1");
+  PDX_REQUIRE(prm->k <= 4096, "k = %d exceeds this build's limit of 4096", prm->k);
+  PDX_REQUIRE(prm->selection_fraction > 0.0 && prm->selection_fraction <= 1.0,
+              "selection_fraction must be in (0, 1]");
+  PDX_REQUIRE(prm->initial_step >= 1, "initial_step must be >= 1");
+  PDX_REQUIRE(prm->metric >= 0 && prm->metric <= 2, "unknown metric %d", prm->metric);
+  PDX_REQUIRE(prm->pruner >= 0 && prm->pruner <= 2, "unknown pruner %d", prm->pruner);
+  PDX_REQUIRE(!(prm->metric == PDX_METRIC_IP && prm->pruner != PDX_PRUNER_NONE),
+              "inner product has no monotone lower bound; use pruner='none' for IP searches");
+  PDX_REQUIRE(!(prm->pruner == PDX_PRUNER_ADS && prm->metric != PDX_METRIC_L2),
+              "the ads pruner applies to squared L2 only");
+  PDX_REQUIRE(prm->pruner != PDX_PRUNER_ADS || prm->ads_epsilon0 > 0.0, "epsilon0 must be positive");
+  PDX_REQUIRE(prm->pruner != PDX_PRUNER_ADS || prm->ads_d >= 1, "ads d must be >= 1");
+  PDX_REQUIRE(store->d >= 1 && store->d <= 65535, "dimensionality %d unsupported", store->d);
+  PDX_REQUIRE(store->group == 1 || store->group == 8, "group must be 1 or 8");
+  PDX_REQUIRE(store->d_pad % store->group == 0 && store->d_pad >= store->d, "bad d_pad");
+  PDX_REQUIRE(nq >= 0 && nq <= 0x7fffffff, "bad query count");
+  PDX_REQUIRE(nseg >= 0, "bad segment count");
+  PDX_REQUIRE(!d_seg_bucket || nseg >= 0, "bad segments");
+  PDX_REQUIRE(d_seg_bucket || nseg <= store->nbuckets, "segments exceed buckets");
+  if (nq == 0) return PDX_OK;
+  const int nsteps = schedule_steps(store->d, prm->initial_step);
+  PDX_REQUIRE(nsteps <= kMaxSteps, "step schedule too long (%d steps)", nsteps);
+
+  int dev = 0, sms = 0, optin = 0;
+  PDX_CUDA_CHECK(cudaGetDevice(&dev));
+  PDX_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PDX_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  int W = prm->warps > 0 ? prm->warps : 8;
+  if (W > 16) W = 16;
+  size_t smem = scan_smem_bytes(W, prm->k, nsteps, store->d_pad);
+  while (W > 1 && smem > (size_t)optin) {
+    W /= 2;
+    smem = scan_smem_bytes(W, prm->k, nsteps, store->d_pad);
+  }
+  PDX_REQUIRE(smem <= (size_t)optin, "k/d too large for shared memory (%zu bytes)", smem);
+
+  const int64_t maxvis = (int64_t)nseg * store->max_bucket_blocks;
+  // visit lists: query-independent when no per-query bucket selection is given
+  const int64_t nlists = d_seg_bucket ? nq : 1;
+  const int64_t need = pdx_search_workspace(store, nlists, nseg);
+  PDX_REQUIRE(d_work && work_bytes >= need, "workspace too small (%lld < %lld)",
+              (long long)work_bytes, (long long)need);
+  unsigned char* w = reinterpret_cast<unsigned char*>(d_work);
+  int32_t* d_overflow = reinterpret_cast<int32_t*>(w);
+  int32_t* d_counts = reinterpret_cast<int32_t*>(w + 256);
+  VisitEntry* d_vis = reinterpret_cast<VisitEntry*>(
+      w + 256 + ((nlists * sizeof(int32_t) + 255) / 256) * 256);
+  cudaStream_t st = as_stream(stream);
+  PDX_CUDA_CHECK(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), st));
+  if (nseg > 0 && maxvis > 0) {
+    build_visits_kernel<<<(unsigned)nlists, 256, 0, st>>>(
+        d_seg_bucket, nseg, store->d_bucket_block, store->d_block_tile, store->d_block_m, d_vis,
+        maxvis, d_counts, d_overflow);
+  } else {
+    PDX_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, nlists * sizeof(int32_t), st));
+  }
+  PDX_LAUNCH_CHECK();
+
+  ScanArgs A;
+  memset(&A, 0, sizeof(A));
+  A.tiles = store->d_tiles;
+  A.tile_ids = store->d_tile_ids;
+  A.d = store->d;
+  A.d_pad = store->d_pad;
+  A.tile_stride = (int64_t)store->d_pad * kTile;
+  A.vis = d_vis;
+  A.vis_qstride = d_seg_bucket ? maxvis : 0;
+  A.vis_count = d_counts;
+  A.vis_count_qstride = d_seg_bucket ? 1 : 0;
+  A.queries = d_queries;
+  A.orders = d_orders;
+  A.oqs = order_qstride;
+  A.oss = order_sstride;
+  A.k = prm->k;
+  A.pruner = prm->pruner;
+  A.initial_step = prm->initial_step;
+  A.nsteps = nsteps;
+  A.sf = prm->selection_fraction;
+  A.ads_d = prm->ads_d >= 1 ? prm->ads_d : store->d;
+  A.eps0 = prm->ads_epsilon0;
+  A.out_dist = out->d_dist;
+  A.out_ids = out->d_ids;
+  A.out_count = out->d_count;
+  A.out_touched = out->d_touched;
+  A.out_total = out->d_total;
+  A.trace = out->d_trace;
+  A.trace_cap = out->d_trace ? out->trace_cap : 0;
+  A.trace_len = out->d_trace_len;
+  PDX_REQUIRE(A.out_dist && A.out_ids, "output buffers required");
+
+  cudaError_t e;
+  const bool ord = d_orders != nullptr;
+  if (store->group == 8)
+    e = ord ? launch_metric<8, true>(prm->metric, A, (int)nq, W, smem, st)
+            : launch_metric<8, false>(prm->metric, A, (int)nq, W, smem, st);
+  else
+    e = ord ? launch_metric<1, true>(prm->metric, A, (int)nq, W, smem, st)
+            : launch_metric<1, false>(prm->metric, A, (int)nq, W, smem, st);
+  PDX_CUDA_CHECK(e);
+  return PDX_OK;
+}

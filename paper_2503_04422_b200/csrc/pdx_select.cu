@@ -1,0 +1,124 @@
+// K2: IVF bucket selection — ivf_select_buckets (index.py:111-127).
+//
+// Stage 1: every (query, centroid) float32 distance with the vertical
+// kernel's per-op rounding, summed over dims 0..d-1 in order (exactly what
+// vertical_accumulate over the centroid chain computes, index.py:120-124).
+// It is a dense nq x nlist x d product, tiled 64x64 through shared memory;
+// the sequential, unfused accumulation is what keeps the distances (and so
+// the bucket order and every later decision) bit-identical to the
+// reference, which is why this is not a tensor-core GEMM.
+// Stage 2: per query the nprobe smallest (key, bucket) pairs, key = dist
+// (or -dist for IP) — numpy's stable argsort followed by [:nprobe].
+#include "pdx_common.cuh"
+#include "pdx_sort.cuh"
+
+namespace pdx {
+
+constexpr int kQT = 64, kCT = 64, kDC = 16;
+
+template <int METRIC>
+__global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restrict__ Q, int64_t nq,
+                                                            const float* __restrict__ Cm, int nlist,
+                                                            int d, float* __restrict__ out) {
+  __shared__ float qs[kDC][kQT + 4];
+  __shared__ float cs[kDC][kCT + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t q0 = (int64_t)blockIdx.y * kQT;
+  const int c0 = blockIdx.x * kCT;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int j0 = 0; j0 < d; j0 += kDC) {
+#pragma unroll
+    for (int it = 0; it < (kQT * kDC) / 256; ++it) {
+      const int e = threadIdx.x + 256 * it;
+      const int r = e / kDC, c = e % kDC;
+      const int64_t qr = q0 + r;
+      const int dj = j0 + c;
+      qs[c][r] = (qr < nq && dj < d) ? Q[qr * d + dj] : 0.f;
+      const int cr = c0 + r;
+      cs[c][r] = (cr < nlist && dj < d) ? Cm[(int64_t)cr * d + dj] : 0.f;
+    }
+    __syncthreads();
+    const int jn = min(kDC, d - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      float qv[4], cv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qv[i] = qs[jj][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cv[j] = cs[jj][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = upd<METRIC>(acc[i][j], qv[i], cv[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t qr = q0 + ty * 4 + i;
+    if (qr >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cr = c0 + tx * 4 + j;
+      if (cr < nlist) out[qr * nlist + cr] = acc[i][j];
+    }
+  }
+}
+
+constexpr int kSelChunk = 2048;
+
+__global__ void __launch_bounds__(512) select_kernel(const float* __restrict__ dists, int nlist,
+                                                     int nprobe, int negate,
+                                                     int32_t* __restrict__ sel) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n2 = pow2_ceil(nprobe + min(kSelChunk, nlist));
+  uint64_t* bk = reinterpret_cast<uint64_t*>(smem);
+  int32_t* bv = reinterpret_cast<int32_t*>(bk + n2);
+  const float* row = dists + (int64_t)blockIdx.x * nlist;
+  block_top_p<uint64_t, int32_t>(nlist, nprobe, min(kSelChunk, nlist), bk, bv, ~0ull, 0x7fffffff,
+                                 [&](int i, uint64_t& k, int32_t& v) {
+                                   const float f = row[i];
+                                   k = ((uint64_t)float_key(negate ? -f : f) << 32) | (uint32_t)i;
+                                   v = i;
+                                 });
+  for (int i = threadIdx.x; i < nprobe; i += blockDim.x)
+    sel[(int64_t)blockIdx.x * nprobe + i] = bv[i];
+}
+
+}  // namespace pdx
+
+using namespace pdx;
+
+extern "C" int pdx_select_buckets(const float* d_queries, int64_t nq, int32_t d,
+                                  const float* d_centroids, int32_t nlist, int32_t metric,
+                                  int32_t nprobe, float* d_scratch, int32_t* d_sel, void* stream) {
+  PDX_REQUIRE(nlist >= 1, "nlist must be >= 1");
+  PDX_REQUIRE(nprobe >= 1 && nprobe <= nlist, "nprobe must be in [1, %d], got %d", nlist, nprobe);
+  PDX_REQUIRE(nprobe <= 4096, "nprobe %d exceeds this build's limit of 4096", nprobe);
+  PDX_REQUIRE(d >= 1, "dimensionality must be >= 1");
+  PDX_REQUIRE(metric >= 0 && metric <= 2, "unknown metric");
+  PDX_REQUIRE(nq >= 0 && nq < (1ll << 31) * kQT, "bad query count");
+  if (nq == 0) return PDX_OK;
+  cudaStream_t st = as_stream(stream);
+  dim3 grid((nlist + kCT - 1) / kCT, (unsigned)((nq + kQT - 1) / kQT));
+  switch (metric) {
+    case PDX_METRIC_L2:
+      centroid_dist_kernel<PDX_METRIC_L2><<<grid, 256, 0, st>>>(d_queries, nq, d_centroids, nlist, d, d_scratch);
+      break;
+    case PDX_METRIC_L1:
+      centroid_dist_kernel<PDX_METRIC_L1><<<grid, 256, 0, st>>>(d_queries, nq, d_centroids, nlist, d, d_scratch);
+      break;
+    default:
+      centroid_dist_kernel<PDX_METRIC_IP><<<grid, 256, 0, st>>>(d_queries, nq, d_centroids, nlist, d, d_scratch);
+  }
+  PDX_LAUNCH_CHECK();
+  const int n2 = pow2_ceil(nprobe + (nlist < kSelChunk ? nlist : kSelChunk));
+  const size_t smem = (size_t)n2 * (sizeof(uint64_t) + sizeof(int32_t));
+  PDX_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  select_kernel<<<(unsigned)nq, 512, smem, st>>>(d_scratch, nlist, nprobe, metric == PDX_METRIC_IP, d_sel);
+  PDX_LAUNCH_CHECK();
+  return PDX_OK;
+}

@@ -1,0 +1,424 @@
+"""IVF bucket index and flat partitioning over the HBM store (index.py:1-191).
+
+Build (``lloyd_kmeans``/``ivf_build``/``flat_build``) runs on the GPU:
+k-means distances are a cuBLAS fp32 GEMM in the reference's expansion form
+(index.py:67-72), the centroid update and every mean use the float64
+segment-mean kernel (numpy's order), bucket packing is kernel K1.  Search
+(``ivf_search``/``exact_search`` and their batched forms) runs kernels
+K2 (bucket selection), K4 (orders) and K5/K6 (pruned scan + top-k).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .kernels import Metric
+from .layout import Block, VectorCollection, to_blocks
+from .pruning import OrderCriteria, dimension_orders_device
+from .search import (SearchParams, SearchStats, TopK, _fill_stats, _trace_cap, run_search)
+from .store import DeviceStore, device, segment_means_rows, to_device
+
+DEFAULT_PARTITION_SIZE = 10_000
+DEFAULT_KMEANS_ITERS = 20
+KMEANS_SHIFT_TOL = 1e-4
+
+
+# ------------------------------------------------------------------ k-means
+def _pairwise_l2_dev(x, c):
+    """max(|x|^2 + |c|^2 - 2 x.c, 0) in float32 (index.py:67-72), cuBLAS fp32."""
+    import torch
+    xx = (x * x).sum(1, keepdim=True)
+    cc = (c * c).sum(1)[None, :]
+    return torch.clamp(xx + cc - 2.0 * (x @ c.T), min=0.0)
+
+
+def _argmin_chunked(x, c, chunk=1 << 17):
+    import torch
+    out = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
+    for s in range(0, x.shape[0], chunk):
+        out[s:s + chunk] = torch.argmin(_pairwise_l2_dev(x[s:s + chunk], c), dim=1)
+    return out
+
+
+def _bucket_layout(assign, nlist):
+    """Members of every bucket in ascending original index (index.py:100)."""
+    import torch
+    order = torch.sort(assign, stable=True).indices
+    counts = torch.bincount(assign, minlength=nlist)
+    off = torch.zeros(nlist + 1, dtype=torch.int64, device=assign.device)
+    off[1:] = torch.cumsum(counts, 0)
+    return order, counts, off
+
+
+def lloyd_kmeans_device(x, nlist: int, seed: int, max_iters: int = DEFAULT_KMEANS_ITERS):
+    """Lloyd iterations of index.py:27-64 on device tensors.
+
+    Same seeded sample init, float64 member means (pdx_segment_means, the
+    reference's summation order), largest-cluster split for empty clusters
+    and relative-shift stop.  Returns (centroids f32 [nlist,d], assign i64)."""
+    import torch
+    n = x.shape[0]
+    if not 1 <= nlist <= n:
+        raise ValueError(f"nlist must be in [1, {n}], got {nlist}")
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        rng = np.random.default_rng(seed)
+        init = rng.choice(n, size=nlist, replace=False)
+        centroids = x[torch.from_numpy(init).to(x.device)].clone()
+        for _ in range(max_iters):
+            assign = _argmin_chunked(x, centroids)
+            order, counts, off = _bucket_layout(assign, nlist)
+            means = torch.zeros((nlist, x.shape[1]), dtype=torch.float64, device=x.device)
+            _lib.check(_lib.lib().pdx_segment_means(_lib.ptr(x), x.shape[1], _lib.ptr(order),
+                                                    _lib.ptr(off), nlist, _lib.ptr(means),
+                                                    _lib.stream_handle()))
+            nonempty = counts > 0
+            new_centroids = centroids.clone()
+            new_centroids[nonempty] = means[nonempty].to(torch.float32)
+            empties = torch.nonzero(~nonempty).flatten().tolist()
+            if empties:
+                counts_h = counts.cpu().numpy().copy()
+                for c in empties:
+                    if counts_h[c] > 0:
+                        continue
+                    largest = int(np.argmax(counts_h))
+                    members = torch.nonzero(assign == largest).flatten()
+                    gaps = _pairwise_l2_dev(x[members], new_centroids[largest][None, :])[:, 0]
+                    stray = int(members[int(torch.argmax(gaps).item())].item())
+                    new_centroids[c] = x[stray]
+                    assign[stray] = c
+                    counts_h[largest] -= 1
+                    counts_h[c] += 1
+            shift = torch.linalg.norm(new_centroids - centroids, dim=1)
+            scale = torch.linalg.norm(centroids, dim=1) + 1e-30
+            centroids = new_centroids
+            if float(torch.max(shift / scale).item()) < KMEANS_SHIFT_TOL:
+                break
+        assign = _argmin_chunked(x, centroids)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return centroids, assign
+
+
+def lloyd_kmeans(data, nlist: int, seed: int, max_iters: int = DEFAULT_KMEANS_ITERS):
+    """index.py:27-64 → (centroids float32 (nlist, d), assignments intp (n,))."""
+    import torch
+    x = to_device(np.asarray(data, np.float32) if not isinstance(data, torch.Tensor) else data,
+                  torch.float32)
+    c, a = lloyd_kmeans_device(x, nlist, seed, max_iters)
+    return c.cpu().numpy(), a.cpu().numpy().astype(np.intp)
+
+
+# ---------------------------------------------------------------- IvfIndex
+class IvfIndex:
+    """k-means buckets as block chains in HBM (index.py:75-88).
+
+    Device state: ``store`` (tiles of every bucket chain, buckets in index
+    order, members ascending by original row), ``centroids_dev`` (f32
+    row-major), ``means_dev`` (f64 per-bucket means).  The reference's host
+    views (``centroid_blocks``, ``buckets``, ``bucket_means``) are built on
+    first access."""
+
+    def __init__(self, nlist, centroids, store, means_dev, training_seed, block_size,
+                 host_data=None, order=None, ids=None, counts=None):
+        self.nlist = int(nlist)
+        self.centroids = np.ascontiguousarray(centroids, dtype=np.float32)
+        self.store = store
+        self.centroids_dev = to_device(self.centroids)
+        self.means_dev = means_dev
+        self.training_seed = training_seed
+        self.block_size = int(block_size)
+        self._host_data = host_data
+        self._order = order
+        self._ids = ids
+        self._counts = counts
+        self._buckets = None
+
+    @property
+    def d(self) -> int:
+        return self.centroids.shape[1]
+
+    @property
+    def centroid_blocks(self) -> list[Block]:
+        return to_blocks(VectorCollection.from_array(self.centroids), self.block_size)
+
+    @property
+    def bucket_means(self) -> list[np.ndarray]:
+        m = self.means_dev.cpu().numpy()
+        return [m[c] for c in range(self.nlist)]
+
+    @property
+    def buckets(self) -> list[list[Block]]:
+        """Host block chains (index.py:99-102), for inspection and the oracle."""
+        if self._buckets is None:
+            data = self._host_data
+            if data is None:
+                raise RuntimeError("index was built from device data; no host copy kept")
+            order = self._order
+            ids = self._ids if self._ids is not None else np.arange(data.shape[0], dtype=np.int64)
+            off = np.concatenate([[0], np.cumsum(self._counts)])
+            chains = []
+            for c in range(self.nlist):
+                mem = order[off[c]:off[c + 1]]
+                part = VectorCollection(data=data[mem], ids=ids[mem])
+                chains.append(to_blocks(part, self.block_size) if part.n else [])
+            self._buckets = chains
+        return self._buckets
+
+    @classmethod
+    def from_assignment(cls, collection: VectorCollection, centroids, assign, nlist=None,
+                        training_seed=0, block_size=64, group=8, x_dev=None) -> "IvfIndex":
+        """Pack an index from given centroids and bucket assignments
+        (index.py:98-108): members ascending by row, blocks of block_size,
+        bucket means in float64 (empty bucket: its centroid)."""
+        import torch
+        centroids = np.asarray(centroids, dtype=np.float32)
+        nlist = centroids.shape[0] if nlist is None else nlist
+        x = x_dev if x_dev is not None else to_device(collection.data, torch.float32)
+        a = to_device(np.asarray(assign, np.int64), torch.int64)
+        order, counts, off = _bucket_layout(a, nlist)
+        means = to_device(centroids, torch.float64).clone()
+        _lib.check(_lib.lib().pdx_segment_means(_lib.ptr(x), x.shape[1], _lib.ptr(order),
+                                                _lib.ptr(off), nlist, _lib.ptr(means),
+                                                _lib.stream_handle()))
+        counts_h = counts.cpu().numpy()
+        nblk = (counts_h + block_size - 1) // block_size
+        # vectors per logical block, bucket by bucket
+        ms = []
+        for c in np.flatnonzero(nblk):
+            full, rem = divmod(int(counts_h[c]), block_size)
+            ms.extend([block_size] * full)
+            if rem:
+                ms.append(rem)
+        ms = np.asarray(ms, dtype=np.int64)
+        ids = to_device(collection.ids, torch.int64)
+        store = DeviceStore.pack(x, order, ms, nblk.astype(np.int64), ids=ids, group=group)
+        return cls(nlist, centroids, store, means, training_seed, block_size,
+                   host_data=collection.data, order=order.cpu().numpy(), ids=collection.ids,
+                   counts=counts_h)
+
+
+def ivf_build(collection: VectorCollection, nlist: int | None = None, seed: int = 0,
+              max_iters: int = DEFAULT_KMEANS_ITERS, block_size: int = 64, group: int = 8,
+              x_dev=None) -> IvfIndex:
+    """Cluster and pack (index.py:91-108), all on the GPU."""
+    import torch
+    if nlist is None:
+        nlist = max(1, round(math.sqrt(collection.n)))
+    x = x_dev if x_dev is not None else to_device(collection.data, torch.float32)
+    centroids, assign = lloyd_kmeans_device(x, nlist, seed, max_iters)
+    return IvfIndex.from_assignment(collection, centroids.cpu().numpy(), assign, nlist=nlist,
+                                    training_seed=seed, block_size=block_size, group=group,
+                                    x_dev=x)
+
+
+# --------------------------------------------------------------- selection
+def select_buckets_device(index: IvfIndex, Q, nprobe: int, metric=Metric.L2, scratch=None):
+    """Kernel K2 for a device batch: int32 [nq, nprobe] bucket ids."""
+    import torch
+    if not 1 <= nprobe <= index.nlist:
+        raise ValueError(f"nprobe must be in [1, {index.nlist}], got {nprobe}")
+    nq = Q.shape[0]
+    if scratch is None or scratch.numel() < nq * index.nlist:
+        scratch = torch.empty((nq * index.nlist,), dtype=torch.float32, device=Q.device)
+    sel = torch.empty((nq, nprobe), dtype=torch.int32, device=Q.device)
+    _lib.check(_lib.lib().pdx_select_buckets(_lib.ptr(Q), nq, index.d,
+                                             _lib.ptr(index.centroids_dev), index.nlist,
+                                             _lib.METRIC[Metric(metric).value], nprobe,
+                                             _lib.ptr(scratch), _lib.ptr(sel),
+                                             _lib.stream_handle()))
+    return sel
+
+
+def ivf_select_buckets(index: IvfIndex, query, nprobe: int, metric: Metric = Metric.L2) -> np.ndarray:
+    """index.py:111-127: the nprobe nearest buckets, ascending distance."""
+    import torch
+    if not 1 <= nprobe <= index.nlist:
+        raise ValueError(f"nprobe must be in [1, {index.nlist}], got {nprobe}")
+    q = to_device(np.asarray(query, np.float32)[None, :], torch.float32)
+    return select_buckets_device(index, q, nprobe, metric)[0].cpu().numpy().astype(np.intp)
+
+
+# ------------------------------------------------------------------ search
+class IvfSearcher:
+    """Batched IVF search with device-resident buffers (ivf_search,
+    index.py:130-156, for a whole query batch): K2 selection, K4 orders
+    (BOND with a query-aware criterion), K5/K6 scan."""
+
+    def __init__(self, index: IvfIndex, params: SearchParams, nprobe: int,
+                 criteria=OrderCriteria.SEQUENTIAL, zone_width=None, warps: int = 0):
+        if not 1 <= nprobe <= index.nlist:
+            raise ValueError(f"nprobe must be in [1, {index.nlist}], got {nprobe}")
+        self.index, self.params, self.nprobe = index, params, nprobe
+        self.criteria = OrderCriteria(criteria)
+        self.zone_width = zone_width
+        self.warps = warps
+        self._buf = {}
+        self._scratch = None
+
+    def run(self, Q, stats=False, trace_cap=0, timed=False, phase_times=None):
+        import torch
+        ev = None
+        if phase_times is not None:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+        sel = select_buckets_device(self.index, Q, self.nprobe, self.params.metric,
+                                    self._scratch)
+        orders, oss = None, 0
+        if self.params.pruner == "bond" and self.criteria is not OrderCriteria.SEQUENTIAL:
+            orders = dimension_orders_device(Q, self.index.means_dev, self.criteria,
+                                             self.zone_width, mean_index=sel, nsets=self.nprobe)
+            oss = 1
+        if ev:
+            ev[1].record()
+        res = run_search(self.index.store, Q, self.params, seg_bucket=sel, nseg=self.nprobe,
+                         orders=orders, order_qstride=self.nprobe, order_sstride=oss,
+                         stats=stats, trace_cap=trace_cap, warps=self.warps, out=self._buf,
+                         timed=timed)
+        if ev:
+            ev[2].record()
+            ev[2].synchronize()
+            phase_times["find_nearest_buckets"] = ev[0].elapsed_time(ev[1]) / 1e3
+            phase_times["distance_calculation"] = ev[1].elapsed_time(ev[2]) / 1e3
+            phase_times["bounds_evaluation"] = 0.0
+            phase_times.setdefault("query_preprocessing", 0.0)
+        res.selected = sel
+        return res
+
+
+def ivf_search(index: IvfIndex, query, params: SearchParams, nprobe: int,
+               criteria: OrderCriteria = OrderCriteria.SEQUENTIAL, zone_width: int | None = None,
+               stats: SearchStats | None = None, phase_times: dict | None = None) -> TopK:
+    """index.py:130-156 for one query (see ivf_search_batch for batches)."""
+    import torch
+    q = np.asarray(query, np.float32)
+    if q.shape != (index.d,):
+        raise ValueError(f"query length {q.shape} does not match d={index.d}")
+    s = IvfSearcher(index, params, nprobe, criteria, zone_width)
+    want = stats is not None
+    res = s.run(to_device(q[None, :], torch.float32), stats=want,
+                trace_cap=_trace_cap(nprobe * max(1, index.store.max_bucket_blocks), index.d,
+                                     params.initial_step) if want else 0,
+                timed=want, phase_times=phase_times)
+    _fill_stats(stats, res)
+    return res.topk(0, params.k)
+
+
+def ivf_search_batch(index: IvfIndex, queries, params: SearchParams, nprobe: int,
+                     criteria=OrderCriteria.SEQUENTIAL, zone_width=None, stats=False,
+                     trace=False):
+    """All queries in one launch per kernel; returns host arrays
+    (dist, ids, count[, touched, total, survivors, selected])."""
+    import torch
+    Q = to_device(np.asarray(queries, np.float32), torch.float32)
+    if Q.shape[1] != index.d:
+        raise ValueError(f"query dimensionality {Q.shape[1]} != {index.d}")
+    s = IvfSearcher(index, params, nprobe, criteria, zone_width)
+    cap = _trace_cap(nprobe * max(1, index.store.max_bucket_blocks), index.d,
+                     params.initial_step) if trace else 0
+    res = s.run(Q, stats=stats or trace, trace_cap=cap)
+    out = res.host()
+    out["selected"] = res.selected.cpu().numpy()
+    return out
+
+
+# -------------------------------------------------------------------- flat
+@dataclass
+class FlatPartitioning:
+    """Equally sized horizontal partitions, each one wide block (index.py:159-168)."""
+
+    store: DeviceStore
+    global_means: np.ndarray
+    partition_size: int
+    _host: VectorCollection | None = None
+    _partitions: list | None = field(default=None, repr=False)
+
+    @property
+    def d(self) -> int:
+        return self.store.d
+
+    @property
+    def partitions(self) -> list[Block]:
+        if self._partitions is None:
+            if self._host is None:
+                raise RuntimeError("no host copy kept")
+            self._partitions = to_blocks(self._host, self.partition_size, pad=False)
+        return self._partitions
+
+
+def flat_build(collection: VectorCollection, partition_size: int = DEFAULT_PARTITION_SIZE,
+               group: int = 8, x_dev=None) -> FlatPartitioning:
+    """index.py:171-179: partitions of partition_size (one unpadded wide
+    block each), global float64 means."""
+    import torch
+    if partition_size < 1:
+        raise ValueError("partition_size must be >= 1")
+    if collection.n == 0:
+        raise ValueError("cannot partition an empty collection")
+    x = x_dev if x_dev is not None else to_device(collection.data, torch.float32)
+    n = collection.n
+    full, rem = divmod(n, partition_size)
+    ms = np.array([partition_size] * full + ([rem] if rem else []), dtype=np.int64)
+    order = torch.arange(n, dtype=torch.int64, device=x.device)
+    store = DeviceStore.pack(x, order, ms, np.array([len(ms)], np.int64),
+                             ids=to_device(collection.ids, torch.int64), group=group)
+    means = segment_means_rows(x)
+    return FlatPartitioning(store=store, global_means=means, partition_size=partition_size,
+                            _host=collection)
+
+
+class ExactSearcher:
+    """Batched exact_search (index.py:182-191) with device buffers."""
+
+    def __init__(self, part: FlatPartitioning, params: SearchParams,
+                 criteria=OrderCriteria.SEQUENTIAL, zone_width=None, warps: int = 0):
+        self.part, self.params = part, params
+        self.criteria = OrderCriteria(criteria)
+        self.zone_width = zone_width
+        self.warps = warps
+        self._buf = {}
+        self._means = None
+
+    def run(self, Q, stats=False, trace_cap=0, timed=False):
+        orders = None
+        if self.params.pruner == "bond" and self.criteria is not OrderCriteria.SEQUENTIAL:
+            if self._means is None:
+                self._means = to_device(self.part.global_means[None, :])
+            orders = dimension_orders_device(Q, self._means, self.criteria, self.zone_width)
+        return run_search(self.part.store, Q, self.params, nseg=1, orders=orders,
+                          order_qstride=1, order_sstride=0, stats=stats, trace_cap=trace_cap,
+                          warps=self.warps, out=self._buf, timed=timed)
+
+
+def exact_search(partitioning: FlatPartitioning, query, params: SearchParams,
+                 criteria: OrderCriteria = OrderCriteria.SEQUENTIAL, zone_width: int | None = None,
+                 stats: SearchStats | None = None) -> TopK:
+    """index.py:182-191 for one query."""
+    import torch
+    q = np.asarray(query, np.float32)
+    if q.shape != (partitioning.d,):
+        raise ValueError(f"query length {q.shape} does not match d={partitioning.d}")
+    want = stats is not None
+    s = ExactSearcher(partitioning, params, criteria, zone_width)
+    res = s.run(to_device(q[None, :], torch.float32), stats=want,
+                trace_cap=_trace_cap(partitioning.store.nblocks, partitioning.d,
+                                     params.initial_step) if want else 0, timed=want)
+    _fill_stats(stats, res)
+    return res.topk(0, params.k)
+
+
+def exact_search_batch(partitioning: FlatPartitioning, queries, params: SearchParams,
+                       criteria=OrderCriteria.SEQUENTIAL, zone_width=None, stats=False,
+                       trace=False):
+    import torch
+    Q = to_device(np.asarray(queries, np.float32), torch.float32)
+    if Q.shape[1] != partitioning.d:
+        raise ValueError(f"query dimensionality {Q.shape[1]} != {partitioning.d}")
+    s = ExactSearcher(partitioning, params, criteria, zone_width)
+    cap = _trace_cap(partitioning.store.nblocks, partitioning.d, params.initial_step) if trace else 0
+    return s.run(Q, stats=stats or trace, trace_cap=cap).host()

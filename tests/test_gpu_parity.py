@@ -1,0 +1,291 @@
+"""GPU path (libpdx_b200.so through the package API) against the reference's
+golden outputs and the C oracle: identical ids, bit-identical float32
+distances, identical values_touched / values_total and survivor traces."""
+import numpy as np
+import pytest
+
+import recipes
+from conftest import decode_survivors, host_means
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2503_04422_b200 as P
+    from paper_2503_04422_b200 import _lib
+    _lib.lib()
+    return P
+
+
+def _items(tk):
+    it = tk.items()
+    return [i for _, i in it], np.array([d for d, _ in it], np.float32)
+
+
+def test_search_cases_match_reference(P, golden):
+    arrays, manifest = golden
+    for case in manifest["search"]:
+        x = recipes.data(case["kind"], case["n"], case["d"], case["seed"])
+        Q = recipes.queries("near", x, 3, case["seed"] + 1)
+        col = P.VectorCollection.from_array(x)
+        blocks = P.to_blocks(col, case["block_size"])
+        mu = host_means(x)
+        params = P.SearchParams(k=case["k"], metric=case["metric"], pruner=case["pruner"],
+                                selection_fraction=case["sf"], initial_step=case["step"],
+                                ads=P.AdsPruner(d=case["d"], epsilon0=case["eps"]))
+        for qi, qc in enumerate(case["queries"]):
+            orders = None
+            if case["criteria"] != "sequential":
+                orders = P.bond_dimension_order(Q[qi], mu, case["criteria"])
+            st = P.SearchStats()
+            tk = P.search(blocks, Q[qi], params, orders=orders, stats=st)
+            ids, dist = _items(tk)
+            key = qc["key"]
+            assert ids == arrays[key + "_ids"].tolist(), key
+            np.testing.assert_array_equal(dist, arrays[key + "_dist"], err_msg=key)
+            assert st.values_touched == qc["touched"], key
+            assert st.values_total == qc["total"], key
+            assert st.survivors == decode_survivors(arrays[key + "_surv"]), key
+
+
+@pytest.mark.parametrize("group", [1, 8])
+def test_flat_cases_match_reference(P, golden, group):
+    arrays, manifest = golden
+    for case in manifest["flat"]:
+        x = recipes.data(case["kind"], case["n"], case["d"], case["seed"])
+        Q = recipes.queries("near", x, 3, case["seed"] + 1)
+        flat = P.flat_build(P.VectorCollection.from_array(x), case["partition_size"], group=group)
+        np.testing.assert_array_equal(flat.global_means, host_means(x))
+        params = P.SearchParams(k=10, pruner=case["pruner"])
+        out = P.exact_search_batch(flat, Q, params, criteria=case["criteria"], trace=True)
+        for qi, qc in enumerate(case["queries"]):
+            key = qc["key"]
+            n = out["count"][qi]
+            assert out["ids"][qi, :n].tolist() == arrays[key + "_ids"].tolist(), key
+            np.testing.assert_array_equal(out["dist"][qi, :n], arrays[key + "_dist"])
+            assert out["touched"][qi] == qc["touched"] and out["total"][qi] == qc["total"], key
+            assert out["survivors"][qi] == decode_survivors(arrays[key + "_surv"]), key
+
+
+@pytest.mark.parametrize("group", [1, 8])
+def test_ivf_cases_match_reference(P, golden, group):
+    arrays, manifest = golden
+    for case in manifest["ivf"]:
+        key0 = f"i{case['seed'] - 3000}"
+        x = recipes.data(case["kind"], case["n"], case["d"], case["seed"])
+        col = P.VectorCollection.from_array(x)
+        index = P.IvfIndex.from_assignment(col, arrays[key0 + "_centroids"],
+                                           arrays[key0 + "_assign"], nlist=case["nlist"],
+                                           group=group)
+        np.testing.assert_array_equal(index.means_dev.cpu().numpy(), arrays[key0 + "_means"])
+        Q = recipes.queries("near", x, 4, case["seed"] + 1)
+        for run in case["runs"]:
+            params = P.SearchParams(k=10, pruner=run["pruner"],
+                                    ads=P.AdsPruner(d=case["d"], epsilon0=run["eps"]))
+            out = P.ivf_search_batch(index, Q[run["q"]:run["q"] + 1], params, run["nprobe"],
+                                     criteria=run["criteria"], trace=True)
+            key = run["key"]
+            n = out["count"][0]
+            assert out["selected"][0].tolist() == arrays[key + "_sel"].tolist(), key
+            assert out["ids"][0, :n].tolist() == arrays[key + "_ids"].tolist(), key
+            np.testing.assert_array_equal(out["dist"][0, :n], arrays[key + "_dist"])
+            assert out["touched"][0] == run["touched"] and out["total"][0] == run["total"], key
+            assert out["survivors"][0] == decode_survivors(arrays[key + "_surv"]), key
+
+
+def test_orders_match_reference(P, golden):
+    arrays, manifest = golden
+    for o in manifest["orders"]:
+        got = P.bond_dimension_order(arrays[o["key"] + "_q"], arrays[o["key"] + "_mu"],
+                                     o["criteria"], o["zone_width"])
+        np.testing.assert_array_equal(got, arrays[o["key"] + "_order"], err_msg=o["key"])
+
+
+# ---------------------------------------------------------- vs the oracle
+def _oracle_ivf(O, index, x):
+    chains = index.buckets
+    return O.IvfView(index.centroid_blocks, chains, index.means_dev.cpu().numpy())
+
+
+@pytest.mark.parametrize("pruner,criteria", [("none", "sequential"), ("bond", "sequential"),
+                                             ("bond", "dmeans"), ("bond", "zones")])
+def test_config1_exact_vs_oracle(P, oracle, pruner, criteria):
+    """BASELINE config 1 (100K x 128, sigma_j=(j+1)^-0.5, 64-blocks), 40 queries."""
+    x = recipes.data("decay", 100_000, 128, 0)
+    Q = recipes.data("decay", 40, 128, 1)
+    col = P.VectorCollection.from_array(x)
+    group = 1 if criteria != "sequential" else 8
+    flat = P.flat_build(col, 64, group=group)
+    params = P.SearchParams(k=10, pruner=pruner)
+    out = P.exact_search_batch(flat, Q, params, criteria=criteria, trace=True)
+    ref = oracle.exact_search_batch(P.to_blocks(col, 64), host_means(x), Q, 10, pruner=pruner,
+                                    criteria=criteria, survivors_cap=1 << 18)
+    np.testing.assert_array_equal(out["ids"], ref["ids"])
+    np.testing.assert_array_equal(out["dist"], ref["dist"])
+    np.testing.assert_array_equal(out["touched"], ref["touched"])
+    np.testing.assert_array_equal(out["total"], ref["total"])
+    assert out["survivors"] == ref["survivor_lists"]
+
+
+@pytest.mark.parametrize("eps,nprobe", [(2.1, 8), (2.1, 32), (0.7, 16)])
+def test_ivf_ads_vs_oracle(P, oracle, eps, nprobe):
+    """IVF + ADS on rotated mixture data (config-2 recipe, 200K x 128): the
+    threshold chain, every decision and the stats equal the oracle's."""
+    import torch
+    x = recipes.data("mixture", 200_000, 128, 7)
+    Q = recipes.queries("near", x, 64, 8)
+    T = P.generate_orthogonal(128, 0)
+    xr = P.apply_transform(T, x)
+    qr = P.apply_transform(T, Q)
+    np.testing.assert_allclose(qr, Q @ T.matrix.T, rtol=1e-5, atol=1e-5)
+    col = P.VectorCollection.from_array(xr)
+    index = P.ivf_build(col, nlist=256, seed=0)
+    params = P.SearchParams(k=10, pruner="ads", ads=P.AdsPruner(d=128, epsilon0=eps))
+    out = P.ivf_search_batch(index, qr, params, nprobe, trace=True)
+    view = _oracle_ivf(oracle, index, xr)
+    ref = oracle.ivf_search_batch(view, qr, 10, nprobe, pruner="ads", eps0=eps,
+                                  survivors_cap=1 << 18)
+    np.testing.assert_array_equal(out["selected"], ref["selected"])
+    np.testing.assert_array_equal(out["ids"], ref["ids"])
+    np.testing.assert_array_equal(out["dist"], ref["dist"])
+    np.testing.assert_array_equal(out["touched"], ref["touched"])
+    assert out["survivors"] == ref["survivor_lists"]
+    del torch
+
+
+@pytest.mark.parametrize("metric,pruner,criteria,k", [("l2", "bond", "decreasing", 100),
+                                                      ("l1", "bond", "dmeans", 10),
+                                                      ("ip", "none", "sequential", 32),
+                                                      ("l2", "none", "sequential", 1)])
+def test_ivf_metrics_vs_oracle(P, oracle, metric, pruner, criteria, k):
+    x = recipes.data("skewed", 30_000, 48, 11)
+    Q = recipes.queries("near", x, 32, 12)
+    col = P.VectorCollection.from_array(x)
+    index = P.ivf_build(col, nlist=64, seed=3, block_size=64,
+                        group=1 if criteria != "sequential" else 8)
+    params = P.SearchParams(k=k, metric=metric, pruner=pruner)
+    out = P.ivf_search_batch(index, Q, params, 12, criteria=criteria, trace=True)
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, x), Q, k, 12, metric=metric,
+                                  pruner=pruner, criteria=criteria, survivors_cap=1 << 18)
+    np.testing.assert_array_equal(out["ids"], ref["ids"])
+    np.testing.assert_array_equal(out["dist"], ref["dist"])
+    np.testing.assert_array_equal(out["touched"], ref["touched"])
+    assert out["survivors"] == ref["survivor_lists"]
+
+
+def test_wide_partitions_and_block_sizes_vs_oracle(P, oracle):
+    """10,000-wide partitions (ExactNearestNeighbors' default), odd block sizes."""
+    x = recipes.data("skewed", 23_456, 96, 21)
+    Q = recipes.queries("near", x, 16, 22)
+    col = P.VectorCollection.from_array(x)
+    for psize, step, sf in [(10_000, 2, 0.2), (777, 1, 0.05), (130, 8, 0.4)]:
+        flat = P.flat_build(col, psize, group=1)
+        params = P.SearchParams(k=10, pruner="bond", initial_step=step, selection_fraction=sf)
+        out = P.exact_search_batch(flat, Q, params, criteria="dmeans", trace=True)
+        ref = oracle.exact_search_batch(P.to_blocks(col, psize, pad=False), host_means(x), Q, 10,
+                                        pruner="bond", criteria="dmeans", initial_step=step,
+                                        selection_fraction=sf, survivors_cap=1 << 18)
+        np.testing.assert_array_equal(out["ids"], ref["ids"])
+        np.testing.assert_array_equal(out["dist"], ref["dist"])
+        np.testing.assert_array_equal(out["touched"], ref["touched"])
+        assert out["survivors"] == ref["survivor_lists"]
+
+
+# ------------------------------------------------------------ edge cases
+def test_edge_cases(P, oracle):
+    # empty list, single vector, k > n, d = 1
+    assert len(P.search([], np.zeros(4, np.float32), P.SearchParams(k=5))) == 0
+    x = np.array([[3.0]], np.float32)
+    tk = P.search(P.to_blocks(P.VectorCollection.from_array(x), 64), np.array([1.0], np.float32),
+                  P.SearchParams(k=4, pruner="bond"))
+    assert tk.items() == [(4.0, 0)]
+    x = recipes.data("normal", 70, 1, 3)
+    blocks = P.to_blocks(P.VectorCollection.from_array(x), 64)
+    q = np.array([0.1], np.float32)
+    for k in (1, 69, 70, 200):
+        got = P.search(blocks, q, P.SearchParams(k=k, pruner="bond")).items()
+        ref, _ = oracle.search(blocks, q, k, pruner="bond")
+        assert got == ref
+    with pytest.raises(ValueError):
+        P.search(blocks, np.zeros(2, np.float32), P.SearchParams(k=1))
+    # identical vectors: ties resolve to the lower id
+    dup = np.ones((300, 8), np.float32)
+    tk = P.search(P.to_blocks(P.VectorCollection.from_array(dup), 64), np.zeros(8, np.float32),
+                  P.SearchParams(k=10, pruner="bond"))
+    assert tk.ids() == list(range(10))
+
+
+def test_large_k_vs_oracle(P, oracle):
+    x = recipes.data("normal", 20_000, 32, 31)
+    Q = recipes.queries("near", x, 4, 32)
+    blocks = P.to_blocks(P.VectorCollection.from_array(x), 64)
+    for k in (1000, 4096):
+        for q in Q:
+            got = P.search(blocks, q, P.SearchParams(k=k, pruner="bond")).items()
+            ref, _ = oracle.search(blocks, q, k, pruner="bond")
+            assert got == ref
+
+
+def test_select_buckets_vs_oracle(P, oracle):
+    x = recipes.data("mixture", 50_000, 64, 41)
+    col = P.VectorCollection.from_array(x)
+    index = P.ivf_build(col, nlist=3000, seed=0)
+    Q = recipes.queries("near", x, 16, 42)
+    view = _oracle_ivf(oracle, index, x)
+    for metric in ("l2", "ip", "l1"):
+        for nprobe in (1, 100, 3000):
+            got = P.index.select_buckets_device(index, P.store.to_device(Q), nprobe, metric)
+            got = got.cpu().numpy()
+            for i, q in enumerate(Q):
+                ref = oracle.select_buckets(view.cent, index.nlist, q, metric, nprobe)
+                np.testing.assert_array_equal(got[i], ref)
+
+
+def test_merge_topk_matches_host(P):
+    import torch
+    from paper_2503_04422_b200 import _lib
+    rng = np.random.default_rng(0)
+    parts, nq, k = 5, 33, 17
+    dist = np.sort(rng.integers(0, 20, (parts, nq, k)).astype(np.float32), axis=2)
+    ids = rng.permutation(parts * nq * k).reshape(parts, nq, k).astype(np.int64)
+    ids[:, :, -3:] = -1
+    dist[:, :, -3:] = np.inf
+    D = torch.from_numpy(dist).cuda()
+    I = torch.from_numpy(ids).cuda()
+    od = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    oi = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().pdx_merge_topk(_lib.ptr(D), _lib.ptr(I), parts, nq, k, _lib.ptr(od),
+                                         _lib.ptr(oi), _lib.stream_handle()))
+    for q in range(nq):
+        pairs = sorted((float(dist[p, q, j]), int(ids[p, q, j])) for p in range(parts)
+                       for j in range(k) if ids[p, q, j] >= 0)[:k]
+        assert oi[q].cpu().tolist()[:len(pairs)] == [i for _, i in pairs]
+
+
+def test_ground_truth_and_estimators(P):
+    x = recipes.data("clustered", 20_000, 32, 51)
+    Q = recipes.queries("near", x, 20, 52)
+    col = P.VectorCollection.from_array(x)
+    gt = P.compute_ground_truth(col, Q, 10)
+    for i, q in enumerate(Q):
+        d = ((x.astype(np.float64) - q.astype(np.float64)) ** 2).sum(1)
+        ref = np.argsort(d, kind="stable")[:10]
+        assert sorted(gt.ids[i].tolist()) == sorted(ref.tolist())
+    est = P.ExactNearestNeighbors(partition_size=2000).fit(x)
+    dist, ids = est.kneighbors(Q, 10)
+    assert dist.dtype == np.float64 and ids.dtype == np.int64
+    for i in range(len(Q)):
+        assert sorted(ids[i].tolist()) == sorted(gt.ids[i].tolist())
+    assert np.all(np.diff(dist, axis=1) >= 0)
+    ivf = P.IvfNearestNeighbors(pruner="bond", criteria="dmeans", nlist=30, nprobe=30).fit(x)
+    _, ids = ivf.kneighbors(Q, 10)
+    for i in range(len(Q)):
+        assert sorted(ids[i].tolist()) == sorted(gt.ids[i].tolist())
+    ads = P.IvfNearestNeighbors(pruner="ads", nlist=40, seed=7).fit(x)
+    _, ids = ads.kneighbors(Q, 10, nprobe=40)
+    rec = np.mean([P.recall_at_k(gt.ids[i], ids[i], 10) for i in range(len(Q))])
+    assert rec >= 0.95
+    # padding when k exceeds the probed vectors
+    d2, i2 = P.ExactNearestNeighbors(partition_size=64).fit(x[:5]).kneighbors(Q[:2], 8)
+    assert np.all(i2[:, 5:] == -1) and np.all(np.isinf(d2[:, 5:]))
