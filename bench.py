@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark: IVF + ADSampling search (BASELINE.json configs[1]) on B200.
+
+Workload: N = 1,000,000 float32 vectors, D = 128, drawn from a 1,000-centre
+Gaussian mixture (centres ~ N(0, 4I), noise ~ N(0, I)), rotated by the
+seeded orthogonal projection, 1,024 k-means buckets, epsilon0 = 2.1, K = 10,
+1,000 queries from the same mixture, nprobe = 32 (8 and 128 reported as
+extras).  Synthetic data of the paper-dataset shape (the real datasets are
+not in the container).  A step = one pass of the whole query batch through
+the search hot path: query projection (K3), bucket selection (K2), pruned
+PDX scan + top-k (K5/K6).
+
+Arms:
+  default            our sm_100a path.  `value`: inputs resident in HBM;
+                     `e2e`: IvfNearestNeighbors.kneighbors on host arrays.
+  --impl reference   the reference algorithm on the host CPU (the C oracle
+                     port of dimscan, all host threads), same index/queries.
+Multi-GPU (torchrun): buckets are sharded over ranks (LPT by size), each
+rank scans its buckets of the globally selected probes, per-rank top-k are
+all-gathered over NCCL and merged on device (K7).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_DEFAULT, D, NCENT, NLIST, NQ, K, EPS = 1_000_000, 128, 1000, 1024, 1000, 10, 2.1
+
+
+def make_data(n, nq, seed=0):
+    """BASELINE configs[1] recipe: centres N(0, 4I), labels
+    uniform, noise N(0, I); queries from the same mixture."""
+    rng = np.random.default_rng(seed)
+    C = rng.standard_normal((NCENT, D)) * 2.0
+    lab = rng.integers(0, NCENT, n)
+    X = (C[lab] + rng.standard_normal((n, D))).astype(np.float32)
+    lq = rng.integers(0, NCENT, nq)
+    Q = (C[lq] + rng.standard_normal((nq, D))).astype(np.float32)
+    return X, Q
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, gpu=0):
+        self.samples, self.gpu, self._stop = [], gpu, threading.Event()
+        self.max_mhz = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_index(X, nlist, seed=0):
+    import torch
+    import paper_2503_04422_b200 as P
+    T = P.generate_orthogonal(D, seed)
+    xr = P.apply_transform(T, P.store.to_device(X))
+    col = P.VectorCollection(data=np.empty((0, D), np.float32), ids=np.empty(0, np.int64))
+    # the collection's host copy is only needed for the oracle views
+    col = P.VectorCollection.from_array(xr.cpu().numpy())
+    t0 = time.perf_counter()
+    index = P.ivf_build(col, nlist=nlist, seed=seed, x_dev=xr)
+    torch.cuda.synchronize()
+    return T, col, index, time.perf_counter() - t0
+
+
+def cpu_oracle_qps(index, Qr, nprobe, budget_s=12.0, max_q=None, threads=None):
+    """The C oracle (dimscan restated) over a bounded prefix of the queries."""
+    from oracle import oracle as O
+    O.build()
+    view = O.IvfView(index.centroid_blocks, index.buckets, index.means_dev.cpu().numpy())
+    threads = threads or os.cpu_count() or 1
+    done, t_total, chunk = 0, 0.0, max(threads, 16)
+    limit = Qr.shape[0] if max_q is None else min(max_q, Qr.shape[0])
+    # untimed warm query (cli.py:171-172)
+    O.ivf_search_batch(view, Qr[:1], K, nprobe, pruner="ads", eps0=EPS, nthreads=1)
+    while done < limit and t_total < budget_s:
+        q = Qr[done:min(limit, done + chunk)]
+        t0 = time.perf_counter()
+        O.ivf_search_batch(view, q, K, nprobe, pruner="ads", eps0=EPS, nthreads=threads)
+        t_total += time.perf_counter() - t0
+        done += q.shape[0]
+    return done / t_total, done, t_total, threads, view
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--nq", type=int, default=NQ)
+    ap.add_argument("--nprobe", type=int, default=32)
+    ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    ws, rank, local = dist_env()
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    X, Q = make_data(args.n, args.nq)
+    config = {"workload": f"ivf-ads N={args.n} D={D} nlist={NLIST} nprobe={args.nprobe} "
+                          f"nq={args.nq} K={K} eps0={EPS}",
+              "n": args.n, "d": D, "nlist": NLIST, "nprobe": args.nprobe, "queries": args.nq,
+              "k": K, "epsilon0": EPS, "pruner": "ads", "layout": "tiles [D/8][64][8] f32",
+              "l2_flush": "256 MiB write between timed steps", "parallelism": f"buckets x{ws}"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import paper_2503_04422_b200 as P
+        T, col, index, _ = build_index(X, NLIST)
+        Qr = Q @ T.matrix.T
+        threads = os.cpu_count() or 1
+        from oracle import oracle as O
+        O.build()
+        view = O.IvfView(index.centroid_blocks, index.buckets, index.means_dev.cpu().numpy())
+        sample = min(args.nq, 100)
+        O.ivf_search_batch(view, Qr[:1], K, args.nprobe, pruner="ads", eps0=EPS, nthreads=1)
+        times = []
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.ivf_search_batch(view, Qr[:sample], K, args.nprobe, pruner="ads", eps0=EPS,
+                               nthreads=threads)
+            if s >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        qps = sample * len(times) / sum(times)
+        print(json.dumps({
+            "impl": "reference", "metric": "queries/sec at recall@10", "value": qps,
+            "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config,
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
+                             "sample": f"first {sample} queries per step; index built once "
+                                       "(build not timed)"},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return
+
+    import paper_2503_04422_b200 as P
+    from paper_2503_04422_b200 import _lib
+    _lib.lib()
+    dev = torch.device("cuda", local)
+    T, col, index, build_s = build_index(X, NLIST)
+    if ws > 1:
+        from paper_2503_04422_b200.sharded import shard_index
+        index = shard_index(index, col, rank, ws)
+    params = P.SearchParams(k=K, pruner="ads", ads=P.AdsPruner(d=D, epsilon0=EPS))
+    searcher = P.IvfSearcher(index, params, args.nprobe, warps=args.warps)
+    Qd = P.store.to_device(Q)
+    Tm = P.store.to_device(T.matrix)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(Qin, ev=None):
+        Qr = torch.empty_like(Qin)
+        _lib.check(_lib.lib().pdx_project(_lib.ptr(Qin), Qin.shape[0], D, _lib.ptr(Tm),
+                                          _lib.ptr(Qr), _lib.stream_handle()))
+        res = searcher.run(Qr, scan_events=ev)
+        if ws > 1:
+            from paper_2503_04422_b200.sharded import gather_merge
+            return gather_merge(res, K)
+        return res.dist, res.ids
+
+    # exactness of the kernel's stats pass and the algorithmic byte count
+    Qr_dev = P.apply_transform(T, Qd)
+    st_res = searcher.run(Qr_dev, stats=True)
+    touched = int(st_res.touched.sum().item())
+    total = int(st_res.total.sum().item())
+    alg_bytes = 4 * touched
+
+    for _ in range(args.warmup):
+        step(Qd)
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    step_ms, scan_ms = [], []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            torch.cuda.synchronize()
+            ev[0].record()
+            step(Qd, ev=ev)
+            ev[3].record()
+            torch.cuda.synchronize()
+            step_ms.append(ev[0].elapsed_time(ev[3]))
+            scan_ms.append(ev[1].elapsed_time(ev[2]))
+    t_step = float(np.mean(step_ms))
+    t_scan = float(np.mean(scan_ms))
+    if ws > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_step, t_scan], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_scan = float(tt[0]), float(tt[1])
+    qps = args.nq / (t_step / 1e3)
+
+    # e2e through the public estimator-style API with host buffers
+    est = P.IvfNearestNeighbors(pruner="ads", nlist=NLIST, nprobe=args.nprobe, seed=0)
+    est.n_features_in_, est.transform_, est.index_ = D, T, index
+    Qpin = torch.from_numpy(Q).pin_memory()
+    for _ in range(2):
+        est.kneighbors_pinned(Qpin, K)
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(max(3, args.steps // 2)):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d_h, i_h = est.kneighbors_pinned(Qpin, K)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_qps = args.nq / (float(np.mean(e2e_ms)) / 1e3)
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.barrier()
+        return
+    # recall@10 against float64 brute force on the unrotated data
+    gt = P.compute_ground_truth(P.VectorCollection.from_array(X), Q, K)
+    recall = float(np.mean([P.recall_at_k(gt.ids[i], i_h[i], K) for i in range(args.nq)]))
+    peak = 6556.2
+    try:
+        peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+        peak_src = "measured"
+    except Exception:
+        peak_src = "fallback"
+    achieved = alg_bytes / (t_scan / 1e3) / 1e9
+    line = {
+        "metric": "queries/sec at recall@10", "value": qps, "unit": "queries/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture, BASELINE configs[1] recipe)",
+        "config": config, "recall_at_10": recall,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src, "traffic": None,
+                     "kernel": "pdx_scan_kernel<8,false,L2>",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "full_scan_bytes_per_launch": 4 * total,
+                     "pruning_power": 1 - touched / total, "scan_ms": t_scan},
+        "e2e": {"value": e2e_qps, "unit": "queries/s",
+                "h2d_bytes_per_step": int(Q.nbytes),
+                "d2h_bytes_per_step": int(args.nq * K * (4 + 8 + 0) + args.nq * 4)},
+        "gpu_launches": 5 * args.steps,
+        "index_build_s": build_s,
+    }
+    line["clocks"] = clk.summary()
+    if not args.no_extras:
+        extras = {}
+        for npb in (8, 128):
+            s2 = P.IvfSearcher(index, params, npb, warps=args.warps)
+            for _ in range(3):
+                s2.run(Qr_dev)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(5):
+                flush.fill_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r2 = s2.run(Qr_dev)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ids2 = r2.ids.cpu().numpy()
+            rec2 = float(np.mean([P.recall_at_k(gt.ids[i], ids2[i], K) for i in range(args.nq)]))
+            extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.mean(ts) / 1e3), "recall_at_10": rec2}
+        line["extras"] = extras
+    if ws == 1:
+        cq, done, secs, threads, _ = cpu_oracle_qps(index, Qr_dev.cpu().numpy(), args.nprobe,
+                                                    budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": cq, "unit": "queries/s", "cores": threads, "kind": "port",
+                                "sample": f"{done} queries ({secs:.1f} s wall) of the same "
+                                          "workload, C oracle, one query per host thread"}
+    print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -180,7 +180,8 @@ class IvfIndex:
         centroids = np.asarray(centroids, dtype=np.float32)
         nlist = centroids.shape[0] if nlist is None else nlist
         x = x_dev if x_dev is not None else to_device(collection.data, torch.float32)
-        a = to_device(np.asarray(assign, np.int64), torch.int64)
+        a = to_device(assign if isinstance(assign, torch.Tensor) else np.asarray(assign, np.int64),
+                      torch.int64)
         order, counts, off = _bucket_layout(a, nlist)
         means = to_device(centroids, torch.float64).clone()
         _lib.check(_lib.lib().pdx_segment_means(_lib.ptr(x), x.shape[1], _lib.ptr(order),
@@ -261,7 +262,7 @@ class IvfSearcher:
         self._buf = {}
         self._scratch = None
 
-    def run(self, Q, stats=False, trace_cap=0, timed=False, phase_times=None):
+    def run(self, Q, stats=False, trace_cap=0, timed=False, phase_times=None, scan_events=None):
         import torch
         ev = None
         if phase_times is not None:
@@ -276,10 +277,14 @@ class IvfSearcher:
             oss = 1
         if ev:
             ev[1].record()
+        if scan_events is not None:
+            scan_events[1].record()
         res = run_search(self.index.store, Q, self.params, seg_bucket=sel, nseg=self.nprobe,
                          orders=orders, order_qstride=self.nprobe, order_sstride=oss,
                          stats=stats, trace_cap=trace_cap, warps=self.warps, out=self._buf,
                          timed=timed)
+        if scan_events is not None:
+            scan_events[2].record()
         if ev:
             ev[2].record()
             ev[2].synchronize()
