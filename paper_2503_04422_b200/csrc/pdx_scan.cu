@@ -7,23 +7,29 @@
 // best distance when the block STARTED (the heap only changes when the
 // block's survivors are pushed at its end).
 //
-// B200 mapping.  One CTA per query.  Its W warps each take one 64-vector
-// tile per round and run it SPECULATIVELY with a threshold T' >= T_b (the
-// live threshold at round start, or T_b itself for a block already open),
-// recording every slot's partial sum at every schedule step in shared
-// memory.  Because the partial sums do not depend on the threshold and both
-// bounds are monotone in T, the speculative survivor set is a superset of
-// the reference's at every step.  Warp 0 then COMMITS the round's tiles in
-// visit order with the exact T_b: it replays the decisions from the
-// recorded partials, pushes the exact survivors into the top-k and keeps
-// the reference's survivor counts and values_touched.  Results, threshold
-// chain, decisions and stats are therefore the reference's, while the data
-// reads (the only HBM traffic) proceed W tiles at a time per query.
+// B200 mapping.  One CTA per query: warp 0 is the COMMIT warp, warps 1..W
+// are COMPUTE warps.  Rounds are double-buffered: while the compute warps
+// scan round r's W tiles (64 vectors each), the commit warp commits round
+// r-1 in visit order and schedules round r+1.
+//  * A compute warp scans its tile SPECULATIVELY with a threshold T' >= T_b
+//    (the committed threshold when the tile was scheduled, or T_b itself for
+//    a block whose first tile is already committed), recording each slot's
+//    partial sum after every schedule step in shared memory together with
+//    its own per-step survivor counts and final survivor mask.  Partial sums
+//    do not depend on the threshold and both bounds are monotone in T, so
+//    the speculative survivors are a superset of the reference's at every
+//    step.
+//  * The commit warp knows T_b exactly.  If T' == T_b (the usual case: the
+//    top-k rarely changes inside the speculation window) the tile's own
+//    counts and survivors ARE the reference's; otherwise it replays the
+//    decisions from the recorded partials.  It pushes the exact survivors
+//    into the top-k and keeps the reference's values_touched / survivors.
+// Results, threshold chain, decisions and stats are the reference's.
 //
 // HBM layout (pdx_b200.h): tiles [d_pad/G][64][G].  G = 8 puts one slot's 8
-// consecutive dims in one 32-byte sector: the dense early steps read whole
-// 2 KB groups (coalesced float4 loads), and a pruned survivor later costs
-// one sector per 8 dims instead of one per dim.
+// consecutive dims in one 32-byte sector: dense early steps read whole 2 KB
+// groups (coalesced float4 loads), and a pruned survivor later costs one
+// sector per 8 dims instead of one per dim.
 #include <cub/block/block_scan.cuh>
 
 #include "pdx_common.cuh"
@@ -44,7 +50,13 @@ struct TileDesc {
   int32_t block_m;
   int32_t vis;
   float tspec;
-  int32_t flags;  // bit0 valid, bit1 first tile of block, bit2 last tile of block
+  int32_t flags;  // bit1 first tile of block, bit2 last tile of block
+};
+
+// What a compute warp reports about its tile besides the partials.
+struct TileSum {
+  int32_t cnt[kMaxSteps];  // survivors after each step under tspec
+  uint32_t alive0, alive1; // final speculative survivors: bit l = slot 2l / 2l+1
 };
 
 struct ScanArgs {
@@ -74,13 +86,15 @@ struct ScanArgs {
 };
 
 struct Control {
-  int32_t n;         // entries in the top-k
-  int32_t cur_t;     // next tile within the current visit entry
-  int64_t cur_v;     // next visit entry
-  int64_t open_vis;  // visit index of a block begun but not finished (-1: none)
-  float tblk;        // T_b of the open block
-  int32_t linear;    // open block is linear
-  int32_t nvalid;    // tiles scheduled this round
+  int32_t n;            // entries in the top-k
+  int32_t cur_t;        // next tile within the current visit entry
+  int64_t cur_v;        // next visit entry
+  int64_t open_vis;     // visit index of a block whose first tile is committed but not its last
+  float tblk;           // T_b of the open block
+  int32_t linear;       // open block is linear
+  int32_t warm_min;     // smallest survivor count that keeps WARMUP for the open block
+  int32_t warm_m;       // the block size warm_min was computed for
+  int32_t nvalid[3];    // tiles scheduled per round (mod 3)
   int64_t touched, total, tlen;
 };
 
@@ -96,10 +110,22 @@ __device__ __forceinline__ float ads_or_bond_bound(int pruner, float T, int dims
   return __double2float_rn(t);
 }
 
+// Smallest survivor count p with float64(p / m) >= sf: search.py:148's
+// WARMUP test `len(positions) / block.m >= selection_fraction` is then an
+// integer compare (the quotient is monotone in p).
+__device__ __forceinline__ int warm_min_count(int m, double sf) {
+  int p = (int)ceil(sf * (double)m);
+  p = p < 0 ? 0 : (p > m ? m : p);
+  while (p > 0 && __ddiv_rn((double)(p - 1), (double)m) >= sf) --p;
+  while (p < m && __ddiv_rn((double)p, (double)m) < sf) ++p;
+  return p;
+}
+
 // ----------------------------------------------------------- speculation
-// One warp scans one tile with threshold tspec.  Lane l owns slots 2l, 2l+1.
-// part[s*64 + slot] receives the slot's partial after step s (+inf once the
-// slot is pruned speculatively); ids of slots alive at the end go to sid.
+// One warp scans one tile with threshold t.tspec.  Lane l owns slots 2l,
+// 2l+1.  part[s*64 + slot] receives the slot's partial after step s (+inf
+// once the slot is pruned speculatively); sum gets the per-step survivor
+// counts and the final survivor mask; ids of final survivors go to sid.
 template <int G, bool ORD, int METRIC>
 __device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
                                           const uint16_t* __restrict__ ord,
@@ -107,8 +133,8 @@ __device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
                                           const int32_t* __restrict__ s_ends,
                                           const double* __restrict__ s_ratio,
                                           const double* __restrict__ s_band,
-                                          float* __restrict__ part, int64_t* __restrict__ sid,
-                                          int lane) {
+                                          float* __restrict__ part, TileSum& sum,
+                                          int64_t* __restrict__ sid, int lane) {
   const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
   const int s0 = 2 * lane, s1 = s0 + 1;
   bool al0 = s0 < t.m_tile, al1 = s1 < t.m_tile;
@@ -120,7 +146,8 @@ __device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
   if (prune && lane < nsteps)
     mybnd = ads_or_bond_bound(A.pruner, tspec, s_ends[lane], A.ads_d, s_ratio[lane], s_band[lane]);
 
-  // G = 8 sequential: cached last group (two slots x 8 dims).
+  // G = 8 sequential: the last loaded group stays in registers (steps do
+  // not end on group boundaries).
   float4 ca0 = make_float4(0.f, 0.f, 0.f, 0.f), cb0 = ca0, ca1 = ca0, cb1 = ca0;
   int cg = -1;
 
@@ -131,10 +158,10 @@ __device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
     if (!__any_sync(kFull, al0 || al1)) break;
     if (G == 8 && !ORD) {
       const int glast = (b - 1) >> 3;
-      for (int g0 = a >> 3; g0 <= glast; g0 += 4) {
-        float4 r[4][4];
+      for (int g0 = a >> 3; g0 <= glast; g0 += 2) {
+        float4 r[2][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
           const int g = g0 + u;
           r[u][0] = r[u][1] = r[u][2] = r[u][3] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (g <= glast) {
@@ -148,20 +175,29 @@ __device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
           const int g = g0 + u;
           if (g <= glast) {
             const float x0[8] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w,
                                  r[u][1].x, r[u][1].y, r[u][1].z, r[u][1].w};
             const float x1[8] = {r[u][2].x, r[u][2].y, r[u][2].z, r[u][2].w,
                                  r[u][3].x, r[u][3].y, r[u][3].z, r[u][3].w};
+            const int jlo = max(a - g * 8, 0), jhi = min(b - g * 8, 8);
+            if (jlo == 0 && jhi == 8) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int j = g * 8 + e;
-              if (j >= a && j < b) {
-                const float qj = s_q[j];
+              for (int e = 0; e < 8; ++e) {
+                const float qj = s_q[g * 8 + e];
                 acc0 = upd<METRIC>(acc0, qj, x0[e]);
                 acc1 = upd<METRIC>(acc1, qj, x1[e]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                if (e >= jlo && e < jhi) {
+                  const float qj = s_q[g * 8 + e];
+                  acc0 = upd<METRIC>(acc0, qj, x0[e]);
+                  acc1 = upd<METRIC>(acc1, qj, x1[e]);
+                }
               }
             }
             cg = g; ca0 = r[u][0]; cb0 = r[u][1]; ca1 = r[u][2]; cb1 = r[u][3];
@@ -218,10 +254,19 @@ __device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
       al0 = al0 && (acc0 < bs);
       al1 = al1 && (acc1 < bs);
     }
+    const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
+    if (lane == 0) sum.cnt[s] = c;
     a = b;
   }
-  for (; s < nsteps; ++s)
-    *reinterpret_cast<float2*>(part + s * kTile + s0) = make_float2(INFINITY, INFINITY);
+  for (int s2 = s; s2 < nsteps; ++s2) {
+    *reinterpret_cast<float2*>(part + s2 * kTile + s0) = make_float2(INFINITY, INFINITY);
+    if (lane == 0) sum.cnt[s2] = 0;
+  }
+  const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
+  if (lane == 0) {
+    sum.alive0 = m0;
+    sum.alive1 = m1;
+  }
   const int64_t* ids = A.tile_ids + t.tile * kTile;
   if (al0) sid[s0] = __ldg(ids + s0);
   if (al1) sid[s1] = __ldg(ids + s1);
@@ -279,11 +324,11 @@ __device__ __forceinline__ void topk_push_lanes(Control& c, int k, float* tkd, i
 
 // ------------------------------------------------------------------ kernel
 template <int G, bool ORD, int METRIC>
-__global__ void __launch_bounds__(512) pdx_scan_kernel(const ScanArgs A) {
+__global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int q = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int W = blockDim.x >> 5;
+  const int W = (blockDim.x >> 5) - 1;  // compute warps
   const int nsteps = A.nsteps, k = A.k;
 
   // shared-memory carve-up (must match scan_smem_bytes)
@@ -294,10 +339,11 @@ __global__ void __launch_bounds__(512) pdx_scan_kernel(const ScanArgs A) {
   int32_t* s_ends = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kMaxSteps;
   float* s_bnd = reinterpret_cast<float*>(p); p += sizeof(float) * kMaxSteps;
   int32_t* s_cnt = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kMaxSteps;
-  TileDesc* s_desc = reinterpret_cast<TileDesc*>(p); p += sizeof(TileDesc) * 32;
-  int64_t* s_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * kTile * W;
+  TileDesc* s_desc = reinterpret_cast<TileDesc*>(p); p += sizeof(TileDesc) * 2 * W;
+  TileSum* s_sum = reinterpret_cast<TileSum*>(p); p += sizeof(TileSum) * 2 * W;
+  int64_t* s_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * kTile * 2 * W;
   int64_t* tki = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * ((k + 1) & ~1);
-  float* s_part = reinterpret_cast<float*>(p); p += sizeof(float) * kTile * nsteps * W;
+  float* s_part = reinterpret_cast<float*>(p); p += sizeof(float) * kTile * nsteps * 2 * W;
   float* tkd = reinterpret_cast<float*>(p); p += sizeof(float) * ((k + 3) & ~3);
   float* s_q = reinterpret_cast<float*>(p);
 
@@ -318,6 +364,9 @@ __global__ void __launch_bounds__(512) pdx_scan_kernel(const ScanArgs A) {
     ctl.open_vis = -1;
     ctl.tblk = INFINITY;
     ctl.linear = 1;
+    ctl.warm_min = 0;
+    ctl.warm_m = -1;
+    ctl.nvalid[0] = ctl.nvalid[1] = ctl.nvalid[2] = 0;
     ctl.touched = ctl.total = ctl.tlen = 0;
   }
   __syncthreads();
@@ -328,161 +377,187 @@ __global__ void __launch_bounds__(512) pdx_scan_kernel(const ScanArgs A) {
   }
   const VisitEntry* vis = A.vis + (int64_t)q * A.vis_qstride;
   const int64_t nvis = A.vis_count[(int64_t)q * A.vis_count_qstride];
-  const int64_t* trace = nullptr;
-  (void)trace;
   int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
 
-  // warp 0's register windows of visit entries: lane l holds entry base+l
+  // commit warp's register windows of visit entries: lane l holds entry base+l
   int64_t wbase = 0;
   VisitEntry cur = {0, 0, 0}, nxt = {0, 0, 0};
+
+  // schedule W tiles in visit order into desc buffer `buf` (commit warp)
+  auto schedule = [&](int buf, int slot3) {
+    const float tlive = topk_threshold(ctl, k, tkd);
+    int nvalid = 0;
+    int64_t cv = ctl.cur_v;
+    int ct = ctl.cur_t;
+    for (int w = 0; w < W; ++w) {
+      if (cv >= nvis) break;
+      if (cv >= wbase + 32) {  // slide the window; prefetch the one after
+        wbase += 32;
+        cur = nxt;
+        nxt = VisitEntry{0, 0, 0};
+        if (wbase + 32 + lane < nvis) nxt = vis[wbase + 32 + lane];
+      }
+      const int src = (int)(cv - wbase);
+      const int64_t tile0 = __shfl_sync(kFull, cur.tile0, src);
+      const int m = __shfl_sync(kFull, cur.m, src);
+      const int seg = __shfl_sync(kFull, cur.seg, src);
+      const int ntl = (m + kTile - 1) / kTile;
+      if (lane == 0) {
+        TileDesc t;
+        t.tile = tile0 + ct;
+        t.m_tile = min(kTile, m - kTile * ct);
+        t.seg = seg;
+        t.block_m = m;
+        t.vis = (int32_t)cv;
+        t.flags = (ct == 0 ? 2 : 0) | (ct == ntl - 1 ? 4 : 0);
+        if (A.pruner == PDX_PRUNER_NONE) t.tspec = INFINITY;
+        else t.tspec = (cv == ctl.open_vis) ? ctl.tblk : tlive;
+        s_desc[buf * W + w] = t;
+      }
+      ++nvalid;
+      if (++ct == ntl) {
+        ct = 0;
+        ++cv;
+      }
+    }
+    if (lane == 0) {
+      ctl.cur_v = cv;
+      ctl.cur_t = ct;
+      ctl.nvalid[slot3] = nvalid;
+    }
+    __syncwarp();
+  };
+
+  // commit round tiles of desc buffer `buf` in visit order (commit warp)
+  auto commit = [&](int buf, int nv) {
+    for (int w = 0; w < nv; ++w) {
+      const TileDesc t = s_desc[buf * W + w];
+      const TileSum& sm = s_sum[buf * W + w];
+      const float* part = s_part + (size_t)(buf * W + w) * nsteps * kTile;
+      if (t.flags & 2) {  // first tile of its block: T_b is fixed now
+        const float T = topk_threshold(ctl, k, tkd);
+        const int lin = (t.vis == 0 || A.pruner == PDX_PRUNER_NONE || T == INFINITY);
+        if (lane < nsteps) {
+          s_cnt[lane] = 0;
+          if (!lin)
+            s_bnd[lane] = ads_or_bond_bound(A.pruner, T, s_ends[lane], A.ads_d, s_ratio[lane],
+                                            s_band[lane]);
+        }
+        if (lane == 0) {
+          ctl.tblk = T;
+          ctl.linear = lin;
+          if (!lin && t.block_m != ctl.warm_m) {
+            ctl.warm_min = warm_min_count(t.block_m, A.sf);
+            ctl.warm_m = t.block_m;
+          }
+        }
+        __syncwarp();
+      }
+      const int s0 = 2 * lane, s1 = s0 + 1;
+      bool c0, c1;
+      if (ctl.linear) {
+        c0 = s0 < t.m_tile;
+        c1 = s1 < t.m_tile;
+      } else if (t.tspec == ctl.tblk) {
+        // the speculation ran with the exact threshold: its counts and
+        // survivors are the reference's
+        if (lane < nsteps) s_cnt[lane] += sm.cnt[lane];
+        c0 = (sm.alive0 >> lane) & 1;
+        c1 = (sm.alive1 >> lane) & 1;
+      } else {
+        c0 = s0 < t.m_tile;
+        c1 = s1 < t.m_tile;
+        int mycnt = 0;
+        for (int s = 0; s < nsteps; ++s) {
+          const float bs = s_bnd[s];
+          const float2 pv = *reinterpret_cast<const float2*>(part + s * kTile + s0);
+          c0 = c0 && (pv.x < bs);
+          c1 = c1 && (pv.y < bs);
+          const int cnt = __popc(__ballot_sync(kFull, c0)) + __popc(__ballot_sync(kFull, c1));
+          if (lane == s) mycnt = cnt;
+        }
+        if (lane < nsteps) s_cnt[lane] += mycnt;
+      }
+      if (__any_sync(kFull, c0 || c1)) {
+        const float2 fin = *reinterpret_cast<const float2*>(part + (nsteps - 1) * kTile + s0);
+        const int64_t* sid = s_ids + (size_t)(buf * W + w) * kTile;
+        const float key0 = METRIC == PDX_METRIC_IP ? -fin.x : fin.x;
+        const float key1 = METRIC == PDX_METRIC_IP ? -fin.y : fin.y;
+        topk_push_lanes(ctl, k, tkd, tki, c0, key0, c0 ? sid[s0] : 0, lane);
+        topk_push_lanes(ctl, k, tkd, tki, c1, key1, c1 ? sid[s1] : 0, lane);
+      }
+      __syncwarp();
+      if (t.flags & 4) {  // last tile: the block's stats (search.py:132, :169)
+        if (lane == 0) {
+          const int64_t m = t.block_m;
+          ctl.total += m * A.d;
+          if (ctl.linear) {
+            ctl.touched += m * A.d;
+            if (tr) {
+              if (ctl.tlen >= 0 && ctl.tlen + 2 <= A.trace_cap) {
+                tr[ctl.tlen] = 1;
+                tr[ctl.tlen + 1] = (int32_t)m;
+                ctl.tlen += 2;
+              } else {
+                ctl.tlen = -1;
+              }
+            }
+          } else {
+            bool warm = true;
+            int64_t prev = m;
+            int a = 0;
+            for (int s = 0; s < nsteps; ++s) {
+              const int w_s = s_ends[s] - a;
+              a = s_ends[s];
+              if (warm && prev >= ctl.warm_min) {
+                ctl.touched += m * w_s;
+              } else {
+                warm = false;
+                ctl.touched += prev * w_s;
+              }
+              prev = s_cnt[s];
+            }
+            if (tr) {
+              if (ctl.tlen >= 0 && ctl.tlen + 1 + nsteps <= A.trace_cap) {
+                tr[ctl.tlen] = nsteps;
+                for (int s = 0; s < nsteps; ++s) tr[ctl.tlen + 1 + s] = s_cnt[s];
+                ctl.tlen += 1 + nsteps;
+              } else {
+                ctl.tlen = -1;
+              }
+            }
+          }
+          ctl.open_vis = -1;
+        }
+      } else if (lane == 0) {
+        ctl.open_vis = t.vis;
+      }
+      __syncwarp();
+    }
+  };
+
   if (warp == 0) {
     if (lane < nvis) cur = vis[lane];
     if (32 + lane < nvis) nxt = vis[32 + lane];
+    schedule(0, 0);
   }
   __syncthreads();
 
-  bool have_round = false;  // a round's speculation results await commit
-  for (;;) {
+  for (int r = 0;; ++r) {
+    const int nv_cur = ctl.nvalid[r % 3];
+    const int nv_prev = r > 0 ? ctl.nvalid[(r + 2) % 3] : 0;
+    if (nv_cur == 0 && nv_prev == 0) break;
     if (warp == 0) {
-      // ---------------- commit the previous round in visit order
-      if (have_round) {
-        for (int w = 0; w < ctl.nvalid; ++w) {
-          const TileDesc t = s_desc[w];
-          const float* part = s_part + (size_t)w * nsteps * kTile;
-          if (t.flags & 2) {  // first tile of its block: T_b is fixed now
-            const float T = topk_threshold(ctl, k, tkd);
-            const int lin = (t.vis == 0 || A.pruner == PDX_PRUNER_NONE || T == INFINITY);
-            if (lane < nsteps) {
-              s_cnt[lane] = 0;
-              if (!lin)
-                s_bnd[lane] = ads_or_bond_bound(A.pruner, T, s_ends[lane], A.ads_d,
-                                                s_ratio[lane], s_band[lane]);
-            }
-            if (lane == 0) {
-              ctl.tblk = T;
-              ctl.linear = lin;
-            }
-            __syncwarp();
-          }
-          const int s0 = 2 * lane, s1 = s0 + 1;
-          bool c0 = s0 < t.m_tile, c1 = s1 < t.m_tile;
-          if (!ctl.linear) {
-            for (int s = 0; s < nsteps; ++s) {
-              const float bs = s_bnd[s];
-              const float2 pv = *reinterpret_cast<const float2*>(part + s * kTile + s0);
-              c0 = c0 && (pv.x < bs);
-              c1 = c1 && (pv.y < bs);
-              const int cnt = __popc(__ballot_sync(kFull, c0)) + __popc(__ballot_sync(kFull, c1));
-              if (lane == 0) s_cnt[s] += cnt;
-            }
-          }
-          const float2 fin = *reinterpret_cast<const float2*>(part + (nsteps - 1) * kTile + s0);
-          const int64_t* sid = s_ids + (size_t)w * kTile;
-          const float key0 = METRIC == PDX_METRIC_IP ? -fin.x : fin.x;
-          const float key1 = METRIC == PDX_METRIC_IP ? -fin.y : fin.y;
-          topk_push_lanes(ctl, k, tkd, tki, c0, key0, c0 ? sid[s0] : 0, lane);
-          topk_push_lanes(ctl, k, tkd, tki, c1, key1, c1 ? sid[s1] : 0, lane);
-          if (t.flags & 4) {  // last tile: the block's stats (search.py:132, :169)
-            if (lane == 0) {
-              const int64_t m = t.block_m;
-              ctl.total += m * A.d;
-              if (ctl.linear) {
-                ctl.touched += m * A.d;
-                if (tr) {
-                  if (ctl.tlen >= 0 && ctl.tlen + 2 <= A.trace_cap) {
-                    tr[ctl.tlen] = 1;
-                    tr[ctl.tlen + 1] = (int32_t)m;
-                    ctl.tlen += 2;
-                  } else {
-                    ctl.tlen = -1;
-                  }
-                }
-              } else {
-                bool warm = true;
-                int64_t prev = m;
-                int a = 0;
-                for (int s = 0; s < nsteps; ++s) {
-                  const int w_s = s_ends[s] - a;
-                  a = s_ends[s];
-                  if (warm && ((double)prev / (double)m) >= A.sf) {
-                    ctl.touched += m * w_s;
-                  } else {
-                    warm = false;
-                    ctl.touched += prev * w_s;
-                  }
-                  prev = s_cnt[s];
-                }
-                if (tr) {
-                  if (ctl.tlen >= 0 && ctl.tlen + 1 + nsteps <= A.trace_cap) {
-                    tr[ctl.tlen] = nsteps;
-                    for (int s = 0; s < nsteps; ++s) tr[ctl.tlen + 1 + s] = s_cnt[s];
-                    ctl.tlen += 1 + nsteps;
-                  } else {
-                    ctl.tlen = -1;
-                  }
-                }
-              }
-              ctl.open_vis = -1;
-            }
-          } else if (lane == 0) {
-            ctl.open_vis = t.vis;
-          }
-          __syncwarp();
-        }
-      }
-      // ---------------- schedule the next round: W tiles in visit order
-      const float tlive = topk_threshold(ctl, k, tkd);
-      int nvalid = 0;
-      int64_t cv = ctl.cur_v;
-      int ct = ctl.cur_t;
-      for (int w = 0; w < W; ++w) {
-        if (cv >= nvis) break;
-        if (cv >= wbase + 32) {  // slide the window; prefetch the one after
-          wbase += 32;
-          cur = nxt;
-          nxt = VisitEntry{0, 0, 0};
-          if (wbase + 32 + lane < nvis) nxt = vis[wbase + 32 + lane];
-        }
-        const int src = (int)(cv - wbase);
-        const int64_t tile0 = __shfl_sync(kFull, cur.tile0, src);
-        const int m = __shfl_sync(kFull, cur.m, src);
-        const int seg = __shfl_sync(kFull, cur.seg, src);
-        const int ntl = (m + kTile - 1) / kTile;
-        if (lane == 0) {
-          TileDesc t;
-          t.tile = tile0 + ct;
-          t.m_tile = min(kTile, m - kTile * ct);
-          t.seg = seg;
-          t.block_m = m;
-          t.vis = (int32_t)cv;
-          t.flags = 1 | (ct == 0 ? 2 : 0) | (ct == ntl - 1 ? 4 : 0);
-          if (A.pruner == PDX_PRUNER_NONE) t.tspec = INFINITY;
-          else t.tspec = (cv == ctl.open_vis) ? ctl.tblk : tlive;
-          s_desc[w] = t;
-        }
-        ++nvalid;
-        if (++ct == ntl) {
-          ct = 0;
-          ++cv;
-        }
-      }
-      if (lane == 0) {
-        ctl.cur_v = cv;
-        ctl.cur_t = ct;
-        ctl.nvalid = nvalid;
-      }
-    }
-    __syncthreads();
-    const int nvalid = ctl.nvalid;
-    if (nvalid == 0) break;
-    have_round = true;
-    if (warp < nvalid) {
-      const TileDesc t = s_desc[warp];
+      if (nv_prev) commit((r + 1) & 1, nv_prev);
+      schedule((r + 1) & 1, (r + 1) % 3);
+    } else if (warp - 1 < nv_cur) {
+      const int w = warp - 1, buf = r & 1;
+      const TileDesc t = s_desc[buf * W + w];
       const uint16_t* ord =
           ORD ? A.orders + ((int64_t)q * A.oqs + (int64_t)t.seg * A.oss) * A.d : nullptr;
       speculate<G, ORD, METRIC>(A, t, ord, s_q, s_ends, s_ratio, s_band,
-                                s_part + (size_t)warp * nsteps * kTile, s_ids + (size_t)warp * kTile,
-                                lane);
+                                s_part + (size_t)(buf * W + w) * nsteps * kTile,
+                                s_sum[buf * W + w], s_ids + (size_t)(buf * W + w) * kTile, lane);
     }
     __syncthreads();
   }
@@ -503,8 +578,9 @@ __global__ void __launch_bounds__(512) pdx_scan_kernel(const ScanArgs A) {
 
 size_t scan_smem_bytes(int W, int k, int nsteps, int d_pad) {
   size_t b = 128 + sizeof(double) * kMaxSteps * 2 + sizeof(int32_t) * kMaxSteps * 3 +
-             sizeof(TileDesc) * 32 + sizeof(int64_t) * kTile * W + sizeof(int64_t) * ((k + 1) & ~1) +
-             sizeof(float) * kTile * nsteps * W + sizeof(float) * ((k + 3) & ~3) +
+             sizeof(TileDesc) * 2 * W + sizeof(TileSum) * 2 * W +
+             sizeof(int64_t) * kTile * 2 * W + sizeof(int64_t) * ((k + 1) & ~1) +
+             sizeof(float) * kTile * nsteps * 2 * W + sizeof(float) * ((k + 3) & ~3) +
              sizeof(float) * d_pad;
   return (b + 15) & ~(size_t)15;
 }
@@ -567,7 +643,7 @@ static cudaError_t launch_scan(const ScanArgs& A, int nq, int W, size_t smem, cu
   auto fn = pdx_scan_kernel<G, ORD, METRIC>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<nq, W * 32, smem, st>>>(A);
+  fn<<<nq, (W + 1) * 32, smem, st>>>(A);
   return cudaGetLastError();
 }
 
@@ -626,18 +702,16 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   PDX_REQUIRE(store->d_pad % store->group == 0 && store->d_pad >= store->d, "bad d_pad");
   PDX_REQUIRE(nq >= 0 && nq <= 0x7fffffff, "bad query count");
   PDX_REQUIRE(nseg >= 0, "bad segment count");
-  PDX_REQUIRE(!d_seg_bucket || nseg >= 0, "bad segments");
   PDX_REQUIRE(d_seg_bucket || nseg <= store->nbuckets, "segments exceed buckets");
   if (nq == 0) return PDX_OK;
   const int nsteps = schedule_steps(store->d, prm->initial_step);
   PDX_REQUIRE(nsteps <= kMaxSteps, "step schedule too long (%d steps)", nsteps);
 
-  int dev = 0, sms = 0, optin = 0;
+  int dev = 0, optin = 0;
   PDX_CUDA_CHECK(cudaGetDevice(&dev));
-  PDX_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   PDX_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  int W = prm->warps > 0 ? prm->warps : 8;
-  if (W > 16) W = 16;
+  int W = prm->warps > 0 ? prm->warps : 4;  // compute warps per query CTA
+  if (W > 8) W = 8;
   size_t smem = scan_smem_bytes(W, prm->k, nsteps, store->d_pad);
   while (W > 1 && smem > (size_t)optin) {
     W /= 2;
