@@ -142,11 +142,12 @@ def main():
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--nq", type=int, default=NQ)
     ap.add_argument("--nprobe", type=int, default=32)
-    ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--warps", default="0", help="compute warps per query CTA, or W,tiles_per_warp")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    args.warps = tuple(int(v) for v in str(args.warps).split(",")) if "," in str(args.warps) else int(args.warps)
 
     ws, rank, local = dist_env()
     import torch

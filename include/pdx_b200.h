@@ -99,8 +99,10 @@ typedef struct pdx_search_params {
   int32_t initial_step;
   double selection_fraction;
   int32_t ads_d;    /* AdsPruner.d (the reference defaults it to the data d) */
-  int32_t warps;    /* warps per query CTA (0 = auto) */
+  int32_t warps;    /* compute warps per query CTA (0 = auto) */
   double ads_epsilon0;
+  int32_t tiles_per_warp; /* 64-vector tiles per compute warp per round (0 = auto) */
+  int32_t _reserved;
 } pdx_search_params;
 
 /* Outputs of pdx_search.  Per query q (row q of each array):

@@ -39,7 +39,8 @@ class PdxStore(C.Structure):
 class PdxSearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("metric", C.c_int32), ("pruner", C.c_int32),
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
-                ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double)]
+                ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
+                ("tiles_per_warp", C.c_int32), ("_reserved", C.c_int32)]
 
 
 class PdxSearchOut(C.Structure):

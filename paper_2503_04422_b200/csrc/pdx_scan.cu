@@ -9,16 +9,15 @@
 //
 // B200 mapping.  One CTA per query: warp 0 is the COMMIT warp, warps 1..W
 // are COMPUTE warps.  Rounds are double-buffered: while the compute warps
-// scan round r's W tiles (64 vectors each), the commit warp commits round
+// scan round r (W x tpw tiles of 64 vectors), the commit warp commits round
 // r-1 in visit order and schedules round r+1.
-//  * A compute warp scans its tile SPECULATIVELY with a threshold T' >= T_b
-//    (the committed threshold when the tile was scheduled, or T_b itself for
-//    a block whose first tile is already committed), recording each slot's
-//    partial sum after every schedule step in shared memory together with
-//    its own per-step survivor counts and final survivor mask.  Partial sums
-//    do not depend on the threshold and both bounds are monotone in T, so
-//    the speculative survivors are a superset of the reference's at every
-//    step.
+//  * A compute warp scans its tiles SPECULATIVELY (pdx_scan_spec.cuh) with a
+//    threshold T' >= T_b (the committed threshold when the tile was
+//    scheduled, or T_b itself for a block whose first tile is committed),
+//    recording each slot's partial sum after every schedule step plus its
+//    own per-step survivor counts and final survivor mask.  Partial sums do
+//    not depend on the threshold and both bounds are monotone in T, so the
+//    speculative survivors are a superset of the reference's at every step.
 //  * The commit warp knows T_b exactly.  If T' == T_b (the usual case: the
 //    top-k rarely changes inside the speculation window) the tile's own
 //    counts and survivors ARE the reference's; otherwise it replays the
@@ -33,82 +32,23 @@
 #include <cub/block/block_scan.cuh>
 
 #include "pdx_common.cuh"
+#include "pdx_scan_spec.cuh"
 
 namespace pdx {
 
-struct VisitEntry {
-  int64_t tile0;
-  int32_t m;
-  int32_t seg;
-};
-static_assert(sizeof(VisitEntry) == 16, "visit entry is 16 bytes");
-
-struct TileDesc {
-  int64_t tile;
-  int32_t m_tile;
-  int32_t seg;
-  int32_t block_m;
-  int32_t vis;
-  float tspec;
-  int32_t flags;  // bit1 first tile of block, bit2 last tile of block
-};
-
-// What a compute warp reports about its tile besides the partials.
-struct TileSum {
-  int32_t cnt[kMaxSteps];  // survivors after each step under tspec
-  uint32_t alive0, alive1; // final speculative survivors: bit l = slot 2l / 2l+1
-};
-
-struct ScanArgs {
-  const float* tiles;
-  const int64_t* tile_ids;
-  int32_t d, d_pad;
-  int64_t tile_stride;
-  const VisitEntry* vis;
-  int64_t vis_qstride;
-  const int32_t* vis_count;
-  int32_t vis_count_qstride;
-  const float* queries;
-  const uint16_t* orders;
-  int64_t oqs, oss;
-  int32_t k, pruner, initial_step, nsteps;
-  double sf;
-  int32_t ads_d;
-  double eps0;
-  float* out_dist;
-  int64_t* out_ids;
-  int32_t* out_count;
-  int64_t* out_touched;
-  int64_t* out_total;
-  int32_t* trace;
-  int64_t trace_cap;
-  int64_t* trace_len;
-};
-
 struct Control {
-  int32_t n;            // entries in the top-k
-  int32_t cur_t;        // next tile within the current visit entry
-  int64_t cur_v;        // next visit entry
-  int64_t open_vis;     // visit index of a block whose first tile is committed but not its last
-  float tblk;           // T_b of the open block
-  int32_t linear;       // open block is linear
-  int32_t warm_min;     // smallest survivor count that keeps WARMUP for the open block
-  int32_t warm_m;       // the block size warm_min was computed for
-  int32_t nvalid[3];    // tiles scheduled per round (mod 3)
+  int32_t n;          // entries in the top-k
+  int32_t cur_t;      // next tile within the current visit entry
+  int64_t cur_v;      // next visit entry
+  int64_t open_vis;   // visit index of a block whose first tile is committed but not its last
+  float tblk;         // T_b of the open block
+  int32_t linear;     // open block is linear
+  int32_t warm_min;   // smallest survivor count that keeps WARMUP for the open block
+  int32_t warm_m;     // the block size warm_min was computed for
+  int32_t nvalid[3];  // tiles scheduled per round (mod 3)
   int64_t touched, total, tlen;
 };
-
-constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ float ads_or_bond_bound(int pruner, float T, int dims_seen, int ads_d,
-                                                   double ratio, double band) {
-  if (pruner != PDX_PRUNER_ADS || dims_seen >= ads_d) return T;  // bond: acc < T
-  // pruning.py:88: threshold * (dims_seen / d) * band * band, in float64,
-  // left to right; the comparison then happens in float32 (numpy casts the
-  // Python float to the array's float32).
-  const double t = __dmul_rn(__dmul_rn(__dmul_rn((double)T, ratio), band), band);
-  return __double2float_rn(t);
-}
+static_assert(sizeof(Control) <= 128, "control block");
 
 // Smallest survivor count p with float64(p / m) >= sf: search.py:148's
 // WARMUP test `len(positions) / block.m >= selection_fraction` is then an
@@ -119,157 +59,6 @@ __device__ __forceinline__ int warm_min_count(int m, double sf) {
   while (p > 0 && __ddiv_rn((double)(p - 1), (double)m) >= sf) --p;
   while (p < m && __ddiv_rn((double)p, (double)m) < sf) ++p;
   return p;
-}
-
-// ----------------------------------------------------------- speculation
-// One warp scans one tile with threshold t.tspec.  Lane l owns slots 2l,
-// 2l+1.  part[s*64 + slot] receives the slot's partial after step s (+inf
-// once the slot is pruned speculatively); sum gets the per-step survivor
-// counts and the final survivor mask; ids of final survivors go to sid.
-template <int G, bool ORD, int METRIC>
-__device__ __forceinline__ void speculate(const ScanArgs& A, const TileDesc& t,
-                                          const uint16_t* __restrict__ ord,
-                                          const float* __restrict__ s_q,
-                                          const int32_t* __restrict__ s_ends,
-                                          const double* __restrict__ s_ratio,
-                                          const double* __restrict__ s_band,
-                                          float* __restrict__ part, TileSum& sum,
-                                          int64_t* __restrict__ sid, int lane) {
-  const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
-  const int s0 = 2 * lane, s1 = s0 + 1;
-  bool al0 = s0 < t.m_tile, al1 = s1 < t.m_tile;
-  float acc0 = 0.f, acc1 = 0.f;
-  const float tspec = t.tspec;
-  const bool prune = tspec != INFINITY;
-  const int nsteps = A.nsteps;
-  float mybnd = INFINITY;
-  if (prune && lane < nsteps)
-    mybnd = ads_or_bond_bound(A.pruner, tspec, s_ends[lane], A.ads_d, s_ratio[lane], s_band[lane]);
-
-  // G = 8 sequential: the last loaded group stays in registers (steps do
-  // not end on group boundaries).
-  float4 ca0 = make_float4(0.f, 0.f, 0.f, 0.f), cb0 = ca0, ca1 = ca0, cb1 = ca0;
-  int cg = -1;
-
-  int a = 0;
-  int s = 0;
-  for (; s < nsteps; ++s) {
-    const int b = s_ends[s];
-    if (!__any_sync(kFull, al0 || al1)) break;
-    if (G == 8 && !ORD) {
-      const int glast = (b - 1) >> 3;
-      for (int g0 = a >> 3; g0 <= glast; g0 += 2) {
-        float4 r[2][4];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int g = g0 + u;
-          r[u][0] = r[u][1] = r[u][2] = r[u][3] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (g <= glast) {
-            if (g == cg) {
-              r[u][0] = ca0; r[u][1] = cb0; r[u][2] = ca1; r[u][3] = cb1;
-            } else {
-              const float* p = tb + ((int64_t)g * kTile + s0) * 8;
-              if (al0) { r[u][0] = ldg4(p); r[u][1] = ldg4(p + 4); }
-              if (al1) { r[u][2] = ldg4(p + 8); r[u][3] = ldg4(p + 12); }
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int g = g0 + u;
-          if (g <= glast) {
-            const float x0[8] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w,
-                                 r[u][1].x, r[u][1].y, r[u][1].z, r[u][1].w};
-            const float x1[8] = {r[u][2].x, r[u][2].y, r[u][2].z, r[u][2].w,
-                                 r[u][3].x, r[u][3].y, r[u][3].z, r[u][3].w};
-            const int jlo = max(a - g * 8, 0), jhi = min(b - g * 8, 8);
-            if (jlo == 0 && jhi == 8) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const float qj = s_q[g * 8 + e];
-                acc0 = upd<METRIC>(acc0, qj, x0[e]);
-                acc1 = upd<METRIC>(acc1, qj, x1[e]);
-              }
-            } else {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                if (e >= jlo && e < jhi) {
-                  const float qj = s_q[g * 8 + e];
-                  acc0 = upd<METRIC>(acc0, qj, x0[e]);
-                  acc1 = upd<METRIC>(acc1, qj, x1[e]);
-                }
-              }
-            }
-            cg = g; ca0 = r[u][0]; cb0 = r[u][1]; ca1 = r[u][2]; cb1 = r[u][3];
-          }
-        }
-      }
-    } else {
-      for (int j0 = a; j0 < b; j0 += 8) {
-        int dim[8];
-        float x0[8], x1[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = j0 + e;
-          dim[e] = 0;
-          x0[e] = x1[e] = 0.f;
-          if (j < b) dim[e] = ORD ? (int)__ldg(ord + j) : j;
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (j0 + e < b) {
-            const int dm = dim[e];
-            if (G == 1) {
-              if (al0 && al1) {
-                const float2 v = ldg2(tb + (int64_t)dm * kTile + s0);
-                x0[e] = v.x; x1[e] = v.y;
-              } else if (al0) {
-                x0[e] = __ldg(tb + (int64_t)dm * kTile + s0);
-              } else if (al1) {
-                x1[e] = __ldg(tb + (int64_t)dm * kTile + s1);
-              }
-            } else {
-              const float* p = tb + ((int64_t)(dm >> 3) * kTile + s0) * 8 + (dm & 7);
-              if (al0) x0[e] = __ldg(p);
-              if (al1) x1[e] = __ldg(p + 8);
-            }
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (j0 + e < b) {
-            const float qj = s_q[dim[e]];
-            acc0 = upd<METRIC>(acc0, qj, x0[e]);
-            acc1 = upd<METRIC>(acc1, qj, x1[e]);
-          }
-        }
-      }
-    }
-    float2 pv;
-    pv.x = al0 ? acc0 : INFINITY;
-    pv.y = al1 ? acc1 : INFINITY;
-    *reinterpret_cast<float2*>(part + s * kTile + s0) = pv;
-    if (prune) {
-      const float bs = __shfl_sync(kFull, mybnd, s);
-      al0 = al0 && (acc0 < bs);
-      al1 = al1 && (acc1 < bs);
-    }
-    const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
-    if (lane == 0) sum.cnt[s] = c;
-    a = b;
-  }
-  for (int s2 = s; s2 < nsteps; ++s2) {
-    *reinterpret_cast<float2*>(part + s2 * kTile + s0) = make_float2(INFINITY, INFINITY);
-    if (lane == 0) sum.cnt[s2] = 0;
-  }
-  const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
-  if (lane == 0) {
-    sum.alive0 = m0;
-    sum.alive1 = m1;
-  }
-  const int64_t* ids = A.tile_ids + t.tile * kTile;
-  if (al0) sid[s0] = __ldg(ids + s0);
-  if (al1) sid[s1] = __ldg(ids + s1);
 }
 
 // ------------------------------------------------------------------ top-k
@@ -322,39 +111,85 @@ __device__ __forceinline__ void topk_push_lanes(Control& c, int k, float* tkd, i
   }
 }
 
+// Shared-memory carve-up, shared by the kernel and the host launch code.
+struct ScanSmem {
+  size_t ctl, ratio, band, ends, bnd, cnt, wmin, desc, sum, items, wbnd, ids, tki, part, tkd, q,
+      bmask, total;
+};
+
+__host__ __device__ inline ScanSmem scan_smem_layout(int W, int tpw, int k, int nsteps, int d_pad) {
+  const int nt = 2 * W * tpw;  // tiles in flight (two rounds)
+  ScanSmem L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = (o + bytes + 15) & ~(size_t)15;
+    return at;
+  };
+  L.ctl = take(128);
+  L.ratio = take(sizeof(double) * kMaxSteps);
+  L.band = take(sizeof(double) * kMaxSteps);
+  L.ends = take(sizeof(int32_t) * kMaxSteps);
+  L.bnd = take(sizeof(float) * kMaxSteps);
+  L.cnt = take(sizeof(int32_t) * kMaxSteps);
+  L.wmin = take(sizeof(int32_t) * (kTile + 1));
+  L.desc = take(sizeof(TileDesc) * nt);
+  L.sum = take(sizeof(TileSum) * nt);
+  L.items = take(sizeof(SparseItem) * 32 * W);
+  L.wbnd = take(sizeof(float) * kMaxSteps * W * tpw);
+  L.ids = take(sizeof(int64_t) * kTile * nt);
+  L.tki = take(sizeof(int64_t) * k);
+  L.part = take(sizeof(float) * kTile * nsteps * nt);
+  L.tkd = take(sizeof(float) * k);
+  L.q = take(sizeof(float) * ((d_pad + 7) / 8) * 8);
+  L.bmask = take((d_pad + 7) / 8);
+  L.total = o;
+  return L;
+}
+
 // ------------------------------------------------------------------ kernel
 template <int G, bool ORD, int METRIC>
-__global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
+__global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const int tpw) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int q = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int W = (blockDim.x >> 5) - 1;  // compute warps
+  const int RT = W * tpw;               // tiles per round
   const int nsteps = A.nsteps, k = A.k;
 
-  // shared-memory carve-up (must match scan_smem_bytes)
-  unsigned char* p = smem;
-  Control& ctl = *reinterpret_cast<Control*>(p); p += 128;
-  double* s_ratio = reinterpret_cast<double*>(p); p += sizeof(double) * kMaxSteps;
-  double* s_band = reinterpret_cast<double*>(p); p += sizeof(double) * kMaxSteps;
-  int32_t* s_ends = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kMaxSteps;
-  float* s_bnd = reinterpret_cast<float*>(p); p += sizeof(float) * kMaxSteps;
-  int32_t* s_cnt = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kMaxSteps;
-  TileDesc* s_desc = reinterpret_cast<TileDesc*>(p); p += sizeof(TileDesc) * 2 * W;
-  TileSum* s_sum = reinterpret_cast<TileSum*>(p); p += sizeof(TileSum) * 2 * W;
-  int64_t* s_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * kTile * 2 * W;
-  int64_t* tki = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * ((k + 1) & ~1);
-  float* s_part = reinterpret_cast<float*>(p); p += sizeof(float) * kTile * nsteps * 2 * W;
-  float* tkd = reinterpret_cast<float*>(p); p += sizeof(float) * ((k + 3) & ~3);
-  float* s_q = reinterpret_cast<float*>(p);
+  const ScanSmem L = scan_smem_layout(W, tpw, k, nsteps, A.d_pad);
+  Control& ctl = *reinterpret_cast<Control*>(smem + L.ctl);
+  double* s_ratio = reinterpret_cast<double*>(smem + L.ratio);
+  double* s_band = reinterpret_cast<double*>(smem + L.band);
+  int32_t* s_ends = reinterpret_cast<int32_t*>(smem + L.ends);
+  float* s_bnd = reinterpret_cast<float*>(smem + L.bnd);
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(smem + L.cnt);
+  TileDesc* s_desc = reinterpret_cast<TileDesc*>(smem + L.desc);
+  TileSum* s_sum = reinterpret_cast<TileSum*>(smem + L.sum);
+  SparseItem* s_items = reinterpret_cast<SparseItem*>(smem + L.items);
+  float* s_wbnd = reinterpret_cast<float*>(smem + L.wbnd);
+  int64_t* s_ids = reinterpret_cast<int64_t*>(smem + L.ids);
+  int64_t* tki = reinterpret_cast<int64_t*>(smem + L.tki);
+  float* s_part = reinterpret_cast<float*>(smem + L.part);
+  float* tkd = reinterpret_cast<float*>(smem + L.tkd);
+  float* s_q = reinterpret_cast<float*>(smem + L.q);
+  uint8_t* s_bmask = reinterpret_cast<uint8_t*>(smem + L.bmask);
+  int32_t* s_wmin = reinterpret_cast<int32_t*>(smem + L.wmin);
 
   // ---- setup
   const float* qg = A.queries + (int64_t)q * A.d;
-  for (int j = threadIdx.x; j < A.d_pad; j += blockDim.x) s_q[j] = j < A.d ? qg[j] : 0.f;
+  const int ngroups = (A.d_pad + 7) / 8;
+  for (int j = threadIdx.x; j < ngroups * 8; j += blockDim.x) s_q[j] = j < A.d ? qg[j] : 0.f;
+  for (int j = threadIdx.x; j < ngroups; j += blockDim.x) s_bmask[j] = 0;
+  for (int m = threadIdx.x; m <= kTile; m += blockDim.x)
+    s_wmin[m] = m > 0 ? warm_min_count(m, A.sf) : 0;
+  __syncthreads();
   if (threadIdx.x == 0) {
     int64_t start = 0, width = A.initial_step;  // step_schedule (search.py:106-117)
     for (int s = 0; s < nsteps; ++s) {
       const int64_t end = start + width < A.d ? start + width : A.d;
       s_ends[s] = (int32_t)end;
+      s_bmask[(end - 1) >> 3] |= (uint8_t)(1u << ((end - 1) & 7));
       start = end;
       width *= 2;
     }
@@ -383,13 +218,13 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
   int64_t wbase = 0;
   VisitEntry cur = {0, 0, 0}, nxt = {0, 0, 0};
 
-  // schedule W tiles in visit order into desc buffer `buf` (commit warp)
+  // schedule RT tiles in visit order into desc buffer `buf` (commit warp)
   auto schedule = [&](int buf, int slot3) {
     const float tlive = topk_threshold(ctl, k, tkd);
     int nvalid = 0;
     int64_t cv = ctl.cur_v;
     int ct = ctl.cur_t;
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < RT; ++w) {
       if (cv >= nvis) break;
       if (cv >= wbase + 32) {  // slide the window; prefetch the one after
         wbase += 32;
@@ -412,7 +247,7 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
         t.flags = (ct == 0 ? 2 : 0) | (ct == ntl - 1 ? 4 : 0);
         if (A.pruner == PDX_PRUNER_NONE) t.tspec = INFINITY;
         else t.tspec = (cv == ctl.open_vis) ? ctl.tblk : tlive;
-        s_desc[buf * W + w] = t;
+        s_desc[buf * RT + w] = t;
       }
       ++nvalid;
       if (++ct == ntl) {
@@ -428,12 +263,79 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
     __syncwarp();
   };
 
-  // commit round tiles of desc buffer `buf` in visit order (commit warp)
+  // commit the tiles of desc buffer `buf` in visit order (commit warp)
   auto commit = [&](int buf, int nv) {
-    for (int w = 0; w < nv; ++w) {
-      const TileDesc t = s_desc[buf * W + w];
-      const TileSum& sm = s_sum[buf * W + w];
-      const float* part = s_part + (size_t)(buf * W + w) * nsteps * kTile;
+    int w = 0;
+    {
+      // Parallel fast path.  A leading run of tiles that are whole blocks,
+      // non-linear, speculated with the current threshold and without
+      // survivors changes nothing but the stats: the threshold stays put
+      // across the run, so every tile's own counts are the reference's.
+      const float T = topk_threshold(ctl, k, tkd);
+      bool simple = false;
+      TileDesc t;
+      const TileSum* sm = nullptr;
+      if (lane < nv) {
+        const int ti = buf * RT + lane;
+        t = s_desc[ti];
+        sm = &s_sum[ti];
+        simple = t.flags == 6 && t.vis != 0 && A.pruner != PDX_PRUNER_NONE && T != INFINITY &&
+                 t.tspec == T && t.block_m <= kTile && sm->alive0 == 0 && sm->alive1 == 0;
+      }
+      const unsigned stop = __ballot_sync(kFull, !simple);
+      const int np = min(nv, stop ? __ffs(stop) - 1 : 32);
+      if (np > 0) {
+        int64_t touched = 0, total = 0;
+        if (lane < np) {
+          const int64_t m = t.block_m;
+          const int wmin = s_wmin[m];
+          bool warm = true;
+          int64_t prev = m;
+          int a = 0;
+          for (int s = 0; s < nsteps; ++s) {
+            const int w_s = s_ends[s] - a;
+            a = s_ends[s];
+            if (warm && prev >= wmin) {
+              touched += m * w_s;
+            } else {
+              warm = false;
+              touched += prev * w_s;
+            }
+            prev = sm->cnt[s];
+          }
+          total = m * A.d;
+          if (tr && ctl.tlen >= 0 && ctl.tlen + (int64_t)np * (1 + nsteps) <= A.trace_cap) {
+            int32_t* rec = tr + ctl.tlen + (int64_t)lane * (1 + nsteps);
+            rec[0] = nsteps;
+            for (int s = 0; s < nsteps; ++s) rec[1 + s] = sm->cnt[s];
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          touched += __shfl_xor_sync(kFull, touched, o);
+          total += __shfl_xor_sync(kFull, total, o);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          ctl.touched += touched;
+          ctl.total += total;
+          if (tr) {
+            if (ctl.tlen >= 0 && ctl.tlen + (int64_t)np * (1 + nsteps) <= A.trace_cap)
+              ctl.tlen += (int64_t)np * (1 + nsteps);
+            else
+              ctl.tlen = -1;
+          }
+          ctl.open_vis = -1;
+        }
+        __syncwarp();
+        w = np;
+      }
+    }
+    for (; w < nv; ++w) {
+      const int ti = buf * RT + w;
+      const TileDesc t = s_desc[ti];
+      const TileSum& sm = s_sum[ti];
+      const float* part = s_part + (size_t)ti * nsteps * kTile;
       if (t.flags & 2) {  // first tile of its block: T_b is fixed now
         const float T = topk_threshold(ctl, k, tkd);
         const int lin = (t.vis == 0 || A.pruner == PDX_PRUNER_NONE || T == INFINITY);
@@ -469,6 +371,10 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
         c1 = s1 < t.m_tile;
         int mycnt = 0;
         for (int s = 0; s < nsteps; ++s) {
+          if (s == sm.dense_steps) {  // later partials exist only for parked slots
+            c0 = c0 && ((sm.items0 >> lane) & 1);
+            c1 = c1 && ((sm.items1 >> lane) & 1);
+          }
           const float bs = s_bnd[s];
           const float2 pv = *reinterpret_cast<const float2*>(part + s * kTile + s0);
           c0 = c0 && (pv.x < bs);
@@ -480,7 +386,7 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
       }
       if (__any_sync(kFull, c0 || c1)) {
         const float2 fin = *reinterpret_cast<const float2*>(part + (nsteps - 1) * kTile + s0);
-        const int64_t* sid = s_ids + (size_t)(buf * W + w) * kTile;
+        const int64_t* sid = s_ids + (size_t)ti * kTile;
         const float key0 = METRIC == PDX_METRIC_IP ? -fin.x : fin.x;
         const float key1 = METRIC == PDX_METRIC_IP ? -fin.y : fin.y;
         topk_push_lanes(ctl, k, tkd, tki, c0, key0, c0 ? sid[s0] : 0, lane);
@@ -550,14 +456,33 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
     if (warp == 0) {
       if (nv_prev) commit((r + 1) & 1, nv_prev);
       schedule((r + 1) & 1, (r + 1) % 3);
-    } else if (warp - 1 < nv_cur) {
+    } else {
       const int w = warp - 1, buf = r & 1;
-      const TileDesc t = s_desc[buf * W + w];
-      const uint16_t* ord =
-          ORD ? A.orders + ((int64_t)q * A.oqs + (int64_t)t.seg * A.oss) * A.d : nullptr;
-      speculate<G, ORD, METRIC>(A, t, ord, s_q, s_ends, s_ratio, s_band,
-                                s_part + (size_t)(buf * W + w) * nsteps * kTile,
-                                s_sum[buf * W + w], s_ids + (size_t)(buf * W + w) * kTile, lane);
+      const int t0 = buf * RT + w * tpw;  // this warp's slice of the round
+      const int nt = min(tpw, nv_cur - w * tpw);
+      if (nt > 0) {
+        SliceRefs R;
+        R.desc = s_desc + t0;
+        R.part = s_part + (size_t)t0 * nsteps * kTile;
+        R.sum = s_sum + t0;
+        R.sid = s_ids + (size_t)t0 * kTile;
+        R.bnd = s_wbnd + (size_t)w * tpw * kMaxSteps;
+        R.items = s_items + 32 * w;
+        QueryRefs Q;
+        Q.q = s_q;
+        Q.ends = s_ends;
+        Q.ratio = s_ratio;
+        Q.band = s_band;
+        Q.bmask = s_bmask;
+        int nitems = 0;
+        for (int j = 0; j < nt; ++j) {
+          if (G == 8 && !ORD)
+            dense_tile_g8<METRIC>(A, R.desc[j], j, Q, R, nitems, lane);
+          else
+            dense_tile_generic<G, ORD, METRIC>(A, q, R.desc[j], j, Q, R, nitems, lane);
+        }
+        sparse_phase<G, ORD, METRIC>(A, q, Q, R, nitems, lane);
+      }
     }
     __syncthreads();
   }
@@ -574,15 +499,6 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A) {
     if (A.out_total) A.out_total[q] = ctl.total;
     if (A.trace_len) A.trace_len[q] = ctl.tlen;
   }
-}
-
-size_t scan_smem_bytes(int W, int k, int nsteps, int d_pad) {
-  size_t b = 128 + sizeof(double) * kMaxSteps * 2 + sizeof(int32_t) * kMaxSteps * 3 +
-             sizeof(TileDesc) * 2 * W + sizeof(TileSum) * 2 * W +
-             sizeof(int64_t) * kTile * 2 * W + sizeof(int64_t) * ((k + 1) & ~1) +
-             sizeof(float) * kTile * nsteps * 2 * W + sizeof(float) * ((k + 3) & ~3) +
-             sizeof(float) * d_pad;
-  return (b + 15) & ~(size_t)15;
 }
 
 // ------------------------------------------------------------ visit lists
@@ -639,21 +555,22 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
 }
 
 template <int G, bool ORD, int METRIC>
-static cudaError_t launch_scan(const ScanArgs& A, int nq, int W, size_t smem, cudaStream_t st) {
+static cudaError_t launch_scan(const ScanArgs& A, int nq, int W, int tpw, size_t smem,
+                               cudaStream_t st) {
   auto fn = pdx_scan_kernel<G, ORD, METRIC>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<nq, (W + 1) * 32, smem, st>>>(A);
+  fn<<<nq, (W + 1) * 32, smem, st>>>(A, tpw);
   return cudaGetLastError();
 }
 
 template <int G, bool ORD>
-static cudaError_t launch_metric(int metric, const ScanArgs& A, int nq, int W, size_t smem,
-                                 cudaStream_t st) {
+static cudaError_t launch_metric(int metric, const ScanArgs& A, int nq, int W, int tpw,
+                                 size_t smem, cudaStream_t st) {
   switch (metric) {
-    case PDX_METRIC_L2: return launch_scan<G, ORD, PDX_METRIC_L2>(A, nq, W, smem, st);
-    case PDX_METRIC_L1: return launch_scan<G, ORD, PDX_METRIC_L1>(A, nq, W, smem, st);
-    default: return launch_scan<G, ORD, PDX_METRIC_IP>(A, nq, W, smem, st);
+    case PDX_METRIC_L2: return launch_scan<G, ORD, PDX_METRIC_L2>(A, nq, W, tpw, smem, st);
+    case PDX_METRIC_L1: return launch_scan<G, ORD, PDX_METRIC_L1>(A, nq, W, tpw, smem, st);
+    default: return launch_scan<G, ORD, PDX_METRIC_IP>(A, nq, W, tpw, smem, st);
   }
 }
 
@@ -712,10 +629,13 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   PDX_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   int W = prm->warps > 0 ? prm->warps : 4;  // compute warps per query CTA
   if (W > 8) W = 8;
-  size_t smem = scan_smem_bytes(W, prm->k, nsteps, store->d_pad);
-  while (W > 1 && smem > (size_t)optin) {
-    W /= 2;
-    smem = scan_smem_bytes(W, prm->k, nsteps, store->d_pad);
+  int tpw = prm->tiles_per_warp > 0 ? prm->tiles_per_warp : 2;
+  if (tpw > kMaxTpw) tpw = kMaxTpw;
+  size_t smem = scan_smem_layout(W, tpw, prm->k, nsteps, store->d_pad).total;
+  while ((W > 1 || tpw > 1) && smem > (size_t)optin) {
+    if (tpw > 1) tpw /= 2;
+    else W /= 2;
+    smem = scan_smem_layout(W, tpw, prm->k, nsteps, store->d_pad).total;
   }
   PDX_REQUIRE(smem <= (size_t)optin, "k/d too large for shared memory (%zu bytes)", smem);
 
@@ -776,11 +696,11 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   cudaError_t e;
   const bool ord = d_orders != nullptr;
   if (store->group == 8)
-    e = ord ? launch_metric<8, true>(prm->metric, A, (int)nq, W, smem, st)
-            : launch_metric<8, false>(prm->metric, A, (int)nq, W, smem, st);
+    e = ord ? launch_metric<8, true>(prm->metric, A, (int)nq, W, tpw, smem, st)
+            : launch_metric<8, false>(prm->metric, A, (int)nq, W, tpw, smem, st);
   else
-    e = ord ? launch_metric<1, true>(prm->metric, A, (int)nq, W, smem, st)
-            : launch_metric<1, false>(prm->metric, A, (int)nq, W, smem, st);
+    e = ord ? launch_metric<1, true>(prm->metric, A, (int)nq, W, tpw, smem, st)
+            : launch_metric<1, false>(prm->metric, A, (int)nq, W, tpw, smem, st);
   PDX_CUDA_CHECK(e);
   return PDX_OK;
 }

@@ -1,0 +1,434 @@
+// Speculative tile scan for the compute warps of pdx_scan_kernel.
+//
+// A compute warp owns `tpw` consecutive tiles of a round.  For each tile it
+// runs the DENSE phase — lane l owns slots 2l and 2l+1, the whole warp
+// reads the live slots' dims group by group — until at most kSparseMax of
+// the tile's 64 slots survive.  Those survivors are parked in a
+// warp-private list; after the warp's last tile the SPARSE phase finishes
+// them one survivor per lane, so the long tail of the schedule (where a few
+// of 64 slots live) runs on full warps instead of nearly empty ones.
+// Either way the tile reports, in shared memory, each slot's partial sum
+// after every step it reached, its per-step survivor counts under tspec,
+// its final survivor mask and the ids of its final survivors — the commit
+// warp consumes exactly that.
+//
+// Record contract (TileSum): part[s][slot] is valid for every slot for
+// s < dense_steps (+inf once the slot is pruned under tspec); for
+// s >= dense_steps only for slots in items0/items1 (the parked survivors),
+// up to the step where they are pruned.
+#pragma once
+#include "pdx_common.cuh"
+
+namespace pdx {
+
+constexpr int kSparseMax = 16;  // a tile goes sparse once <= this many slots survive
+constexpr int kMaxTpw = 2;      // tiles per compute warp per round (kSparseMax * kMaxTpw <= 32)
+constexpr unsigned kFull = 0xffffffffu;
+
+struct VisitEntry {
+  int64_t tile0;
+  int32_t m;
+  int32_t seg;
+};
+static_assert(sizeof(VisitEntry) == 16, "visit entry is 16 bytes");
+
+struct TileDesc {
+  int64_t tile;
+  int32_t m_tile;
+  int32_t seg;
+  int32_t block_m;
+  int32_t vis;
+  float tspec;
+  int32_t flags;  // bit1 first tile of block, bit2 last tile of block
+};
+
+// What a compute warp reports about a tile besides the partials.
+struct TileSum {
+  int32_t cnt[kMaxSteps];   // survivors after each step under tspec
+  uint32_t alive0, alive1;  // final speculative survivors: bit l = slot 2l / 2l+1
+  uint32_t items0, items1;  // slots parked for the sparse phase
+  int32_t dense_steps;      // steps recorded for every slot
+  int32_t _pad;
+};
+
+struct SparseItem {
+  int16_t tj;    // tile index within the warp's slice of the round
+  int16_t slot;  // slot within the tile
+  int16_t step;  // next schedule step
+  int16_t pos;   // next dimension
+  float acc;     // partial sum so far
+};
+
+struct ScanArgs {
+  const float* tiles;
+  const int64_t* tile_ids;
+  int32_t d, d_pad;
+  int64_t tile_stride;
+  const VisitEntry* vis;
+  int64_t vis_qstride;
+  const int32_t* vis_count;
+  int32_t vis_count_qstride;
+  const float* queries;
+  const uint16_t* orders;
+  int64_t oqs, oss;
+  int32_t k, pruner, initial_step, nsteps;
+  double sf;
+  int32_t ads_d;
+  double eps0;
+  float* out_dist;
+  int64_t* out_ids;
+  int32_t* out_count;
+  int64_t* out_touched;
+  int64_t* out_total;
+  int32_t* trace;
+  int64_t trace_cap;
+  int64_t* trace_len;
+};
+
+// Shared-memory views of one round slice (the tiles of one compute warp).
+struct SliceRefs {
+  const TileDesc* desc;  // [tpw]
+  float* part;           // [tpw][nsteps][64]
+  TileSum* sum;          // [tpw]
+  int64_t* sid;          // [tpw][64]
+  float* bnd;            // [tpw][kMaxSteps] speculative bound per step
+  SparseItem* items;     // [32]
+};
+
+// Per-query constants shared by all warps.
+struct QueryRefs {
+  const float* q;        // [d_pad] query, zero padded
+  const int32_t* ends;   // [nsteps] step ends
+  const double* ratio;   // [nsteps] dims_seen / ads_d
+  const double* band;    // [nsteps] 1 + eps0 / sqrt(dims_seen)
+  const uint8_t* bmask;  // [d_pad/8] bit e of group g: a step ends after dim 8g+e
+};
+
+__device__ __forceinline__ float ads_or_bond_bound(int pruner, float T, int dims_seen, int ads_d,
+                                                   double ratio, double band) {
+  if (pruner != PDX_PRUNER_ADS || dims_seen >= ads_d) return T;  // bond: acc < T
+  // pruning.py:88: threshold * (dims_seen / d) * band * band, in float64,
+  // left to right; the comparison then happens in float32 (numpy casts the
+  // Python float to the array's float32).
+  const double t = __dmul_rn(__dmul_rn(__dmul_rn((double)T, ratio), band), band);
+  return __double2float_rn(t);
+}
+
+__device__ __forceinline__ const uint16_t* order_of(const ScanArgs& A, int q, int seg) {
+  return A.orders + ((int64_t)q * A.oqs + (int64_t)seg * A.oss) * A.d;
+}
+
+// Lane `lane` < nsteps holds the tile's speculative bound for step `lane`.
+__device__ __forceinline__ float tile_bounds(const ScanArgs& A, const TileDesc& t,
+                                             const QueryRefs& Q, const SliceRefs& R, int tj,
+                                             int lane) {
+  float b = INFINITY;
+  if (t.tspec != INFINITY && lane < A.nsteps)
+    b = ads_or_bond_bound(A.pruner, t.tspec, Q.ends[lane], A.ads_d, Q.ratio[lane], Q.band[lane]);
+  if (lane < A.nsteps) R.bnd[tj * kMaxSteps + lane] = b;
+  return b;
+}
+
+// Park the live slots (al0/al1) of tile tj as sparse items at (step, pos).
+__device__ __forceinline__ void park(const SliceRefs& R, TileSum& sum, int tj, int s, int pos,
+                                     bool al0, bool al1, float acc0, float acc1, int nsteps,
+                                     int& nitems, int lane) {
+  const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
+  if (lane == 0) {
+    sum.alive0 = 0;
+    sum.alive1 = 0;
+    sum.items0 = m0;
+    sum.items1 = m1;
+    sum.dense_steps = s;
+  }
+  if (lane >= s && lane < nsteps) sum.cnt[lane] = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  const int pre = __popc(m0 & lt) + __popc(m1 & lt);
+  if (al0) R.items[nitems + pre] = SparseItem{(int16_t)tj, (int16_t)(2 * lane), (int16_t)s, (int16_t)pos, acc0};
+  if (al1) R.items[nitems + pre + (al0 ? 1 : 0)] = SparseItem{(int16_t)tj, (int16_t)(2 * lane + 1), (int16_t)s, (int16_t)pos, acc1};
+  nitems += __popc(m0) + __popc(m1);
+}
+
+__device__ __forceinline__ void finish_dense(const ScanArgs& A, const TileDesc& t,
+                                             const SliceRefs& R, TileSum& sum, int tj, bool al0,
+                                             bool al1, int lane) {
+  const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
+  if (lane == 0) {
+    sum.alive0 = m0;
+    sum.alive1 = m1;
+    sum.items0 = 0;
+    sum.items1 = 0;
+    sum.dense_steps = A.nsteps;
+  }
+  const int64_t* ids = A.tile_ids + t.tile * kTile;
+  if (al0) R.sid[tj * kTile + 2 * lane] = __ldg(ids + 2 * lane);
+  if (al1) R.sid[tj * kTile + 2 * lane + 1] = __ldg(ids + 2 * lane + 1);
+}
+
+// ----------------------------------------------- dense phase, G = 8, natural order
+template <int METRIC>
+__device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc& t, int tj,
+                                              const QueryRefs& Q, const SliceRefs& R,
+                                              int& nitems, int lane) {
+  const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
+  float* __restrict__ part = R.part + (size_t)tj * A.nsteps * kTile;
+  TileSum& sum = R.sum[tj];
+  const int nsteps = A.nsteps;
+  const int s0 = 2 * lane;
+  bool al0 = s0 < t.m_tile, al1 = s0 + 1 < t.m_tile;
+  const bool prune = t.tspec != INFINITY;
+  const float mybnd = tile_bounds(A, t, Q, R, tj, lane);
+  float acc0 = 0.f, acc1 = 0.f;
+  if (t.m_tile <= kSparseMax) {  // small tile: straight to the sparse phase
+    park(R, sum, tj, 0, 0, al0, al1, acc0, acc1, nsteps, nitems, lane);
+    return;
+  }
+  const int ng = A.d_pad >> 3;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 na = z, nb = z, nc = z, nd = z;  // prefetched group
+  {
+    const float* p = tb + (size_t)s0 * 8;
+    if (al0) { na = ldg4(p); nb = ldg4(p + 4); }
+    if (al1) { nc = ldg4(p + 8); nd = ldg4(p + 12); }
+  }
+  int s = 0;
+  for (int g = 0; g < ng; ++g) {
+    const float x0[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
+    const float x1[8] = {nc.x, nc.y, nc.z, nc.w, nd.x, nd.y, nd.z, nd.w};
+    if (g + 1 < ng) {  // prefetch the next group for the slots alive now
+      const float* p = tb + ((size_t)(g + 1) * kTile + s0) * 8;
+      na = nb = nc = nd = z;
+      if (al0) { na = ldg4(p); nb = ldg4(p + 4); }
+      if (al1) { nc = ldg4(p + 8); nd = ldg4(p + 12); }
+    }
+    const float4 qa = *reinterpret_cast<const float4*>(Q.q + g * 8);
+    const float4 qb = *reinterpret_cast<const float4*>(Q.q + g * 8 + 4);
+    const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+    const unsigned bm = Q.bmask[g];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      acc0 = upd<METRIC>(acc0, qv[e], x0[e]);
+      acc1 = upd<METRIC>(acc1, qv[e], x1[e]);
+      if (bm & (1u << e)) {  // step s ends after dim 8g+e (warp-uniform)
+        float2 pv;
+        pv.x = al0 ? acc0 : INFINITY;
+        pv.y = al1 ? acc1 : INFINITY;
+        *reinterpret_cast<float2*>(part + s * kTile + s0) = pv;
+        if (prune) {
+          const float bs = __shfl_sync(kFull, mybnd, s);
+          al0 = al0 && (acc0 < bs);
+          al1 = al1 && (acc1 < bs);
+        }
+        const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
+        if (lane == 0) sum.cnt[s] = c;
+        ++s;
+        if (s == nsteps) {
+          finish_dense(A, t, R, sum, tj, al0, al1, lane);
+          return;
+        }
+        if (c <= kSparseMax) {
+          park(R, sum, tj, s, g * 8 + e + 1, al0, al1, acc0, acc1, nsteps, nitems, lane);
+          return;
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------- dense phase, generic (G = 1 and/or a visit order)
+template <int G, bool ORD, int METRIC>
+__device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, const TileDesc& t,
+                                                   int tj, const QueryRefs& Q,
+                                                   const SliceRefs& R, int& nitems, int lane) {
+  const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
+  const uint16_t* __restrict__ ord = ORD ? order_of(A, q, t.seg) : nullptr;
+  float* __restrict__ part = R.part + (size_t)tj * A.nsteps * kTile;
+  TileSum& sum = R.sum[tj];
+  const int nsteps = A.nsteps;
+  const int s0 = 2 * lane, s1 = s0 + 1;
+  bool al0 = s0 < t.m_tile, al1 = s1 < t.m_tile;
+  const bool prune = t.tspec != INFINITY;
+  const float mybnd = tile_bounds(A, t, Q, R, tj, lane);
+  float acc0 = 0.f, acc1 = 0.f;
+  if (t.m_tile <= kSparseMax) {
+    park(R, sum, tj, 0, 0, al0, al1, acc0, acc1, nsteps, nitems, lane);
+    return;
+  }
+  int a = 0;
+  for (int s = 0; s < nsteps; ++s) {
+    const int b = Q.ends[s];
+    for (int j0 = a; j0 < b; j0 += 8) {
+      int dim[8];
+      float x0[8], x1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = j0 + e;
+        dim[e] = 0;
+        x0[e] = x1[e] = 0.f;
+        if (j < b) dim[e] = ORD ? (int)__ldg(ord + j) : j;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (j0 + e < b) {
+          const int dm = dim[e];
+          if (G == 1) {
+            if (al0 && al1) {
+              const float2 v = ldg2(tb + (int64_t)dm * kTile + s0);
+              x0[e] = v.x; x1[e] = v.y;
+            } else if (al0) {
+              x0[e] = __ldg(tb + (int64_t)dm * kTile + s0);
+            } else if (al1) {
+              x1[e] = __ldg(tb + (int64_t)dm * kTile + s1);
+            }
+          } else {
+            const float* p = tb + ((int64_t)(dm >> 3) * kTile + s0) * 8 + (dm & 7);
+            if (al0) x0[e] = __ldg(p);
+            if (al1) x1[e] = __ldg(p + 8);
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (j0 + e < b) {
+          const float qj = Q.q[dim[e]];
+          acc0 = upd<METRIC>(acc0, qj, x0[e]);
+          acc1 = upd<METRIC>(acc1, qj, x1[e]);
+        }
+      }
+    }
+    float2 pv;
+    pv.x = al0 ? acc0 : INFINITY;
+    pv.y = al1 ? acc1 : INFINITY;
+    *reinterpret_cast<float2*>(part + s * kTile + s0) = pv;
+    if (prune) {
+      const float bs = __shfl_sync(kFull, mybnd, s);
+      al0 = al0 && (acc0 < bs);
+      al1 = al1 && (acc1 < bs);
+    }
+    const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
+    if (lane == 0) sum.cnt[s] = c;
+    a = b;
+    if (s + 1 < nsteps && c <= kSparseMax) {
+      park(R, sum, tj, s + 1, b, al0, al1, acc0, acc1, nsteps, nitems, lane);
+      return;
+    }
+  }
+  finish_dense(A, t, R, sum, tj, al0, al1, lane);
+}
+
+// ----------------------------------------------------------- sparse phase
+// Lane i finishes item i.  It walks its slot's remaining dims, records the
+// partial at each step end, decides against its tile's speculative bound,
+// and reports counts / survivors with shared-memory atomics.
+template <int G, bool ORD, int METRIC>
+__device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const QueryRefs& Q,
+                                             const SliceRefs& R, int nitems, int lane) {
+  if (nitems == 0) return;
+  __syncwarp();
+  const int nsteps = A.nsteps;
+  bool act = lane < nitems;
+  const SparseItem it = act ? R.items[lane] : SparseItem{0, 0, 0, 0, 0.f};
+  const TileDesc& t = R.desc[it.tj];
+  const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
+  float* __restrict__ part = R.part + (size_t)it.tj * nsteps * kTile;
+  TileSum& sum = R.sum[it.tj];
+  const float* bnd = R.bnd + it.tj * kMaxSteps;
+  const bool prune = t.tspec != INFINITY;
+  const int slot = it.slot;
+  int s = it.step;
+  float acc = it.acc;
+  int pos = it.pos;
+  if (G == 8 && !ORD) {
+    const int ng = A.d_pad >> 3;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    int g = pos >> 3;
+    float4 na = z, nb = z;
+    if (act) {
+      const float* p = tb + ((size_t)g * kTile + slot) * 8;
+      na = ldg4(p);
+      nb = ldg4(p + 4);
+    }
+    while (__any_sync(kFull, act)) {
+      if (act) {
+        const float x[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
+        if (g + 1 < ng) {
+          const float* p = tb + ((size_t)(g + 1) * kTile + slot) * 8;
+          na = ldg4(p);
+          nb = ldg4(p + 4);
+        }
+        const float4 qa = *reinterpret_cast<const float4*>(Q.q + g * 8);
+        const float4 qb = *reinterpret_cast<const float4*>(Q.q + g * 8 + 4);
+        const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        const unsigned bm = Q.bmask[g];
+        const int e0 = pos - g * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (act && e >= e0) {
+            acc = upd<METRIC>(acc, qv[e], x[e]);
+            if (bm & (1u << e)) {
+              part[s * kTile + slot] = acc;
+              const bool ok = !prune || acc < bnd[s];
+              if (ok) atomicAdd(&sum.cnt[s], 1);
+              ++s;
+              if (!ok) {
+                act = false;
+              } else if (s == nsteps) {
+                atomicOr(slot & 1 ? &sum.alive1 : &sum.alive0, 1u << (slot >> 1));
+                R.sid[it.tj * kTile + slot] = __ldg(A.tile_ids + t.tile * kTile + slot);
+                act = false;
+              }
+            }
+          }
+        }
+        ++g;
+        pos = g * 8;
+      }
+    }
+  } else {
+    const uint16_t* __restrict__ ord = ORD ? order_of(A, q, t.seg) : nullptr;
+    int end = act ? Q.ends[s] : 0;
+    while (__any_sync(kFull, act)) {
+      if (act) {
+        const int jend = min(end, pos + 8);
+        int dim[8];
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          dim[e] = 0;
+          x[e] = 0.f;
+          if (pos + e < jend) dim[e] = ORD ? (int)__ldg(ord + pos + e) : pos + e;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (pos + e < jend) {
+            const int dm = dim[e];
+            x[e] = G == 1 ? __ldg(tb + (int64_t)dm * kTile + slot)
+                          : __ldg(tb + ((int64_t)(dm >> 3) * kTile + slot) * 8 + (dm & 7));
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (pos + e < jend) acc = upd<METRIC>(acc, Q.q[dim[e]], x[e]);
+        pos = jend;
+        if (pos == end) {
+          part[s * kTile + slot] = acc;
+          const bool ok = !prune || acc < bnd[s];
+          if (ok) atomicAdd(&sum.cnt[s], 1);
+          ++s;
+          if (!ok) {
+            act = false;
+          } else if (s == nsteps) {
+            atomicOr(slot & 1 ? &sum.alive1 : &sum.alive0, 1u << (slot >> 1));
+            R.sid[it.tj * kTile + slot] = __ldg(A.tile_ids + t.tile * kTile + slot);
+            act = false;
+          } else {
+            end = Q.ends[s];
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+}  // namespace pdx

@@ -163,12 +163,14 @@ def decode_trace(buf, n):
     return out
 
 
-def make_params(params: SearchParams, d: int, warps: int = 0) -> _lib.PdxSearchParams:
+def make_params(params: SearchParams, d: int, warps=0) -> _lib.PdxSearchParams:
+    """``warps``: compute warps per query CTA, or (warps, tiles_per_warp); 0 = auto."""
     ads = params.ads if params.ads is not None else AdsPruner(d=d)
+    w, tpw = (warps if isinstance(warps, tuple) else (warps, 0))
     return _lib.PdxSearchParams(int(params.k), _lib.METRIC[Metric(params.metric).value],
                                 _lib.PRUNER[params.pruner], int(params.initial_step),
-                                float(params.selection_fraction), int(ads.d), int(warps),
-                                float(ads.epsilon0))
+                                float(params.selection_fraction), int(ads.d), int(w),
+                                float(ads.epsilon0), int(tpw), 0)
 
 
 def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None, orders=None,
