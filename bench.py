@@ -144,6 +144,7 @@ def main():
     ap.add_argument("--nprobe", type=int, default=32)
     ap.add_argument("--warps", default="0", help="compute warps per query CTA, or W,tiles_per_warp")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--debug", action="store_true", help="print kernel diagnostics to stderr")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -227,6 +228,18 @@ def main():
     touched = int(st_res.touched.sum().item())
     total = int(st_res.total.sum().item())
     alg_bytes = 4 * touched
+    if args.debug:
+        dbg = torch.zeros((args.nq, 8), dtype=torch.int64, device=dev)
+        searcher._buf["debug_buf"] = dbg
+        searcher.run(Qr_dev)
+        torch.cuda.synchronize()
+        del searcher._buf["debug_buf"]
+        d = dbg.cpu().numpy().astype(np.float64)
+        names = ["cycles", "tiles", "fast", "serial", "replay", "commit_idle", "ring_waits",
+                 "sparse_items"]
+        print("DEBUG per-query mean:", {n: round(float(d[:, i].mean()), 1)
+                                        for i, n in enumerate(names)},
+              "max cycles", int(d[:, 0].max()), file=sys.stderr)
 
     for _ in range(args.warmup):
         step(Qd)

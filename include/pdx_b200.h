@@ -84,11 +84,12 @@ typedef struct pdx_store {
   int64_t nblocks;
   const float* d_tiles;
   const int64_t* d_tile_ids;
-  const int64_t* d_block_tile;
+  const int64_t* d_block_tile;  /* [nblocks+1] first tile of each block (prefix) */
   const int32_t* d_block_m;
   const int64_t* d_bucket_block;
   int32_t max_bucket_blocks; /* max over buckets of (#blocks) */
-  int32_t _reserved;
+  int32_t max_bucket_tiles;  /* max over buckets of (#tiles) */
+  const int32_t* d_tile_block;  /* [ntiles] logical block of each tile */
 } pdx_store;
 
 /* SearchParams (search.py:61-85) + AdsPruner (pruning.py:56-65). */
@@ -101,8 +102,8 @@ typedef struct pdx_search_params {
   int32_t ads_d;    /* AdsPruner.d (the reference defaults it to the data d) */
   int32_t warps;    /* compute warps per query CTA (0 = auto) */
   double ads_epsilon0;
-  int32_t tiles_per_warp; /* 64-vector tiles per compute warp per round (0 = auto) */
-  int32_t _reserved;
+  int32_t tiles_per_warp; /* 64-vector tiles a compute warp claims at once (0 = auto) */
+  int32_t ring_slots;     /* tiles in flight per query CTA (0 = auto) */
 } pdx_search_params;
 
 /* Outputs of pdx_search.  Per query q (row q of each array):
@@ -124,6 +125,10 @@ typedef struct pdx_search_out {
   int32_t* d_trace;
   int64_t trace_cap;
   int64_t* d_trace_len;
+  /* optional [nq][8] kernel diagnostics: cycles, tiles, fast-path commits,
+   * serial commits, replays, commit-warp idle polls, compute-warp ring
+   * waits, sparse items */
+  int64_t* d_debug;
 } pdx_search_out;
 
 int pdx_abi_version(void);

@@ -33,20 +33,20 @@ class PdxStore(C.Structure):
                 ("d_tiles", C.c_void_p), ("d_tile_ids", C.c_void_p),
                 ("d_block_tile", C.c_void_p), ("d_block_m", C.c_void_p),
                 ("d_bucket_block", C.c_void_p), ("max_bucket_blocks", C.c_int32),
-                ("_reserved", C.c_int32)]
+                ("max_bucket_tiles", C.c_int32), ("d_tile_block", C.c_void_p)]
 
 
 class PdxSearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("metric", C.c_int32), ("pruner", C.c_int32),
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
                 ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
-                ("tiles_per_warp", C.c_int32), ("_reserved", C.c_int32)]
+                ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32)]
 
 
 class PdxSearchOut(C.Structure):
     _fields_ = [("d_dist", C.c_void_p), ("d_ids", C.c_void_p), ("d_count", C.c_void_p),
                 ("d_touched", C.c_void_p), ("d_total", C.c_void_p), ("d_trace", C.c_void_p),
-                ("trace_cap", C.c_int64), ("d_trace_len", C.c_void_p)]
+                ("trace_cap", C.c_int64), ("d_trace_len", C.c_void_p), ("d_debug", C.c_void_p)]
 
 
 def build(force: bool = False, quiet: bool = True) -> Path:

@@ -79,5 +79,16 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
 __device__ __forceinline__ float2 ldg2(const float* p) {
   return __ldg(reinterpret_cast<const float2*>(p));
 }
+// One 256-bit load (LDG.E.ENL2.256): the 8 dims of one slot in a G = 8 tile
+// group, a full 32-byte sector.  p must be 32-byte aligned.
+__device__ __forceinline__ void ldg8(const float* p, float (&x)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
+                 "=f"(x[6]), "=f"(x[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 }  // namespace pdx

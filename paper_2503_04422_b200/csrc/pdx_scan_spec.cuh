@@ -21,16 +21,21 @@
 
 namespace pdx {
 
-constexpr int kSparseMax = 16;  // a tile goes sparse once <= this many slots survive
-constexpr int kMaxTpw = 2;      // tiles per compute warp per round (kSparseMax * kMaxTpw <= 32)
+// a tile goes sparse once <= A.sparse_max (= 32 / tiles per claim) slots survive
+constexpr int kMaxTpw = 8;  // tiles per compute-warp claim (sparse_max * tpw <= 32)
 constexpr unsigned kFull = 0xffffffffu;
 
-struct VisitEntry {
-  int64_t tile0;
-  int32_t m;
-  int32_t seg;
+// One tile of a query's visit list (built by build_visits_kernel).
+struct TileEntry {
+  int64_t tile;     // tile index in the store
+  int32_t m_tile;   // valid slots in this tile
+  int32_t block_m;  // vectors in its logical block
+  int32_t seg;      // visit segment (selected bucket) — picks the visit order
+  int32_t vis;      // ordinal of its block in the query's block sequence
+  int32_t tib;      // tile index within its block
+  int32_t flags;    // bit1 first tile of block, bit2 last tile of block
 };
-static_assert(sizeof(VisitEntry) == 16, "visit entry is 16 bytes");
+static_assert(sizeof(TileEntry) == 32, "tile entry is 32 bytes");
 
 struct TileDesc {
   int64_t tile;
@@ -49,6 +54,7 @@ struct TileSum {
   uint32_t items0, items1;  // slots parked for the sparse phase
   int32_t dense_steps;      // steps recorded for every slot
   int32_t _pad;
+  int64_t touched_spec;     // values_touched of the block if the speculation is exact
 };
 
 struct SparseItem {
@@ -64,7 +70,7 @@ struct ScanArgs {
   const int64_t* tile_ids;
   int32_t d, d_pad;
   int64_t tile_stride;
-  const VisitEntry* vis;
+  const TileEntry* vis;
   int64_t vis_qstride;
   const int32_t* vis_count;
   int32_t vis_count_qstride;
@@ -83,6 +89,8 @@ struct ScanArgs {
   int32_t* trace;
   int64_t trace_cap;
   int64_t* trace_len;
+  int64_t* debug;  // optional [nq][8] counters (see pdx_search_out)
+  int32_t sparse_max;  // a tile goes sparse once at most this many slots survive
 };
 
 // Shared-memory views of one round slice (the tiles of one compute warp).
@@ -90,7 +98,6 @@ struct SliceRefs {
   const TileDesc* desc;  // [tpw]
   float* part;           // [tpw][nsteps][64]
   TileSum* sum;          // [tpw]
-  int64_t* sid;          // [tpw][64]
   float* bnd;            // [tpw][kMaxSteps] speculative bound per step
   SparseItem* items;     // [32]
 };
@@ -144,8 +151,8 @@ __device__ __forceinline__ void park(const SliceRefs& R, TileSum& sum, int tj, i
   if (lane >= s && lane < nsteps) sum.cnt[lane] = 0;
   const unsigned lt = (1u << lane) - 1u;
   const int pre = __popc(m0 & lt) + __popc(m1 & lt);
-  if (al0) R.items[nitems + pre] = SparseItem{(int16_t)tj, (int16_t)(2 * lane), (int16_t)s, (int16_t)pos, acc0};
-  if (al1) R.items[nitems + pre + (al0 ? 1 : 0)] = SparseItem{(int16_t)tj, (int16_t)(2 * lane + 1), (int16_t)s, (int16_t)pos, acc1};
+  if (al0) R.items[nitems + pre] = SparseItem{(int16_t)tj, (int16_t)lane, (int16_t)s, (int16_t)pos, acc0};
+  if (al1) R.items[nitems + pre + (al0 ? 1 : 0)] = SparseItem{(int16_t)tj, (int16_t)(lane + 32), (int16_t)s, (int16_t)pos, acc1};
   nitems += __popc(m0) + __popc(m1);
 }
 
@@ -160,9 +167,6 @@ __device__ __forceinline__ void finish_dense(const ScanArgs& A, const TileDesc& 
     sum.items1 = 0;
     sum.dense_steps = A.nsteps;
   }
-  const int64_t* ids = A.tile_ids + t.tile * kTile;
-  if (al0) R.sid[tj * kTile + 2 * lane] = __ldg(ids + 2 * lane);
-  if (al1) R.sid[tj * kTile + 2 * lane + 1] = __ldg(ids + 2 * lane + 1);
 }
 
 // ----------------------------------------------- dense phase, G = 8, natural order
@@ -174,32 +178,36 @@ __device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc&
   float* __restrict__ part = R.part + (size_t)tj * A.nsteps * kTile;
   TileSum& sum = R.sum[tj];
   const int nsteps = A.nsteps;
-  const int s0 = 2 * lane;
-  bool al0 = s0 < t.m_tile, al1 = s0 + 1 < t.m_tile;
+  const int s0 = lane, s1 = lane + 32;  // a 256-bit load per slot is contiguous across lanes
+  bool al0 = s0 < t.m_tile, al1 = s1 < t.m_tile;
   const bool prune = t.tspec != INFINITY;
   const float mybnd = tile_bounds(A, t, Q, R, tj, lane);
   float acc0 = 0.f, acc1 = 0.f;
-  if (t.m_tile <= kSparseMax) {  // small tile: straight to the sparse phase
+  if (t.m_tile <= A.sparse_max) {  // small tile: straight to the sparse phase
     park(R, sum, tj, 0, 0, al0, al1, acc0, acc1, nsteps, nitems, lane);
     return;
   }
   const int ng = A.d_pad >> 3;
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 na = z, nb = z, nc = z, nd = z;  // prefetched group
+  float n0[8], n1[8];  // prefetched group
+#pragma unroll
+  for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
   {
     const float* p = tb + (size_t)s0 * 8;
-    if (al0) { na = ldg4(p); nb = ldg4(p + 4); }
-    if (al1) { nc = ldg4(p + 8); nd = ldg4(p + 12); }
+    if (al0) ldg8(p, n0);
+    if (al1) ldg8(p + 32 * 8, n1);
   }
   int s = 0;
   for (int g = 0; g < ng; ++g) {
-    const float x0[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-    const float x1[8] = {nc.x, nc.y, nc.z, nc.w, nd.x, nd.y, nd.z, nd.w};
+    float x0[8], x1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      x0[e] = n0[e];
+      x1[e] = n1[e];
+    }
     if (g + 1 < ng) {  // prefetch the next group for the slots alive now
       const float* p = tb + ((size_t)(g + 1) * kTile + s0) * 8;
-      na = nb = nc = nd = z;
-      if (al0) { na = ldg4(p); nb = ldg4(p + 4); }
-      if (al1) { nc = ldg4(p + 8); nd = ldg4(p + 12); }
+      if (al0) ldg8(p, n0);
+      if (al1) ldg8(p + 32 * 8, n1);
     }
     const float4 qa = *reinterpret_cast<const float4*>(Q.q + g * 8);
     const float4 qb = *reinterpret_cast<const float4*>(Q.q + g * 8 + 4);
@@ -210,10 +218,8 @@ __device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc&
       acc0 = upd<METRIC>(acc0, qv[e], x0[e]);
       acc1 = upd<METRIC>(acc1, qv[e], x1[e]);
       if (bm & (1u << e)) {  // step s ends after dim 8g+e (warp-uniform)
-        float2 pv;
-        pv.x = al0 ? acc0 : INFINITY;
-        pv.y = al1 ? acc1 : INFINITY;
-        *reinterpret_cast<float2*>(part + s * kTile + s0) = pv;
+        part[s * kTile + s0] = al0 ? acc0 : INFINITY;
+        part[s * kTile + s1] = al1 ? acc1 : INFINITY;
         if (prune) {
           const float bs = __shfl_sync(kFull, mybnd, s);
           al0 = al0 && (acc0 < bs);
@@ -226,7 +232,7 @@ __device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc&
           finish_dense(A, t, R, sum, tj, al0, al1, lane);
           return;
         }
-        if (c <= kSparseMax) {
+        if (c <= A.sparse_max) {
           park(R, sum, tj, s, g * 8 + e + 1, al0, al1, acc0, acc1, nsteps, nitems, lane);
           return;
         }
@@ -245,12 +251,12 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
   float* __restrict__ part = R.part + (size_t)tj * A.nsteps * kTile;
   TileSum& sum = R.sum[tj];
   const int nsteps = A.nsteps;
-  const int s0 = 2 * lane, s1 = s0 + 1;
+  const int s0 = lane, s1 = lane + 32;
   bool al0 = s0 < t.m_tile, al1 = s1 < t.m_tile;
   const bool prune = t.tspec != INFINITY;
   const float mybnd = tile_bounds(A, t, Q, R, tj, lane);
   float acc0 = 0.f, acc1 = 0.f;
-  if (t.m_tile <= kSparseMax) {
+  if (t.m_tile <= A.sparse_max) {
     park(R, sum, tj, 0, 0, al0, al1, acc0, acc1, nsteps, nitems, lane);
     return;
   }
@@ -271,19 +277,13 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
       for (int e = 0; e < 8; ++e) {
         if (j0 + e < b) {
           const int dm = dim[e];
-          if (G == 1) {
-            if (al0 && al1) {
-              const float2 v = ldg2(tb + (int64_t)dm * kTile + s0);
-              x0[e] = v.x; x1[e] = v.y;
-            } else if (al0) {
-              x0[e] = __ldg(tb + (int64_t)dm * kTile + s0);
-            } else if (al1) {
-              x1[e] = __ldg(tb + (int64_t)dm * kTile + s1);
-            }
+          if (G == 1) {  // a 256-byte PDX row: two coalesced 128-byte halves
+            if (al0) x0[e] = __ldg(tb + (int64_t)dm * kTile + s0);
+            if (al1) x1[e] = __ldg(tb + (int64_t)dm * kTile + s1);
           } else {
             const float* p = tb + ((int64_t)(dm >> 3) * kTile + s0) * 8 + (dm & 7);
             if (al0) x0[e] = __ldg(p);
-            if (al1) x1[e] = __ldg(p + 8);
+            if (al1) x1[e] = __ldg(p + 32 * 8);
           }
         }
       }
@@ -296,10 +296,8 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
         }
       }
     }
-    float2 pv;
-    pv.x = al0 ? acc0 : INFINITY;
-    pv.y = al1 ? acc1 : INFINITY;
-    *reinterpret_cast<float2*>(part + s * kTile + s0) = pv;
+    part[s * kTile + s0] = al0 ? acc0 : INFINITY;
+    part[s * kTile + s1] = al1 ? acc1 : INFINITY;
     if (prune) {
       const float bs = __shfl_sync(kFull, mybnd, s);
       al0 = al0 && (acc0 < bs);
@@ -308,7 +306,7 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
     const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
     if (lane == 0) sum.cnt[s] = c;
     a = b;
-    if (s + 1 < nsteps && c <= kSparseMax) {
+    if (s + 1 < nsteps && c <= A.sparse_max) {
       park(R, sum, tj, s + 1, b, al0, al1, acc0, acc1, nsteps, nitems, lane);
       return;
     }
@@ -340,22 +338,17 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
   int pos = it.pos;
   if (G == 8 && !ORD) {
     const int ng = A.d_pad >> 3;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     int g = pos >> 3;
-    float4 na = z, nb = z;
-    if (act) {
-      const float* p = tb + ((size_t)g * kTile + slot) * 8;
-      na = ldg4(p);
-      nb = ldg4(p + 4);
-    }
+    float nx[8];  // prefetched group: one 256-bit load per 8 dims
+#pragma unroll
+    for (int e = 0; e < 8; ++e) nx[e] = 0.f;
+    if (act) ldg8(tb + ((size_t)g * kTile + slot) * 8, nx);
     while (__any_sync(kFull, act)) {
       if (act) {
-        const float x[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-        if (g + 1 < ng) {
-          const float* p = tb + ((size_t)(g + 1) * kTile + slot) * 8;
-          na = ldg4(p);
-          nb = ldg4(p + 4);
-        }
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = nx[e];
+        if (g + 1 < ng) ldg8(tb + ((size_t)(g + 1) * kTile + slot) * 8, nx);
         const float4 qa = *reinterpret_cast<const float4*>(Q.q + g * 8);
         const float4 qb = *reinterpret_cast<const float4*>(Q.q + g * 8 + 4);
         const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
@@ -373,8 +366,7 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
               if (!ok) {
                 act = false;
               } else if (s == nsteps) {
-                atomicOr(slot & 1 ? &sum.alive1 : &sum.alive0, 1u << (slot >> 1));
-                R.sid[it.tj * kTile + slot] = __ldg(A.tile_ids + t.tile * kTile + slot);
+                atomicOr(slot >= 32 ? &sum.alive1 : &sum.alive0, 1u << (slot & 31));
                 act = false;
               }
             }
@@ -418,8 +410,7 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
           if (!ok) {
             act = false;
           } else if (s == nsteps) {
-            atomicOr(slot & 1 ? &sum.alive1 : &sum.alive0, 1u << (slot >> 1));
-            R.sid[it.tj * kTile + slot] = __ldg(A.tile_ids + t.tile * kTile + slot);
+            atomicOr(slot >= 32 ? &sum.alive1 : &sum.alive0, 1u << (slot & 31));
             act = false;
           } else {
             end = Q.ends[s];

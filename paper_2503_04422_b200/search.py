@@ -164,13 +164,14 @@ def decode_trace(buf, n):
 
 
 def make_params(params: SearchParams, d: int, warps=0) -> _lib.PdxSearchParams:
-    """``warps``: compute warps per query CTA, or (warps, tiles_per_warp); 0 = auto."""
+    """``warps``: compute warps per query CTA, or (warps, tiles_per_warp[,
+    ring_slots]); 0 = auto."""
     ads = params.ads if params.ads is not None else AdsPruner(d=d)
-    w, tpw = (warps if isinstance(warps, tuple) else (warps, 0))
+    w, tpw, rb = (tuple(warps) + (0, 0))[:3] if isinstance(warps, tuple) else (warps, 0, 0)
     return _lib.PdxSearchParams(int(params.k), _lib.METRIC[Metric(params.metric).value],
                                 _lib.PRUNER[params.pruner], int(params.initial_step),
                                 float(params.selection_fraction), int(ads.d), int(w),
-                                float(ads.epsilon0), int(tpw), 0)
+                                float(ads.epsilon0), int(tpw), int(rb))
 
 
 def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None, orders=None,
@@ -206,8 +207,12 @@ def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None,
     if trace_cap:
         trace = torch.zeros((nq, trace_cap), dtype=torch.int32, device=dev)
         trace_len = torch.zeros((nq,), dtype=torch.int64, device=dev)
+    debug = out.get("debug_buf")
+    if debug is not None and debug.shape != (nq, 8):
+        debug = None
     so = _lib.PdxSearchOut(_lib.ptr(dist), _lib.ptr(ids), _lib.ptr(count), _lib.ptr(touched),
-                           _lib.ptr(total), _lib.ptr(trace), int(trace_cap), _lib.ptr(trace_len))
+                           _lib.ptr(total), _lib.ptr(trace), int(trace_cap), _lib.ptr(trace_len),
+                           _lib.ptr(debug))
     L = _lib.lib()
     nlists = nq if seg_bucket is not None else 1
     wb = int(L.pdx_search_workspace(store.ref, nlists, nseg))

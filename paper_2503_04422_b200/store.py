@@ -68,7 +68,11 @@ class DeviceStore:
     """A packed store in HBM plus the ``pdx_store`` ABI view of it."""
 
     def __init__(self, tiles, tile_ids, block_tile, block_m, bucket_block, d, group,
-                 max_bucket_blocks):
+                 tile_block=None):
+        """block_tile: int64 [nblocks+1] tile prefix; bucket_block: int64
+        [nbuckets+1] block prefix; tile_block: int32 [ntiles] (derived when
+        omitted)."""
+        torch = _torch()
         self.tiles = tiles
         self.tile_ids = tile_ids
         self.block_tile = block_tile
@@ -79,12 +83,21 @@ class DeviceStore:
         self.d_pad = (self.d + 7) // 8 * 8 if self.group == 8 else self.d
         self.nblocks = int(block_m.numel())
         self.nbuckets = int(bucket_block.numel()) - 1
-        self.ntiles = int(tiles.shape[0]) if tiles.dim() else 0
-        self.max_bucket_blocks = int(max_bucket_blocks)
+        self.ntiles = int(block_tile[-1].item()) if self.nblocks else 0
+        if tile_block is None:
+            ntl = block_tile[1:] - block_tile[:-1]
+            tile_block = torch.repeat_interleave(
+                torch.arange(self.nblocks, dtype=torch.int32, device=tiles.device), ntl)
+        self.tile_block = tile_block.to(torch.int32).contiguous()
+        nbk = bucket_block[1:] - bucket_block[:-1]
+        ntk = block_tile[bucket_block[1:]] - block_tile[bucket_block[:-1]]
+        self.max_bucket_blocks = int(nbk.max().item()) if nbk.numel() else 0
+        self.max_bucket_tiles = int(ntk.max().item()) if ntk.numel() else 0
         self.c = _lib.PdxStore(self.d, self.d_pad, self.group, self.nbuckets, self.ntiles,
                                self.nblocks, _lib.ptr(tiles), _lib.ptr(tile_ids),
                                _lib.ptr(block_tile), _lib.ptr(block_m), _lib.ptr(bucket_block),
-                               self.max_bucket_blocks, 0)
+                               self.max_bucket_blocks, self.max_bucket_tiles,
+                               _lib.ptr(self.tile_block))
 
     @property
     def ref(self):
@@ -98,10 +111,8 @@ class DeviceStore:
         """Same tiles, another grouping of logical blocks into buckets."""
         torch = _torch()
         bb = to_device(bucket_block, torch.int64)
-        counts = (bb[1:] - bb[:-1])
-        mx = int(counts.max().item()) if counts.numel() else 0
         return DeviceStore(self.tiles, self.tile_ids, self.block_tile, self.block_m, bb,
-                           self.d, self.group, mx)
+                           self.d, self.group, self.tile_block)
 
     def per_block_buckets(self) -> "DeviceStore":
         torch = _torch()
@@ -152,9 +163,7 @@ class DeviceStore:
         bucket_block = torch.zeros(bucket_nblocks.numel() + 1, dtype=torch.int64, device=dev)
         if bucket_nblocks.numel():
             bucket_block[1:] = torch.cumsum(bucket_nblocks, 0)
-        mx = int(bucket_nblocks.max().item()) if bucket_nblocks.numel() else 0
-        return cls(tiles, tile_ids, block_tile[:-1].contiguous(), block_m.to(torch.int32),
-                   bucket_block, d, group, mx)
+        return cls(tiles, tile_ids, block_tile, block_m.to(torch.int32), bucket_block, d, group)
 
     @classmethod
     def from_blocks(cls, blocks, group=8, one_bucket_per_block=True) -> "DeviceStore":
