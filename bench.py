@@ -219,7 +219,7 @@ def main():
         res = searcher.run(Qr, scan_events=ev)
         if ws > 1:
             from paper_2503_04422_b200.sharded import gather_merge
-            return gather_merge(res, K)
+            return gather_merge(res.dist, res.ids, K)
         return res.dist, res.ids
 
     # exactness of the kernel's stats pass and the algorithmic byte count

@@ -182,10 +182,10 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   int W = prm->warps > 0 ? prm->warps : 8;  // compute warps per query CTA
   if (W > 8) W = 8;
   int tpw = 1;  // tiles per claim: a power of two <= kMaxTpw
-  while (tpw * 2 <= (prm->tiles_per_warp > 0 ? prm->tiles_per_warp : 2) && tpw * 2 <= kMaxTpw)
+  while (tpw * 2 <= (prm->tiles_per_warp > 0 ? prm->tiles_per_warp : 4) && tpw * 2 <= kMaxTpw)
     tpw *= 2;
   int rb = 2 * tpw;  // ring slots: a power of two (masks, not divisions, in the kernel)
-  while (rb < (prm->ring_slots > 0 ? prm->ring_slots : 2 * W * tpw)) rb *= 2;
+  while (rb < (prm->ring_slots > 0 ? prm->ring_slots : W * tpw)) rb *= 2;
   ScanSmem L = scan_smem_layout(W, tpw, rb, prm->k, nsteps, store->d_pad);
   while (rb > 2 * tpw && L.total > optin) {
     rb /= 2;

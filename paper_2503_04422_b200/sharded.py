@@ -32,6 +32,12 @@ def plan_shards(bucket_sizes, world: int) -> np.ndarray:
     return owner
 
 
+def owned_rows(assign, owner, rank: int) -> np.ndarray:
+    """Rows (ascending) whose bucket this rank owns."""
+    assign = np.asarray(assign)
+    return np.flatnonzero(np.asarray(owner)[assign] == rank)
+
+
 def shard_index(index, collection, rank: int, world: int, x_dev=None):
     """This rank's IvfIndex: same nlist and centroids, only owned buckets
     populated (members keep their original ids and ascending order)."""
@@ -42,12 +48,10 @@ def shard_index(index, collection, rank: int, world: int, x_dev=None):
     counts = np.asarray(index._counts)
     owner = plan_shards(counts, world)
     off = np.concatenate([[0], np.cumsum(counts)])
-    mine = np.flatnonzero(owner == rank)
-    rows = np.sort(np.concatenate([index._order[off[c]:off[c + 1]] for c in mine])) \
-        if mine.size else np.empty(0, np.int64)
     assign = np.empty(collection.n, dtype=np.int64)
     for c in range(index.nlist):
         assign[index._order[off[c]:off[c + 1]]] = c
+    rows = owned_rows(assign, owner, rank)
     sub = VectorCollection(data=collection.data[rows], ids=collection.ids[rows])
     xd = None
     if x_dev is not None:
@@ -70,15 +74,14 @@ def merge_device(dist_all, ids_all, k: int):
     return od, oi
 
 
-def gather_merge(res, k: int, group=None, merge=merge_device):
-    """All-gather every rank's (dist, ids) top-k over the process group and
-    merge; returns the global (dist, ids) on every rank."""
+def gather_merge(dist, ids, k: int, group=None, merge=merge_device):
+    """All-gather every rank's (dist [nq,k], ids [nq,k]) over the process
+    group (NCCL on GPUs) and merge; the global (dist, ids) on every rank."""
     import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    nq = res.dist.shape[0]
-    dall = torch.empty((world, nq, k), dtype=res.dist.dtype, device=res.dist.device)
-    iall = torch.empty((world, nq, k), dtype=res.ids.dtype, device=res.ids.device)
-    dist.all_gather_into_tensor(dall, res.dist.contiguous(), group=group)
-    dist.all_gather_into_tensor(iall, res.ids.contiguous(), group=group)
-    return merge(dall, iall, k)
+    import torch.distributed as dist_
+    world = dist_.get_world_size(group)
+    dl = [torch.empty_like(dist) for _ in range(world)]
+    il = [torch.empty_like(ids) for _ in range(world)]
+    dist_.all_gather(dl, dist.contiguous(), group=group)
+    dist_.all_gather(il, ids.contiguous(), group=group)
+    return merge(torch.stack(dl), torch.stack(il), k)

@@ -289,3 +289,26 @@ def test_ground_truth_and_estimators(P):
     # padding when k exceeds the probed vectors
     d2, i2 = P.ExactNearestNeighbors(partition_size=64).fit(x[:5]).kneighbors(Q[:2], 8)
     assert np.all(i2[:, 5:] == -1) and np.all(np.isinf(d2[:, 5:]))
+
+
+def test_sharded_index_merge_exact(P):
+    """Two bucket shards scanned separately on one GPU and merged by K7 equal
+    the unsharded search for BOND (exact); ADS keeps its recall."""
+    import torch
+    from paper_2503_04422_b200.sharded import merge_device, shard_index
+    x = recipes.data("mixture", 40_000, 32, 91)
+    Q = recipes.queries("near", x, 24, 92)
+    col = P.VectorCollection.from_array(x)
+    index = P.ivf_build(col, nlist=64, seed=1)
+    for pruner in ("bond", "none"):
+        params = P.SearchParams(k=10, pruner=pruner)
+        full = P.ivf_search_batch(index, Q, params, 16)
+        dl, il = [], []
+        for rank in range(2):
+            sh = shard_index(index, col, rank, 2)
+            r = P.ivf_search_batch(sh, Q, params, 16)
+            dl.append(torch.from_numpy(r["dist"]))
+            il.append(torch.from_numpy(r["ids"]))
+        d, i = merge_device(torch.stack(dl).cuda(), torch.stack(il).cuda(), 10)
+        np.testing.assert_array_equal(i.cpu().numpy(), full["ids"])
+        np.testing.assert_array_equal(d.cpu().numpy(), full["dist"])
