@@ -51,25 +51,35 @@ def make_data(n, nq, seed=0):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock and clock-event reasons sampled through NVML every 10 ms
+    during the timed region (the same counters nvidia-smi reports)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, gpu=0):
         self.samples, self.gpu, self._stop = [], gpu, threading.Event()
         self.max_mhz = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        except Exception:
+            return
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                self.samples.append([s.strip() for s in out.split(",")])
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, [n for n, a in self.REASONS.items()
+                                          if rs & getattr(N, a)]))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01)
 
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
@@ -82,15 +92,20 @@ class Clocks:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({r for s in self.samples for r in s[1]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the scan kernel from the committed ncu
+    capture summary (profiles/ncu_scan.json, written by tools/ncu_summary.py)."""
+    try:
+        return json.loads((ROOT / "profiles" / "ncu_scan.json").read_text())
+    except Exception:
+        return None
 
 
 def dist_env():
@@ -120,12 +135,14 @@ def cpu_oracle_qps(index, Qr, nprobe, budget_s=12.0, max_q=None, threads=None):
     O.build()
     view = O.IvfView(index.centroid_blocks, index.buckets, index.means_dev.cpu().numpy())
     threads = threads or os.cpu_count() or 1
-    done, t_total, chunk = 0, 0.0, max(threads, 16)
+    done, t_total, chunk = 0, 0.0, max(4 * threads, 64)
     limit = Qr.shape[0] if max_q is None else min(max_q, Qr.shape[0])
     # untimed warm query (cli.py:171-172)
     O.ivf_search_batch(view, Qr[:1], K, nprobe, pruner="ads", eps0=EPS, nthreads=1)
-    while done < limit and t_total < budget_s:
-        q = Qr[done:min(limit, done + chunk)]
+    # passes over the query set (wrapping around) until the time budget is spent
+    while t_total < budget_s:
+        s = done % limit
+        q = Qr[s:min(limit, s + chunk)]
         t0 = time.perf_counter()
         O.ivf_search_batch(view, q, K, nprobe, pruner="ads", eps0=EPS, nthreads=threads)
         t_total += time.perf_counter() - t0
@@ -136,7 +153,7 @@ def cpu_oracle_qps(index, Qr, nprobe, budget_s=12.0, max_q=None, threads=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT)
@@ -298,6 +315,10 @@ def main():
     except Exception:
         peak_src = "fallback"
     achieved = alg_bytes / (t_scan / 1e3) / 1e9
+    prof = ncu_traffic()
+    traffic = None
+    if prof and prof.get("workload") == config["workload"]:
+        traffic = prof.get("dram_bytes_per_launch")
     line = {
         "metric": "queries/sec at recall@10", "value": qps, "unit": "queries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
@@ -305,8 +326,10 @@ def main():
         "data": "synthetic (seeded Gaussian mixture, BASELINE configs[1] recipe)",
         "config": config, "recall_at_10": recall,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_source": peak_src, "traffic": None,
+                     "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic,
+                     "traffic_source": (prof or {}).get("source"),
                      "kernel": "pdx_scan_kernel<8,false,L2>",
+                     "time_share_ncu": (prof or {}).get("scan_time_share"),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "full_scan_bytes_per_launch": 4 * total,
                      "pruning_power": 1 - touched / total, "scan_ms": t_scan},
@@ -341,8 +364,10 @@ def main():
         cq, done, secs, threads, _ = cpu_oracle_qps(index, Qr_dev.cpu().numpy(), args.nprobe,
                                                     budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": cq, "unit": "queries/s", "cores": threads, "kind": "port",
-                                "sample": f"{done} queries ({secs:.1f} s wall) of the same "
-                                          "workload, C oracle, one query per host thread"}
+                                "sample": f"{done} query searches ({secs:.1f} s wall; passes over "
+                                          f"the {args.nq} queries) of the same workload and "
+                                          "index, C oracle of the reference, one query per "
+                                          "host thread"}
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.barrier()
