@@ -112,6 +112,10 @@ static cudaError_t launch_scan(const ScanArgs& A, const ScanSmem& L, int nq, int
   auto fn = pdx_scan_kernel<G, ORD, METRIC>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (e != cudaSuccess) return e;
+  // several query CTAs per SM need the full shared-memory carveout
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   fn<<<nq, (W + 1) * 32, L.total, st>>>(A, L, tpw);
   return cudaGetLastError();
 }

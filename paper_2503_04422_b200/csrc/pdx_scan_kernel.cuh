@@ -17,6 +17,10 @@
 #include "pdx_common.cuh"
 #include "pdx_scan_spec.cuh"
 
+#ifndef PDX_SCAN_MIN_BLOCKS
+#define PDX_SCAN_MIN_BLOCKS 3  // 3 query CTAs of 9 warps per SM: <= 75 registers
+#endif
+
 namespace pdx {
 
 struct Control {
@@ -113,6 +117,21 @@ template <typename T>
 __device__ __forceinline__ void vstore(T& x, T v) {
   *reinterpret_cast<volatile T*>(&x) = v;
 }
+// acquire / release on a shared-memory word (CTA scope): the data written
+// before a release is visible to the warp whose acquire observes the value
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];"
+               : "=r"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
+}
 
 // ------------------------------------------------------------------ top-k
 __device__ __forceinline__ float topk_threshold(const Control& c, int k, const float* tkd) {
@@ -166,7 +185,7 @@ __device__ __forceinline__ void topk_push_lanes(Control& c, int k, float* tkd, i
 
 // ------------------------------------------------------------------ kernel
 template <int G, bool ORD, int METRIC>
-__global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const ScanSmem L,
+__global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(const ScanArgs A, const ScanSmem L,
                                                        const int tpw) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int q = blockIdx.x;
@@ -261,11 +280,13 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
       nnext = claim(enext);
       const int nt = min(tpw, ntiles - n0);
       // ring slots n0.. are free once tile n0+nt-1-RB is committed
-      while (vload(ctl.com_pub) < n0 + nt - RB) {
-        if (A.debug && lane == 0) atomicAdd(&ctl.ring_waits, 1);
-        __nanosleep(64);
+      // (back off: spinning warps would steal issue slots from working ones)
+      int spins = 0;
+      while (ld_acquire(&ctl.com_pub) < n0 + nt - RB) {
+        __nanosleep(spins < 2 ? 200 : 800);
+        ++spins;
       }
-      __threadfence_block();
+      if (A.debug && spins && lane == 0) atomicAdd(&ctl.ring_waits, spins);
       const int sl = n0 & RMASK;  // RB is a multiple of tpw: the slice is contiguous
       if (lane < nt) {
         TileDesc t;
@@ -279,8 +300,7 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
           t.tspec = INFINITY;
         } else {
           const int first = n0 + lane - e.tib;  // the block's first tile
-          const int com = vload(ctl.com_pub);
-          __threadfence_block();
+          const int com = ld_acquire(&ctl.com_pub);
           t.tspec = com > first ? vload(ctl.tblk_pub) : vload(ctl.t_pub);
         }
         s_desc[sl + lane] = t;
@@ -310,14 +330,21 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
                                : 0;
       }
       __syncwarp();
-      __threadfence_block();
-      if (lane < nt) vstore(s_flag[sl + lane], 2);
+      if (lane < nt) st_release(&s_flag[sl + lane], 2);
     }
   } else {
     // ======================================================== commit warp
+    // The commit warp's state lives in registers (the same value in every
+    // lane; the running stats in lane 0): each commit run is on the query's
+    // critical path, so it avoids shared-memory round trips it can skip.
     int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
     const long long t_start = clock64();
     int64_t dbg_fast = 0, dbg_serial = 0, dbg_replay = 0, dbg_idle = 0;
+    float T = INFINITY;      // current threshold, TopK.threshold()
+    float tblk = INFINITY;   // T_b of the open block
+    bool linear = true;      // the open block is linear
+    int warm_min = 0, warm_m = -1;
+    int64_t r_touched = 0, r_total = 0, r_tlen = 0;  // lane 0
 
     // commit one tile (serial path)
     auto commit_one = [&](int sl) {
@@ -325,31 +352,27 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
       const TileSum& sm = s_sum[sl];
       const float* part = s_part + (size_t)sl * nsteps * kTile;
       if (t.flags & 2) {  // first tile of its block: T_b is fixed now
-        const float T = topk_threshold(ctl, k, tkd);
-        const int lin = (t.vis == 0 || A.pruner == PDX_PRUNER_NONE || T == INFINITY);
+        linear = (t.vis == 0 || A.pruner == PDX_PRUNER_NONE || T == INFINITY);
+        tblk = T;
         if (lane < nsteps) {
           s_cnt[lane] = 0;
-          if (!lin)
+          if (!linear)
             s_bnd[lane] = ads_or_bond_bound(A.pruner, T, s_ends[lane], A.ads_d, s_ratio[lane],
                                             s_band[lane]);
         }
-        if (lane == 0) {
-          ctl.tblk = T;
-          vstore(ctl.tblk_pub, T);
-          ctl.linear = lin;
-          if (!lin && t.block_m != ctl.warm_m) {
-            ctl.warm_min = t.block_m <= kTile ? s_wmin[t.block_m] : warm_min_count(t.block_m, A.sf);
-            ctl.warm_m = t.block_m;
-          }
+        if (lane == 0) vstore(ctl.tblk_pub, T);
+        if (!linear && t.block_m != warm_m) {
+          warm_min = t.block_m <= kTile ? s_wmin[t.block_m] : warm_min_count(t.block_m, A.sf);
+          warm_m = t.block_m;
         }
         __syncwarp();
       }
       const int s0 = lane, s1 = lane + 32;  // bit `lane` of alive0 / alive1
       bool c0, c1;
-      if (ctl.linear) {
+      if (linear) {
         c0 = s0 < t.m_tile;
         c1 = s1 < t.m_tile;
-      } else if (t.tspec == ctl.tblk) {
+      } else if (t.tspec == tblk) {
         // the speculation ran with the exact threshold: its counts and
         // survivors are the reference's
         if (lane < nsteps) s_cnt[lane] += sm.cnt[lane];
@@ -375,40 +398,41 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
         if (lane < nsteps) s_cnt[lane] += mycnt;
       }
       if (__any_sync(kFull, c0 || c1)) {
-        const float2 fin = make_float2(part[(nsteps - 1) * kTile + s0],
-                                       part[(nsteps - 1) * kTile + s1]);
+        const float f0 = part[(nsteps - 1) * kTile + s0], f1 = part[(nsteps - 1) * kTile + s1];
         // ids of the (rare) pushed slots come straight from HBM / L2
         const int64_t* gid = A.tile_ids + t.tile * kTile;
-        const float key0 = METRIC == PDX_METRIC_IP ? -fin.x : fin.x;
-        const float key1 = METRIC == PDX_METRIC_IP ? -fin.y : fin.y;
+        const float key0 = METRIC == PDX_METRIC_IP ? -f0 : f0;
+        const float key1 = METRIC == PDX_METRIC_IP ? -f1 : f1;
         const int64_t id0 = c0 ? __ldg(gid + s0) : 0, id1 = c1 ? __ldg(gid + s1) : 0;
         topk_push_lanes(ctl, k, tkd, tki, c0, key0, id0, lane);
         topk_push_lanes(ctl, k, tkd, tki, c1, key1, id1, lane);
+        __syncwarp();
+        T = topk_threshold(ctl, k, tkd);
       }
       __syncwarp();
       if ((t.flags & 4) && lane == 0) {  // last tile: the block's stats (search.py:132, :169)
         const int64_t m = t.block_m;
-        ctl.total += m * A.d;
-        if (ctl.linear) {
-          ctl.touched += m * A.d;
+        r_total += m * A.d;
+        if (linear) {
+          r_touched += m * A.d;
           if (tr) {
-            if (ctl.tlen >= 0 && ctl.tlen + 2 <= A.trace_cap) {
-              tr[ctl.tlen] = 1;
-              tr[ctl.tlen + 1] = (int32_t)m;
-              ctl.tlen += 2;
+            if (r_tlen >= 0 && r_tlen + 2 <= A.trace_cap) {
+              tr[r_tlen] = 1;
+              tr[r_tlen + 1] = (int32_t)m;
+              r_tlen += 2;
             } else {
-              ctl.tlen = -1;
+              r_tlen = -1;
             }
           }
         } else {
-          ctl.touched += block_touched(m, ctl.warm_min, s_cnt, s_ends, nsteps);
+          r_touched += block_touched(m, warm_min, s_cnt, s_ends, nsteps);
           if (tr) {
-            if (ctl.tlen >= 0 && ctl.tlen + 1 + nsteps <= A.trace_cap) {
-              tr[ctl.tlen] = nsteps;
-              for (int s = 0; s < nsteps; ++s) tr[ctl.tlen + 1 + s] = s_cnt[s];
-              ctl.tlen += 1 + nsteps;
+            if (r_tlen >= 0 && r_tlen + 1 + nsteps <= A.trace_cap) {
+              tr[r_tlen] = nsteps;
+              for (int s = 0; s < nsteps; ++s) tr[r_tlen + 1 + s] = s_cnt[s];
+              r_tlen += 1 + nsteps;
             } else {
-              ctl.tlen = -1;
+              r_tlen = -1;
             }
           }
         }
@@ -423,17 +447,17 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
     // put), so it is committed in parallel, one tile per lane, with the
     // values_touched the compute warp pre-computed.
     auto commit_run = [&](int com, int nr) -> int {
-      const float T = topk_threshold(ctl, k, tkd);
       bool simple = false;
+      int touched = 0, m = 0;
       const TileSum* sm = nullptr;
-      int64_t m = 0;
       if (lane < nr) {
         const int sl = (com + lane) & RMASK;
         const TileDesc& t = s_desc[sl];
         sm = &s_sum[sl];
         m = t.block_m;
+        touched = (int)sm->touched_spec;
         simple = t.flags == 6 && t.vis != 0 && A.pruner != PDX_PRUNER_NONE && T != INFINITY &&
-                 t.tspec == T && m <= kTile && sm->alive0 == 0 && sm->alive1 == 0;
+                 t.tspec == T && m <= kTile && (sm->alive0 | sm->alive1) == 0;
       }
       const unsigned stop = __ballot_sync(kFull, !simple);
       const int np = min(nr, stop ? __ffs(stop) - 1 : 32);
@@ -443,23 +467,23 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
         return 1;
       }
       // per tile: touched <= 64 * d and total = m * d, so 32 of each fit int32
-      const int touched = __reduce_add_sync(kFull, lane < np ? (int)sm->touched_spec : 0);
-      const int total = __reduce_add_sync(kFull, lane < np ? (int)m : 0) * A.d;
+      const int tsum = __reduce_add_sync(kFull, lane < np ? touched : 0);
+      const int msum = __reduce_add_sync(kFull, lane < np ? m : 0);
       if (tr) {
-        const bool fits = ctl.tlen >= 0 && ctl.tlen + (int64_t)np * (1 + nsteps) <= A.trace_cap;
-        if (lane < np && fits) {
-          int32_t* rec = tr + ctl.tlen + (int64_t)lane * (1 + nsteps);
+        const bool fits = r_tlen >= 0 && r_tlen + (int64_t)np * (1 + nsteps) <= A.trace_cap;
+        const int64_t base = __shfl_sync(kFull, r_tlen, 0);
+        const int fits0 = __shfl_sync(kFull, (int)fits, 0);  // lane 0 holds the stats
+        if (lane < np && fits0) {
+          int32_t* rec = tr + base + (int64_t)lane * (1 + nsteps);
           rec[0] = nsteps;
           for (int s = 0; s < nsteps; ++s) rec[1 + s] = sm->cnt[s];
         }
-        __syncwarp();
-        if (lane == 0) ctl.tlen = fits ? ctl.tlen + (int64_t)np * (1 + nsteps) : -1;
+        if (lane == 0) r_tlen = fits ? r_tlen + (int64_t)np * (1 + nsteps) : -1;
       }
       if (lane == 0) {
-        ctl.touched += touched;
-        ctl.total += total;
+        r_touched += tsum;
+        r_total += (int64_t)msum * A.d;
       }
-      __syncwarp();
       dbg_fast += np;
       return np;
     };
@@ -467,30 +491,33 @@ __global__ void __launch_bounds__(288) pdx_scan_kernel(const ScanArgs A, const S
     int com = 0, polls = 0;
     while (com < ntiles) {
       // never look past one ring turn: lane >= RB would alias an earlier slot
-      const bool rdy = lane < RB && com + lane < ntiles && vload(s_flag[(com + lane) & RMASK]) == 2;
+      const bool rdy =
+          lane < RB && com + lane < ntiles && ld_acquire(&s_flag[(com + lane) & RMASK]) == 2;
       const unsigned rm = __ballot_sync(kFull, rdy);
       const int nr = (~rm) ? __ffs(~rm) - 1 : 32;
       // batch: a run of tiles costs the commit warp about as much as one
-      const int want = min(min(RB, 32) / 4, ntiles - com);
-      if (nr == 0 || (nr < want && polls < 2)) {
+      const int want = min(min(RB, 32) / 2, ntiles - com);
+      if (nr == 0 || (nr < want && polls < 3)) {
         ++dbg_idle;
         ++polls;
-        __nanosleep(32);
+        __nanosleep(48);
         continue;
       }
       polls = 0;
-      __threadfence_block();
       int done = 0;
       while (done < nr) done += commit_run(com + done, nr - done);
       if (lane < done) s_flag[(com + lane) & RMASK] = 0;
       com += done;
       __syncwarp();
       if (lane == 0) {
-        vstore(ctl.t_pub, topk_threshold(ctl, k, tkd));
-        __threadfence_block();
-        vstore(ctl.com_pub, com);
+        vstore(ctl.t_pub, T);
+        st_release(&ctl.com_pub, com);
       }
-      __syncwarp();
+    }
+    if (lane == 0) {
+      ctl.touched = r_touched;
+      ctl.total = r_total;
+      ctl.tlen = r_tlen;
     }
     if (A.debug && lane == 0) {
       int64_t* dg = A.debug + (int64_t)q * 8;
