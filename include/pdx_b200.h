@@ -44,10 +44,13 @@ extern "C" {
 #define PDX_METRIC_L1 1
 #define PDX_METRIC_IP 2
 
-/* SearchParams.pruner (search.py:65, :78-79) */
+/* SearchParams.pruner (search.py:65, :78-79).  BSA is not in the reference
+ * (SPEC.md:14); it is this build's restatement: prune at step s iff
+ * partial >= fl32(T * beta[s]) with learned beta. */
 #define PDX_PRUNER_NONE 0
 #define PDX_PRUNER_ADS 1
 #define PDX_PRUNER_BOND 2
+#define PDX_PRUNER_BSA 3
 
 /* OrderCriteria (pruning.py:91-95) */
 #define PDX_ORDER_SEQUENTIAL 0
@@ -104,6 +107,7 @@ typedef struct pdx_search_params {
   double ads_epsilon0;
   int32_t tiles_per_warp; /* 64-vector tiles a compute warp claims at once (0 = auto) */
   int32_t ring_slots;     /* tiles in flight per query CTA (0 = auto) */
+  const double* bsa_beta; /* DEVICE array, one factor per schedule step (BSA only) */
 } pdx_search_params;
 
 /* Outputs of pdx_search.  Per query q (row q of each array):

@@ -32,6 +32,7 @@
 #define ORC_PRUNER_NONE 0
 #define ORC_PRUNER_ADS 1
 #define ORC_PRUNER_BOND 2
+#define ORC_PRUNER_BSA 3 /* this build's restatement, not in the reference */
 
 #define ORC_SEQUENTIAL 0
 #define ORC_DECREASING 1
@@ -66,6 +67,7 @@ typedef struct {
   int32_t ads_d;
   int32_t _pad;
   double ads_eps0;
+  const double* bsa_beta; /* BSA: one learned factor per schedule step */
 } orc_params;
 
 /* SearchStats (search.py:88-103).  survivors, when non-NULL, receives one
@@ -263,6 +265,8 @@ static void search_block(const orc_blocks* B, int64_t bi, const float* q, const 
       float bound;
       if (p->pruner == ORC_PRUNER_ADS)
         bound = (float)orc_ads_bound(b, p->ads_d, p->ads_eps0, (double)threshold);
+      else if (p->pruner == ORC_PRUNER_BSA) /* partial >= T * beta_s prunes */
+        bound = (float)((double)threshold * p->bsa_beta[s]);
       else
         bound = threshold;
       int32_t w = 0;

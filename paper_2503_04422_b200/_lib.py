@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 
 PDX_OK, PDX_EINVAL, PDX_ECUDA, PDX_ENOSUPPORT = 0, 1, 2, 3
 METRIC = {"l2": 0, "l1": 1, "ip": 2}
-PRUNER = {"none": 0, "ads": 1, "bond": 2}
+PRUNER = {"none": 0, "ads": 1, "bond": 2, "bsa": 3}
 CRITERIA = {"sequential": 0, "decreasing": 1, "dmeans": 2, "zones": 3}
 TILE = 64
 
@@ -40,7 +40,8 @@ class PdxSearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("metric", C.c_int32), ("pruner", C.c_int32),
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
                 ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
-                ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32)]
+                ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32),
+                ("bsa_beta", C.c_void_p)]
 
 
 class PdxSearchOut(C.Structure):

@@ -106,6 +106,29 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
   if (threadIdx.x == 0) counts[q] = (int32_t)(run_t < maxtiles ? run_t : maxtiles);
 }
 
+// Per-step bound factors for ads_or_bond_bound, [0][s] = ratio, [1][s] = band:
+// ADS ratio = d'/D and band = 1 + eps0/sqrt(d') in float64 (pruning.py:80-88),
+// BSA ratio = beta[s] (device array) and band = 1, and ratio = band = 1
+// wherever the reference compares against T itself (BOND, none, d' >= D).
+__global__ void bound_factors_kernel(int pruner, int d, int initial_step, int nsteps, int ads_d,
+                                     double eps0, const double* __restrict__ beta,
+                                     double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  int64_t e = 0, width = initial_step;  // step_schedule (search.py:106-117)
+  for (int s = 0; s < nsteps; ++s, width *= 2) {
+    e = e + width < d ? e + width : d;
+    double ratio = 1.0, band = 1.0;
+    if (pruner == PDX_PRUNER_BSA) {
+      ratio = beta[s];
+    } else if (pruner == PDX_PRUNER_ADS && e < ads_d) {
+      ratio = __ddiv_rn((double)e, (double)ads_d);
+      band = __dadd_rn(1.0, __ddiv_rn(eps0, __dsqrt_rn((double)e)));
+    }
+    out[s] = ratio;
+    out[kMaxSteps + s] = band;
+  }
+}
+
 template <int G, bool ORD, int METRIC>
 static cudaError_t launch_scan(const ScanArgs& A, const ScanSmem& L, int nq, int W, int tpw,
                                cudaStream_t st) {
@@ -148,7 +171,7 @@ static int schedule_steps(int d, int initial_step) {
 extern "C" int64_t pdx_search_workspace(const pdx_store* store, int64_t nq, int32_t nseg) {
   if (!store || nq < 0 || nseg < 0) return -1;
   const int64_t maxvis = (int64_t)nseg * store->max_bucket_tiles;
-  return 256 + nq * (int64_t)sizeof(int32_t) + 256 + nq * maxvis * (int64_t)sizeof(TileEntry) + 256;
+  return 512 + nq * (int64_t)sizeof(int32_t) + 256 + nq * maxvis * (int64_t)sizeof(TileEntry) + 256;
 }
 
 extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
@@ -163,11 +186,14 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
               "selection_fraction must be in (0, 1]");
   PDX_REQUIRE(prm->initial_step >= 1, "initial_step must be >= 1");
   PDX_REQUIRE(prm->metric >= 0 && prm->metric <= 2, "unknown metric %d", prm->metric);
-  PDX_REQUIRE(prm->pruner >= 0 && prm->pruner <= 2, "unknown pruner %d", prm->pruner);
+  PDX_REQUIRE(prm->pruner >= 0 && prm->pruner <= 3, "unknown pruner %d", prm->pruner);
   PDX_REQUIRE(!(prm->metric == PDX_METRIC_IP && prm->pruner != PDX_PRUNER_NONE),
               "inner product has no monotone lower bound; use pruner='none' for IP searches");
   PDX_REQUIRE(!(prm->pruner == PDX_PRUNER_ADS && prm->metric != PDX_METRIC_L2),
               "the ads pruner applies to squared L2 only");
+  PDX_REQUIRE(!(prm->pruner == PDX_PRUNER_BSA && prm->metric != PDX_METRIC_L2),
+              "the bsa pruner applies to squared L2 only");
+  PDX_REQUIRE(prm->pruner != PDX_PRUNER_BSA || prm->bsa_beta, "bsa needs its beta factors");
   PDX_REQUIRE(prm->pruner != PDX_PRUNER_ADS || prm->ads_epsilon0 > 0.0, "epsilon0 must be positive");
   PDX_REQUIRE(prm->pruner != PDX_PRUNER_ADS || prm->ads_d >= 1, "ads d must be >= 1");
   PDX_REQUIRE(store->d >= 1 && store->d <= 65535, "dimensionality %d unsupported", store->d);
@@ -205,11 +231,15 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
               (long long)work_bytes, (long long)need);
   unsigned char* w = reinterpret_cast<unsigned char*>(d_work);
   int32_t* d_overflow = reinterpret_cast<int32_t*>(w);
-  int32_t* d_counts = reinterpret_cast<int32_t*>(w + 256);
+  double* d_factors = reinterpret_cast<double*>(w + 64);  // [2][kMaxSteps], header < 512 B
+  int32_t* d_counts = reinterpret_cast<int32_t*>(w + 512);
   TileEntry* d_vis = reinterpret_cast<TileEntry*>(
-      w + 256 + ((nlists * sizeof(int32_t) + 255) / 256) * 256);
+      w + 512 + ((nlists * sizeof(int32_t) + 255) / 256) * 256);
   cudaStream_t st = as_stream(stream);
   PDX_CUDA_CHECK(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), st));
+  bound_factors_kernel<<<1, 32, 0, st>>>(prm->pruner, store->d, prm->initial_step, nsteps,
+                                         prm->ads_d >= 1 ? prm->ads_d : store->d,
+                                         prm->ads_epsilon0, prm->bsa_beta, d_factors);
   if (nseg > 0 && maxvis > 0) {
     build_visits_kernel<<<(unsigned)nlists, 256, 0, st>>>(
         d_seg_bucket, nseg, store->d_bucket_block, store->d_block_tile, store->d_block_m,
@@ -240,7 +270,8 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   A.initial_step = prm->initial_step;
   A.nsteps = nsteps;
   A.sf = prm->selection_fraction;
-  A.ads_d = prm->ads_d >= 1 ? prm->ads_d : store->d;
+  A.ads_d = (prm->ads_d >= 1 && prm->pruner != PDX_PRUNER_BSA) ? prm->ads_d : store->d;
+  A.factors = d_factors;
   A.eps0 = prm->ads_epsilon0;
   A.out_dist = out->d_dist;
   A.out_ids = out->d_ids;

@@ -242,10 +242,9 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     ctl.items = 0;
   }
   __syncthreads();
-  if (threadIdx.x < nsteps) {
-    const double ds = (double)s_ends[threadIdx.x];
-    s_ratio[threadIdx.x] = __ddiv_rn(ds, (double)A.ads_d);
-    s_band[threadIdx.x] = __dadd_rn(1.0, __ddiv_rn(A.eps0, __dsqrt_rn(ds)));
+  if (threadIdx.x < nsteps) {  // bound factors (bound_factors_kernel, pdx_scan.cu)
+    s_ratio[threadIdx.x] = A.factors[threadIdx.x];
+    s_band[threadIdx.x] = A.factors[kMaxSteps + threadIdx.x];
   }
   __syncthreads();
   const TileEntry* vis = A.vis + (int64_t)q * A.vis_qstride;
@@ -357,8 +356,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
         if (lane < nsteps) {
           s_cnt[lane] = 0;
           if (!linear)
-            s_bnd[lane] = ads_or_bond_bound(A.pruner, T, s_ends[lane], A.ads_d, s_ratio[lane],
-                                            s_band[lane]);
+            s_bnd[lane] = ads_or_bond_bound(T, s_ratio[lane], s_band[lane]);
         }
         if (lane == 0) vstore(ctl.tblk_pub, T);
         if (!linear && t.block_m != warm_m) {

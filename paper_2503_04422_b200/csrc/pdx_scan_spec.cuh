@@ -91,6 +91,7 @@ struct ScanArgs {
   int64_t* trace_len;
   int64_t* debug;  // optional [nq][8] counters (see pdx_search_out)
   int32_t sparse_max;  // a tile goes sparse once at most this many slots survive
+  const double* factors;  // [2][kMaxSteps]: per-step bound ratio, band
 };
 
 // Shared-memory views of one round slice (the tiles of one compute warp).
@@ -111,12 +112,16 @@ struct QueryRefs {
   const uint8_t* bmask;  // [d_pad/8] bit e of group g: a step ends after dim 8g+e
 };
 
-__device__ __forceinline__ float ads_or_bond_bound(int pruner, float T, int dims_seen, int ads_d,
-                                                   double ratio, double band) {
-  if (pruner != PDX_PRUNER_ADS || dims_seen >= ads_d) return T;  // bond: acc < T
-  // pruning.py:88: threshold * (dims_seen / d) * band * band, in float64,
-  // left to right; the comparison then happens in float32 (numpy casts the
-  // Python float to the array's float32).
+// A slot survives step s iff acc < bound(T).  pruning.py:88: threshold *
+// (dims_seen / d) * band * band, in float64, left to right; the comparison
+// then happens in float32 (numpy casts the Python float to the array's
+// float32).  The host sets ratio = band = 1 wherever the reference compares
+// against T itself (BOND, none, ADS once dims_seen >= d): T * 1 * 1 * 1
+// rounds back to T exactly, so one branch-free formula serves every pruner.
+__device__ __forceinline__ float ads_or_bond_bound(float T, double ratio, double band) {
+  // bound_factors_kernel never pairs ratio 1 with band != 1: same value as the
+  // formula, fewer live registers
+  if (ratio == 1.0) return T;
   const double t = __dmul_rn(__dmul_rn(__dmul_rn((double)T, ratio), band), band);
   return __double2float_rn(t);
 }
@@ -131,7 +136,7 @@ __device__ __forceinline__ float tile_bounds(const ScanArgs& A, const TileDesc& 
                                              int lane) {
   float b = INFINITY;
   if (t.tspec != INFINITY && lane < A.nsteps)
-    b = ads_or_bond_bound(A.pruner, t.tspec, Q.ends[lane], A.ads_d, Q.ratio[lane], Q.band[lane]);
+    b = ads_or_bond_bound(t.tspec, Q.ratio[lane], Q.band[lane]);
   if (lane < A.nsteps) R.bnd[tj * kMaxSteps + lane] = b;
   return b;
 }

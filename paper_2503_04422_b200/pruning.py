@@ -98,6 +98,118 @@ def ads_bound(dims_seen: int, pruner: AdsPruner, threshold_l2: float) -> float:
     return threshold_l2 * (dims_seen / pruner.d) * band * band
 
 
+# ------------------------------------------------------------------ BSA
+# The reference names BSA but does not implement it
+# (SPEC.md:14).  This build's restatement: project onto the
+# principal components (largest variance first), then after each schedule
+# step s prune a candidate iff  partial_s >= T * beta_s,  where beta_s is
+# `multiplier` x the `quantile` of partial_s / full over (training query,
+# true k-NN) pairs, capped at 1 and exactly 1 at full dimensionality.  The
+# bound is monotone in T, so the scan's speculate-and-commit exactness holds.
+
+@dataclass(frozen=True)
+class BsaPruner:
+    """Learned per-step bound factors for PCA-projected data (L2 only)."""
+
+    beta: tuple  # one factor per step of step_schedule(d, initial_step)
+    d: int
+    initial_step: int = 2
+    quantile: float = 0.99
+    multiplier: float = 1.0
+
+    def __post_init__(self):
+        from .search import step_schedule
+        n = len(step_schedule(self.d, self.initial_step))
+        if len(self.beta) != n:
+            raise ValueError(f"bsa needs {n} factors for d={self.d}, initial_step="
+                             f"{self.initial_step}; got {len(self.beta)}")
+        if any(not (0.0 <= b <= 1.0) for b in self.beta):
+            raise ValueError("bsa factors must lie in [0, 1]")
+        if self.beta[-1] != 1.0:
+            raise ValueError("the last bsa factor must be 1 (exact at full dimensionality)")
+
+    def device_beta(self, device):
+        """The factors as a float64 device tensor (cached per device)."""
+        import torch
+        cache = self.__dict__.setdefault("_dev", {})
+        key = str(device)
+        if key not in cache:
+            cache[key] = torch.tensor(self.beta, dtype=torch.float64, device=device)
+        return cache[key]
+
+
+def bsa_should_prune(partial_l2: float, step: int, pruner: BsaPruner, threshold_l2: float) -> bool:
+    """The BSA test at schedule step ``step`` (float32 comparison, as the scan)."""
+    bound = np.float32(threshold_l2 * pruner.beta[step])
+    return bool(np.float32(partial_l2) >= bound)
+
+
+def fit_pca(x, sample: int = 200_000, seed: int = 0) -> OrthogonalTransform:
+    """Principal axes of ``x`` (n x d, numpy or CUDA tensor) as an orthogonal
+    transform, largest variance first.  Covariance in float64 on the device
+    over a seeded row sample; eigenvectors on the host (numpy eigh); each
+    axis' sign fixed so its largest-magnitude entry is positive."""
+    import torch
+    from .store import to_device
+    xt = to_device(np.asarray(x, dtype=np.float32) if not isinstance(x, torch.Tensor) else x,
+                   torch.float32)
+    n, d = int(xt.shape[0]), int(xt.shape[1])
+    if n < 2:
+        raise ValueError("pca needs at least two vectors")
+    if n > sample:
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        rows = torch.randperm(n, generator=g)[:sample].to(xt.device)
+        xt = xt.index_select(0, rows)
+    xs = xt.double()
+    xs = xs - xs.mean(0, keepdim=True)
+    cov = (xs.T @ xs / (xs.shape[0] - 1)).cpu().numpy()
+    w, v = np.linalg.eigh(cov)
+    v = v[:, np.argsort(-w, kind="stable")]
+    v = v * np.where(v[np.abs(v).argmax(0), np.arange(d)] < 0, -1.0, 1.0)
+    return OrthogonalTransform(matrix=np.ascontiguousarray(v.T).astype(np.float32), seed=-1)
+
+
+def fit_bsa(x_proj, d: int | None = None, initial_step: int = 2, k: int = 10,
+            quantile: float = 0.99, multiplier: float = 1.0, ntrain: int = 1000,
+            seed: int = 0) -> BsaPruner:
+    """Learn BSA factors from projected data ``x_proj`` (CUDA tensor n x d):
+    ``ntrain`` seeded rows act as training queries, their exact k nearest
+    other rows (kernel K9) as the neighbours whose partial/full ratios the
+    quantile is taken over."""
+    import torch
+    from .search import step_schedule
+    from .synthetic import ground_truth_device
+    if not 0.0 < quantile <= 1.0:
+        raise ValueError("quantile must be in (0, 1]")
+    if multiplier <= 0:
+        raise ValueError("multiplier must be positive")
+    n, dd = int(x_proj.shape[0]), int(x_proj.shape[1])
+    d = dd if d is None else d
+    if n < 2:
+        raise ValueError("bsa training needs at least two vectors")
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    rows = torch.randperm(n, generator=g)[:min(ntrain, n)].to(x_proj.device)
+    Q = x_proj.index_select(0, rows).contiguous()
+    kk = min(k + 1, n)
+    ids, _ = ground_truth_device(x_proj, Q, kk)
+    keep = ids != rows[:, None]  # drop the training row itself
+    nb = x_proj.index_select(0, ids.reshape(-1)).reshape(ids.shape[0], kk, dd)
+    diff2 = (nb.double() - Q.double()[:, None, :]) ** 2
+    cum = diff2.cumsum(-1)
+    full = cum[..., -1]
+    ends = torch.tensor([e for _, e in step_schedule(d, initial_step)], device=x_proj.device)
+    ok = keep & (full > 0)
+    ratio = (cum[..., ends - 1] / full.clamp_min(1e-300)[..., None])[ok]  # pairs x steps
+    if ratio.shape[0] == 0:
+        beta = [1.0] * int(ends.numel())
+    else:
+        qv = torch.quantile(ratio.float(), quantile, dim=0).double().cpu().numpy()
+        beta = [float(min(1.0, multiplier * v)) for v in qv]
+    beta[-1] = 1.0
+    return BsaPruner(beta=tuple(beta), d=d, initial_step=initial_step, quantile=quantile,
+                     multiplier=multiplier)
+
+
 class OrderCriteria(str, Enum):
     SEQUENTIAL = "sequential"
     DECREASING = "decreasing"

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .kernels import Metric
-from .pruning import AdsPruner
+from .pruning import AdsPruner, BsaPruner
 
 DEFAULT_SELECTION_FRACTION = 0.20
 DEFAULT_INITIAL_STEP = 2
@@ -73,6 +73,7 @@ class SearchParams:
     selection_fraction: float = DEFAULT_SELECTION_FRACTION
     initial_step: int = DEFAULT_INITIAL_STEP
     ads: AdsPruner | None = None
+    bsa: BsaPruner | None = None  # pruner="bsa" (this build's restatement)
 
     def __post_init__(self):
         if self.k < 1:
@@ -82,8 +83,15 @@ class SearchParams:
         if self.initial_step < 1:
             raise ValueError("initial_step must be >= 1")
         self.metric = Metric(self.metric)
-        if self.pruner not in ("none", "ads", "bond"):
+        if self.pruner not in ("none", "ads", "bond", "bsa"):
             raise ValueError(f"unknown pruner: {self.pruner!r}")
+        if self.pruner == "bsa":
+            if self.metric is not Metric.L2:
+                raise ValueError("the bsa pruner applies to squared L2 only")
+            if self.bsa is None:
+                raise ValueError("pruner='bsa' needs a fitted BsaPruner (pruning.fit_bsa)")
+            if self.bsa.initial_step != self.initial_step:
+                raise ValueError("the BsaPruner was fitted for another initial_step")
         if self.pruner == "bond" and self.metric is Metric.IP:
             raise ValueError("inner product has no monotone lower bound; "
                              "use pruner='none' for IP searches")
@@ -163,15 +171,20 @@ def decode_trace(buf, n):
     return out
 
 
-def make_params(params: SearchParams, d: int, warps=0) -> _lib.PdxSearchParams:
+def make_params(params: SearchParams, d: int, warps=0, device=None) -> _lib.PdxSearchParams:
     """``warps``: compute warps per query CTA, or (warps, tiles_per_warp[,
     ring_slots]); 0 = auto."""
     ads = params.ads if params.ads is not None else AdsPruner(d=d)
     w, tpw, rb = (tuple(warps) + (0, 0))[:3] if isinstance(warps, tuple) else (warps, 0, 0)
+    beta = None
+    if params.pruner == "bsa":
+        if params.bsa.d != d:
+            raise ValueError(f"the BsaPruner was fitted for d={params.bsa.d}, not {d}")
+        beta = params.bsa.device_beta(device if device is not None else "cuda")
     return _lib.PdxSearchParams(int(params.k), _lib.METRIC[Metric(params.metric).value],
                                 _lib.PRUNER[params.pruner], int(params.initial_step),
                                 float(params.selection_fraction), int(ads.d), int(w),
-                                float(ads.epsilon0), int(tpw), int(rb))
+                                float(ads.epsilon0), int(tpw), int(rb), _lib.ptr(beta))
 
 
 def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None, orders=None,
@@ -220,7 +233,7 @@ def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None,
     if work is None or work.numel() < wb:
         work = torch.empty((wb,), dtype=torch.uint8, device=dev)
         out["work"] = work
-    p = make_params(params, store.d, warps)
+    p = make_params(params, store.d, warps, dev)
     sb = None if seg_bucket is None else seg_bucket.contiguous()
     st = _lib.stream_handle()
     ev0 = ev1 = None

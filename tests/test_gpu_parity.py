@@ -312,3 +312,69 @@ def test_sharded_index_merge_exact(P):
         d, i = merge_device(torch.stack(dl).cuda(), torch.stack(il).cuda(), 10)
         np.testing.assert_array_equal(i.cpu().numpy(), full["ids"])
         np.testing.assert_array_equal(d.cpu().numpy(), full["dist"])
+
+
+# ----------------------------------------------------------------- BSA
+# BSA is this build's restatement (not in the reference):
+# parity is GPU vs the C oracle restatement, not vs reference output.
+
+def _bsa_setup(P, n=100_000, d=96, nq=48):
+    x = recipes.data("mixture", n, d, 31)
+    Q = recipes.queries("near", x, nq, 32)
+    T = P.fit_pca(x, seed=0)
+    m = T.matrix.astype(np.float64)
+    np.testing.assert_allclose(m @ m.T, np.eye(d), atol=1e-5)
+    xr = P.apply_transform(T, x)
+    qr = P.apply_transform(T, Q)
+    return x, Q, xr, qr
+
+
+@pytest.mark.parametrize("quantile,multiplier", [(0.99, 1.0), (0.9, 1.0), (0.5, 0.8)])
+def test_ivf_bsa_vs_oracle(P, oracle, quantile, multiplier):
+    """Learned factors (aggressive ones included): results, every decision and
+    the stats equal the oracle's BSA restatement."""
+    import torch
+    x, Q, xr, qr = _bsa_setup(P)
+    bsa = P.fit_bsa(torch.from_numpy(xr).cuda(), quantile=quantile, multiplier=multiplier)
+    assert bsa.beta[-1] == 1.0 and all(0 < b <= 1 for b in bsa.beta)
+    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=128, seed=0)
+    params = P.SearchParams(k=10, pruner="bsa", bsa=bsa)
+    out = P.ivf_search_batch(index, qr, params, 16, trace=True)
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, 10, 16, pruner="bsa",
+                                  bsa_beta=np.asarray(bsa.beta), survivors_cap=1 << 18)
+    np.testing.assert_array_equal(out["ids"], ref["ids"])
+    np.testing.assert_array_equal(out["dist"], ref["dist"])
+    np.testing.assert_array_equal(out["touched"], ref["touched"])
+    assert out["survivors"] == ref["survivor_lists"]
+
+
+def test_bsa_unit_factors_equal_bond(P, oracle):
+    """beta = 1 at every step is exactly the BOND comparison acc < T."""
+    x, Q, xr, qr = _bsa_setup(P, n=30_000, d=64, nq=32)
+    nsteps = len(P.step_schedule(64, 2))
+    bsa = P.BsaPruner(beta=(1.0,) * nsteps, d=64)
+    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=64, seed=0)
+    a = P.ivf_search_batch(index, qr, P.SearchParams(k=10, pruner="bsa", bsa=bsa), 8, trace=True)
+    b = P.ivf_search_batch(index, qr, P.SearchParams(k=10, pruner="bond"), 8, trace=True)
+    for key in ("ids", "dist", "touched"):
+        np.testing.assert_array_equal(a[key], b[key])
+    assert a["survivors"] == b["survivors"]
+
+
+def test_bsa_estimator_recall(P):
+    """BSA prunes harder than BOND yet keeps recall on clustered data."""
+    x = recipes.data("mixture", 100_000, 128, 41)
+    Q = recipes.queries("near", x, 200, 42)
+    gt = P.compute_ground_truth(P.VectorCollection.from_array(x), Q, 10)
+    stats = {}
+    for pruner in ("bond", "bsa"):
+        est = P.IvfNearestNeighbors(pruner=pruner, nlist=128, nprobe=128).fit(x)
+        _, ids = est.kneighbors(Q, 10)
+        out = P.ivf_search_batch(est.index_, P.apply_transform(est.transform_, Q)
+                                 if est.transform_ is not None else Q,
+                                 est.searcher(10).params, 128, stats=True)
+        rec = float(np.mean([P.recall_at_k(gt.ids[i], ids[i], 10) for i in range(len(Q))]))
+        stats[pruner] = (rec, int(out["touched"].sum()))
+    assert stats["bond"][0] == 1.0
+    assert stats["bsa"][0] >= 0.97
+    assert stats["bsa"][1] < stats["bond"][1]

@@ -170,3 +170,21 @@ def test_orthogonal_matches_reference(golden, d, seed):
     from paper_2503_04422_b200.pruning import generate_orthogonal
     arrays, _ = golden
     np.testing.assert_array_equal(generate_orthogonal(d, seed).matrix, arrays[f"orth_{d}_{seed}"])
+
+
+def test_oracle_bsa_unit_factors_equal_bond(oracle):
+    """BSA (this build's restatement) with beta = 1 everywhere is
+    the BOND comparison; smaller factors prune at least as much."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((3000, 32)).astype(np.float32)
+    q = rng.standard_normal(32).astype(np.float32)
+    blocks = to_blocks(VectorCollection.from_array(x), 256, pad=False)
+    n = len(oracle.step_schedule(32, 2))
+    a, sa = oracle.search(blocks, q, 10, pruner="bsa", bsa_beta=np.ones(n))
+    b, sb = oracle.search(blocks, q, 10, pruner="bond")
+    assert a == b and sa == sb
+    beta = np.linspace(0.2, 1.0, n)
+    c, sc = oracle.search(blocks, q, 10, pruner="bsa", bsa_beta=beta)
+    assert sc["values_touched"] <= sb["values_touched"]
+    with pytest.raises(ValueError):
+        oracle.search(blocks, q, 10, pruner="bsa")
