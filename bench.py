@@ -336,7 +336,8 @@ def main():
         "e2e": {"value": e2e_qps, "unit": "queries/s",
                 "h2d_bytes_per_step": int(Q.nbytes),
                 "d2h_bytes_per_step": int(args.nq * K * (4 + 8 + 0) + args.nq * 4)},
-        "gpu_launches": 5 * args.steps,
+        # per step: project, centroid_dist, select, bound_factors, build_visits, scan
+        "gpu_launches": 6 * args.steps,
         "index_build_s": build_s,
     }
     line["clocks"] = clk.summary()
@@ -359,6 +360,29 @@ def main():
             ids2 = r2.ids.cpu().numpy()
             rec2 = float(np.mean([P.recall_at_k(gt.ids[i], ids2[i], K) for i in range(args.nq)]))
             extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.mean(ts) / 1e3), "recall_at_10": rec2}
+        # BSA (this build's restatement) on the same data and nprobe
+        est = P.IvfNearestNeighbors(pruner="bsa", nlist=NLIST, nprobe=args.nprobe, seed=0).fit(X)
+        sb = est.searcher(K)
+        Qb = P.apply_transform(est.transform_, Qd)
+        rs = sb.run(Qb, stats=True)
+        pp_b = 1 - int(rs.touched.sum().item()) / int(rs.total.sum().item())
+        for _ in range(3):
+            sb.run(Qb)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rb = sb.run(Qb)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        idsb = rb.ids.cpu().numpy()
+        recb = float(np.mean([P.recall_at_k(gt.ids[i], idsb[i], K) for i in range(args.nq)]))
+        extras[f"bsa_nprobe_{args.nprobe}"] = {
+            "qps": args.nq / (np.mean(ts) / 1e3), "recall_at_10": recb,
+            "pruning_power": pp_b, "coef": [round(c, 4) for c in est.bsa_.coef]}
         line["extras"] = extras
     if ws == 1:
         cq, done, secs, threads, _ = cpu_oracle_qps(index, Qr_dev.cpu().numpy(), args.nprobe,

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PDX_ABI_VERSION 1
+#define PDX_ABI_VERSION 2
 
 #define PDX_OK 0
 #define PDX_EINVAL 1    /* bad argument (Python: ValueError) */
@@ -45,8 +45,13 @@ extern "C" {
 #define PDX_METRIC_IP 2
 
 /* SearchParams.pruner (search.py:65, :78-79).  BSA is not in the reference
- * (SPEC.md:14); it is this build's restatement: prune at step s iff
- * partial >= fl32(T * beta[s]) with learned beta. */
+ * (SPEC.md:14); it is this build's restatement (DESIGN.md
+ * §7), squared L2 on PCA-projected data: after step s (dims [0, e_s) seen)
+ *   est = ((partial + rx_s) + rq_s) - (coef_s * sqrt(rx_s)) * sqrt(rq_s)
+ * in float32 with per-op rounding, and a vector survives iff est < T.
+ * rx_s / rq_s are the residual energies sum_{j=e_s}^{d-1} v_j^2 of vector and
+ * query (sequential float32 sums in increasing j); coef_s = 2 * m * c_s with
+ * c_s a learned quantile of residual cosines (pdx_bsa_residuals). */
 #define PDX_PRUNER_NONE 0
 #define PDX_PRUNER_ADS 1
 #define PDX_PRUNER_BOND 2
@@ -93,6 +98,11 @@ typedef struct pdx_store {
   int32_t max_bucket_blocks; /* max over buckets of (#blocks) */
   int32_t max_bucket_tiles;  /* max over buckets of (#tiles) */
   const int32_t* d_tile_block;  /* [ntiles] logical block of each tile */
+  /* BSA only: float32 [ntiles][resid_steps][64] residual energy rx_s of each
+   * slot after step s of step_schedule(d, resid_initial_step); NULL otherwise */
+  const float* d_resid;
+  int32_t resid_steps;
+  int32_t resid_initial_step;
 } pdx_store;
 
 /* SearchParams (search.py:61-85) + AdsPruner (pruning.py:56-65). */
@@ -107,7 +117,7 @@ typedef struct pdx_search_params {
   double ads_epsilon0;
   int32_t tiles_per_warp; /* 64-vector tiles a compute warp claims at once (0 = auto) */
   int32_t ring_slots;     /* tiles in flight per query CTA (0 = auto) */
-  const double* bsa_beta; /* DEVICE array, one factor per schedule step (BSA only) */
+  const float* bsa_coef;  /* BSA: DEVICE float32 [nsteps] coef_s (see PDX_PRUNER_BSA) */
 } pdx_search_params;
 
 /* Outputs of pdx_search.  Per query q (row q of each array):
@@ -152,6 +162,16 @@ int pdx_device_info(int32_t* sm_count, int32_t* smem_optin, int32_t* cc_major, i
 int pdx_pack_tiles(const float* d_x, int64_t n, int32_t d, const int64_t* d_slot_src,
                    int64_t ntiles, int32_t group, const int64_t* d_ids_in, float* d_tiles,
                    int64_t* d_tile_ids, void* stream);
+
+/*
+ * BSA residual energies of a packed store (PDX_PRUNER_BSA; not in the
+ * reference): d_resid[t][s][i] = sum_{j=e_s}^{d-1} x_j^2 for slot i of tile t,
+ * e_s the end of step s of step_schedule(d, initial_step) (search.py:106-117),
+ * a sequential float32 sum in increasing j.  d_resid: float32
+ * [ntiles][nsteps][64] (NULL: only report nsteps); nsteps in *nsteps_out.
+ */
+int pdx_bsa_residuals(const pdx_store* store, int32_t initial_step, float* d_resid,
+                      int32_t* nsteps_out, void* stream);
 
 /*
  * K3 — query / data projection y = x @ M^T (float32).

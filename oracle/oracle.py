@@ -48,7 +48,7 @@ class _Params(C.Structure):
     _fields_ = [("k", C.c_int32), ("metric", C.c_int32), ("pruner", C.c_int32),
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
                 ("ads_d", C.c_int32), ("_pad", C.c_int32), ("ads_eps0", C.c_double),
-                ("bsa_beta", C.c_void_p)]
+                ("bsa_coef", C.c_void_p)]
 
 
 class _Stats(C.Structure):
@@ -129,12 +129,12 @@ class BlockList:
                          _p(self.mp), _p(self.ids), _p(self.id_off))
 
 
-def _params(k, metric, pruner, selection_fraction, initial_step, ads_d, eps0, bsa_beta=None):
+def _params(k, metric, pruner, selection_fraction, initial_step, ads_d, eps0, bsa_coef=None):
     beta = None
     if str(pruner) == "bsa":
-        if bsa_beta is None:
-            raise ValueError("pruner='bsa' needs bsa_beta (one factor per schedule step)")
-        beta = np.ascontiguousarray(bsa_beta, dtype=np.float64)
+        if bsa_coef is None:
+            raise ValueError("pruner='bsa' needs bsa_coef (one coefficient per schedule step)")
+        beta = np.ascontiguousarray(bsa_coef, dtype=np.float32)
     p = _Params(int(k), METRICS[str(metric)], PRUNERS[str(pruner)], int(initial_step),
                 float(selection_fraction), int(ads_d), 0, float(eps0), _p(beta))
     p._keep = beta
@@ -201,12 +201,12 @@ def _decode_survivors(buf, n):
 
 def search(blocks, query, k, metric="l2", pruner="none", selection_fraction=0.2,
            initial_step=2, ads_d=None, eps0=2.1, orders=None, survivors_cap=1 << 20,
-           bsa_beta=None):
+           bsa_coef=None):
     """search (search.py:177-205).  Returns (items, stats dict)."""
     bl = blocks if isinstance(blocks, BlockList) else BlockList(blocks)
     q = np.ascontiguousarray(query, dtype=np.float32)
     p = _params(k, metric, pruner, selection_fraction, initial_step,
-                ads_d if ads_d is not None else bl.d, eps0, bsa_beta)
+                ads_d if ads_d is not None else bl.d, eps0, bsa_coef)
     n = bl.nblocks
     ord_arrays, ord_ptrs = [], None
     if orders is not None:
@@ -290,11 +290,11 @@ def _finish(out):
 def ivf_search_batch(ivf: IvfView, queries, k, nprobe, metric="l2", pruner="none",
                      criteria="sequential", zone_width=None, selection_fraction=0.2,
                      initial_step=2, ads_d=None, eps0=2.1, nthreads=None, survivors_cap=0,
-                     bsa_beta=None):
+                     bsa_coef=None):
     Q = np.ascontiguousarray(queries, dtype=np.float32)
     nq = Q.shape[0]
     p = _params(k, metric, pruner, selection_fraction, initial_step,
-                ads_d if ads_d is not None else ivf.cent.d, eps0, bsa_beta)
+                ads_d if ads_d is not None else ivf.cent.d, eps0, bsa_coef)
     out, c = _batch(nq, k, nprobe, survivors_cap)
     _check(lib().orc_ivf_search_batch(C.addressof(ivf.c), _p(Q), nq, C.addressof(p), nprobe,
                                       CRITERIA[str(criteria)], int(zone_width or 0),
@@ -305,13 +305,13 @@ def ivf_search_batch(ivf: IvfView, queries, k, nprobe, metric="l2", pruner="none
 def exact_search_batch(blocks, global_means, queries, k, metric="l2", pruner="none",
                        criteria="sequential", zone_width=None, selection_fraction=0.2,
                        initial_step=2, ads_d=None, eps0=2.1, nthreads=None, survivors_cap=0,
-                       bsa_beta=None):
+                       bsa_coef=None):
     bl = blocks if isinstance(blocks, BlockList) else BlockList(blocks)
     Q = np.ascontiguousarray(queries, dtype=np.float32)
     mu = np.ascontiguousarray(global_means, dtype=np.float64)
     nq = Q.shape[0]
     p = _params(k, metric, pruner, selection_fraction, initial_step,
-                ads_d if ads_d is not None else bl.d, eps0, bsa_beta)
+                ads_d if ads_d is not None else bl.d, eps0, bsa_coef)
     out, c = _batch(nq, k, 0, survivors_cap)
     _check(lib().orc_exact_search_batch(C.addressof(bl.c), _p(mu), _p(Q), nq, C.addressof(p),
                                         CRITERIA[str(criteria)], int(zone_width or 0),

@@ -67,7 +67,7 @@ typedef struct {
   int32_t ads_d;
   int32_t _pad;
   double ads_eps0;
-  const double* bsa_beta; /* BSA: one learned factor per schedule step */
+  const float* bsa_coef; /* BSA: coef_s = 2 m c_s per schedule step */
 } orc_params;
 
 /* SearchStats (search.py:88-103).  survivors, when non-NULL, receives one
@@ -216,6 +216,20 @@ typedef struct {
   int32_t cap_mp;
 } orc_scratch;
 
+/* BSA residual energy sum_{j=from}^{d-1} v_j^2 of column `slot` of a
+ * dimension-major array with row stride `stride` (stride 1 = a plain vector):
+ * a sequential float32 sum in increasing j (pdx_bsa_residuals). */
+static float residual_energy(const float* v, int32_t stride, int32_t slot, int32_t from,
+                             int32_t d) {
+  float r = 0.0f;
+  for (int32_t j = from; j < d; ++j) {
+    const float x = v[(int64_t)j * stride + slot];
+    const float t = x * x;
+    r = r + t;
+  }
+  return r;
+}
+
 /* _linear_block (search.py:125-135). */
 static void linear_block(const orc_blocks* B, int64_t bi, const float* q, const orc_params* p,
                          orc_topk* tk, const int32_t* order, orc_stats* st, orc_scratch* sc) {
@@ -265,13 +279,24 @@ static void search_block(const orc_blocks* B, int64_t bi, const float* q, const 
       float bound;
       if (p->pruner == ORC_PRUNER_ADS)
         bound = (float)orc_ads_bound(b, p->ads_d, p->ads_eps0, (double)threshold);
-      else if (p->pruner == ORC_PRUNER_BSA) /* partial >= T * beta_s prunes */
-        bound = (float)((double)threshold * p->bsa_beta[s]);
       else
         bound = threshold;
       int32_t w = 0;
-      for (int32_t r = 0; r < npos; ++r)
-        if (acc[pos[r]] < bound) pos[w++] = pos[r];
+      if (p->pruner == ORC_PRUNER_BSA) {
+        /* BSA (this build's restatement, pdx_b200.h PDX_PRUNER_BSA): keep iff
+         * ((acc + rx) + rq) - (coef * sqrt(rx)) * sqrt(rq) < T, float32 */
+        const float rq = residual_energy(q, 1, 0, b, d);
+        const float nq = sqrtf(rq), coef = p->bsa_coef[s];
+        for (int32_t r = 0; r < npos; ++r) {
+          const int32_t i = pos[r];
+          const float rx = residual_energy(blk, mp, i, b, d);
+          const float est = ((acc[i] + rx) + rq) - (coef * sqrtf(rx)) * nq;
+          if (est < threshold) pos[w++] = i;
+        }
+      } else {
+        for (int32_t r = 0; r < npos; ++r)
+          if (acc[pos[r]] < bound) pos[w++] = pos[r];
+      }
       npos = w;
     }
     if (st) st->values_touched += touched * (int64_t)(b - a);
@@ -307,7 +332,12 @@ int orc_search(const orc_blocks* B, const int64_t* block_list, int64_t nlisted,
                float* out_dist, int64_t* out_ids, int32_t* out_count, orc_stats* st) {
   orc_topk tk = {p->k, 0, out_dist, out_ids};
   if (p->k < 1) return ORC_EINVAL;
+  if (p->pruner == ORC_PRUNER_BSA && (!p->bsa_coef || p->metric != ORC_L2))
+    return ORC_EINVAL; /* BSA: squared L2 ... */
   if (!block_list) nlisted = B->nblocks;
+  if (p->pruner == ORC_PRUNER_BSA && orders)
+    for (int64_t r = 0; r < nlisted; ++r)
+      if (orders[r]) return ORC_EINVAL; /* ... in natural (principal-axis) order */
   int32_t cap = 1;
   for (int64_t r = 0; r < nlisted; ++r) {
     int64_t bi = block_list ? block_list[r] : r;

@@ -24,7 +24,8 @@ TILE = 64
 # every symbol include/pdx_b200.h declares
 EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_tiles",
            "pdx_project", "pdx_select_buckets", "pdx_dimension_orders", "pdx_search_workspace",
-           "pdx_search", "pdx_merge_topk", "pdx_segment_means", "pdx_ground_truth")
+           "pdx_search", "pdx_merge_topk", "pdx_segment_means", "pdx_ground_truth",
+           "pdx_bsa_residuals")
 
 
 class PdxStore(C.Structure):
@@ -33,7 +34,9 @@ class PdxStore(C.Structure):
                 ("d_tiles", C.c_void_p), ("d_tile_ids", C.c_void_p),
                 ("d_block_tile", C.c_void_p), ("d_block_m", C.c_void_p),
                 ("d_bucket_block", C.c_void_p), ("max_bucket_blocks", C.c_int32),
-                ("max_bucket_tiles", C.c_int32), ("d_tile_block", C.c_void_p)]
+                ("max_bucket_tiles", C.c_int32), ("d_tile_block", C.c_void_p),
+                ("d_resid", C.c_void_p), ("resid_steps", C.c_int32),
+                ("resid_initial_step", C.c_int32)]
 
 
 class PdxSearchParams(C.Structure):
@@ -41,7 +44,7 @@ class PdxSearchParams(C.Structure):
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
                 ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
                 ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32),
-                ("bsa_beta", C.c_void_p)]
+                ("bsa_coef", C.c_void_p)]
 
 
 class PdxSearchOut(C.Structure):
@@ -89,9 +92,10 @@ def lib():
         L.pdx_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
         L.pdx_segment_means.argtypes = [vp, i32, vp, vp, i32, vp, vp]
         L.pdx_ground_truth.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp]
+        L.pdx_bsa_residuals.argtypes = [vp, i32, vp, vp, vp]
         for name in EXPORTS:
             getattr(L, name).restype = getattr(L, name).restype or C.c_int
-        if L.pdx_abi_version() != 1:
+        if L.pdx_abi_version() != 2:
             raise RuntimeError("libpdx_b200.so ABI version mismatch")
         _lib = L
     return _lib

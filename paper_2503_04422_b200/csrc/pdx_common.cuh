@@ -42,9 +42,12 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // The reference's vertical kernels (kernels.py:55-61): every float32 op is
 // rounded on its own (numpy ufuncs never fuse), so use the _rn intrinsics,
 // which nvcc never contracts into FMA.
+// Scan-kernel-internal metric tag: squared L2 with the BSA residual bound.
+constexpr int kMetricL2Bsa = 3;
+
 template <int METRIC>
 __device__ __forceinline__ float upd(float acc, float q, float x) {
-  if (METRIC == PDX_METRIC_L2) {
+  if (METRIC == PDX_METRIC_L2 || METRIC == kMetricL2Bsa) {
     const float t = __fsub_rn(q, x);
     return __fadd_rn(acc, __fmul_rn(t, t));
   } else if (METRIC == PDX_METRIC_L1) {

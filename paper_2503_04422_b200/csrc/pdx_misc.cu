@@ -293,6 +293,50 @@ extern "C" int pdx_segment_means(const float* d_x, int32_t d, const int64_t* d_r
   return PDX_OK;
 }
 
+namespace pdx {
+// BSA residual energies (pdx_bsa_residuals): one thread per slot; each step's
+// suffix sum is its own sequential float32 chain in increasing dim order, the
+// definition the C oracle restates.
+__global__ void __launch_bounds__(256) bsa_resid_kernel(const float* __restrict__ tiles, int64_t ntiles,
+                                                        int d, int d_pad, int group,
+                                                        int initial_step, int nsteps,
+                                                        float* __restrict__ out) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= ntiles * 64) return;
+  const int64_t t = gid >> 6;
+  const int i = (int)(gid & 63);
+  const float* tb = tiles + t * (int64_t)d_pad * 64;
+  int64_t e = 0, width = initial_step;
+  for (int s = 0; s < nsteps; ++s, width *= 2) {
+    e = e + width < d ? e + width : d;
+    float r = 0.f;
+    for (int j = (int)e; j < d; ++j) {
+      const float x = group == 8 ? tb[((int64_t)(j >> 3) * 64 + i) * 8 + (j & 7)]
+                                 : tb[(int64_t)j * 64 + i];
+      r = __fadd_rn(r, __fmul_rn(x, x));
+    }
+    out[(t * nsteps + s) * 64 + i] = r;
+  }
+}
+}  // namespace pdx
+
+extern "C" int pdx_bsa_residuals(const pdx_store* store, int32_t initial_step, float* d_resid,
+                                 int32_t* nsteps_out, void* stream) {
+  PDX_REQUIRE(store && nsteps_out, "pdx_bsa_residuals: null argument");
+  PDX_REQUIRE(initial_step >= 1, "initial_step must be >= 1");
+  PDX_REQUIRE(store->group == 1 || store->group == 8, "group must be 1 or 8");
+  int n = 0;
+  for (int64_t e = 0, w = initial_step; e < store->d; w *= 2, ++n) e = e + w < store->d ? e + w : store->d;
+  *nsteps_out = n;
+  if (store->ntiles == 0 || !d_resid) return PDX_OK;  // NULL output: size query
+  const int64_t threads = store->ntiles * 64;
+  pdx::bsa_resid_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, pdx::as_stream(stream)>>>(
+      store->d_tiles, store->ntiles, store->d, store->d_pad, store->group, initial_step, n,
+      d_resid);
+  PDX_LAUNCH_CHECK();
+  return PDX_OK;
+}
+
 extern "C" int pdx_abi_version(void) { return PDX_ABI_VERSION; }
 
 extern "C" int pdx_last_error(char* buf, size_t cap) {

@@ -107,20 +107,17 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
 }
 
 // Per-step bound factors for ads_or_bond_bound, [0][s] = ratio, [1][s] = band:
-// ADS ratio = d'/D and band = 1 + eps0/sqrt(d') in float64 (pruning.py:80-88),
-// BSA ratio = beta[s] (device array) and band = 1, and ratio = band = 1
-// wherever the reference compares against T itself (BOND, none, d' >= D).
+// ADS ratio = d'/D and band = 1 + eps0/sqrt(d') in float64 (pruning.py:80-88);
+// ratio = band = 1 wherever the comparison is against T itself (BOND, none,
+// BSA — whose per-vector estimate is compared with T — and ADS at d' >= D).
 __global__ void bound_factors_kernel(int pruner, int d, int initial_step, int nsteps, int ads_d,
-                                     double eps0, const double* __restrict__ beta,
-                                     double* __restrict__ out) {
+                                     double eps0, double* __restrict__ out) {
   if (threadIdx.x != 0) return;
   int64_t e = 0, width = initial_step;  // step_schedule (search.py:106-117)
   for (int s = 0; s < nsteps; ++s, width *= 2) {
     e = e + width < d ? e + width : d;
     double ratio = 1.0, band = 1.0;
-    if (pruner == PDX_PRUNER_BSA) {
-      ratio = beta[s];
-    } else if (pruner == PDX_PRUNER_ADS && e < ads_d) {
+    if (pruner == PDX_PRUNER_ADS && e < ads_d) {
       ratio = __ddiv_rn((double)e, (double)ads_d);
       band = __dadd_rn(1.0, __ddiv_rn(eps0, __dsqrt_rn((double)e)));
     }
@@ -149,6 +146,9 @@ static cudaError_t launch_metric(int metric, const ScanArgs& A, const ScanSmem& 
   switch (metric) {
     case PDX_METRIC_L2: return launch_scan<G, ORD, PDX_METRIC_L2>(A, L, nq, W, tpw, st);
     case PDX_METRIC_L1: return launch_scan<G, ORD, PDX_METRIC_L1>(A, L, nq, W, tpw, st);
+    case kMetricL2Bsa:
+      if (!ORD) return launch_scan<G, false, kMetricL2Bsa>(A, L, nq, W, tpw, st);
+      return cudaErrorInvalidValue;
     default: return launch_scan<G, ORD, PDX_METRIC_IP>(A, L, nq, W, tpw, st);
   }
 }
@@ -193,7 +193,9 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
               "the ads pruner applies to squared L2 only");
   PDX_REQUIRE(!(prm->pruner == PDX_PRUNER_BSA && prm->metric != PDX_METRIC_L2),
               "the bsa pruner applies to squared L2 only");
-  PDX_REQUIRE(prm->pruner != PDX_PRUNER_BSA || prm->bsa_beta, "bsa needs its beta factors");
+  PDX_REQUIRE(prm->pruner != PDX_PRUNER_BSA || prm->bsa_coef, "bsa needs its coefficients");
+  PDX_REQUIRE(prm->pruner != PDX_PRUNER_BSA || !d_orders,
+              "bsa visits dimensions in their (principal-axis) order; no visit orders");
   PDX_REQUIRE(prm->pruner != PDX_PRUNER_ADS || prm->ads_epsilon0 > 0.0, "epsilon0 must be positive");
   PDX_REQUIRE(prm->pruner != PDX_PRUNER_ADS || prm->ads_d >= 1, "ads d must be >= 1");
   PDX_REQUIRE(store->d >= 1 && store->d <= 65535, "dimensionality %d unsupported", store->d);
@@ -205,6 +207,11 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   if (nq == 0) return PDX_OK;
   const int nsteps = schedule_steps(store->d, prm->initial_step);
   PDX_REQUIRE(nsteps <= kMaxSteps, "step schedule too long (%d steps)", nsteps);
+  PDX_REQUIRE(prm->pruner != PDX_PRUNER_BSA ||
+                  (store->d_resid && store->resid_steps == nsteps &&
+                   store->resid_initial_step == prm->initial_step),
+              "bsa needs the store's residual energies for this step schedule "
+              "(pdx_bsa_residuals with initial_step %d)", prm->initial_step);
 
   int dev = 0, optin = 0;
   PDX_CUDA_CHECK(cudaGetDevice(&dev));
@@ -239,7 +246,7 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   PDX_CUDA_CHECK(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), st));
   bound_factors_kernel<<<1, 32, 0, st>>>(prm->pruner, store->d, prm->initial_step, nsteps,
                                          prm->ads_d >= 1 ? prm->ads_d : store->d,
-                                         prm->ads_epsilon0, prm->bsa_beta, d_factors);
+                                         prm->ads_epsilon0, d_factors);
   if (nseg > 0 && maxvis > 0) {
     build_visits_kernel<<<(unsigned)nlists, 256, 0, st>>>(
         d_seg_bucket, nseg, store->d_bucket_block, store->d_block_tile, store->d_block_m,
@@ -272,6 +279,8 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   A.sf = prm->selection_fraction;
   A.ads_d = (prm->ads_d >= 1 && prm->pruner != PDX_PRUNER_BSA) ? prm->ads_d : store->d;
   A.factors = d_factors;
+  A.resid = store->d_resid;
+  A.bsa_coef = prm->bsa_coef;
   A.eps0 = prm->ads_epsilon0;
   A.out_dist = out->d_dist;
   A.out_ids = out->d_ids;
@@ -287,12 +296,13 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
 
   cudaError_t e;
   const bool ord = d_orders != nullptr;
+  const int mt = prm->pruner == PDX_PRUNER_BSA ? kMetricL2Bsa : prm->metric;
   if (store->group == 8)
-    e = ord ? launch_metric<8, true>(prm->metric, A, L, (int)nq, W, tpw, st)
-            : launch_metric<8, false>(prm->metric, A, L, (int)nq, W, tpw, st);
+    e = ord ? launch_metric<8, true>(mt, A, L, (int)nq, W, tpw, st)
+            : launch_metric<8, false>(mt, A, L, (int)nq, W, tpw, st);
   else
-    e = ord ? launch_metric<1, true>(prm->metric, A, L, (int)nq, W, tpw, st)
-            : launch_metric<1, false>(prm->metric, A, L, (int)nq, W, tpw, st);
+    e = ord ? launch_metric<1, true>(mt, A, L, (int)nq, W, tpw, st)
+            : launch_metric<1, false>(mt, A, L, (int)nq, W, tpw, st);
   PDX_CUDA_CHECK(e);
   return PDX_OK;
 }

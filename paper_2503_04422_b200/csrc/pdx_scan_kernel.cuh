@@ -42,8 +42,8 @@ static_assert(sizeof(Control) <= 128, "control block");
 // Shared-memory carve-up; computed on the host and passed to the kernel so
 // the offsets live in the constant bank instead of being rematerialised.
 struct ScanSmem {
-  int32_t ctl, ratio, band, ends, bnd, cnt, wmin, flag, desc, sum, items, wbnd, ids, tki, part,
-      tkd, q, bmask, total, rb;
+  int32_t ctl, ratio, band, bsa, ends, bnd, cnt, wmin, flag, desc, sum, items, wbnd, ids, tki,
+      part, tkd, q, bmask, total, rb;
 };
 
 inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int d_pad) {
@@ -57,6 +57,7 @@ inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int 
   L.ctl = take(128);
   L.ratio = take(sizeof(double) * kMaxSteps);
   L.band = take(sizeof(double) * kMaxSteps);
+  L.bsa = take(sizeof(float) * 3 * kMaxSteps);
   L.ends = take(sizeof(int32_t) * kMaxSteps);
   L.bnd = take(sizeof(float) * kMaxSteps);
   L.cnt = take(sizeof(int32_t) * kMaxSteps);
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   Control& ctl = *reinterpret_cast<Control*>(smem + L.ctl);
   double* s_ratio = reinterpret_cast<double*>(smem + L.ratio);
   double* s_band = reinterpret_cast<double*>(smem + L.band);
+  float* s_bsa = reinterpret_cast<float*>(smem + L.bsa);  // BSA: rq, sqrt(rq), coef per step
   int32_t* s_ends = reinterpret_cast<int32_t*>(smem + L.ends);
   float* s_bnd = reinterpret_cast<float*>(smem + L.bnd);
   int32_t* s_cnt = reinterpret_cast<int32_t*>(smem + L.cnt);
@@ -245,6 +247,13 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   if (threadIdx.x < nsteps) {  // bound factors (bound_factors_kernel, pdx_scan.cu)
     s_ratio[threadIdx.x] = A.factors[threadIdx.x];
     s_band[threadIdx.x] = A.factors[kMaxSteps + threadIdx.x];
+    if (METRIC == kMetricL2Bsa) {  // the query's residual energy after this step
+      float r = 0.f;
+      for (int j = s_ends[threadIdx.x]; j < A.d; ++j) r = __fadd_rn(r, __fmul_rn(s_q[j], s_q[j]));
+      s_bsa[threadIdx.x] = r;
+      s_bsa[kMaxSteps + threadIdx.x] = __fsqrt_rn(r);
+      s_bsa[2 * kMaxSteps + threadIdx.x] = A.bsa_coef[threadIdx.x];
+    }
   }
   __syncthreads();
   const TileEntry* vis = A.vis + (int64_t)q * A.vis_qstride;
@@ -258,6 +267,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     Q.ends = s_ends;
     Q.ratio = s_ratio;
     Q.band = s_band;
+    Q.bsa = s_bsa;
     Q.bmask = s_bmask;
     SparseItem* items = reinterpret_cast<SparseItem*>(smem + L.items) + 32 * w;
     float* wbnd = reinterpret_cast<float*>(smem + L.wbnd) + (size_t)w * tpw * kMaxSteps;

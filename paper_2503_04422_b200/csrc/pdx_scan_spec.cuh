@@ -92,6 +92,8 @@ struct ScanArgs {
   int64_t* debug;  // optional [nq][8] counters (see pdx_search_out)
   int32_t sparse_max;  // a tile goes sparse once at most this many slots survive
   const double* factors;  // [2][kMaxSteps]: per-step bound ratio, band
+  const float* resid;     // BSA: [ntiles][nsteps][64] residual energy per slot and step
+  const float* bsa_coef;  // BSA: [nsteps]
 };
 
 // Shared-memory views of one round slice (the tiles of one compute warp).
@@ -109,6 +111,7 @@ struct QueryRefs {
   const int32_t* ends;   // [nsteps] step ends
   const double* ratio;   // [nsteps] dims_seen / ads_d
   const double* band;    // [nsteps] 1 + eps0 / sqrt(dims_seen)
+  const float* bsa;      // BSA: [3][kMaxSteps] query residual energy, its sqrt, coef
   const uint8_t* bmask;  // [d_pad/8] bit e of group g: a step ends after dim 8g+e
 };
 
@@ -124,6 +127,19 @@ __device__ __forceinline__ float ads_or_bond_bound(float T, double ratio, double
   if (ratio == 1.0) return T;
   const double t = __dmul_rn(__dmul_rn(__dmul_rn((double)T, ratio), band), band);
   return __double2float_rn(t);
+}
+
+// BSA estimate after step s (PDX_PRUNER_BSA in pdx_b200.h), float32 per-op
+// rounding: ((acc + rx) + rq) - (coef * sqrt(rx)) * sqrt(rq).  At the last
+// step rx = rq = 0 and the estimate is acc itself.
+__device__ __forceinline__ float bsa_est(const QueryRefs& Q, int s, float acc, float rx) {
+  const float cx = __fmul_rn(Q.bsa[2 * kMaxSteps + s], __fsqrt_rn(rx));
+  return __fsub_rn(__fadd_rn(__fadd_rn(acc, rx), Q.bsa[s]), __fmul_rn(cx, Q.bsa[kMaxSteps + s]));
+}
+
+// Residual energy of slot `slot` of tile `tile` after step s.
+__device__ __forceinline__ float bsa_resid(const ScanArgs& A, int64_t tile, int s, int slot) {
+  return __ldg(A.resid + ((size_t)tile * A.nsteps + s) * kTile + slot);
 }
 
 __device__ __forceinline__ const uint16_t* order_of(const ScanArgs& A, int q, int seg) {
@@ -192,6 +208,12 @@ __device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc&
     park(R, sum, tj, 0, 0, al0, al1, acc0, acc1, nsteps, nitems, lane);
     return;
   }
+  constexpr bool kBsa = METRIC == kMetricL2Bsa;
+  float rx0 = 0.f, rx1 = 0.f;  // BSA: residual energies for step s, loaded a step ahead
+  if (kBsa) {
+    if (al0) rx0 = bsa_resid(A, t.tile, 0, s0);
+    if (al1) rx1 = bsa_resid(A, t.tile, 0, s1);
+  }
   const int ng = A.d_pad >> 3;
   float n0[8], n1[8];  // prefetched group
 #pragma unroll
@@ -223,12 +245,14 @@ __device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc&
       acc0 = upd<METRIC>(acc0, qv[e], x0[e]);
       acc1 = upd<METRIC>(acc1, qv[e], x1[e]);
       if (bm & (1u << e)) {  // step s ends after dim 8g+e (warp-uniform)
-        part[s * kTile + s0] = al0 ? acc0 : INFINITY;
-        part[s * kTile + s1] = al1 ? acc1 : INFINITY;
+        const float v0 = kBsa ? bsa_est(Q, s, acc0, rx0) : acc0;
+        const float v1 = kBsa ? bsa_est(Q, s, acc1, rx1) : acc1;
+        part[s * kTile + s0] = al0 ? v0 : INFINITY;
+        part[s * kTile + s1] = al1 ? v1 : INFINITY;
         if (prune) {
           const float bs = __shfl_sync(kFull, mybnd, s);
-          al0 = al0 && (acc0 < bs);
-          al1 = al1 && (acc1 < bs);
+          al0 = al0 && (v0 < bs);
+          al1 = al1 && (v1 < bs);
         }
         const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
         if (lane == 0) sum.cnt[s] = c;
@@ -240,6 +264,10 @@ __device__ __forceinline__ void dense_tile_g8(const ScanArgs& A, const TileDesc&
         if (c <= A.sparse_max) {
           park(R, sum, tj, s, g * 8 + e + 1, al0, al1, acc0, acc1, nsteps, nitems, lane);
           return;
+        }
+        if (kBsa) {
+          rx0 = al0 ? bsa_resid(A, t.tile, s, s0) : 0.f;
+          rx1 = al1 ? bsa_resid(A, t.tile, s, s1) : 0.f;
         }
       }
     }
@@ -265,9 +293,15 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
     park(R, sum, tj, 0, 0, al0, al1, acc0, acc1, nsteps, nitems, lane);
     return;
   }
+  constexpr bool kBsa = METRIC == kMetricL2Bsa;
   int a = 0;
   for (int s = 0; s < nsteps; ++s) {
     const int b = Q.ends[s];
+    float rx0 = 0.f, rx1 = 0.f;  // BSA: issued before the step's dims are read
+    if (kBsa) {
+      if (al0) rx0 = bsa_resid(A, t.tile, s, s0);
+      if (al1) rx1 = bsa_resid(A, t.tile, s, s1);
+    }
     for (int j0 = a; j0 < b; j0 += 8) {
       int dim[8];
       float x0[8], x1[8];
@@ -301,12 +335,14 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
         }
       }
     }
-    part[s * kTile + s0] = al0 ? acc0 : INFINITY;
-    part[s * kTile + s1] = al1 ? acc1 : INFINITY;
+    const float v0 = kBsa ? bsa_est(Q, s, acc0, rx0) : acc0;
+    const float v1 = kBsa ? bsa_est(Q, s, acc1, rx1) : acc1;
+    part[s * kTile + s0] = al0 ? v0 : INFINITY;
+    part[s * kTile + s1] = al1 ? v1 : INFINITY;
     if (prune) {
       const float bs = __shfl_sync(kFull, mybnd, s);
-      al0 = al0 && (acc0 < bs);
-      al1 = al1 && (acc1 < bs);
+      al0 = al0 && (v0 < bs);
+      al1 = al1 && (v1 < bs);
     }
     const int c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
     if (lane == 0) sum.cnt[s] = c;
@@ -341,6 +377,8 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
   int s = it.step;
   float acc = it.acc;
   int pos = it.pos;
+  constexpr bool kBsa = METRIC == kMetricL2Bsa;
+  float rx = (kBsa && act) ? bsa_resid(A, t.tile, s, slot) : 0.f;  // BSA, step s
   if (G == 8 && !ORD) {
     const int ng = A.d_pad >> 3;
     int g = pos >> 3;
@@ -364,8 +402,9 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
           if (act && e >= e0) {
             acc = upd<METRIC>(acc, qv[e], x[e]);
             if (bm & (1u << e)) {
-              part[s * kTile + slot] = acc;
-              const bool ok = !prune || acc < bnd[s];
+              const float v = kBsa ? bsa_est(Q, s, acc, rx) : acc;
+              part[s * kTile + slot] = v;
+              const bool ok = !prune || v < bnd[s];
               if (ok) atomicAdd(&sum.cnt[s], 1);
               ++s;
               if (!ok) {
@@ -373,6 +412,8 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
               } else if (s == nsteps) {
                 atomicOr(slot >= 32 ? &sum.alive1 : &sum.alive0, 1u << (slot & 31));
                 act = false;
+              } else if (kBsa) {
+                rx = bsa_resid(A, t.tile, s, slot);
               }
             }
           }
@@ -408,8 +449,9 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
           if (pos + e < jend) acc = upd<METRIC>(acc, Q.q[dim[e]], x[e]);
         pos = jend;
         if (pos == end) {
-          part[s * kTile + slot] = acc;
-          const bool ok = !prune || acc < bnd[s];
+          const float v = kBsa ? bsa_est(Q, s, acc, rx) : acc;
+          part[s * kTile + slot] = v;
+          const bool ok = !prune || v < bnd[s];
           if (ok) atomicAdd(&sum.cnt[s], 1);
           ++s;
           if (!ok) {
@@ -419,6 +461,7 @@ __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const Que
             act = false;
           } else {
             end = Q.ends[s];
+            if (kBsa) rx = bsa_resid(A, t.tile, s, slot);
           }
         }
       }

@@ -100,48 +100,70 @@ def ads_bound(dims_seen: int, pruner: AdsPruner, threshold_l2: float) -> float:
 
 # ------------------------------------------------------------------ BSA
 # The reference names BSA but does not implement it
-# (SPEC.md:14).  This build's restatement: project onto the
-# principal components (largest variance first), then after each schedule
-# step s prune a candidate iff  partial_s >= T * beta_s,  where beta_s is
-# `multiplier` x the `quantile` of partial_s / full over (training query,
-# true k-NN) pairs, capped at 1 and exactly 1 at full dimensionality.  The
-# bound is monotone in T, so the scan's speculate-and-commit exactness holds.
+# (SPEC.md:14).  This build's restatement:
+# data and queries are projected onto their principal axes (largest variance
+# first); after schedule step s (dims [0, e_s) seen) a candidate survives iff
+#     ((partial + rx_s) + rq_s) - (coef_s * sqrt(rx_s)) * sqrt(rq_s) < T
+# (float32, per-op rounding), rx_s / rq_s the residual energies of vector and
+# query over dims [e_s, d).  coef_s = 2 * min(m * c_s, 1) where c_s is the
+# `quantile` of the residual cosine <x_r, q_r> / (|x_r| |q_r|) over (training
+# query, true k-NN) pairs and m the multiplier; m -> 1 / c_s is the exact
+# Cauchy-Schwarz bound.  The estimate does not depend on T, so the scan's
+# speculate-and-commit exactness carries over unchanged.
 
 @dataclass(frozen=True)
 class BsaPruner:
-    """Learned per-step bound factors for PCA-projected data (L2 only)."""
+    """Learned residual-cosine bound for PCA-projected data (L2 only)."""
 
-    beta: tuple  # one factor per step of step_schedule(d, initial_step)
+    coef: tuple  # float32 coef_s per step of step_schedule(d, initial_step)
     d: int
     initial_step: int = 2
     quantile: float = 0.99
     multiplier: float = 1.0
+    cosines: tuple = ()  # the learned c_s (informational)
 
     def __post_init__(self):
         from .search import step_schedule
         n = len(step_schedule(self.d, self.initial_step))
-        if len(self.beta) != n:
-            raise ValueError(f"bsa needs {n} factors for d={self.d}, initial_step="
-                             f"{self.initial_step}; got {len(self.beta)}")
-        if any(not (0.0 <= b <= 1.0) for b in self.beta):
-            raise ValueError("bsa factors must lie in [0, 1]")
-        if self.beta[-1] != 1.0:
-            raise ValueError("the last bsa factor must be 1 (exact at full dimensionality)")
+        if len(self.coef) != n:
+            raise ValueError(f"bsa needs {n} coefficients for d={self.d}, initial_step="
+                             f"{self.initial_step}; got {len(self.coef)}")
+        if any(not (-2.0 <= c <= 2.0) for c in self.coef):
+            raise ValueError("bsa coefficients must lie in [-2, 2]")
 
-    def device_beta(self, device):
-        """The factors as a float64 device tensor (cached per device)."""
+    def device_coef(self, device):
+        """The coefficients as a float32 device tensor (cached per device)."""
         import torch
         cache = self.__dict__.setdefault("_dev", {})
         key = str(device)
         if key not in cache:
-            cache[key] = torch.tensor(self.beta, dtype=torch.float64, device=device)
+            cache[key] = torch.tensor(np.asarray(self.coef, np.float32), device=device)
         return cache[key]
 
 
-def bsa_should_prune(partial_l2: float, step: int, pruner: BsaPruner, threshold_l2: float) -> bool:
-    """The BSA test at schedule step ``step`` (float32 comparison, as the scan)."""
-    bound = np.float32(threshold_l2 * pruner.beta[step])
-    return bool(np.float32(partial_l2) >= bound)
+def _residual_energy(v: np.ndarray, start: int) -> np.float32:
+    r = np.float32(0.0)
+    for x in np.asarray(v, np.float32)[start:]:
+        r = np.float32(r + np.float32(x * x))
+    return r
+
+
+def bsa_estimate(partial: float, x, q, dims_seen: int, coef: float) -> np.float32:
+    """The scan's BSA estimate for one vector (host restatement, small d)."""
+    rx, rq = _residual_energy(x, dims_seen), _residual_energy(q, dims_seen)
+    c = np.float32(coef)
+    cx = np.float32(c * np.sqrt(rx, dtype=np.float32))
+    return np.float32(np.float32(np.float32(np.float32(partial) + rx) + rq)
+                      - np.float32(cx * np.sqrt(rq, dtype=np.float32)))
+
+
+def bsa_should_prune(partial_l2: float, x, q, step: int, pruner: BsaPruner,
+                     threshold_l2: float) -> bool:
+    """The BSA test after schedule step ``step`` for vector x, query q."""
+    from .search import step_schedule
+    e = step_schedule(pruner.d, pruner.initial_step)[step][1]
+    est = bsa_estimate(partial_l2, x, q, e, pruner.coef[step])
+    return not bool(est < np.float32(threshold_l2))
 
 
 def fit_pca(x, sample: int = 200_000, seed: int = 0) -> OrthogonalTransform:
@@ -172,10 +194,10 @@ def fit_pca(x, sample: int = 200_000, seed: int = 0) -> OrthogonalTransform:
 def fit_bsa(x_proj, d: int | None = None, initial_step: int = 2, k: int = 10,
             quantile: float = 0.99, multiplier: float = 1.0, ntrain: int = 1000,
             seed: int = 0) -> BsaPruner:
-    """Learn BSA factors from projected data ``x_proj`` (CUDA tensor n x d):
-    ``ntrain`` seeded rows act as training queries, their exact k nearest
-    other rows (kernel K9) as the neighbours whose partial/full ratios the
-    quantile is taken over."""
+    """Learn the BSA coefficients from projected data ``x_proj`` (CUDA tensor
+    n x d): ``ntrain`` seeded rows act as training queries and their exact k
+    nearest other rows (kernel K9) as the neighbours whose residual cosines
+    the quantile is taken over (float64 on the device)."""
     import torch
     from .search import step_schedule
     from .synthetic import ground_truth_device
@@ -192,22 +214,28 @@ def fit_bsa(x_proj, d: int | None = None, initial_step: int = 2, k: int = 10,
     Q = x_proj.index_select(0, rows).contiguous()
     kk = min(k + 1, n)
     ids, _ = ground_truth_device(x_proj, Q, kk)
-    keep = ids != rows[:, None]  # drop the training row itself
-    nb = x_proj.index_select(0, ids.reshape(-1)).reshape(ids.shape[0], kk, dd)
-    diff2 = (nb.double() - Q.double()[:, None, :]) ** 2
-    cum = diff2.cumsum(-1)
-    full = cum[..., -1]
-    ends = torch.tensor([e for _, e in step_schedule(d, initial_step)], device=x_proj.device)
-    ok = keep & (full > 0)
-    ratio = (cum[..., ends - 1] / full.clamp_min(1e-300)[..., None])[ok]  # pairs x steps
-    if ratio.shape[0] == 0:
-        beta = [1.0] * int(ends.numel())
-    else:
-        qv = torch.quantile(ratio.float(), quantile, dim=0).double().cpu().numpy()
-        beta = [float(min(1.0, multiplier * v)) for v in qv]
-    beta[-1] = 1.0
-    return BsaPruner(beta=tuple(beta), d=d, initial_step=initial_step, quantile=quantile,
-                     multiplier=multiplier)
+    keep = (ids != rows[:, None]).reshape(-1)  # drop the training row itself
+    X = x_proj.index_select(0, ids.reshape(-1)).double()[keep]
+    Qp = Q.double().repeat_interleave(kk, 0)[keep]
+    # suffix sums over dims [e, d): reverse cumulative sums
+    xq = (X * Qp).flip(-1).cumsum(-1).flip(-1)
+    xx = (X * X).flip(-1).cumsum(-1).flip(-1)
+    qq = (Qp * Qp).flip(-1).cumsum(-1).flip(-1)
+    coef, cos_q = [], []
+    for _, e in step_schedule(d, initial_step):
+        if e >= d:
+            coef.append(0.0)  # no residual left: the estimate is the distance
+            cos_q.append(1.0)
+            continue
+        den = (xx[:, e] * qq[:, e]).sqrt()
+        ok = den > 0
+        c = float(torch.quantile((xq[ok, e] / den[ok]).float(), quantile).item()) \
+            if int(ok.sum()) else 1.0
+        cos_q.append(c)
+        coef.append(float(np.float32(2.0 * max(-1.0, min(1.0, multiplier * c)))))
+    return BsaPruner(coef=tuple(coef), d=d, initial_step=initial_step, quantile=quantile,
+                     multiplier=multiplier, cosines=tuple(cos_q))
+
 
 
 class OrderCriteria(str, Enum):

@@ -176,15 +176,15 @@ def make_params(params: SearchParams, d: int, warps=0, device=None) -> _lib.PdxS
     ring_slots]); 0 = auto."""
     ads = params.ads if params.ads is not None else AdsPruner(d=d)
     w, tpw, rb = (tuple(warps) + (0, 0))[:3] if isinstance(warps, tuple) else (warps, 0, 0)
-    beta = None
+    coef = None
     if params.pruner == "bsa":
         if params.bsa.d != d:
             raise ValueError(f"the BsaPruner was fitted for d={params.bsa.d}, not {d}")
-        beta = params.bsa.device_beta(device if device is not None else "cuda")
+        coef = params.bsa.device_coef(device if device is not None else "cuda")
     return _lib.PdxSearchParams(int(params.k), _lib.METRIC[Metric(params.metric).value],
                                 _lib.PRUNER[params.pruner], int(params.initial_step),
                                 float(params.selection_fraction), int(ads.d), int(w),
-                                float(ads.epsilon0), int(tpw), int(rb), _lib.ptr(beta))
+                                float(ads.epsilon0), int(tpw), int(rb), _lib.ptr(coef))
 
 
 def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None, orders=None,
@@ -233,6 +233,8 @@ def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None,
     if work is None or work.numel() < wb:
         work = torch.empty((wb,), dtype=torch.uint8, device=dev)
         out["work"] = work
+    if params.pruner == "bsa":
+        store.ensure_bsa_residuals(params.initial_step)
     p = make_params(params, store.d, warps, dev)
     sb = None if seg_bucket is None else seg_bucket.contiguous()
     st = _lib.stream_handle()

@@ -103,6 +103,26 @@ class DeviceStore:
     def ref(self):
         return C.byref(self.c)
 
+    def ensure_bsa_residuals(self, initial_step: int):
+        """Residual energies for the BSA pruner (pdx_bsa_residuals), computed
+        once per step schedule and attached to the ABI view."""
+        torch = _torch()
+        cache = self.__dict__.setdefault("_resid", {})
+        if initial_step not in cache:
+            n = C.c_int32(0)
+            _lib.check(_lib.lib().pdx_bsa_residuals(self.ref, int(initial_step), None,
+                                                   C.byref(n), _lib.stream_handle()))
+            buf = torch.empty((max(1, self.ntiles), n.value, 64), dtype=torch.float32,
+                              device=self.tiles.device)
+            _lib.check(_lib.lib().pdx_bsa_residuals(self.ref, int(initial_step), _lib.ptr(buf),
+                                                   C.byref(n), _lib.stream_handle()))
+            cache[initial_step] = (buf, n.value)
+        buf, n = cache[initial_step]
+        self.c.d_resid = _lib.ptr(buf)
+        self.c.resid_steps = n
+        self.c.resid_initial_step = int(initial_step)
+        return buf
+
     @property
     def nbytes(self) -> int:
         return self.tiles.numel() * 4 + self.tile_ids.numel() * 8

@@ -329,36 +329,61 @@ def _bsa_setup(P, n=100_000, d=96, nq=48):
     return x, Q, xr, qr
 
 
-@pytest.mark.parametrize("quantile,multiplier", [(0.99, 1.0), (0.9, 1.0), (0.5, 0.8)])
+@pytest.mark.parametrize("quantile,multiplier", [(0.99, 1.0), (0.9, 1.0), (0.5, 0.7)])
 def test_ivf_bsa_vs_oracle(P, oracle, quantile, multiplier):
-    """Learned factors (aggressive ones included): results, every decision and
-    the stats equal the oracle's BSA restatement."""
+    """Learned coefficients (aggressive ones included): results, every
+    decision and the stats equal the oracle's BSA restatement."""
     import torch
     x, Q, xr, qr = _bsa_setup(P)
     bsa = P.fit_bsa(torch.from_numpy(xr).cuda(), quantile=quantile, multiplier=multiplier)
-    assert bsa.beta[-1] == 1.0 and all(0 < b <= 1 for b in bsa.beta)
+    assert bsa.coef[-1] == 0.0 and len(bsa.coef) == len(P.step_schedule(96, 2))
     index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=128, seed=0)
     params = P.SearchParams(k=10, pruner="bsa", bsa=bsa)
     out = P.ivf_search_batch(index, qr, params, 16, trace=True)
     ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, 10, 16, pruner="bsa",
-                                  bsa_beta=np.asarray(bsa.beta), survivors_cap=1 << 18)
+                                  bsa_coef=np.asarray(bsa.coef, np.float32),
+                                  survivors_cap=1 << 18)
     np.testing.assert_array_equal(out["ids"], ref["ids"])
     np.testing.assert_array_equal(out["dist"], ref["dist"])
     np.testing.assert_array_equal(out["touched"], ref["touched"])
     assert out["survivors"] == ref["survivor_lists"]
 
 
-def test_bsa_unit_factors_equal_bond(P, oracle):
-    """beta = 1 at every step is exactly the BOND comparison acc < T."""
+@pytest.mark.parametrize("group", [1, 8])
+def test_bsa_exact_bound_and_residuals(P, oracle, group):
+    """coef = 2 is the Cauchy-Schwarz bound: BOND's results with fewer values
+    touched; the store's residual energies equal the sequential host sums."""
+    import torch
     x, Q, xr, qr = _bsa_setup(P, n=30_000, d=64, nq=32)
     nsteps = len(P.step_schedule(64, 2))
-    bsa = P.BsaPruner(beta=(1.0,) * nsteps, d=64)
-    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=64, seed=0)
+    bsa = P.BsaPruner(coef=(2.0,) * nsteps, d=64)
+    col = P.VectorCollection.from_array(xr)
+    index = P.ivf_build(col, nlist=64, seed=0, group=group)
     a = P.ivf_search_batch(index, qr, P.SearchParams(k=10, pruner="bsa", bsa=bsa), 8, trace=True)
     b = P.ivf_search_batch(index, qr, P.SearchParams(k=10, pruner="bond"), 8, trace=True)
-    for key in ("ids", "dist", "touched"):
-        np.testing.assert_array_equal(a[key], b[key])
-    assert a["survivors"] == b["survivors"]
+    np.testing.assert_array_equal(a["ids"], b["ids"])
+    np.testing.assert_array_equal(a["dist"], b["dist"])
+    assert (a["touched"] <= b["touched"]).all() and a["touched"].sum() < b["touched"].sum()
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, 10, 8, pruner="bsa",
+                                  bsa_coef=np.full(nsteps, 2.0, np.float32),
+                                  survivors_cap=1 << 18)
+    assert a["survivors"] == ref["survivor_lists"]
+    st = index.store
+    resid = st.ensure_bsa_residuals(2).cpu().numpy()
+    ids = st.tile_ids.cpu().numpy().reshape(-1, 64)
+    ends = [e for _, e in P.step_schedule(64, 2)]
+    rng = np.random.default_rng(0)
+    for t in rng.integers(0, st.ntiles, 6):
+        for i in range(64):
+            if ids[t, i] < 0:
+                continue
+            row = xr[ids[t, i]]
+            for s, e in enumerate(ends):
+                r = np.float32(0)
+                for v in row[e:]:
+                    r = np.float32(r + np.float32(v * v))
+                assert resid[t, s, i] == r
+    del torch
 
 
 def test_bsa_estimator_recall(P):
@@ -376,5 +401,5 @@ def test_bsa_estimator_recall(P):
         rec = float(np.mean([P.recall_at_k(gt.ids[i], ids[i], 10) for i in range(len(Q))]))
         stats[pruner] = (rec, int(out["touched"].sum()))
     assert stats["bond"][0] == 1.0
-    assert stats["bsa"][0] >= 0.97
-    assert stats["bsa"][1] < stats["bond"][1]
+    assert stats["bsa"][0] >= 0.97, stats
+    assert stats["bsa"][1] < stats["bond"][1], stats

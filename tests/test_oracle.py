@@ -172,19 +172,49 @@ def test_orthogonal_matches_reference(golden, d, seed):
     np.testing.assert_array_equal(generate_orthogonal(d, seed).matrix, arrays[f"orth_{d}_{seed}"])
 
 
-def test_oracle_bsa_unit_factors_equal_bond(oracle):
-    """BSA (this build's restatement) with beta = 1 everywhere is
-    the BOND comparison; smaller factors prune at least as much."""
+def test_oracle_bsa_matches_host_restatement(oracle):
+    """BSA (this build's restatement): the C oracle's per-step
+    survivors equal a direct host evaluation of the estimate; coef = 2 (the
+    Cauchy-Schwarz bound) keeps BOND's results."""
+    from paper_2503_04422_b200.pruning import bsa_estimate
+    from paper_2503_04422_b200.search import step_schedule
     rng = np.random.default_rng(5)
-    x = rng.standard_normal((3000, 32)).astype(np.float32)
-    q = rng.standard_normal(32).astype(np.float32)
-    blocks = to_blocks(VectorCollection.from_array(x), 256, pad=False)
-    n = len(oracle.step_schedule(32, 2))
-    a, sa = oracle.search(blocks, q, 10, pruner="bsa", bsa_beta=np.ones(n))
-    b, sb = oracle.search(blocks, q, 10, pruner="bond")
-    assert a == b and sa == sb
-    beta = np.linspace(0.2, 1.0, n)
-    c, sc = oracle.search(blocks, q, 10, pruner="bsa", bsa_beta=beta)
-    assert sc["values_touched"] <= sb["values_touched"]
+    d = 16
+    x = (rng.standard_normal((600, d)) * np.linspace(3, 0.2, d)).astype(np.float32)
+    q = (x[7] + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    blocks = to_blocks(VectorCollection.from_array(x), 64, pad=False)
+    sched = step_schedule(d, 2)
+    coef = np.array([1.6, 1.2, 0.8, 0.0][:len(sched)], np.float32)
+    items, st = oracle.search(blocks, q, 5, pruner="bsa", bsa_coef=coef)
+    # host replay of the same block-synchronous pass
+    import heapq
+    heap, trace = [], []
+    for bi, blk in enumerate(blocks):
+        m = blk.ids.shape[0]
+        acc = np.zeros(m, np.float32)
+        T = np.inf if len(heap) < 5 else -heap[0][0]
+        pos = list(range(m))
+        linear = bi == 0 or T == np.inf
+        rec = []
+        for s, (a, b) in enumerate(sched):
+            for j in range(a, b):
+                t = (q[j] - blk.data[j, :m]).astype(np.float32)
+                acc = (acc + (t * t).astype(np.float32)).astype(np.float32)
+            if not linear:
+                pos = [i for i in pos if bsa_estimate(acc[i], blk.data[:, i], q, b, coef[s]) < T]
+                rec.append(len(pos))
+        trace.append([m] if linear else rec)
+        for i in (range(m) if linear else pos):
+            key = (-float(acc[i]), -int(blk.ids[i]))
+            if len(heap) < 5:
+                heapq.heappush(heap, key)
+            elif key > heap[0]:
+                heapq.heapreplace(heap, key)
+    want = sorted((-a, -b) for a, b in heap)
+    assert [(np.float32(dv), i) for dv, i in items] == [(np.float32(dv), i) for dv, i in want]
+    n = len(sched)
+    a, sa = oracle.search(blocks, q, 5, pruner="bsa", bsa_coef=np.full(n, 2.0, np.float32))
+    b, sb = oracle.search(blocks, q, 5, pruner="bond")
+    assert a == b and sa["values_touched"] <= sb["values_touched"]
     with pytest.raises(ValueError):
-        oracle.search(blocks, q, 10, pruner="bsa")
+        oracle.search(blocks, q, 5, pruner="bsa")
