@@ -38,6 +38,8 @@ extern "C" {
 #define PDX_EINVAL 1    /* bad argument (Python: ValueError) */
 #define PDX_ECUDA 2     /* CUDA runtime / launch failure */
 #define PDX_ENOSUPPORT 3 /* size outside what this build supports */
+#define PDX_EFORMAT 4   /* file does not follow the byte layout (Python: FormatError) */
+#define PDX_EIO 5       /* open / read / write failure (Python: OSError) */
 
 /* Metric (kernels.py:22-25) */
 #define PDX_METRIC_L2 0
@@ -258,6 +260,59 @@ int pdx_segment_means(const float* d_x, int32_t d, const int64_t* d_rows, const 
  */
 int pdx_ground_truth(const float* d_x, int64_t n, int32_t d, const float* d_queries, int64_t nq,
                      int32_t k, int32_t metric, int64_t* d_ids, double* d_dist, void* stream);
+
+/*
+ * .pdx store interchange, HBM <-> file (storage.py:115-194 of the reference;
+ * cli.py:35-76 writes it).  Byte layout, all little-endian:
+ *   header "<8sIIQIIII": magic "PDXv1\0\0\0", version 1, flags (1 = rotation,
+ *     2 = IVF section), n, d, block_size, block_count, reserved
+ *   global means f64 [d]
+ *   [flags & 1] transform seed u64, rotation f32 [d][d]
+ *   block_count x { m u32, m_padded u32, ids i64 [m], data f32 [d][m_padded] }
+ *   [flags & 2] nlist u32, training seed u64, centroids f32 [nlist][d],
+ *     bucket offsets u32 [nlist+1] (into the block list), bucket means f64 [nlist][d]
+ * Block b becomes ceil(m/64) consecutive tiles of the store (pdx_store); the
+ * dims beyond d and slots beyond m are zero.  Saving a loaded store writes
+ * the same bytes back.
+ */
+typedef struct pdx_file_info {
+  int64_t n;              /* vectors (header) */
+  int32_t d;
+  int32_t block_size;
+  int64_t nblocks;
+  int32_t flags;
+  int32_t nlist;          /* 0 without an IVF section */
+  uint64_t transform_seed;
+  uint64_t training_seed;
+  int64_t ntiles;         /* sum over blocks of ceil(m/64) */
+  int64_t max_block_bytes; /* largest block record's data, d * m_padded * 4 */
+} pdx_file_info;
+
+/* Walks the file's sections (no data read) and validates its framing:
+ * bad magic / version, truncation, header n vs the blocks' total. */
+int pdx_file_probe(const char* path, pdx_file_info* info);
+
+/* Streams the blocks of `path` into the tile layout of a store with `group`
+ * (1 or 8) on `stream`: d_tiles f32 [ntiles][d_pad/group][64][group] (d_pad =
+ * d rounded up to group), d_tile_ids i64 [ntiles][64] (-1 padding).  Host
+ * outputs: h_block_m / h_block_mpad i32 [nblocks]; h_global_means f64 [d];
+ * h_transform f32 [d][d] (flags & 1); h_centroids f32 [nlist][d],
+ * h_bucket_offsets i64 [nlist+1], h_bucket_means f64 [nlist][d] (flags & 2).
+ * Returns after the device copies complete. */
+int pdx_file_load(const char* path, const pdx_file_info* info, int32_t group, float* d_tiles,
+                  int64_t* d_tile_ids, int32_t* h_block_m, int32_t* h_block_mpad,
+                  double* h_global_means, float* h_transform, float* h_centroids,
+                  int64_t* h_bucket_offsets, double* h_bucket_means, void* stream);
+
+/* Writes `store` (its logical blocks in order) as a .pdx file.  h_block_mpad
+ * i32 [nblocks] (NULL: m_padded = m); h_transform NULL = no rotation
+ * section; nlist 0 = no IVF section (else h_bucket_offsets i64 [nlist+1] are
+ * logical-block offsets). */
+int pdx_file_save(const char* path, const pdx_store* store, int32_t block_size,
+                  const int32_t* h_block_mpad, const double* h_global_means,
+                  const float* h_transform, uint64_t transform_seed, int32_t nlist,
+                  uint64_t training_seed, const float* h_centroids,
+                  const int64_t* h_bucket_offsets, const double* h_bucket_means, void* stream);
 
 #ifdef __cplusplus
 }

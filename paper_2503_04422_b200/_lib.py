@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libpdx_b200.so"
 CSRC = PKG / "csrc"
 
-PDX_OK, PDX_EINVAL, PDX_ECUDA, PDX_ENOSUPPORT = 0, 1, 2, 3
+PDX_OK, PDX_EINVAL, PDX_ECUDA, PDX_ENOSUPPORT, PDX_EFORMAT, PDX_EIO = 0, 1, 2, 3, 4, 5
 METRIC = {"l2": 0, "l1": 1, "ip": 2}
 PRUNER = {"none": 0, "ads": 1, "bond": 2, "bsa": 3}
 CRITERIA = {"sequential": 0, "decreasing": 1, "dmeans": 2, "zones": 3}
@@ -25,7 +25,7 @@ TILE = 64
 EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_tiles",
            "pdx_project", "pdx_select_buckets", "pdx_dimension_orders", "pdx_search_workspace",
            "pdx_search", "pdx_merge_topk", "pdx_segment_means", "pdx_ground_truth",
-           "pdx_bsa_residuals")
+           "pdx_bsa_residuals", "pdx_file_probe", "pdx_file_load", "pdx_file_save")
 
 
 class PdxStore(C.Structure):
@@ -45,6 +45,13 @@ class PdxSearchParams(C.Structure):
                 ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
                 ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32),
                 ("bsa_coef", C.c_void_p)]
+
+
+class PdxFileInfo(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("block_size", C.c_int32),
+                ("nblocks", C.c_int64), ("flags", C.c_int32), ("nlist", C.c_int32),
+                ("transform_seed", C.c_uint64), ("training_seed", C.c_uint64),
+                ("ntiles", C.c_int64), ("max_block_bytes", C.c_int64)]
 
 
 class PdxSearchOut(C.Structure):
@@ -93,6 +100,10 @@ def lib():
         L.pdx_segment_means.argtypes = [vp, i32, vp, vp, i32, vp, vp]
         L.pdx_ground_truth.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp]
         L.pdx_bsa_residuals.argtypes = [vp, i32, vp, vp, vp]
+        L.pdx_file_probe.argtypes = [C.c_char_p, vp]
+        L.pdx_file_load.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pdx_file_save.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, C.c_uint64, i32,
+                                    C.c_uint64, vp, vp, vp, vp]
         for name in EXPORTS:
             getattr(L, name).restype = getattr(L, name).restype or C.c_int
         if L.pdx_abi_version() != 2:
@@ -116,6 +127,11 @@ def check(rc: int):
         raise ValueError(msg)
     if rc == PDX_ENOSUPPORT:
         raise NotImplementedError(msg)
+    if rc == PDX_EFORMAT:
+        from .storage import FormatError
+        raise FormatError(msg)
+    if rc == PDX_EIO:
+        raise OSError(msg)
     raise RuntimeError(f"CUDA failure in libpdx_b200: {msg}")
 
 
