@@ -314,6 +314,66 @@ int pdx_file_save(const char* path, const pdx_store* store, int32_t block_size,
                   uint64_t training_seed, const float* h_centroids,
                   const int64_t* h_bucket_offsets, const double* h_bucket_means, void* stream);
 
+/*
+ * Owning index handle + one-call search: the drop-in boundary a C / C++ /
+ * FFI caller binds.  It replaces the estimators' fit /
+ * kneighbors pair (estimators.py:54-76, :99-132) and ivf_search /
+ * exact_search (index.py:130-191) for a whole query batch, chaining the
+ * kernels above inside the library: query projection (K3), bucket
+ * selection (K2), dimension orders (K4), the pruned scan with top-k (K5/K6).
+ * A handle is not thread-safe; calls are ordered on `stream`.
+ */
+typedef struct pdx_index pdx_index;
+
+typedef struct pdx_index_desc {
+  /* Either borrow a device store (kept alive by the caller) ... */
+  const pdx_store* store;
+  /* ... or upload host blocks (store == NULL), the reference's Block list:
+   * block b holds block_m[b] vectors in a [d][block_mpad[b]] image. */
+  int32_t d;
+  int32_t group;              /* tile layout: 1 or 8 (0 = 8) */
+  int64_t nblocks;
+  const float* blocks;        /* images back to back, block order */
+  const int32_t* block_m;
+  const int32_t* block_mpad;  /* NULL: m_padded = m */
+  const int64_t* ids;         /* block_m[b] ids per block, back to back */
+  /* metadata (host) */
+  const double* global_means; /* [d]: exact_search's order means (NULL: zeros) */
+  const float* rotation;      /* [d][d] or NULL: queries are projected q @ R^T first */
+  int32_t nlist;              /* 0: flat (exact_search over all blocks) */
+  const float* centroids;     /* [nlist][d] */
+  const int64_t* bucket_offsets; /* [nlist+1] into the blocks (ignored when borrowing) */
+  const double* bucket_means; /* [nlist][d] */
+} pdx_index_desc;
+
+int pdx_index_create(const pdx_index_desc* desc, pdx_index** out);
+/* Opens a .pdx file (pdx_file_load) into a new handle. */
+int pdx_index_open(const char* path, int32_t group, pdx_index** out);
+int pdx_index_destroy(pdx_index* index);
+
+typedef struct pdx_query_params {
+  int32_t k;
+  int32_t metric;            /* PDX_METRIC_* */
+  int32_t pruner;            /* PDX_PRUNER_* */
+  int32_t criteria;          /* PDX_ORDER_* (BOND only) */
+  int32_t zone_width;        /* <= 0: default */
+  int32_t nprobe;            /* IVF only */
+  double selection_fraction;
+  int32_t initial_step;
+  int32_t rotate;            /* 1: project queries with the index rotation */
+  double epsilon0;
+  const float* bsa_coef;     /* host float32 [nsteps] (pruner BSA) */
+  int32_t queries_on_device; /* Q is a device pointer */
+  int32_t outputs_on_device; /* out_* are device pointers */
+} pdx_query_params;
+
+/* Searches nq queries Q [nq][d]; out_dist/out_ids [nq][k] as pdx_search
+ * (ascending (distance, id), +inf / -1 padding, IP negated); out_touched /
+ * out_total [nq] optional (NULL).  Host outputs are complete on return. */
+int pdx_index_search(pdx_index* index, const pdx_query_params* params, const float* Q,
+                     int64_t nq, float* out_dist, int64_t* out_ids, int64_t* out_touched,
+                     int64_t* out_total, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

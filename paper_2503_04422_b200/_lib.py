@@ -25,7 +25,8 @@ TILE = 64
 EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_tiles",
            "pdx_project", "pdx_select_buckets", "pdx_dimension_orders", "pdx_search_workspace",
            "pdx_search", "pdx_merge_topk", "pdx_segment_means", "pdx_ground_truth",
-           "pdx_bsa_residuals", "pdx_file_probe", "pdx_file_load", "pdx_file_save")
+           "pdx_bsa_residuals", "pdx_file_probe", "pdx_file_load", "pdx_file_save",
+           "pdx_index_create", "pdx_index_open", "pdx_index_destroy", "pdx_index_search")
 
 
 class PdxStore(C.Structure):
@@ -52,6 +53,22 @@ class PdxFileInfo(C.Structure):
                 ("nblocks", C.c_int64), ("flags", C.c_int32), ("nlist", C.c_int32),
                 ("transform_seed", C.c_uint64), ("training_seed", C.c_uint64),
                 ("ntiles", C.c_int64), ("max_block_bytes", C.c_int64)]
+
+
+class PdxIndexDesc(C.Structure):
+    _fields_ = [("store", C.c_void_p), ("d", C.c_int32), ("group", C.c_int32),
+                ("nblocks", C.c_int64), ("blocks", C.c_void_p), ("block_m", C.c_void_p),
+                ("block_mpad", C.c_void_p), ("ids", C.c_void_p), ("global_means", C.c_void_p),
+                ("rotation", C.c_void_p), ("nlist", C.c_int32), ("centroids", C.c_void_p),
+                ("bucket_offsets", C.c_void_p), ("bucket_means", C.c_void_p)]
+
+
+class PdxQueryParams(C.Structure):
+    _fields_ = [("k", C.c_int32), ("metric", C.c_int32), ("pruner", C.c_int32),
+                ("criteria", C.c_int32), ("zone_width", C.c_int32), ("nprobe", C.c_int32),
+                ("selection_fraction", C.c_double), ("initial_step", C.c_int32),
+                ("rotate", C.c_int32), ("epsilon0", C.c_double), ("bsa_coef", C.c_void_p),
+                ("queries_on_device", C.c_int32), ("outputs_on_device", C.c_int32)]
 
 
 class PdxSearchOut(C.Structure):
@@ -101,6 +118,10 @@ def lib():
         L.pdx_ground_truth.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp]
         L.pdx_bsa_residuals.argtypes = [vp, i32, vp, vp, vp]
         L.pdx_file_probe.argtypes = [C.c_char_p, vp]
+        L.pdx_index_create.argtypes = [vp, vp]
+        L.pdx_index_open.argtypes = [C.c_char_p, i32, vp]
+        L.pdx_index_destroy.argtypes = [vp]
+        L.pdx_index_search.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp]
         L.pdx_file_load.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.pdx_file_save.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, C.c_uint64, i32,
                                     C.c_uint64, vp, vp, vp, vp]

@@ -1,0 +1,360 @@
+// Owning index handle + one-call batched search (the C boundary of
+// SURVEY.md §8(b); replaces estimators.py:54-132's fit/kneighbors and
+// index.py:130-191's ivf_search / exact_search for a query batch).
+//
+// The handle keeps the store and its metadata resident in HBM and grows one
+// set of device scratch buffers; a search is a fixed chain of stream-ordered
+// launches — K3 projection, K2 bucket selection, K4 orders, K5/K6 scan —
+// with the host<->device copies at its ends, so a caller with host buffers
+// pays one C call per batch.
+#include <cmath>
+#include <vector>
+
+#include "pdx_common.cuh"
+#include "pdx_upload.cuh"
+
+namespace pdx {
+namespace {
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  int need(size_t count) {
+    if (count <= n) return PDX_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    PDX_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+    n = count;
+    return PDX_OK;
+  }
+  int upload(const T* h, size_t count, cudaStream_t st) {
+    PDX_TRY(need(count));
+    if (count)
+      PDX_CUDA_CHECK(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    return PDX_OK;
+  }
+};
+
+int schedule_len(int d, int initial_step) {
+  int n = 0;
+  for (int64_t e = 0, w = initial_step; e < d; w *= 2, ++n) e = e + w < d ? e + w : d;
+  return n;
+}
+
+}  // namespace
+}  // namespace pdx
+
+using namespace pdx;
+
+struct pdx_index {
+  pdx_store st{};
+  int32_t d = 0, nlist = 0;
+  // owned store arrays (empty when borrowing)
+  DevBuf<float> tiles;
+  DevBuf<int64_t> tile_ids, block_tile, bucket_block;
+  DevBuf<int32_t> block_m, tile_block;
+  // metadata
+  DevBuf<float> centroids, rotation;
+  DevBuf<double> bucket_means, global_means;
+  bool has_rotation = false;
+  // BSA residual energies (per initial_step)
+  DevBuf<float> resid;
+  int32_t resid_step = -1;
+  // per-search scratch
+  DevBuf<float> q, qr, scratch, dist, coef;
+  DevBuf<int32_t> sel, count;
+  DevBuf<uint16_t> orders;
+  DevBuf<int64_t> ids, touched, total;
+  DevBuf<unsigned char> work;
+};
+
+namespace {
+
+// Fill st's derived fields from host block_tile / bucket offsets.
+int finish_store(pdx_index* I, const std::vector<int64_t>& btile, const std::vector<int32_t>& bm,
+                 const std::vector<int64_t>& boff, int group, cudaStream_t st) {
+  const int64_t nb = (int64_t)bm.size(), nt = btile.back();
+  std::vector<int32_t> tblk((size_t)nt);
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t t = btile[b]; t < btile[b + 1]; ++t) tblk[t] = (int32_t)b;
+  PDX_TRY(I->block_tile.upload(btile.data(), btile.size(), st));
+  PDX_TRY(I->block_m.upload(bm.data(), bm.size(), st));
+  PDX_TRY(I->bucket_block.upload(boff.data(), boff.size(), st));
+  PDX_TRY(I->tile_block.upload(tblk.data(), tblk.size(), st));
+  int32_t mbb = 0, mbt = 0;
+  for (size_t c = 0; c + 1 < boff.size(); ++c) {
+    const int64_t b0 = boff[c], b1 = boff[c + 1];
+    if (b1 - b0 > mbb) mbb = (int32_t)(b1 - b0);
+    if (btile[b1] - btile[b0] > mbt) mbt = (int32_t)(btile[b1] - btile[b0]);
+  }
+  pdx_store& s = I->st;
+  s.d = I->d;
+  s.group = group;
+  s.d_pad = group == 8 ? (I->d + 7) / 8 * 8 : I->d;
+  s.nbuckets = (int32_t)boff.size() - 1;
+  s.ntiles = nt;
+  s.nblocks = nb;
+  s.d_tiles = I->tiles.p;
+  s.d_tile_ids = I->tile_ids.p;
+  s.d_block_tile = I->block_tile.p;
+  s.d_block_m = I->block_m.p;
+  s.d_bucket_block = I->bucket_block.p;
+  s.max_bucket_blocks = mbb;
+  s.max_bucket_tiles = mbt;
+  s.d_tile_block = I->tile_block.p;
+  PDX_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PDX_OK;
+}
+
+int set_metadata(pdx_index* I, const double* global_means, const float* rotation, int32_t nlist,
+                 const float* centroids, const double* bucket_means, cudaStream_t st) {
+  const size_t d = (size_t)I->d;
+  std::vector<double> zeros(d, 0.0);
+  PDX_TRY(I->global_means.upload(global_means ? global_means : zeros.data(), d, st));
+  I->has_rotation = rotation != nullptr;
+  if (rotation) PDX_TRY(I->rotation.upload(rotation, d * d, st));
+  I->nlist = nlist;
+  if (nlist) {
+    PDX_REQUIRE(centroids && bucket_means, "IVF index needs centroids and bucket means");
+    PDX_TRY(I->centroids.upload(centroids, (size_t)nlist * d, st));
+    PDX_TRY(I->bucket_means.upload(bucket_means, (size_t)nlist * d, st));
+  }
+  PDX_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PDX_OK;
+}
+
+}  // namespace
+
+extern "C" int pdx_index_create(const pdx_index_desc* D, pdx_index** out) {
+  PDX_REQUIRE(D && out, "pdx_index_create: null argument");
+  *out = nullptr;
+  pdx_index* I = new pdx_index();
+  struct Guard {
+    pdx_index*& I;
+    ~Guard() { delete I; }
+  } guard{I};
+  cudaStream_t st = nullptr;
+  if (D->store) {
+    I->st = *D->store;
+    I->d = D->store->d;
+    PDX_REQUIRE(D->nlist == 0 || D->nlist == D->store->nbuckets,
+                "nlist %d does not match the store's %d buckets", D->nlist, D->store->nbuckets);
+  } else {
+    const int group = D->group ? D->group : 8;
+    PDX_REQUIRE(group == 1 || group == 8, "group must be 1 or 8");
+    PDX_REQUIRE(D->d >= 1 && D->d <= 65535, "dimensionality %d unsupported", D->d);
+    PDX_REQUIRE(D->nblocks >= 0 && (D->nblocks == 0 || (D->blocks && D->block_m && D->ids)),
+                "pdx_index_create: block arrays required");
+    I->d = D->d;
+    const int64_t nb = D->nblocks, d = D->d;
+    std::vector<int64_t> btile((size_t)nb + 1, 0);
+    int64_t maxb = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t m = D->block_m[b], mp = D->block_mpad ? D->block_mpad[b] : m;
+      PDX_REQUIRE(m >= 0 && mp >= m, "block %lld: bad m / m_padded", (long long)b);
+      btile[b + 1] = btile[b] + (m + kTile - 1) / kTile;
+      if (4 * d * mp > maxb) maxb = 4 * d * mp;
+    }
+    const int d_pad = group == 8 ? (int)((d + 7) / 8 * 8) : (int)d;
+    PDX_TRY(I->tiles.need((size_t)btile[nb] * d_pad * kTile));
+    PDX_TRY(I->tile_ids.need((size_t)btile[nb] * kTile));
+    struct MemSrc {
+      const pdx_index_desc* D;
+      int64_t d, img = 0, id = 0;
+      int head(int64_t b, uint32_t* mm) {
+        mm[0] = (uint32_t)D->block_m[b];
+        mm[1] = (uint32_t)(D->block_mpad ? D->block_mpad[b] : D->block_m[b]);
+        return PDX_OK;
+      }
+      int body(int64_t, int64_t m, int64_t floats, int64_t* ids, float* data) {
+        memcpy(ids, D->ids + id, 8 * m);
+        memcpy(data, D->blocks + img, 4 * floats);
+        id += m;
+        img += floats;
+        return PDX_OK;
+      }
+    } src{D, d};
+    std::vector<int32_t> bm((size_t)(nb ? nb : 1)), bmp((size_t)(nb ? nb : 1));
+    PDX_TRY(upload_blocks(src, nb, d, group, maxb, I->tiles.p, I->tile_ids.p, bm.data(),
+                          bmp.data(), st));
+    bm.resize((size_t)nb);
+    std::vector<int64_t> boff;
+    if (D->nlist) {
+      PDX_REQUIRE(D->bucket_offsets, "IVF index needs bucket offsets");
+      boff.assign(D->bucket_offsets, D->bucket_offsets + D->nlist + 1);
+      PDX_REQUIRE(boff[0] == 0 && boff.back() == nb, "bucket offsets must span the blocks");
+      for (int c = 0; c < D->nlist; ++c)
+        PDX_REQUIRE(boff[c] <= boff[c + 1], "bucket offsets must not decrease");
+    } else {
+      boff = {0, nb};
+    }
+    PDX_TRY(finish_store(I, btile, bm, boff, group, st));
+  }
+  PDX_TRY(set_metadata(I, D->global_means, D->rotation, D->nlist, D->centroids,
+                       D->bucket_means, st));
+  *out = I;
+  I = nullptr;  // released from the guard
+  return PDX_OK;
+}
+
+extern "C" int pdx_index_open(const char* path, int32_t group, pdx_index** out) {
+  PDX_REQUIRE(path && out, "pdx_index_open: null argument");
+  PDX_REQUIRE(group == 1 || group == 8, "group must be 1 or 8");
+  *out = nullptr;
+  pdx_file_info info;
+  PDX_TRY(pdx_file_probe(path, &info));
+  pdx_index* I = new pdx_index();
+  struct Guard {
+    pdx_index*& I;
+    ~Guard() { delete I; }
+  } guard{I};
+  const int64_t d = info.d, nb = info.nblocks, nl = info.nlist;
+  I->d = info.d;
+  const int d_pad = group == 8 ? (int)((d + 7) / 8 * 8) : (int)d;
+  PDX_TRY(I->tiles.need((size_t)info.ntiles * d_pad * kTile));
+  PDX_TRY(I->tile_ids.need((size_t)info.ntiles * kTile));
+  std::vector<int32_t> bm((size_t)(nb ? nb : 1)), bmp((size_t)(nb ? nb : 1));
+  std::vector<double> gm((size_t)d), bmeans((size_t)(nl ? nl : 1) * d);
+  std::vector<float> rot((info.flags & 1) ? (size_t)(d * d) : 1), cent((size_t)(nl ? nl : 1) * d);
+  std::vector<int64_t> boff((size_t)nl + 1);
+  PDX_TRY(pdx_file_load(path, &info, group, I->tiles.p, I->tile_ids.p, bm.data(), bmp.data(),
+                        gm.data(), rot.data(), cent.data(), boff.data(), bmeans.data(), nullptr));
+  bm.resize((size_t)nb);
+  std::vector<int64_t> btile((size_t)nb + 1, 0);
+  for (int64_t b = 0; b < nb; ++b) btile[b + 1] = btile[b] + (bm[b] + kTile - 1) / kTile;
+  if (!nl) boff = {0, nb};
+  PDX_TRY(finish_store(I, btile, bm, boff, group, nullptr));
+  PDX_TRY(set_metadata(I, gm.data(), (info.flags & 1) ? rot.data() : nullptr, (int32_t)nl,
+                       cent.data(), bmeans.data(), nullptr));
+  *out = I;
+  I = nullptr;
+  return PDX_OK;
+}
+
+extern "C" int pdx_index_destroy(pdx_index* index) {
+  if (index) {
+    cudaDeviceSynchronize();  // no search may still read its buffers
+    delete index;
+  }
+  return PDX_OK;
+}
+
+extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const float* Q,
+                                int64_t nq, float* out_dist, int64_t* out_ids,
+                                int64_t* out_touched, int64_t* out_total, void* stream) {
+  PDX_REQUIRE(I && P, "pdx_index_search: null argument");
+  PDX_REQUIRE(nq >= 0, "bad query count");
+  if (nq == 0) return PDX_OK;
+  PDX_REQUIRE(Q && out_dist && out_ids, "pdx_index_search: null query / output pointer");
+  PDX_REQUIRE(P->k >= 1, "k must be >= 1");
+  PDX_REQUIRE(!P->rotate || I->has_rotation, "the index carries no rotation matrix");
+  const int64_t d = I->d, k = P->k;
+  cudaStream_t st = as_stream(stream);
+  const bool ivf = I->nlist > 0;
+  if (ivf) PDX_REQUIRE(P->nprobe >= 1 && P->nprobe <= I->nlist, "nprobe must be in [1, %d], got %d",
+                       I->nlist, P->nprobe);
+  const int32_t nseg = ivf ? P->nprobe : 1;
+
+  // queries -> device, projected
+  const float* dq = Q;
+  if (!P->queries_on_device) {
+    PDX_TRY(I->q.upload(Q, (size_t)(nq * d), st));
+    dq = I->q.p;
+  }
+  if (P->rotate) {
+    PDX_TRY(I->qr.need((size_t)(nq * d)));
+    PDX_TRY(pdx_project(dq, nq, (int32_t)d, I->rotation.p, I->qr.p, st));
+    dq = I->qr.p;
+  }
+  // bucket selection
+  const int32_t* sel = nullptr;
+  if (ivf) {
+    PDX_TRY(I->scratch.need((size_t)(nq * I->nlist)));
+    PDX_TRY(I->sel.need((size_t)(nq * nseg)));
+    PDX_TRY(pdx_select_buckets(dq, nq, (int32_t)d, I->centroids.p, I->nlist, P->metric, nseg,
+                               I->scratch.p, I->sel.p, st));
+    sel = I->sel.p;
+  }
+  // visit orders (BOND with a query-aware criterion)
+  const uint16_t* orders = nullptr;
+  int64_t oqs = 0, oss = 0;
+  if (P->pruner == PDX_PRUNER_BOND && P->criteria != PDX_ORDER_SEQUENTIAL) {
+    const int32_t nsets = ivf ? nseg : 1;
+    PDX_TRY(I->orders.need((size_t)(nq * nsets * d)));
+    PDX_TRY(pdx_dimension_orders(dq, 0, nq, (int32_t)d,
+                                 ivf ? I->bucket_means.p : I->global_means.p, sel, nsets,
+                                 P->criteria, P->zone_width, I->orders.p, st));
+    orders = I->orders.p;
+    oqs = nsets;
+    oss = ivf ? 1 : 0;
+  }
+  // BSA residual energies for this schedule
+  if (P->pruner == PDX_PRUNER_BSA) {
+    PDX_REQUIRE(P->bsa_coef, "bsa needs its coefficients");
+    if (I->resid_step != P->initial_step) {
+      int32_t ns = 0;
+      PDX_TRY(pdx_bsa_residuals(&I->st, P->initial_step, nullptr, &ns, st));
+      PDX_TRY(I->resid.need((size_t)(I->st.ntiles ? I->st.ntiles : 1) * ns * kTile));
+      PDX_TRY(pdx_bsa_residuals(&I->st, P->initial_step, I->resid.p, &ns, st));
+      I->st.d_resid = I->resid.p;
+      I->st.resid_steps = ns;
+      I->st.resid_initial_step = P->initial_step;
+      I->resid_step = P->initial_step;
+    }
+    PDX_TRY(I->coef.upload(P->bsa_coef, (size_t)schedule_len((int)d, P->initial_step), st));
+  }
+  // scan
+  float* dist = out_dist;
+  int64_t* ids = out_ids;
+  int64_t* touched = out_touched;
+  int64_t* total = out_total;
+  if (!P->outputs_on_device) {
+    PDX_TRY(I->dist.need((size_t)(nq * k)));
+    PDX_TRY(I->ids.need((size_t)(nq * k)));
+    dist = I->dist.p;
+    ids = I->ids.p;
+    if (out_touched || out_total) {
+      PDX_TRY(I->touched.need((size_t)nq));
+      PDX_TRY(I->total.need((size_t)nq));
+      touched = I->touched.p;
+      total = I->total.p;
+    }
+  }
+  PDX_TRY(I->count.need((size_t)nq));
+  pdx_search_params sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.k = P->k;
+  sp.metric = P->metric;
+  sp.pruner = P->pruner;
+  sp.initial_step = P->initial_step;
+  sp.selection_fraction = P->selection_fraction;
+  sp.ads_d = (int32_t)d;
+  sp.ads_epsilon0 = P->epsilon0;
+  sp.bsa_coef = P->pruner == PDX_PRUNER_BSA ? I->coef.p : nullptr;
+  pdx_search_out so;
+  memset(&so, 0, sizeof(so));
+  so.d_dist = dist;
+  so.d_ids = ids;
+  so.d_count = I->count.p;
+  so.d_touched = (out_touched || out_total) ? touched : nullptr;
+  so.d_total = (out_touched || out_total) ? total : nullptr;
+  const int64_t wb = pdx_search_workspace(&I->st, ivf ? nq : 1, nseg);
+  PDX_REQUIRE(wb >= 0, "bad workspace size");
+  PDX_TRY(I->work.need((size_t)wb));
+  PDX_TRY(pdx_search(&I->st, &sp, dq, nq, sel, nseg, orders, oqs, oss, &so, I->work.p, wb, st));
+  if (!P->outputs_on_device) {
+    PDX_CUDA_CHECK(cudaMemcpyAsync(out_dist, dist, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+    PDX_CUDA_CHECK(cudaMemcpyAsync(out_ids, ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
+    if (out_touched)
+      PDX_CUDA_CHECK(cudaMemcpyAsync(out_touched, touched, 8 * nq, cudaMemcpyDeviceToHost, st));
+    if (out_total)
+      PDX_CUDA_CHECK(cudaMemcpyAsync(out_total, total, 8 * nq, cudaMemcpyDeviceToHost, st));
+    PDX_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  return PDX_OK;
+}

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "pdx_common.cuh"
+#include "pdx_upload.cuh"
 
 namespace pdx {
 
@@ -21,64 +22,12 @@ constexpr char kMagic[8] = {'P', 'D', 'X', 'v', '1', 0, 0, 0};
 constexpr uint32_t kVersion = 1;
 constexpr uint32_t kFlagTransform = 1, kFlagIvf = 2;
 constexpr int64_t kHeaderBytes = 40;  // struct "<8sIIQIIII"
-constexpr int64_t kChunkBytes = 64ll << 20;
-constexpr int64_t kChunkTiles = 1 << 16;
 
 #define PDX_FORMAT(...)              \
   do {                               \
     ::pdx::set_error(__VA_ARGS__);   \
     return PDX_EFORMAT;              \
   } while (0)
-
-// One 64-slot tile of a block image in the staging buffer.
-struct TileSrc {
-  int64_t raw_off;  // float offset of the block image [d][mp] in staging
-  int64_t tile;     // destination tile in the store
-  int32_t mp;       // the block's m_padded (image row length)
-  int32_t col;      // first block column of this tile (64 * tile-in-block)
-  int32_t valid;    // block columns of this tile that hold vectors
-  int32_t _pad;
-};
-
-// file image [d][mp] -> tile [d_pad/G][64][G]; dims >= d and slots >= valid are 0
-__global__ void __launch_bounds__(256) blocks_to_tiles_kernel(const float* __restrict__ raw,
-                                                              const TileSrc* __restrict__ src,
-                                                              int d, int d_pad, int group,
-                                                              float* __restrict__ tiles) {
-  const TileSrc s = src[blockIdx.x];
-  float* out = tiles + s.tile * (int64_t)d_pad * kTile;
-  const int total = d_pad * kTile;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    int j, i;
-    if (group == 8) {
-      const int r = e & 511;
-      j = (e >> 9) * 8 + (r & 7);
-      i = r >> 3;
-    } else {
-      j = e >> 6;
-      i = e & 63;
-    }
-    float v = 0.f;
-    if (j < d && i < s.valid) v = raw[s.raw_off + (int64_t)j * s.mp + s.col + i];
-    out[e] = v;
-  }
-}
-
-// tile -> file image columns [col, col + valid) of every dim row
-__global__ void __launch_bounds__(256) tiles_to_blocks_kernel(const float* __restrict__ tiles,
-                                                              const TileSrc* __restrict__ src,
-                                                              int d, int d_pad, int group,
-                                                              float* __restrict__ raw) {
-  const TileSrc s = src[blockIdx.x];
-  const float* in = tiles + s.tile * (int64_t)d_pad * kTile;
-  const int total = d * kTile;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int j = e >> 6, i = e & 63;
-    if (i >= s.valid) continue;
-    const float v = group == 8 ? in[((j >> 3) * kTile + i) * 8 + (j & 7)] : in[j * kTile + i];
-    raw[s.raw_off + (int64_t)j * s.mp + s.col + i] = v;
-  }
-}
 
 struct File {
   FILE* f = nullptr;
@@ -125,11 +74,6 @@ int take(File& F, void* dst, int64_t n) {
   return PDX_OK;
 }
 
-#define PDX_TRY(expr)         \
-  do {                        \
-    const int _rc = (expr);   \
-    if (_rc != PDX_OK) return _rc; \
-  } while (0)
 
 int read_header(File& F, pdx_file_info* I) {
   unsigned char h[kHeaderBytes];
@@ -200,31 +144,6 @@ int walk(File& F, pdx_file_info* I, Layout* L) {
   return PDX_OK;
 }
 
-// RAII for the staging resources of one transfer
-struct Staging {
-  float* h_raw[2] = {nullptr, nullptr};
-  float* d_raw[2] = {nullptr, nullptr};
-  TileSrc* d_src[2] = {nullptr, nullptr};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  ~Staging() {
-    for (int b = 0; b < 2; ++b) {
-      if (ev[b]) cudaEventSynchronize(ev[b]), cudaEventDestroy(ev[b]);
-      if (h_raw[b]) cudaFreeHost(h_raw[b]);
-      if (d_raw[b]) cudaFree(d_raw[b]);
-      if (d_src[b]) cudaFree(d_src[b]);
-    }
-  }
-  int alloc(int64_t bytes, int nbuf) {
-    for (int b = 0; b < nbuf; ++b) {
-      PDX_CUDA_CHECK(cudaMallocHost(&h_raw[b], (size_t)bytes));
-      PDX_CUDA_CHECK(cudaMalloc(&d_raw[b], (size_t)bytes));
-      PDX_CUDA_CHECK(cudaMalloc(&d_src[b], sizeof(TileSrc) * kChunkTiles));
-      PDX_CUDA_CHECK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
-    }
-    return PDX_OK;
-  }
-};
-
 }  // namespace
 }  // namespace pdx
 
@@ -259,7 +178,6 @@ extern "C" int pdx_file_load(const char* path, const pdx_file_info* info, int32_
   PDX_REQUIRE(!(I.flags & kFlagIvf) || (h_centroids && h_bucket_offsets && h_bucket_means),
               "pdx_file_load: file has an IVF section");
   const int64_t d = I.d;
-  const int d_pad = group == 8 ? (int)((d + 7) / 8 * 8) : (int)d;
   cudaStream_t st = as_stream(stream);
 
   if (fseeko(F.f, (off_t)L.means_at, SEEK_SET) != 0) {
@@ -275,58 +193,16 @@ extern "C" int pdx_file_load(const char* path, const pdx_file_info* info, int32_
     PDX_TRY(take(F, h_transform, 4 * d * d));
   }
 
-  const int64_t cap = I.max_block_bytes > kChunkBytes ? I.max_block_bytes : kChunkBytes;
-  Staging S;
-  PDX_TRY(S.alloc(cap, 2));
-  std::vector<TileSrc> src[2];
-  std::vector<int64_t> ids[2];
-  int cur = 0;
-  int64_t used = 0, tile = 0, chunk_tile0 = 0;
-  std::vector<int64_t> bids;
-  auto flush = [&]() -> int {
-    const int64_t nt = (int64_t)src[cur].size();
-    if (nt > 0) {
-      PDX_CUDA_CHECK(cudaMemcpyAsync(S.d_raw[cur], S.h_raw[cur], (size_t)used * 4,
-                                     cudaMemcpyHostToDevice, st));
-      PDX_CUDA_CHECK(cudaMemcpyAsync(S.d_src[cur], src[cur].data(), sizeof(TileSrc) * nt,
-                                     cudaMemcpyHostToDevice, st));
-      PDX_CUDA_CHECK(cudaMemcpyAsync(d_tile_ids + chunk_tile0 * kTile, ids[cur].data(),
-                                     sizeof(int64_t) * kTile * nt, cudaMemcpyHostToDevice, st));
-      blocks_to_tiles_kernel<<<(unsigned)nt, 256, 0, st>>>(S.d_raw[cur], S.d_src[cur], (int)d,
-                                                           d_pad, group, d_tiles);
-      PDX_LAUNCH_CHECK();
+  struct FileSrc {
+    File& F;
+    int head(int64_t, uint32_t* mm) { return take(F, mm, 8); }
+    int body(int64_t, int64_t m, int64_t floats, int64_t* ids, float* data) {
+      PDX_TRY(take(F, ids, 8 * m));
+      return take(F, data, 4 * floats);
     }
-    PDX_CUDA_CHECK(cudaEventRecord(S.ev[cur], st));
-    cur ^= 1;
-    PDX_CUDA_CHECK(cudaEventSynchronize(S.ev[cur]));  // the other buffer is free again
-    src[cur].clear();
-    ids[cur].clear();
-    used = 0;
-    chunk_tile0 = tile;
-    return PDX_OK;
-  };
-  for (int64_t b = 0; b < I.nblocks; ++b) {
-    uint32_t mm[2];
-    PDX_TRY(take(F, mm, 8));
-    const int64_t m = mm[0], mp = mm[1], floats = d * mp;
-    const int64_t nt = (m + kTile - 1) / kTile;
-    if (used + floats > cap / 4 || (int64_t)src[cur].size() + nt > kChunkTiles) PDX_TRY(flush());
-    PDX_REQUIRE(nt <= kChunkTiles, "block %lld spans more than %lld tiles", (long long)b,
-                (long long)kChunkTiles);
-    h_block_m[b] = (int32_t)m;
-    h_block_mpad[b] = (int32_t)mp;
-    bids.resize(m);
-    PDX_TRY(take(F, bids.data(), 8 * m));
-    PDX_TRY(take(F, S.h_raw[cur] + used, 4 * floats));
-    for (int64_t u = 0; u < nt; ++u) {
-      const int32_t valid = (int32_t)(m - u * kTile < kTile ? m - u * kTile : kTile);
-      src[cur].push_back(TileSrc{used, tile, (int32_t)mp, (int32_t)(u * kTile), valid, 0});
-      for (int i = 0; i < kTile; ++i) ids[cur].push_back(i < valid ? bids[u * kTile + i] : -1);
-      ++tile;
-    }
-    used += floats;
-  }
-  PDX_TRY(flush());
+  } src{F};
+  PDX_TRY(upload_blocks(src, I.nblocks, d, group, I.max_block_bytes, d_tiles, d_tile_ids,
+                        h_block_m, h_block_mpad, st));
   if (I.flags & kFlagIvf) {
     PDX_TRY(take(F, nullptr, 12));
     PDX_TRY(take(F, h_centroids, 4 * (int64_t)I.nlist * d));

@@ -1,0 +1,84 @@
+"""The owning native handle (pdx_index_*): one C call per query batch must
+return exactly what the per-kernel Python path and the oracle return."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2503_04422_b200 as P
+from paper_2503_04422_b200 import _lib
+
+GOLD = Path(__file__).resolve().parent / "golden" / "pdx"
+
+
+def test_handle_symbols_exported():
+    L = _lib.lib()
+    for name in ("pdx_index_create", "pdx_index_open", "pdx_index_destroy", "pdx_index_search"):
+        assert hasattr(L, name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pruner,criteria", [("bond", "dmeans"), ("bond", "zones"),
+                                             ("ads", "sequential"), ("none", "sequential")])
+def test_open_pdx_matches_python_path_and_oracle(oracle, pruner, criteria):
+    st = P.read_pdx(GOLD / "ivf.pdx")
+    group = 1 if criteria != "sequential" else 8
+    h = P.PdxIndex.open(GOLD / "ivf.pdx", group=group)
+    Q = np.random.default_rng(3).standard_normal((40, st.d)).astype(np.float32)
+    out = h.search(Q, k=7, pruner=pruner, criteria=criteria, nprobe=5, stats=True)
+    idx = P.load_index(GOLD / "ivf.pdx", group=group)
+    ref = P.ivf_search_batch(idx, Q, P.SearchParams(k=7, pruner=pruner), 5, criteria=criteria,
+                             stats=True)
+    np.testing.assert_array_equal(out["ids"].numpy(), ref["ids"])
+    np.testing.assert_array_equal(out["dist"].numpy(), ref["dist"])
+    np.testing.assert_array_equal(out["touched"].numpy(), ref["touched"])
+    chains = [st.blocks[int(st.ivf.bucket_offsets[c]):int(st.ivf.bucket_offsets[c + 1])]
+              for c in range(st.ivf.nlist)]
+    view = oracle.IvfView(P.to_blocks(P.VectorCollection.from_array(st.ivf.centroids), 64),
+                          chains, st.ivf.bucket_means)
+    o = oracle.ivf_search_batch(view, Q, 7, 5, pruner=pruner, criteria=criteria)
+    np.testing.assert_array_equal(out["ids"].numpy(), o["ids"])
+    np.testing.assert_array_equal(out["touched"].numpy(), o["touched"])
+    h.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["flat64.pdx", "wide.pdx", "flat128.pdx"])
+def test_from_host_blocks_exact_vs_oracle(oracle, name):
+    st = P.read_pdx(GOLD / name)
+    h = P.PdxIndex.from_blocks(st.blocks, global_means=st.global_means, group=1)
+    Q = np.random.default_rng(5).standard_normal((16, st.d)).astype(np.float32)
+    out = h.search(Q, k=5, pruner="bond", criteria="dmeans", stats=True)
+    ref = oracle.exact_search_batch(st.blocks, st.global_means, Q, 5, pruner="bond",
+                                    criteria="dmeans")
+    np.testing.assert_array_equal(out["ids"].numpy(), ref["ids"])
+    np.testing.assert_array_equal(out["dist"].numpy(), ref["dist"])
+    np.testing.assert_array_equal(out["touched"].numpy(), ref["touched"])
+
+
+@pytest.mark.gpu
+def test_borrowed_index_rotation_bsa_and_device_outputs():
+    import torch
+    x = np.random.default_rng(8).standard_normal((20_000, 48)).astype(np.float32)
+    Q = x[:100] + 0.05 * np.random.default_rng(9).standard_normal((100, 48)).astype(np.float32)
+    T = P.generate_orthogonal(48, 0)
+    xr = P.apply_transform(T, x)
+    idx = P.ivf_build(P.VectorCollection.from_array(xr), nlist=64, seed=0)
+    h = P.PdxIndex.from_index(idx, transform=T)
+    params = P.SearchParams(k=10, pruner="ads")
+    ref = P.ivf_search_batch(idx, P.apply_transform(T, Q), params, 12, stats=True)
+    out = h.search(Q, k=10, pruner="ads", nprobe=12, rotate=True, stats=True)
+    # the handle projects with the same K3 kernel, so the decisions match
+    np.testing.assert_array_equal(out["ids"].numpy(), ref["ids"])
+    np.testing.assert_array_equal(out["touched"].numpy(), ref["touched"])
+    bsa = P.fit_bsa(torch.from_numpy(xr).cuda())
+    ref_b = P.ivf_search_batch(idx, P.apply_transform(T, Q),
+                               P.SearchParams(k=10, pruner="bsa", bsa=bsa), 12, stats=True)
+    Qd = torch.from_numpy(P.apply_transform(T, Q)).cuda()
+    out_b = h.search(Qd, k=10, pruner="bsa", bsa=bsa, nprobe=12, stats=True)
+    assert out_b["ids"].is_cuda
+    np.testing.assert_array_equal(out_b["ids"].cpu().numpy(), ref_b["ids"])
+    np.testing.assert_array_equal(out_b["touched"].cpu().numpy(), ref_b["touched"])
+    with pytest.raises(ValueError, match="nprobe"):
+        h.search(Q, k=10, nprobe=65)
+    h.close()
