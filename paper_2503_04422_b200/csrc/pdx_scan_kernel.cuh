@@ -17,6 +17,15 @@
 #include "pdx_common.cuh"
 #include "pdx_scan_spec.cuh"
 
+#ifndef PDX_MBAR_RING
+#define PDX_MBAR_RING 1  // compute warps sleep on mbarriers for free ring slots
+#endif
+#ifndef PDX_MBAR_COMMIT
+#define PDX_MBAR_COMMIT 1  // the commit warp sleeps on mbarriers for ready tiles
+#endif
+#ifndef PDX_MBAR_HINT
+#define PDX_MBAR_HINT 0
+#endif
 #ifndef PDX_SCAN_MIN_BLOCKS
 #define PDX_SCAN_MIN_BLOCKS 3  // 3 query CTAs of 9 warps per SM: <= 75 registers
 #endif
@@ -42,8 +51,8 @@ static_assert(sizeof(Control) <= 128, "control block");
 // Shared-memory carve-up; computed on the host and passed to the kernel so
 // the offsets live in the constant bank instead of being rematerialised.
 struct ScanSmem {
-  int32_t ctl, ratio, band, bsa, ends, bnd, cnt, wmin, flag, desc, sum, items, wbnd, ids, tki,
-      part, tkd, q, bmask, total, rb;
+  int32_t ctl, mbar, ratio, band, bsa, ends, bnd, cnt, wmin, flag, desc, sum, items, wbnd, ids,
+      tki, part, tkd, q, bmask, total, rb;
 };
 
 inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int d_pad) {
@@ -55,6 +64,7 @@ inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int 
     return (int32_t)at;
   };
   L.ctl = take(128);
+  L.mbar = take(sizeof(uint64_t) * 2 * rb);  // ready[rb], free[rb]
   L.ratio = take(sizeof(double) * kMaxSteps);
   L.band = take(sizeof(double) * kMaxSteps);
   L.bsa = take(sizeof(float) * 3 * kMaxSteps);
@@ -134,6 +144,55 @@ __device__ __forceinline__ void st_release(int32_t* p, int v) {
                : "memory");
 }
 
+// mbarriers (count 1) guarding the ring: ready[slot] completes a phase when
+// a compute warp has written the slot's tile, free[slot] when the commit
+// warp has consumed it.  A waiting warp sleeps in hardware (try_wait) instead
+// of spinning, so the issue slots go to the warps that work.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile(
+      "{\n .reg .b64 state;\n mbarrier.arrive.release.cta.shared::cta.b64 state, [%0];\n}" ::"r"(
+          smem_u32(b))
+      : "memory");
+}
+// true once the phase with parity `par` has completed; suspends up to `ns`
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t par, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(par), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+// try_wait without a time hint: the hardware suspends the warp for a
+// system-defined window and wakes it when the phase completes
+__device__ __forceinline__ bool mbar_try_default(uint64_t* b, uint32_t par) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(par)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
+#if PDX_MBAR_HINT
+  while (!mbar_try(b, par, 1u << 20)) {
+  }
+#else
+  while (!mbar_try_default(b, par)) {
+  }
+#endif
+}
+
 // ------------------------------------------------------------------ top-k
 __device__ __forceinline__ float topk_threshold(const Control& c, int k, const float* tkd) {
   return c.n < k ? INFINITY : tkd[k - 1];
@@ -211,13 +270,19 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   float* tkd = reinterpret_cast<float*>(smem + L.tkd);
   float* s_q = reinterpret_cast<float*>(smem + L.q);
   uint8_t* s_bmask = reinterpret_cast<uint8_t*>(smem + L.bmask);
+  uint64_t* s_ready = reinterpret_cast<uint64_t*>(smem + L.mbar);
+  uint64_t* s_free = s_ready + RB;
 
   // ---- setup
   const float* qg = A.queries + (int64_t)q * A.d;
   const int ngroups = (A.d_pad + 7) / 8;
   for (int j = threadIdx.x; j < ngroups * 8; j += blockDim.x) s_q[j] = j < A.d ? qg[j] : 0.f;
   for (int j = threadIdx.x; j < ngroups; j += blockDim.x) s_bmask[j] = 0;
-  for (int j = threadIdx.x; j < RB; j += blockDim.x) s_flag[j] = 0;
+  for (int j = threadIdx.x; j < RB; j += blockDim.x) {
+    s_flag[j] = 0;
+    mbar_init(&s_ready[j]);
+    mbar_init(&s_free[j]);
+  }
   for (int m = threadIdx.x; m <= kTile; m += blockDim.x)
     s_wmin[m] = m > 0 ? warm_min_count(m, A.sf) : 0;
   __syncthreads();
@@ -288,14 +353,29 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       if (n0 >= ntiles) break;
       nnext = claim(enext);
       const int nt = min(tpw, ntiles - n0);
-      // ring slots n0.. are free once tile n0+nt-1-RB is committed
-      // (back off: spinning warps would steal issue slots from working ones)
+      // ring slots n0.. are free once tile n0+nt-1-RB is committed: phase
+      // (last/RB - 1) of free[last's slot] (commits are in order)
+      const int last = n0 + nt - 1;
+#if PDX_MBAR_RING
+      if (last >= RB) {
+        // A parity wait only tells the current phase from the one before: a
+        // warp two ring turns ahead of the commit (possible with lookahead
+        // claims) would alias.  First let the commit reach the previous turn.
+        while (ld_acquire(&ctl.com_pub) < last + 1 - 2 * RB) __nanosleep(256);
+        const uint32_t par = (uint32_t)(last / RB - 1) & 1u;
+        if (!mbar_try_default(&s_free[last & RMASK], par)) {
+          if (A.debug && lane == 0) atomicAdd(&ctl.ring_waits, 1);
+          mbar_wait(&s_free[last & RMASK], par);
+        }
+      }
+#else
       int spins = 0;
-      while (ld_acquire(&ctl.com_pub) < n0 + nt - RB) {
+      while (ld_acquire(&ctl.com_pub) < last + 1 - RB) {
         __nanosleep(spins < 2 ? 200 : 800);
         ++spins;
       }
       if (A.debug && spins && lane == 0) atomicAdd(&ctl.ring_waits, spins);
+#endif
       const int sl = n0 & RMASK;  // RB is a multiple of tpw: the slice is contiguous
       if (lane < nt) {
         TileDesc t;
@@ -339,7 +419,10 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
                                : 0;
       }
       __syncwarp();
-      if (lane < nt) st_release(&s_flag[sl + lane], 2);
+      if (lane < nt) {
+        st_release(&s_flag[sl + lane], 2);
+        mbar_arrive(&s_ready[sl + lane]);
+      }
     }
   } else {
     // ======================================================== commit warp
@@ -506,15 +589,25 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       // batch: a run of tiles costs the commit warp about as much as one
       const int want = min(min(RB, 32) / 2, ntiles - com);
       if (nr == 0 || (nr < want && polls < 3)) {
+        // sleep in hardware until the first missing tile is written
+        // (bounded while some are ready: a run costs about what one tile does)
         ++dbg_idle;
         ++polls;
+#if PDX_MBAR_COMMIT
+        const int n = com + nr;
+        mbar_try(&s_ready[n & RMASK], (uint32_t)(n / RB) & 1u, nr == 0 ? (1u << 20) : 200u);
+#else
         __nanosleep(48);
+#endif
         continue;
       }
       polls = 0;
       int done = 0;
       while (done < nr) done += commit_run(com + done, nr - done);
-      if (lane < done) s_flag[(com + lane) & RMASK] = 0;
+      if (lane < done) {
+        s_flag[(com + lane) & RMASK] = 0;
+        mbar_arrive(&s_free[(com + lane) & RMASK]);
+      }
       com += done;
       __syncwarp();
       if (lane == 0) {
