@@ -246,14 +246,14 @@ def main():
     total = int(st_res.total.sum().item())
     alg_bytes = 4 * touched
     if args.debug:
-        dbg = torch.zeros((args.nq, 8), dtype=torch.int64, device=dev)
+        dbg = torch.zeros((args.nq, 16), dtype=torch.int64, device=dev)
         searcher._buf["debug_buf"] = dbg
         searcher.run(Qr_dev)
         torch.cuda.synchronize()
         del searcher._buf["debug_buf"]
         d = dbg.cpu().numpy().astype(np.float64)
         names = ["cycles", "tiles", "fast", "serial", "replay", "commit_idle", "ring_waits",
-                 "sparse_items"]
+                 "sparse_items", "cw_wait", "cw_dense", "cw_sparse", "cw_rest"]
         print("DEBUG per-query mean:", {n: round(float(d[:, i].mean()), 1)
                                         for i, n in enumerate(names)},
               "max cycles", int(d[:, 0].max()), file=sys.stderr)

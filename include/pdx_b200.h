@@ -141,9 +141,10 @@ typedef struct pdx_search_out {
   int32_t* d_trace;
   int64_t trace_cap;
   int64_t* d_trace_len;
-  /* optional [nq][8] kernel diagnostics: cycles, tiles, fast-path commits,
+  /* optional [nq][16] kernel diagnostics: cycles, tiles, fast-path commits,
    * serial commits, replays, commit-warp idle polls, compute-warp ring
-   * waits, sparse items */
+   * waits, sparse items, then compute-warp cycles summed over warps: ring
+   * wait, dense phase, sparse phase, the rest */
   int64_t* d_debug;
 } pdx_search_out;
 

@@ -24,7 +24,10 @@
 #define PDX_MBAR_COMMIT 1  // the commit warp sleeps on mbarriers for ready tiles
 #endif
 #ifndef PDX_MBAR_HINT
-#define PDX_MBAR_HINT 0
+#define PDX_MBAR_HINT 1
+#endif
+#ifndef PDX_SCAN_PROFILE
+#define PDX_SCAN_PROFILE 0
 #endif
 #ifndef PDX_SCAN_MIN_BLOCKS
 #define PDX_SCAN_MIN_BLOCKS 3  // 3 query CTAs of 9 warps per SM: <= 75 registers
@@ -45,6 +48,7 @@ struct Control {
   int32_t ring_waits;  // diagnostics: compute-warp polls for a free ring slot
   int32_t items;       // diagnostics: sparse items
   int64_t touched, total, tlen;
+  unsigned long long cyc[4];  // diagnostics: compute-warp cycles in ring wait, dense, sparse, rest
 };
 static_assert(sizeof(Control) <= 128, "control block");
 
@@ -307,6 +311,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     ctl.touched = ctl.total = ctl.tlen = 0;
     ctl.ring_waits = 0;
     ctl.items = 0;
+    ctl.cyc[0] = ctl.cyc[1] = ctl.cyc[2] = ctl.cyc[3] = 0;
   }
   __syncthreads();
   if (threadIdx.x < nsteps) {  // bound factors (bound_factors_kernel, pdx_scan.cu)
@@ -347,10 +352,14 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     };
     TileEntry enext = {};
     int nnext = claim(enext);
+    // per-phase cycle counters (diagnostics; compiled in with -DPDX_SCAN_PROFILE=1)
+    constexpr bool kProf = PDX_SCAN_PROFILE != 0;
+    long long c_wait = 0, c_dense = 0, c_sparse = 0, c_all = kProf ? clock64() : 0;
     for (;;) {
       const int n0 = nnext;
       const TileEntry e = enext;
       if (n0 >= ntiles) break;
+      const long long c0 = kProf ? clock64() : 0;
       nnext = claim(enext);
       const int nt = min(tpw, ntiles - n0);
       // ring slots n0.. are free once tile n0+nt-1-RB is committed: phase
@@ -376,6 +385,8 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       }
       if (A.debug && spins && lane == 0) atomicAdd(&ctl.ring_waits, spins);
 #endif
+      const long long c1 = kProf ? clock64() : 0;
+      c_wait += c1 - c0;
       const int sl = n0 & RMASK;  // RB is a multiple of tpw: the slice is contiguous
       if (lane < nt) {
         TileDesc t;
@@ -409,7 +420,10 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
           dense_tile_generic<G, ORD, METRIC>(A, q, R.desc[j], j, Q, R, nitems, lane);
       }
       if (A.debug && lane == 0) atomicAdd(&ctl.items, nitems);
+      const long long c2 = kProf ? clock64() : 0;
+      c_dense += c2 - c1;
       sparse_phase<G, ORD, METRIC>(A, q, Q, R, nitems, lane);
+      if (kProf) c_sparse += clock64() - c2;
       __syncwarp();
       if (lane < nt) {  // values_touched if the commit finds the speculation exact
         const TileDesc& t = R.desc[lane];
@@ -423,6 +437,13 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
         st_release(&s_flag[sl + lane], 2);
         mbar_arrive(&s_ready[sl + lane]);
       }
+    }
+    if (kProf && A.debug && lane == 0) {
+      c_all = clock64() - c_all;
+      atomicAdd(&ctl.cyc[0], (unsigned long long)c_wait);
+      atomicAdd(&ctl.cyc[1], (unsigned long long)c_dense);
+      atomicAdd(&ctl.cyc[2], (unsigned long long)c_sparse);
+      atomicAdd(&ctl.cyc[3], (unsigned long long)(c_all - c_wait - c_dense - c_sparse));
     }
   } else {
     // ======================================================== commit warp
@@ -621,7 +642,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       ctl.tlen = r_tlen;
     }
     if (A.debug && lane == 0) {
-      int64_t* dg = A.debug + (int64_t)q * 8;
+      int64_t* dg = A.debug + (int64_t)q * 16;
       dg[0] = clock64() - t_start;
       dg[1] = ntiles;
       dg[2] = dbg_fast;
@@ -632,8 +653,9 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   }
   __syncthreads();
   if (A.debug && threadIdx.x == 0) {
-    A.debug[(int64_t)q * 8 + 6] = ctl.ring_waits;
-    A.debug[(int64_t)q * 8 + 7] = ctl.items;
+    A.debug[(int64_t)q * 16 + 6] = ctl.ring_waits;
+    A.debug[(int64_t)q * 16 + 7] = ctl.items;
+    for (int i = 0; i < 4; ++i) A.debug[(int64_t)q * 16 + 8 + i] = (int64_t)ctl.cyc[i];
   }
 
   // ---- outputs

@@ -221,7 +221,7 @@ def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None,
         trace = torch.zeros((nq, trace_cap), dtype=torch.int32, device=dev)
         trace_len = torch.zeros((nq,), dtype=torch.int64, device=dev)
     debug = out.get("debug_buf")
-    if debug is not None and debug.shape != (nq, 8):
+    if debug is not None and debug.shape != (nq, 16):
         debug = None
     so = _lib.PdxSearchOut(_lib.ptr(dist), _lib.ptr(ids), _lib.ptr(count), _lib.ptr(touched),
                            _lib.ptr(total), _lib.ptr(trace), int(trace_cap), _lib.ptr(trace_len),
