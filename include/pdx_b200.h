@@ -120,6 +120,14 @@ typedef struct pdx_search_params {
   int32_t tiles_per_warp; /* 64-vector tiles a compute warp claims at once (0 = auto) */
   int32_t ring_slots;     /* tiles in flight per query CTA (0 = auto) */
   const float* bsa_coef;  /* BSA: DEVICE float32 [nsteps] coef_s (see PDX_PRUNER_BSA) */
+  /* Split mode (> 1): each query's visit list is cut, at block starts, into
+   * `splits` ranges scanned by separate CTAs, each with its own threshold
+   * chain from +inf; the per-range top-k lists are merged (K7).  Results are
+   * the exact top-k for pruner none / BOND (the union of exact local top-ks);
+   * values_touched is the split run's own (a throughput mode: the reference
+   * has one chain); ADS / BSA become recall-level.  No survivor traces.
+   * Lets one query use the whole GPU (batch-1 exact search, C4). */
+  int32_t splits;
 } pdx_search_params;
 
 /* Outputs of pdx_search.  Per query q (row q of each array):

@@ -45,7 +45,7 @@ class PdxSearchParams(C.Structure):
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
                 ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
                 ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32),
-                ("bsa_coef", C.c_void_p)]
+                ("bsa_coef", C.c_void_p), ("splits", C.c_int32)]
 
 
 class PdxFileInfo(C.Structure):

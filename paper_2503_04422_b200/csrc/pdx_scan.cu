@@ -126,6 +126,16 @@ __global__ void bound_factors_kernel(int pruner, int d, int initial_step, int ns
   }
 }
 
+// len(TopK) after a split-mode merge: the valid ids of each row
+__global__ void count_valid_kernel(const int64_t* __restrict__ ids, int64_t nq, int k,
+                                   int32_t* __restrict__ count) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int c = 0;
+  for (int j = 0; j < k; ++j) c += ids[q * k + j] >= 0;
+  count[q] = c;
+}
+
 template <int G, bool ORD, int METRIC>
 static cudaError_t launch_scan(const ScanArgs& A, const ScanSmem& L, int nq, int W, int tpw,
                                cudaStream_t st) {
@@ -294,15 +304,69 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   A.sparse_max = 32 / tpw;
   PDX_REQUIRE(A.out_dist && A.out_ids, "output buffers required");
 
+  // split mode: CTA b scans range b / nq of query b % nq into row b of a
+  // part-major [nsplit][nq][k] scratch, merged below by K7 (in two levels
+  // when nsplit * k exceeds one merge CTA)
+  int nsplit = prm->splits > 1 ? prm->splits : 1;
+  const int g2 = 8192 / prm->k > 1 ? 8192 / prm->k : 1;  // lists one merge CTA sorts
+  int g1 = 1;
+  if (nsplit > g2) {
+    g1 = (nsplit + g2 - 1) / g2;
+    nsplit = g1 * g2;
+    PDX_REQUIRE(g1 <= g2, "too many splits (%d) for k = %d", prm->splits, prm->k);
+  }
+  PDX_REQUIRE(nsplit == 1 || !out->d_trace, "split mode keeps no survivor traces");
+  PDX_REQUIRE(nq * nsplit <= 0x7fffffffll, "too many query ranges");
+  A.nq = (int32_t)nq;
+  A.nsplit = nsplit;
+  float* tdist = nullptr;
+  int64_t* tids = nullptr;
+  if (nsplit > 1) {
+    PDX_CUDA_CHECK(cudaMallocAsync(&tdist, sizeof(float) * nq * nsplit * prm->k, st));
+    PDX_CUDA_CHECK(cudaMallocAsync(&tids, sizeof(int64_t) * nq * nsplit * prm->k, st));
+    A.out_dist = tdist;
+    A.out_ids = tids;
+    A.out_count = nullptr;
+    A.debug = nullptr;
+    if (A.out_touched) PDX_CUDA_CHECK(cudaMemsetAsync(A.out_touched, 0, 8 * nq, st));
+    if (A.out_total) PDX_CUDA_CHECK(cudaMemsetAsync(A.out_total, 0, 8 * nq, st));
+  }
+
   cudaError_t e;
   const bool ord = d_orders != nullptr;
   const int mt = prm->pruner == PDX_PRUNER_BSA ? kMetricL2Bsa : prm->metric;
+  const int grid = (int)(nq * nsplit);
   if (store->group == 8)
-    e = ord ? launch_metric<8, true>(mt, A, L, (int)nq, W, tpw, st)
-            : launch_metric<8, false>(mt, A, L, (int)nq, W, tpw, st);
+    e = ord ? launch_metric<8, true>(mt, A, L, grid, W, tpw, st)
+            : launch_metric<8, false>(mt, A, L, grid, W, tpw, st);
   else
-    e = ord ? launch_metric<1, true>(mt, A, L, (int)nq, W, tpw, st)
-            : launch_metric<1, false>(mt, A, L, (int)nq, W, tpw, st);
+    e = ord ? launch_metric<1, true>(mt, A, L, grid, W, tpw, st)
+            : launch_metric<1, false>(mt, A, L, grid, W, tpw, st);
   PDX_CUDA_CHECK(e);
+  if (nsplit > 1) {
+    int rc = PDX_OK;
+    if (g1 == 1) {
+      rc = pdx_merge_topk(tdist, tids, nsplit, nq, prm->k, out->d_dist, out->d_ids, stream);
+    } else {
+      // level 1: rows (a, q) over parts b, where split = b * g1 + a
+      float* mdist = nullptr;
+      int64_t* mids = nullptr;
+      PDX_CUDA_CHECK(cudaMallocAsync(&mdist, sizeof(float) * nq * g1 * prm->k, st));
+      PDX_CUDA_CHECK(cudaMallocAsync(&mids, sizeof(int64_t) * nq * g1 * prm->k, st));
+      rc = pdx_merge_topk(tdist, tids, g2, nq * g1, prm->k, mdist, mids, stream);
+      if (rc == PDX_OK)
+        rc = pdx_merge_topk(mdist, mids, g1, nq, prm->k, out->d_dist, out->d_ids, stream);
+      cudaFreeAsync(mdist, st);
+      cudaFreeAsync(mids, st);
+    }
+    cudaFreeAsync(tdist, st);
+    cudaFreeAsync(tids, st);
+    if (rc != PDX_OK) return rc;
+    if (out->d_count) {
+      count_valid_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(out->d_ids, nq, prm->k,
+                                                                        out->d_count);
+      PDX_LAUNCH_CHECK();
+    }
+  }
   return PDX_OK;
 }

@@ -252,7 +252,8 @@ template <int G, bool ORD, int METRIC>
 __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(const ScanArgs A, const ScanSmem L,
                                                        const int tpw) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int q = blockIdx.x;
+  // split mode: CTA b scans range b / nq of query b % nq and writes row b
+  const int q = A.nsplit > 1 ? (int)(blockIdx.x % (unsigned)A.nq) : (int)blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int RB = L.rb;  // a power of two
   const int RMASK = RB - 1;
@@ -327,7 +328,18 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   }
   __syncthreads();
   const TileEntry* vis = A.vis + (int64_t)q * A.vis_qstride;
-  const int ntiles = A.vis_count[(int64_t)q * A.vis_count_qstride];
+  int ntiles = A.vis_count[(int64_t)q * A.vis_count_qstride];
+  if (A.nsplit > 1) {  // this CTA's range, both ends moved back to a block start
+    const int sp = (int)(blockIdx.x / (unsigned)A.nq);
+    const int all = ntiles;
+    auto start = [&](int x) {
+      const int p = (int)((int64_t)x * all / A.nsplit);
+      return p >= all ? all : p - vis[p].tib;
+    };
+    const int t0 = start(sp), t1 = start(sp + 1);
+    vis += t0;
+    ntiles = t1 - t0;
+  }
 
   if (warp > 0) {
     // ======================================================= compute warp
@@ -659,15 +671,23 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   }
 
   // ---- outputs
+  const int64_t row = blockIdx.x;  // == q unless split
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     const bool v = i < ctl.n;
-    A.out_dist[(int64_t)q * k + i] = v ? tkd[i] : INFINITY;
-    A.out_ids[(int64_t)q * k + i] = v ? tki[i] : -1;
+    A.out_dist[row * k + i] = v ? tkd[i] : INFINITY;
+    A.out_ids[row * k + i] = v ? tki[i] : -1;
   }
   if (threadIdx.x == 0) {
-    if (A.out_count) A.out_count[q] = ctl.n;
-    if (A.out_touched) A.out_touched[q] = ctl.touched;
-    if (A.out_total) A.out_total[q] = ctl.total;
+    if (A.out_count) A.out_count[row] = ctl.n;
+    if (A.nsplit > 1) {  // the split ranges' stats add up (outputs zeroed by the host)
+      if (A.out_touched) atomicAdd(reinterpret_cast<unsigned long long*>(&A.out_touched[q]),
+                                   (unsigned long long)ctl.touched);
+      if (A.out_total) atomicAdd(reinterpret_cast<unsigned long long*>(&A.out_total[q]),
+                                 (unsigned long long)ctl.total);
+    } else {
+      if (A.out_touched) A.out_touched[q] = ctl.touched;
+      if (A.out_total) A.out_total[q] = ctl.total;
+    }
     if (A.trace_len) A.trace_len[q] = ctl.tlen;
   }
 }

@@ -92,6 +92,7 @@ struct ScanArgs {
   int64_t* debug;  // optional [nq][8] counters (see pdx_search_out)
   int32_t sparse_max;  // a tile goes sparse once at most this many slots survive
   const double* factors;  // [2][kMaxSteps]: per-step bound ratio, band
+  int32_t nq, nsplit;     // split mode: CTA b scans range b / nq of query b % nq
   const float* resid;     // BSA: [ntiles][nsteps][64] residual energy per slot and step
   const float* bsa_coef;  // BSA: [nsteps]
 };

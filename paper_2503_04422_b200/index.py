@@ -378,11 +378,18 @@ def flat_build(collection: VectorCollection, partition_size: int = DEFAULT_PARTI
 
 
 class ExactSearcher:
-    """Batched exact_search (index.py:182-191) with device buffers."""
+    """Batched exact_search (index.py:182-191) with device buffers.
+
+    ``splits`` > 1 cuts each query's partition list into that many ranges
+    scanned by separate CTAs and merged (pdx_search_params.splits): exact
+    results for none / BOND with the split run's own values_touched, so one
+    query can use the whole GPU."""
 
     def __init__(self, part: FlatPartitioning, params: SearchParams,
-                 criteria=OrderCriteria.SEQUENTIAL, zone_width=None, warps: int = 0):
+                 criteria=OrderCriteria.SEQUENTIAL, zone_width=None, warps: int = 0,
+                 splits: int = 0):
         self.part, self.params = part, params
+        self.splits = int(splits)
         self.criteria = OrderCriteria(criteria)
         self.zone_width = zone_width
         self.warps = warps
@@ -397,7 +404,7 @@ class ExactSearcher:
             orders = dimension_orders_device(Q, self._means, self.criteria, self.zone_width)
         return run_search(self.part.store, Q, self.params, nseg=1, orders=orders,
                           order_qstride=1, order_sstride=0, stats=stats, trace_cap=trace_cap,
-                          warps=self.warps, out=self._buf, timed=timed)
+                          warps=self.warps, out=self._buf, timed=timed, splits=self.splits)
 
 
 def exact_search(partitioning: FlatPartitioning, query, params: SearchParams,
@@ -419,11 +426,11 @@ def exact_search(partitioning: FlatPartitioning, query, params: SearchParams,
 
 def exact_search_batch(partitioning: FlatPartitioning, queries, params: SearchParams,
                        criteria=OrderCriteria.SEQUENTIAL, zone_width=None, stats=False,
-                       trace=False):
+                       trace=False, splits=0):
     import torch
     Q = to_device(np.asarray(queries, np.float32), torch.float32)
     if Q.shape[1] != partitioning.d:
         raise ValueError(f"query dimensionality {Q.shape[1]} != {partitioning.d}")
-    s = ExactSearcher(partitioning, params, criteria, zone_width)
+    s = ExactSearcher(partitioning, params, criteria, zone_width, splits=splits)
     cap = _trace_cap(partitioning.store.nblocks, partitioning.d, params.initial_step) if trace else 0
     return s.run(Q, stats=stats or trace, trace_cap=cap).host()

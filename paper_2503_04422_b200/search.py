@@ -171,7 +171,8 @@ def decode_trace(buf, n):
     return out
 
 
-def make_params(params: SearchParams, d: int, warps=0, device=None) -> _lib.PdxSearchParams:
+def make_params(params: SearchParams, d: int, warps=0, device=None,
+                splits: int = 0) -> _lib.PdxSearchParams:
     """``warps``: compute warps per query CTA, or (warps, tiles_per_warp[,
     ring_slots]); 0 = auto."""
     ads = params.ads if params.ads is not None else AdsPruner(d=d)
@@ -184,12 +185,13 @@ def make_params(params: SearchParams, d: int, warps=0, device=None) -> _lib.PdxS
     return _lib.PdxSearchParams(int(params.k), _lib.METRIC[Metric(params.metric).value],
                                 _lib.PRUNER[params.pruner], int(params.initial_step),
                                 float(params.selection_fraction), int(ads.d), int(w),
-                                float(ads.epsilon0), int(tpw), int(rb), _lib.ptr(coef))
+                                float(ads.epsilon0), int(tpw), int(rb), _lib.ptr(coef),
+                                int(splits))
 
 
 def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None, orders=None,
                order_qstride=0, order_sstride=0, stats=False, trace_cap=0, warps=0, out=None,
-               timed=False):
+               timed=False, splits=0):
     """Launch pdx_search over ``store`` for a device batch ``queries`` (nq x d).
 
     seg_bucket: int32 [nq, nseg] bucket per visit segment (None: segment s
@@ -235,7 +237,7 @@ def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None,
         out["work"] = work
     if params.pruner == "bsa":
         store.ensure_bsa_residuals(params.initial_step)
-    p = make_params(params, store.d, warps, dev)
+    p = make_params(params, store.d, warps, dev, splits)
     sb = None if seg_bucket is None else seg_bucket.contiguous()
     st = _lib.stream_handle()
     ev0 = ev1 = None

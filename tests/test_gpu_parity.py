@@ -403,3 +403,29 @@ def test_bsa_estimator_recall(P):
     assert stats["bond"][0] == 1.0
     assert stats["bsa"][0] >= 0.97, stats
     assert stats["bsa"][1] < stats["bond"][1], stats
+
+
+# ------------------------------------------------------------ split mode
+@pytest.mark.parametrize("metric,pruner,k,splits", [("l2", "bond", 10, 7), ("l2", "none", 100, 100),
+                                                    ("ip", "none", 10, 300), ("l1", "bond", 5, 3)])
+def test_split_mode_exact(P, metric, pruner, k, splits):
+    """Split ranges + K7 merge (two levels when splits * k > 8192) return the
+    exact top-k of the single-chain scan; values_total is unchanged and
+    values_touched is the split run's own (>= BOND's single chain)."""
+    x = recipes.data("skewed", 40_000, 40, 51)
+    Q = recipes.queries("near", x, 12, 52)
+    col = P.VectorCollection.from_array(x)
+    flat = P.flat_build(col, 64, group=8)
+    params = P.SearchParams(k=k, metric=metric, pruner=pruner)
+    one = P.exact_search_batch(flat, Q, params, stats=True)
+    many = P.exact_search_batch(flat, Q, params, stats=True, splits=splits)
+    np.testing.assert_array_equal(many["ids"], one["ids"])
+    np.testing.assert_array_equal(many["dist"], one["dist"])
+    np.testing.assert_array_equal(many["count"], one["count"])
+    np.testing.assert_array_equal(many["total"], one["total"])
+    if pruner == "none":
+        np.testing.assert_array_equal(many["touched"], one["touched"])
+    else:
+        assert (many["touched"] >= one["touched"]).all()
+    with pytest.raises(ValueError, match="traces"):
+        P.exact_search_batch(flat, Q[:1], params, trace=True, splits=4)
