@@ -9,6 +9,8 @@
 // reference, which is why this is not a tensor-core GEMM.
 // Stage 2: per query the nprobe smallest (key, bucket) pairs, key = dist
 // (or -dist for IP) — numpy's stable argsort followed by [:nprobe].
+#include <cub/block/block_radix_sort.cuh>
+
 #include "pdx_common.cuh"
 #include "pdx_sort.cuh"
 
@@ -88,6 +90,33 @@ __global__ void __launch_bounds__(512) select_kernel(const float* __restrict__ d
     sel[(int64_t)blockIdx.x * nprobe + i] = bv[i];
 }
 
+// Stage 2 for nlist <= 256 * IPT: a stable block radix sort of the 32-bit
+// order-preserving keys with the bucket index as value (loaded in index
+// order, so equal keys keep ascending buckets: numpy's stable argsort).
+template <int IPT>
+__global__ void __launch_bounds__(256) select_radix_kernel(const float* __restrict__ dists,
+                                                           int nlist, int nprobe, int negate,
+                                                           int32_t* __restrict__ sel) {
+  using Sort = cub::BlockRadixSort<uint32_t, 256, IPT, int32_t>;
+  __shared__ typename Sort::TempStorage tmp;
+  const float* row = dists + (int64_t)blockIdx.x * nlist;
+  uint32_t key[IPT];
+  int32_t val[IPT];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const int i = threadIdx.x * IPT + j;  // blocked arrangement = index order
+    const float f = i < nlist ? row[i] : 0.f;
+    key[j] = i < nlist ? float_key(negate ? -f : f) : 0xffffffffu;
+    val[j] = i;
+  }
+  Sort(tmp).Sort(key, val);
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const int r = threadIdx.x * IPT + j;
+    if (r < nprobe) sel[(int64_t)blockIdx.x * nprobe + r] = val[j];
+  }
+}
+
 }  // namespace pdx
 
 using namespace pdx;
@@ -115,6 +144,17 @@ extern "C" int pdx_select_buckets(const float* d_queries, int64_t nq, int32_t d,
       centroid_dist_kernel<PDX_METRIC_IP><<<grid, 256, 0, st>>>(d_queries, nq, d_centroids, nlist, d, d_scratch);
   }
   PDX_LAUNCH_CHECK();
+  const int neg = metric == PDX_METRIC_IP;
+  if (nlist <= 256 * 4) {
+    select_radix_kernel<4><<<(unsigned)nq, 256, 0, st>>>(d_scratch, nlist, nprobe, neg, d_sel);
+    PDX_LAUNCH_CHECK();
+    return PDX_OK;
+  }
+  if (nlist <= 256 * 8) {
+    select_radix_kernel<8><<<(unsigned)nq, 256, 0, st>>>(d_scratch, nlist, nprobe, neg, d_sel);
+    PDX_LAUNCH_CHECK();
+    return PDX_OK;
+  }
   const int n2 = pow2_ceil(nprobe + (nlist < kSelChunk ? nlist : kSelChunk));
   const size_t smem = (size_t)n2 * (sizeof(uint64_t) + sizeof(int32_t));
   PDX_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
