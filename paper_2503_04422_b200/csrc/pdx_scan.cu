@@ -71,10 +71,19 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
     s_toff[threadIdx.x] = toff;
     s_boff[threadIdx.x] = boff;
     __syncthreads();
+    // every tile of this chunk of segments in parallel: tile v of the chunk
+    // belongs to the last segment i with toff[i] <= v (binary search)
     const int cnt = min(256, nseg - base);
-    for (int i = 0; i < cnt; ++i) {
-      for (int64_t j = threadIdx.x; j < s_nt[i]; j += 256) {
-        const int64_t v = run_t + s_toff[i] + j;
+    for (int64_t vv = threadIdx.x; vv < ttot; vv += 256) {
+      int lo = 0, hi = cnt - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_toff[mid] <= vv) lo = mid; else hi = mid - 1;
+      }
+      const int i = lo;
+      const int64_t j = vv - s_toff[i];
+      {
+        const int64_t v = run_t + vv;
         if (v < maxtiles) {
           const int64_t tile = s_t0[i] + j;
           const int32_t blk = tile_block[tile];
