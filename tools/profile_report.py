@@ -19,7 +19,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 STEP_KERNELS = ("pdx_scan_kernel", "build_visits_kernel", "centroid_dist_kernel",
-                "select_kernel", "project_kernel")
+                "select_kernel", "select_radix_kernel", "project_kernel", "bound_factors_kernel")
 
 
 def raw_metrics(rep):
