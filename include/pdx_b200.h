@@ -324,6 +324,34 @@ int pdx_file_save(const char* path, const pdx_store* store, int32_t block_size,
                   const int64_t* h_bucket_offsets, const double* h_bucket_means, void* stream);
 
 /*
+ * K8 — batched exact search with tensor-core candidate generation (L2, IP;
+ * pruner none), for batches where Q X^T is a real dense GEMM (C4).  The
+ * caller runs S = Q X^T chunk by chunk on the tensor cores (TF32 GEMM) and
+ * passes each chunk to pdx_k8_filter; pdx_k8_rescore then recomputes the
+ * candidates exactly as the scan does.  Results equal pdx_search's (the
+ * candidate set provably contains the exact top-k: |S - ref| <= margin *
+ * |q| |x|, pdx_k8_margin); a query whose candidates overflow C is reported
+ * through d_ccount > C and must be answered by pdx_search.
+ *   pdx_k8_norms : squared row norms of float32 [n][d]
+ *   pdx_k8_filter: S chunk [nq][R] (row stride ldS) for rows row0..row0+R-1
+ *       with their squared norms; d_prev / d_next float32 [nq][k] the k
+ *       smallest upper bounds so far (init +inf; swap per chunk); appends
+ *       row ids to d_cand [nq][C], counting in d_ccount [nq] (init 0).
+ *   pdx_k8_rescore: exact keys of the candidates of a flat store whose
+ *       logical blocks all hold part_size vectors (the last may hold fewer),
+ *       row r = vector r of block r / part_size; outputs as pdx_search.
+ */
+int pdx_k8_norms(const float* d_x, int64_t n, int32_t d, float* d_n2, void* stream);
+float pdx_k8_margin(int32_t d, int32_t metric);
+int pdx_k8_filter(const float* d_S, int64_t ldS, int64_t nq, int32_t R, int64_t row0,
+                  const float* d_xn2, const float* d_qn2, int32_t metric, int32_t d, int32_t k,
+                  const float* d_prev, float* d_next, int64_t* d_cand, int32_t* d_ccount,
+                  int32_t C, void* stream);
+int pdx_k8_rescore(const pdx_store* store, int64_t part_size, const float* d_queries, int64_t nq,
+                   int32_t metric, int32_t k, const int64_t* d_cand, const int32_t* d_ccount,
+                   int32_t C, float* d_dist, int64_t* d_ids, void* stream);
+
+/*
  * Owning index handle + one-call search: the drop-in boundary a C / C++ /
  * FFI caller binds.  It replaces the estimators' fit /
  * kneighbors pair (estimators.py:54-76, :99-132) and ivf_search /

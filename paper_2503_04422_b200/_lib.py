@@ -26,7 +26,8 @@ EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_til
            "pdx_project", "pdx_select_buckets", "pdx_dimension_orders", "pdx_search_workspace",
            "pdx_search", "pdx_merge_topk", "pdx_segment_means", "pdx_ground_truth",
            "pdx_bsa_residuals", "pdx_file_probe", "pdx_file_load", "pdx_file_save",
-           "pdx_index_create", "pdx_index_open", "pdx_index_destroy", "pdx_index_search")
+           "pdx_index_create", "pdx_index_open", "pdx_index_destroy", "pdx_index_search",
+           "pdx_k8_norms", "pdx_k8_margin", "pdx_k8_filter", "pdx_k8_rescore")
 
 
 class PdxStore(C.Structure):
@@ -122,6 +123,12 @@ def lib():
         L.pdx_index_open.argtypes = [C.c_char_p, i32, vp]
         L.pdx_index_destroy.argtypes = [vp]
         L.pdx_index_search.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp]
+        L.pdx_k8_norms.argtypes = [vp, i64, i32, vp, vp]
+        L.pdx_k8_margin.argtypes = [i32, i32]
+        L.pdx_k8_margin.restype = C.c_float
+        L.pdx_k8_filter.argtypes = [vp, i64, i64, i32, i64, vp, vp, i32, i32, i32, vp, vp, vp,
+                                    vp, i32, vp]
+        L.pdx_k8_rescore.argtypes = [vp, i64, vp, i64, i32, i32, vp, vp, i32, vp, vp, vp]
         L.pdx_file_load.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.pdx_file_save.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, C.c_uint64, i32,
                                     C.c_uint64, vp, vp, vp, vp]

@@ -429,3 +429,33 @@ def test_split_mode_exact(P, metric, pruner, k, splits):
         assert (many["touched"] >= one["touched"]).all()
     with pytest.raises(ValueError, match="traces"):
         P.exact_search_batch(flat, Q[:1], params, trace=True, splits=4)
+
+
+# ------------------------------------------------------- K8 tensor cores
+@pytest.mark.parametrize("metric,k,normalize", [("ip", 100, True), ("l2", 10, False),
+                                                 ("l2", 100, True), ("ip", 7, False)])
+def test_tensor_core_exact_equals_scan(P, metric, k, normalize):
+    """TF32 candidate generation + exact rescoring returns the scan's exact
+    top-k bit for bit (ids, float32 keys, counts), also across chunk edges
+    and with partitions that are not multiples of 64."""
+    import torch
+    rng = np.random.default_rng(61)
+    c = rng.standard_normal((64, 96)).astype(np.float32)
+    x = c[rng.integers(0, 64, 30_000)] + 0.5 * rng.standard_normal((30_000, 96)).astype(np.float32)
+    q = c[rng.integers(0, 64, 200)] + 0.5 * rng.standard_normal((200, 96)).astype(np.float32)
+    if normalize:
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+    col = P.VectorCollection.from_array(x)
+    for psize, group in ((64, 8), (1000, 1)):
+        flat = P.flat_build(col, psize, group=group)
+        params = P.SearchParams(k=k, metric=metric)
+        Qd = torch.from_numpy(q).cuda()
+        ref = P.ExactSearcher(flat, params).run(Qd)
+        tc = P.TensorCoreExactSearcher(flat, params, chunk=7_000)
+        out = tc.run(Qd)
+        assert tc.overflow == 0
+        np.testing.assert_array_equal(out.ids.cpu().numpy(), ref.ids.cpu().numpy())
+        np.testing.assert_array_equal(out.dist.cpu().numpy(), ref.dist.cpu().numpy())
+        np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
+        assert int(tc.candidates.max()) < 4096

@@ -143,6 +143,20 @@ def c4():
                     "qps": nb_q / sec, "batch_s": sec,
                     "algorithmic_GBps": 4 * rb.touched.sum().item() / sec / 1e9,
                     "pruning_power": 1 - rb.touched.sum().item() / rb.total.sum().item()})
+        if pruner == "none":  # K8: tensor-core candidates + exact rescoring, batch 1024
+            tc = P.TensorCoreExactSearcher(flat, params)
+            sec = timed(lambda: tc.run(q), reps=3, warm=1)
+            rt = tc.run(q)
+            same = bool((rt.ids[:nb_q] == rb.ids).all().item() and
+                        (rt.dist[:nb_q] == rb.dist).all().item())
+            flops = 2.0 * 1024 * n * d
+            out.append({"config": "C4", "metric": metric, "pruner": pruner, "batch": 1024, "k": k,
+                        "path": "K8 TF32 tensor-core candidates + exact rescoring",
+                        "qps": 1024 / sec, "batch_s": sec, "gemm_TFLOPs_effective": flops / sec / 1e12,
+                        "candidates_mean": float(tc.candidates.float().mean().item()),
+                        "candidates_max": int(tc.candidates.max().item()),
+                        "fallback_queries": tc.overflow,
+                        "identical_to_scan_on_first_256": same})
     return out
 
 
