@@ -13,7 +13,7 @@ ROOT = Path(__file__).resolve().parents[1]
 def declared_symbols():
     text = (ROOT / "include" / "pdx_b200.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t)\s+(pdx_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|float)\s+(pdx_\w+)\s*\(", text, flags=re.M)))
 
 
 @pytest.fixture(scope="module")
