@@ -459,3 +459,14 @@ def test_tensor_core_exact_equals_scan(P, metric, k, normalize):
         np.testing.assert_array_equal(out.dist.cpu().numpy(), ref.dist.cpu().numpy())
         np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
         assert int(tc.candidates.max()) < 4096
+
+
+def test_exact_estimator_tensor_core_auto(P):
+    x = recipes.data("skewed", 20_000, 48, 71)
+    Q = recipes.queries("near", x, 80, 72)
+    a = P.ExactNearestNeighbors(pruner="none", criteria="sequential", tensor_cores=True).fit(x)
+    b = P.ExactNearestNeighbors(pruner="none", criteria="sequential", tensor_cores=False).fit(x)
+    da, ia = a.kneighbors(Q, 10)
+    db, ib = b.kneighbors(Q, 10)
+    np.testing.assert_array_equal(ia, ib)
+    np.testing.assert_array_equal(da, db)
