@@ -26,7 +26,7 @@
 //
 // HBM layout (pdx_b200.h): tiles [d_pad/G][64][G].  G = 8 puts one slot's 8
 // consecutive dims in one 32-byte sector: dense early steps read whole 2 KB
-// groups (coalesced float4 loads), and a pruned survivor later costs one
+// groups (coalesced 256-bit loads), and a pruned survivor later costs one
 // sector per 8 dims instead of one per dim.
 #include <cub/block/block_scan.cuh>
 
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
     int32_t* __restrict__ counts, int32_t* __restrict__ overflow) {
   using Scan = cub::BlockScan<int64_t, 256>;
   __shared__ typename Scan::TempStorage tmp;
-  __shared__ int64_t s_b0[256], s_t0[256], s_nt[256], s_toff[256], s_boff[256];
+  __shared__ int64_t s_b0[256], s_t0[256], s_toff[256], s_boff[256];
   __shared__ int64_t run_t, run_b;
   const int q = blockIdx.x;
   if (threadIdx.x == 0) run_t = run_b = 0;
@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
     Scan(tmp).ExclusiveSum(nb, boff, btot);
     s_b0[threadIdx.x] = b0;
     s_t0[threadIdx.x] = t0;
-    s_nt[threadIdx.x] = nt;
     s_toff[threadIdx.x] = toff;
     s_boff[threadIdx.x] = boff;
     __syncthreads();

@@ -1,8 +1,8 @@
 // Speculative tile scan for the compute warps of pdx_scan_kernel.
 //
 // A compute warp owns `tpw` consecutive tiles of a round.  For each tile it
-// runs the DENSE phase — lane l owns slots 2l and 2l+1, the whole warp
-// reads the live slots' dims group by group — until at most kSparseMax of
+// runs the DENSE phase — lane l owns slots l and l+32, the whole warp
+// reads the live slots' dims group by group — until at most sparse_max of
 // the tile's 64 slots survive.  Those survivors are parked in a
 // warp-private list; after the warp's last tile the SPARSE phase finishes
 // them one survivor per lane, so the long tail of the schedule (where a few
