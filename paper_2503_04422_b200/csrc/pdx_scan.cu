@@ -340,6 +340,17 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
     if (A.out_total) PDX_CUDA_CHECK(cudaMemsetAsync(A.out_total, 0, 8 * nq, st));
   }
 
+  // keep the stream-ordered pool mapped between calls (split-mode scratch)
+  static bool pool_kept = false;
+  if (!pool_kept) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_kept = true;
+  }
+
   cudaError_t e;
   const bool ord = d_orders != nullptr;
   const int mt = prm->pruner == PDX_PRUNER_BSA ? kMetricL2Bsa : prm->metric;
