@@ -402,6 +402,10 @@ typedef struct pdx_query_params {
   const float* bsa_coef;     /* host float32 [nsteps] (pruner BSA) */
   int32_t queries_on_device; /* Q is a device pointer */
   int32_t outputs_on_device; /* out_* are device pointers */
+  /* Flat index, pruner none, L2 / IP, nq >= 64: answer through K8 (TF32
+   * tensor-core candidates + exact rescoring; identical results).  0 = off,
+   * 1 = when applicable. */
+  int32_t tensor_cores;
 } pdx_query_params;
 
 /* Searches nq queries Q [nq][d]; out_dist/out_ids [nq][k] as pdx_search

@@ -69,7 +69,8 @@ class PdxQueryParams(C.Structure):
                 ("criteria", C.c_int32), ("zone_width", C.c_int32), ("nprobe", C.c_int32),
                 ("selection_fraction", C.c_double), ("initial_step", C.c_int32),
                 ("rotate", C.c_int32), ("epsilon0", C.c_double), ("bsa_coef", C.c_void_p),
-                ("queries_on_device", C.c_int32), ("outputs_on_device", C.c_int32)]
+                ("queries_on_device", C.c_int32), ("outputs_on_device", C.c_int32),
+                ("tensor_cores", C.c_int32)]
 
 
 class PdxSearchOut(C.Structure):

@@ -7,6 +7,8 @@
 // launches — K3 projection, K2 bucket selection, K4 orders, K5/K6 scan —
 // with the host<->device copies at its ends, so a caller with host buffers
 // pays one C call per batch.
+#include <cublas_v2.h>
+
 #include <cmath>
 #include <vector>
 
@@ -40,6 +42,22 @@ struct DevBuf {
   }
 };
 
+// row r of a flat index = vector r % part of block r / part, row-major
+__global__ void __launch_bounds__(256) tiles_to_rows_kernel(const float* __restrict__ tiles,
+                                                            int64_t tile_stride, int d, int group,
+                                                            const int64_t* __restrict__ block_tile,
+                                                            int64_t part, int64_t n,
+                                                            float* __restrict__ rows) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const int64_t b = r / part, w = r - b * part;
+  const float* tb = tiles + (block_tile[b] + w / kTile) * tile_stride;
+  const int slot = (int)(w % kTile);
+  for (int j = threadIdx.x & 31; j < d; j += 32)
+    rows[r * d + j] = group == 8 ? tb[((j >> 3) * kTile + slot) * 8 + (j & 7)]
+                                 : tb[(int64_t)j * kTile + slot];
+}
+
 int schedule_len(int d, int initial_step) {
   int n = 0;
   for (int64_t e = 0, w = initial_step; e < d; w *= 2, ++n) e = e + w < d ? e + w : d;
@@ -71,9 +89,30 @@ struct pdx_index {
   DevBuf<uint16_t> orders;
   DevBuf<int64_t> ids, touched, total;
   DevBuf<unsigned char> work;
+  // K8 (flat indexes whose blocks hold part_size vectors, the last fewer)
+  int64_t part_size = 0, nrows = 0;
+  DevBuf<float> rows, rn2, qn2, kprev, knext, S;
+  DevBuf<int64_t> cand;
+  DevBuf<int32_t> ccount;
+  cublasHandle_t blas = nullptr;
+  ~pdx_index() {
+    if (blas) cublasDestroy(blas);
+  }
 };
 
 namespace {
+
+// K8 needs blocks of one size (the last may be smaller): record it (0 = no)
+void set_part_size(pdx_index* I, const std::vector<int32_t>& bm) {
+  I->part_size = 0;
+  I->nrows = 0;
+  if (bm.empty() || bm[0] < 1) return;
+  for (size_t b = 0; b + 1 < bm.size(); ++b)
+    if (bm[b] != bm[0]) return;
+  if (bm.back() > bm[0]) return;
+  I->part_size = bm[0];
+  for (int32_t m : bm) I->nrows += m;
+}
 
 // Fill st's derived fields from host block_tile / bucket offsets.
 int finish_store(pdx_index* I, const std::vector<int64_t>& btile, const std::vector<int32_t>& bm,
@@ -107,6 +146,7 @@ int finish_store(pdx_index* I, const std::vector<int64_t>& btile, const std::vec
   s.max_bucket_blocks = mbb;
   s.max_bucket_tiles = mbt;
   s.d_tile_block = I->tile_block.p;
+  set_part_size(I, bm);
   PDX_CUDA_CHECK(cudaStreamSynchronize(st));
   return PDX_OK;
 }
@@ -130,6 +170,83 @@ int set_metadata(pdx_index* I, const double* global_means, const float* rotation
 
 }  // namespace
 
+namespace {
+// K8 inside the handle: TF32 GEMM chunks (cuBLAS) -> pdx_k8_filter ->
+// pdx_k8_rescore.  PDX_ENOSUPPORT when some query's candidates overflowed.
+int k8_search(pdx_index* I, const pdx_query_params* P, const float* dq, int64_t nq,
+              float* out_dist, int64_t* out_ids, cudaStream_t st) {
+  const int d = I->d, k = P->k;
+  const int64_t n = I->nrows;
+  constexpr int C = 4096;
+  PDX_REQUIRE(k <= C, "k too large for the tensor-core path");
+  if (!I->blas) {
+    if (cublasCreate(&I->blas) != CUBLAS_STATUS_SUCCESS) {
+      set_error("cublasCreate failed");
+      return PDX_ECUDA;
+    }
+    cublasSetMathMode(I->blas, CUBLAS_TF32_TENSOR_OP_MATH);
+  }
+  cublasSetStream(I->blas, st);
+  if (I->rows.n < (size_t)(n * d)) {  // row-major copy of the vectors, once
+    PDX_TRY(I->rows.need((size_t)(n * d)));
+    PDX_TRY(I->rn2.need((size_t)n));
+    tiles_to_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
+        I->st.d_tiles, (int64_t)I->st.d_pad * kTile, d, I->st.group, I->st.d_block_tile,
+        I->part_size, n, I->rows.p);
+    PDX_LAUNCH_CHECK();
+    PDX_TRY(pdx_k8_norms(I->rows.p, n, d, I->rn2.p, st));
+  }
+  const int64_t R = 65536;
+  PDX_TRY(I->qn2.need((size_t)nq));
+  PDX_TRY(I->kprev.need((size_t)(nq * k)));
+  PDX_TRY(I->knext.need((size_t)(nq * k)));
+  PDX_TRY(I->cand.need((size_t)(nq * C)));
+  PDX_TRY(I->ccount.need((size_t)nq));
+  PDX_TRY(I->S.need((size_t)(nq * R)));
+  PDX_TRY(pdx_k8_norms(dq, nq, d, I->qn2.p, st));
+  std::vector<float> inf((size_t)(nq * k), INFINITY);
+  PDX_CUDA_CHECK(cudaMemcpyAsync(I->kprev.p, inf.data(), 4 * nq * k, cudaMemcpyHostToDevice, st));
+  PDX_CUDA_CHECK(cudaMemsetAsync(I->ccount.p, 0, 4 * nq, st));
+  float* prev = I->kprev.p;
+  float* next = I->knext.p;
+  const float one = 1.f, zero = 0.f;
+  for (int64_t r0 = 0; r0 < n; r0 += R) {
+    const int rr = (int)(n - r0 < R ? n - r0 : R);
+    // S^T (rr x nq, column-major) = X_c (rr x d) * Q^T: S [nq][rr] row-major
+    if (cublasSgemm(I->blas, CUBLAS_OP_T, CUBLAS_OP_N, rr, (int)nq, d, &one, I->rows.p + r0 * d,
+                    d, dq, d, &zero, I->S.p, rr) != CUBLAS_STATUS_SUCCESS) {
+      set_error("cublasSgemm failed");
+      return PDX_ECUDA;
+    }
+    PDX_TRY(pdx_k8_filter(I->S.p, rr, nq, rr, r0, I->rn2.p + r0, I->qn2.p, P->metric, d, k, prev,
+                          next, I->cand.p, I->ccount.p, C, st));
+    float* t = prev;
+    prev = next;
+    next = t;
+  }
+  std::vector<int32_t> cc((size_t)nq);
+  PDX_CUDA_CHECK(cudaMemcpyAsync(cc.data(), I->ccount.p, 4 * nq, cudaMemcpyDeviceToHost, st));
+  PDX_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (int32_t c : cc)
+    if (c > C) return PDX_ENOSUPPORT;
+  float* dist = out_dist;
+  int64_t* ids = out_ids;
+  if (!P->outputs_on_device) {
+    PDX_TRY(I->dist.need((size_t)(nq * k)));
+    PDX_TRY(I->ids.need((size_t)(nq * k)));
+    dist = I->dist.p;
+    ids = I->ids.p;
+  }
+  PDX_TRY(pdx_k8_rescore(&I->st, I->part_size, dq, nq, P->metric, k, I->cand.p, I->ccount.p, C,
+                         dist, ids, st));
+  if (!P->outputs_on_device) {
+    PDX_CUDA_CHECK(cudaMemcpyAsync(out_dist, dist, 4 * nq * k, cudaMemcpyDeviceToHost, st));
+    PDX_CUDA_CHECK(cudaMemcpyAsync(out_ids, ids, 8 * nq * k, cudaMemcpyDeviceToHost, st));
+  }
+  return PDX_OK;
+}
+}  // namespace
+
 extern "C" int pdx_index_create(const pdx_index_desc* D, pdx_index** out) {
   PDX_REQUIRE(D && out, "pdx_index_create: null argument");
   *out = nullptr;
@@ -142,6 +259,12 @@ extern "C" int pdx_index_create(const pdx_index_desc* D, pdx_index** out) {
   if (D->store) {
     I->st = *D->store;
     I->d = D->store->d;
+    if (D->store->nbuckets == 1 && D->store->nblocks > 0) {  // flat: K8 eligibility
+      std::vector<int32_t> bm((size_t)D->store->nblocks);
+      PDX_CUDA_CHECK(cudaMemcpy(bm.data(), D->store->d_block_m, 4 * bm.size(),
+                                cudaMemcpyDeviceToHost));
+      set_part_size(I, bm);
+    }
     PDX_REQUIRE(D->nlist == 0 || D->nlist == D->store->nbuckets,
                 "nlist %d does not match the store's %d buckets", D->nlist, D->store->nbuckets);
   } else {
@@ -307,6 +430,27 @@ extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const f
       I->resid_step = P->initial_step;
     }
     PDX_TRY(I->coef.upload(P->bsa_coef, (size_t)schedule_len((int)d, P->initial_step), st));
+  }
+  // K8: batched exact L2 / IP over a flat index through the tensor cores
+  if (P->tensor_cores && !ivf && P->pruner == PDX_PRUNER_NONE && !P->rotate &&
+      (P->metric == PDX_METRIC_L2 || P->metric == PDX_METRIC_IP) && nq >= 64 &&
+      I->part_size > 0 && I->nrows >= k) {
+    const int rc = k8_search(I, P, dq, nq, out_dist, out_ids, st);
+    if (rc != PDX_ENOSUPPORT) {  // candidate overflow: answered by the scan below
+      if (rc != PDX_OK) return rc;
+      if (out_touched || out_total) {  // an unpruned exact scan touches every value
+        std::vector<int64_t> all((size_t)nq, I->nrows * d);
+        for (int64_t* o : {out_touched, out_total}) {
+          if (!o) continue;
+          if (P->outputs_on_device)
+            PDX_CUDA_CHECK(cudaMemcpyAsync(o, all.data(), 8 * nq, cudaMemcpyHostToDevice, st));
+          else
+            memcpy(o, all.data(), 8 * nq);
+        }
+      }
+      PDX_CUDA_CHECK(cudaStreamSynchronize(st));
+      return PDX_OK;
+    }
   }
   // scan
   float* dist = out_dist;

@@ -80,7 +80,7 @@ class PdxIndex:
     def search(self, Q, k: int = 10, metric="l2", pruner="none", criteria="sequential",
                nprobe: int = 8, selection_fraction: float = 0.2, initial_step: int = 2,
                epsilon0: float = 2.1, rotate: bool | None = None, bsa=None, stats=False,
-               out=None, stream=None):
+               out=None, stream=None, tensor_cores: bool = True):
         """One pdx_index_search call.  Q: host array (numpy / CPU tensor,
         pinned for overlap) or a CUDA tensor; outputs live where Q lives
         (or in ``out`` = dict of preallocated dist/ids[/touched/total])."""
@@ -108,7 +108,7 @@ class PdxIndex:
                                 _lib.CRITERIA[OrderCriteria(criteria).value], 0,
                                 int(nprobe) if self.nlist else 0, float(selection_fraction),
                                 int(initial_step), int(rot), float(epsilon0), _lib.ptr(coef),
-                                int(on_dev), int(on_dev))
+                                int(on_dev), int(on_dev), int(bool(tensor_cores)))
         _lib.check(_lib.lib().pdx_index_search(
             self._h, C.byref(p), _lib.ptr(Q), nq, _lib.ptr(out["dist"]), _lib.ptr(out["ids"]),
             _lib.ptr(out.get("touched")), _lib.ptr(out.get("total")),

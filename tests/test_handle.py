@@ -82,3 +82,23 @@ def test_borrowed_index_rotation_bsa_and_device_outputs():
     with pytest.raises(ValueError, match="nprobe"):
         h.search(Q, k=10, nprobe=65)
     h.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("metric", ["ip", "l2"])
+def test_handle_tensor_core_path_identical(metric):
+    """pdx_index_search routes large exact batches through K8 (cuBLAS TF32 +
+    exact rescoring inside the library): identical to the scan."""
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((40_000, 64)).astype(np.float32)
+    Q = rng.standard_normal((128, 64)).astype(np.float32)
+    blocks = P.to_blocks(P.VectorCollection.from_array(x), 64)
+    h = P.PdxIndex.from_blocks(blocks, group=8)
+    a = h.search(Q, k=20, metric=metric, stats=True, tensor_cores=True)
+    b = h.search(Q, k=20, metric=metric, stats=True, tensor_cores=False)
+    for key in ("ids", "dist", "touched", "total"):
+        np.testing.assert_array_equal(a[key].numpy(), b[key].numpy())
+    flat = P.flat_build(P.VectorCollection.from_array(x), 64)
+    hb = P.PdxIndex.from_index(flat)  # borrowed store, same path
+    c = hb.search(Q, k=20, metric=metric, tensor_cores=True)
+    np.testing.assert_array_equal(c["ids"].numpy(), b["ids"].numpy())
