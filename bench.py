@@ -253,7 +253,7 @@ def main():
         del searcher._buf["debug_buf"]
         d = dbg.cpu().numpy().astype(np.float64)
         names = ["cycles", "tiles", "fast", "serial", "replay", "commit_idle", "ring_waits",
-                 "sparse_items", "cw_wait", "cw_dense", "cw_sparse", "cw_rest"]
+                 "sparse_items", "cw_wait", "cw_dense", "cw_sparse", "cw_rest", "commit_busy"]
         print("DEBUG per-query mean:", {n: round(float(d[:, i].mean()), 1)
                                         for i, n in enumerate(names)},
               "max cycles", int(d[:, 0].max()), file=sys.stderr)

@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     };
 
     int com = 0, polls = 0;
+    long long c_busy = 0;  // profile build: cycles committing (the rest is waiting)
     while (com < ntiles) {
       // never look past one ring turn: lane >= RB would alias an earlier slot
       const bool rdy =
@@ -636,7 +637,9 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       }
       polls = 0;
       int done = 0;
+      const long long cb = PDX_SCAN_PROFILE ? clock64() : 0;
       while (done < nr) done += commit_run(com + done, nr - done);
+      if (PDX_SCAN_PROFILE) c_busy += clock64() - cb;
       if (lane < done) {
         s_flag[(com + lane) & RMASK] = 0;
         mbar_arrive(&s_free[(com + lane) & RMASK]);
@@ -661,6 +664,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       dg[3] = dbg_serial;
       dg[4] = dbg_replay;
       dg[5] = dbg_idle;
+      dg[12] = c_busy;
     }
   }
   __syncthreads();
