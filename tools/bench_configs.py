@@ -217,6 +217,14 @@ def c1():
         out.append({"config": "C1", "pruner": pruner, "criteria": crit, "queries": nq,
                     "qps": nq / sec, "pruning_power":
                     1 - r.touched.sum().item() / r.total.sum().item()})
+        # throughput mode: each query's blocks over 8 CTAs (exact results, own stats)
+        s8 = P.ExactSearcher(flat, P.SearchParams(k=k, pruner=pruner), crit, splits=8)
+        r8 = s8.run(Qd, stats=True)
+        same = bool((r8.ids == r.ids).all().item() and (r8.dist == r.dist).all().item())
+        sec8 = timed(lambda: s8.run(Qd))
+        out.append({"config": "C1", "pruner": pruner, "criteria": crit, "queries": nq,
+                    "splits": 8, "qps": nq / sec8, "same_results": same,
+                    "pruning_power": 1 - r8.touched.sum().item() / r8.total.sum().item()})
     return out
 
 
