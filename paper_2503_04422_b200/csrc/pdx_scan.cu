@@ -309,7 +309,7 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   A.trace_cap = out->d_trace ? out->trace_cap : 0;
   A.trace_len = out->d_trace_len;
   A.debug = out->d_debug;
-  A.sparse_max = 32 / tpw;
+  A.sparse_max = kItemsPerWarp / tpw;
   PDX_REQUIRE(A.out_dist && A.out_ids, "output buffers required");
 
   // split mode: CTA b scans range b / nq of query b % nq into row b of a

@@ -79,7 +79,7 @@ inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int 
   L.flag = take(sizeof(int32_t) * rb);
   L.desc = take(sizeof(TileDesc) * rb);
   L.sum = take(sizeof(TileSum) * rb);
-  L.items = take(sizeof(SparseItem) * 32 * W);
+  L.items = take(sizeof(SparseItem) * kItemsPerWarp * W);
   L.wbnd = take(sizeof(float) * kMaxSteps * W * tpw);
   L.ids = take(0);
   L.tki = take(sizeof(int64_t) * k);
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     Q.band = s_band;
     Q.bsa = s_bsa;
     Q.bmask = s_bmask;
-    SparseItem* items = reinterpret_cast<SparseItem*>(smem + L.items) + 32 * w;
+    SparseItem* items = reinterpret_cast<SparseItem*>(smem + L.items) + kItemsPerWarp * w;
     float* wbnd = reinterpret_cast<float*>(smem + L.wbnd) + (size_t)w * tpw * kMaxSteps;
     // claims are made one ahead so the next tiles' entries load while the
     // current ones are scanned

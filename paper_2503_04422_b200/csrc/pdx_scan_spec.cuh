@@ -22,7 +22,13 @@
 namespace pdx {
 
 // a tile goes sparse once <= A.sparse_max (= 32 / tiles per claim) slots survive
-constexpr int kMaxTpw = 8;  // tiles per compute-warp claim (sparse_max * tpw <= 32)
+constexpr int kMaxTpw = 8;  // tiles per compute-warp claim
+#ifndef PDX_ITEMS_PER_WARP
+#define PDX_ITEMS_PER_WARP 32
+#endif
+// sparse items a compute warp parks per claim (sparse_max * tpw); the sparse
+// phase finishes them 32 at a time
+constexpr int kItemsPerWarp = PDX_ITEMS_PER_WARP;
 constexpr unsigned kFull = 0xffffffffu;
 
 // One tile of a query's visit list (built by build_visits_kernel).
@@ -361,13 +367,24 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
 // partial at each step end, decides against its tile's speculative bound,
 // and reports counts / survivors with shared-memory atomics.
 template <int G, bool ORD, int METRIC>
+__device__ __forceinline__ void sparse_round(const ScanArgs& A, int q, const QueryRefs& Q,
+                                             const SliceRefs& R, int base, int nitems, int lane);
+
+template <int G, bool ORD, int METRIC>
 __device__ __forceinline__ void sparse_phase(const ScanArgs& A, int q, const QueryRefs& Q,
                                              const SliceRefs& R, int nitems, int lane) {
   if (nitems == 0) return;
   __syncwarp();
+  for (int base = 0; base < nitems; base += 32)
+    sparse_round<G, ORD, METRIC>(A, q, Q, R, base, nitems, lane);
+}
+
+template <int G, bool ORD, int METRIC>
+__device__ __forceinline__ void sparse_round(const ScanArgs& A, int q, const QueryRefs& Q,
+                                             const SliceRefs& R, int base, int nitems, int lane) {
   const int nsteps = A.nsteps;
-  bool act = lane < nitems;
-  const SparseItem it = act ? R.items[lane] : SparseItem{0, 0, 0, 0, 0.f};
+  bool act = base + lane < nitems;
+  const SparseItem it = act ? R.items[base + lane] : SparseItem{0, 0, 0, 0, 0.f};
   const TileDesc& t = R.desc[it.tj];
   const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
   float* __restrict__ part = R.part + (size_t)it.tj * nsteps * kTile;
