@@ -241,10 +241,11 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
     tpw *= 2;
   int rb = 2 * tpw;  // ring slots: a power of two (masks, not divisions, in the kernel)
   while (rb < (prm->ring_slots > 0 ? prm->ring_slots : W * tpw)) rb *= 2;
-  ScanSmem L = scan_smem_layout(W, tpw, rb, prm->k, nsteps, store->d_pad);
+  const bool has_ord = d_orders != nullptr;
+  ScanSmem L = scan_smem_layout(W, tpw, rb, prm->k, nsteps, store->d_pad, has_ord);
   while (rb > 2 * tpw && L.total > optin) {
     rb /= 2;
-    L = scan_smem_layout(W, tpw, rb, prm->k, nsteps, store->d_pad);
+    L = scan_smem_layout(W, tpw, rb, prm->k, nsteps, store->d_pad, has_ord);
   }
   PDX_REQUIRE(L.total <= optin, "k/d too large for shared memory (%d bytes)", L.total);
 

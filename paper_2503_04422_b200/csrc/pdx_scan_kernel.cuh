@@ -56,10 +56,11 @@ static_assert(sizeof(Control) <= 128, "control block");
 // the offsets live in the constant bank instead of being rematerialised.
 struct ScanSmem {
   int32_t ctl, mbar, ratio, band, bsa, ends, bnd, cnt, wmin, flag, desc, sum, items, wbnd, ids,
-      tki, part, tkd, q, bmask, total, rb;
+      tki, part, tkd, q, bmask, ordc, ordseg, total, rb;
 };
 
-inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int d_pad) {
+inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int d_pad,
+                                 bool ord = false) {
   ScanSmem L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -87,6 +88,9 @@ inline ScanSmem scan_smem_layout(int W, int tpw, int rb, int k, int nsteps, int 
   L.tkd = take(sizeof(float) * k);
   L.q = take(sizeof(float) * ((d_pad + 7) / 8) * 8);
   L.bmask = take((d_pad + 7) / 8);
+  // visit orders: each compute warp keeps its current segment's order on chip
+  L.ordc = take(ord ? sizeof(uint16_t) * d_pad * W : 0);
+  L.ordseg = take(ord ? sizeof(int32_t) * W : 0);
   L.total = (int32_t)o;
   L.rb = rb;
   return L;
@@ -283,6 +287,9 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   const int ngroups = (A.d_pad + 7) / 8;
   for (int j = threadIdx.x; j < ngroups * 8; j += blockDim.x) s_q[j] = j < A.d ? qg[j] : 0.f;
   for (int j = threadIdx.x; j < ngroups; j += blockDim.x) s_bmask[j] = 0;
+  if (ORD)  // one staged-order tag per compute warp
+    for (int j = threadIdx.x; j < (int)(blockDim.x >> 5) - 1; j += blockDim.x)
+      reinterpret_cast<int32_t*>(smem + L.ordseg)[j] = -1;
   for (int j = threadIdx.x; j < RB; j += blockDim.x) {
     s_flag[j] = 0;
     mbar_init(&s_ready[j]);
@@ -424,6 +431,8 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
       R.sum = s_sum + sl;
       R.bnd = wbnd;
       R.items = items;
+      R.ordc = ORD ? reinterpret_cast<uint16_t*>(smem + L.ordc) + (size_t)w * A.d_pad : nullptr;
+      R.ordseg = ORD ? reinterpret_cast<int32_t*>(smem + L.ordseg) + w : nullptr;
       int nitems = 0;
       for (int j = 0; j < nt; ++j) {
         if (G == 8 && !ORD)

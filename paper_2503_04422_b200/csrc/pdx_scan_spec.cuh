@@ -109,7 +109,9 @@ struct SliceRefs {
   float* part;           // [tpw][nsteps][64]
   TileSum* sum;          // [tpw]
   float* bnd;            // [tpw][kMaxSteps] speculative bound per step
-  SparseItem* items;     // [32]
+  SparseItem* items;     // [kItemsPerWarp]
+  uint16_t* ordc;        // this warp's staged visit order (ORD), d entries
+  int32_t* ordseg;       // the segment it belongs to (-1: none)
 };
 
 // Per-query constants shared by all warps.
@@ -151,6 +153,21 @@ __device__ __forceinline__ float bsa_resid(const ScanArgs& A, int64_t tile, int 
 
 __device__ __forceinline__ const uint16_t* order_of(const ScanArgs& A, int q, int seg) {
   return A.orders + ((int64_t)q * A.oqs + (int64_t)seg * A.oss) * A.d;
+}
+
+// The warp's visit order for segment `seg` (warp-uniform), staged in shared
+// memory once per segment: the per-dim index reads then cost no L2 trip.
+__device__ __forceinline__ const uint16_t* warp_order(const ScanArgs& A, int q, int seg,
+                                                      const SliceRefs& R, int lane) {
+  if (*R.ordseg != seg) {
+    __syncwarp();
+    const uint16_t* g = order_of(A, q, seg);
+    for (int j = lane; j < A.d; j += 32) R.ordc[j] = __ldg(g + j);
+    __syncwarp();
+    if (lane == 0) *R.ordseg = seg;
+    __syncwarp();
+  }
+  return R.ordc;
 }
 
 // Lane `lane` < nsteps holds the tile's speculative bound for step `lane`.
@@ -287,7 +304,7 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
                                                    int tj, const QueryRefs& Q,
                                                    const SliceRefs& R, int& nitems, int lane) {
   const float* __restrict__ tb = A.tiles + t.tile * A.tile_stride;
-  const uint16_t* __restrict__ ord = ORD ? order_of(A, q, t.seg) : nullptr;
+  const uint16_t* __restrict__ ord = ORD ? warp_order(A, q, t.seg, R, lane) : nullptr;
   float* __restrict__ part = R.part + (size_t)tj * A.nsteps * kTile;
   TileSum& sum = R.sum[tj];
   const int nsteps = A.nsteps;
@@ -317,7 +334,7 @@ __device__ __forceinline__ void dense_tile_generic(const ScanArgs& A, int q, con
         const int j = j0 + e;
         dim[e] = 0;
         x0[e] = x1[e] = 0.f;
-        if (j < b) dim[e] = ORD ? (int)__ldg(ord + j) : j;
+        if (j < b) dim[e] = ORD ? (int)ord[j] : j;
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -441,7 +458,9 @@ __device__ __forceinline__ void sparse_round(const ScanArgs& A, int q, const Que
       }
     }
   } else {
-    const uint16_t* __restrict__ ord = ORD ? order_of(A, q, t.seg) : nullptr;
+    // the staged order when the item's segment is the warp's current one
+    const uint16_t* __restrict__ ord =
+        ORD ? (t.seg == *R.ordseg ? R.ordc : order_of(A, q, t.seg)) : nullptr;
     int end = act ? Q.ends[s] : 0;
     while (__any_sync(kFull, act)) {
       if (act) {
@@ -452,7 +471,7 @@ __device__ __forceinline__ void sparse_round(const ScanArgs& A, int q, const Que
         for (int e = 0; e < 8; ++e) {
           dim[e] = 0;
           x[e] = 0.f;
-          if (pos + e < jend) dim[e] = ORD ? (int)__ldg(ord + pos + e) : pos + e;
+          if (pos + e < jend) dim[e] = ORD ? (int)ord[pos + e] : pos + e;
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
