@@ -163,6 +163,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--debug", action="store_true", help="print kernel diagnostics to stderr")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--batched", type=int, default=0,
+                    help="pdx_search_params.batched: 0 auto, 1 per-query scan, 2 batched")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     args.warps = tuple(int(v) for v in str(args.warps).split(",")) if "," in str(args.warps) else int(args.warps)
@@ -224,7 +226,7 @@ def main():
         from paper_2503_04422_b200.sharded import shard_index
         index = shard_index(index, col, rank, ws)
     params = P.SearchParams(k=K, pruner="ads", ads=P.AdsPruner(d=D, epsilon0=EPS))
-    searcher = P.IvfSearcher(index, params, args.nprobe, warps=args.warps)
+    searcher = P.IvfSearcher(index, params, args.nprobe, warps=args.warps, batched=args.batched)
     Qd = P.store.to_device(Q)
     Tm = P.store.to_device(T.matrix)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)

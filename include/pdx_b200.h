@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PDX_ABI_VERSION 2
+#define PDX_ABI_VERSION 3
 
 #define PDX_OK 0
 #define PDX_EINVAL 1    /* bad argument (Python: ValueError) */
@@ -128,6 +128,15 @@ typedef struct pdx_search_params {
    * has one chain); ADS / BSA become recall-level.  No survivor traces.
    * Lets one query use the whole GPU (batch-1 exact search, C4). */
   int32_t splits;
+  /* IVF query batches (per-query bucket selection, 64-vector blocks, G = 8
+   * tiles, natural dimension order, pruner ads / bond / bsa, no split):
+   *   0 = auto: the bucket-major batched pipeline when the batch has at
+   *       least 32 queries, else the per-query scan;
+   *   1 = always the per-query scan;  2 = batched whenever eligible.
+   * Both give the reference's results, decisions and stats bit for bit
+   * (DESIGN.md §3.2); the batched one evaluates each tile once for every
+   * query that probes its bucket. */
+  int32_t batched;
 } pdx_search_params;
 
 /* Outputs of pdx_search.  Per query q (row q of each array):

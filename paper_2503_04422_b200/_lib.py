@@ -46,7 +46,8 @@ class PdxSearchParams(C.Structure):
                 ("initial_step", C.c_int32), ("selection_fraction", C.c_double),
                 ("ads_d", C.c_int32), ("warps", C.c_int32), ("ads_epsilon0", C.c_double),
                 ("tiles_per_warp", C.c_int32), ("ring_slots", C.c_int32),
-                ("bsa_coef", C.c_void_p), ("splits", C.c_int32)]
+                ("bsa_coef", C.c_void_p), ("splits", C.c_int32),
+                ("batched", C.c_int32)]
 
 
 class PdxFileInfo(C.Structure):
@@ -135,7 +136,7 @@ def lib():
                                     C.c_uint64, vp, vp, vp, vp]
         for name in EXPORTS:
             getattr(L, name).restype = getattr(L, name).restype or C.c_int
-        if L.pdx_abi_version() != 2:
+        if L.pdx_abi_version() != 3:
             raise RuntimeError("libpdx_b200.so ABI version mismatch")
         _lib = L
     return _lib

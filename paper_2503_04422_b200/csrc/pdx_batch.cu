@@ -1,0 +1,1071 @@
+// Bucket-major batched IVF search: the reference's ivf_search (index.py:130-156)
+// for a whole query batch, with results, every prune decision and the stats
+// of the reference (search.py:125-205), bit for bit.
+//
+// Why: at IVF scale a probed bucket is shared by many queries of a batch
+// (C2: ~31 queries per probed bucket), but the per-query scan
+// (pdx_scan_kernel) re-reads and re-evaluates each tile once per query along
+// a latency-bound chain.  Here each tile's head dimensions are loaded into
+// registers ONCE per work item and evaluated for every query probing it.
+//
+// The reference's threshold chain is sequential per query (T_b = the k-th
+// best distance when block b starts, search.py:159).  Exactness comes from
+// three facts: partial sums do not depend on T, the ADS / BOND / BSA bounds
+// are monotone in T, and the top-k after a set of pushes does not depend on
+// their order (TopK keeps the k smallest (dist, id) pairs, search.py:44-51).
+//
+//  Phase 1  the per-query scan over each query's FIRST selected bucket only:
+//           heap H (exact), T' = its k-th distance.  Every later block has
+//           T_b <= T'.
+//  Phase 2  (bscan_kernel) every (query, tile) pair of the remaining buckets
+//           under the fixed bound B_s(T'): per-step survivor counts, the
+//           pair's certainty margin rho = max over (slot, step) surviving
+//           under T' of v_s / beta_s (beta_s: the bound's factor, B_s(T) ~
+//           T beta_s), and the T'-survivors with their distances.
+//  Chain    (bchain_kernel) per query: T^_p = the k-th smallest of H and the
+//           T'-survivors of pairs before p — the reference's T_b provided
+//           every T'-survivor is a real survivor.  A pair whose decisions
+//           could differ between T^_p and T' (T^_p < T' and rho_p >= T^_p,
+//           with slack) is listed as uncertain.
+//  Recompute (bscan_kernel MODE 1) re-evaluates each uncertain pair exactly
+//           under T^_p, tile-major like phase 2, overwriting its stats and
+//           confirming its real survivors.  A T'-survivor it does not
+//           confirm is dropped; if its distance is below T^_p (an ADS prune
+//           of the exact chain that T' did not make) the assumption behind
+//           T^ broke and the query is flagged.
+//  Final    (bfinal_kernel) top-k = k smallest of H and all T'-survivors,
+//           values_touched / values_total / survivor traces summed per pair.
+//  Fallback flagged queries (and any whose phase-1 heap is not full, or
+//           whose buffers overflowed) are re-run by the per-query scan.
+//
+// Certain pairs: for T in [T^_p, T'] a slot pruned under T' is pruned under
+// T (monotone), and a slot surviving step s under T' has v_s < B_s(T^_p) <=
+// B_s(T), so the decisions, counts and survivors are T'-s.  By induction
+// over the pairs the chain's T_b equals T^_p everywhere when no query is
+// flagged.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "pdx_batch.cuh"
+#include "pdx_common.cuh"
+#include "pdx_scan_kernel.cuh"
+
+namespace pdx {
+namespace {
+
+constexpr int kBW = 8;          // warps per work-item CTA
+constexpr int kQC = 32;         // queries per work item
+constexpr int kHeadDims = 16;   // dims every pair evaluates for all 64 slots
+constexpr int kMaxHead = 5;     // steps inside the head (initial_step 1: 1,3,7,15)
+constexpr int kDeepCap = 64;    // deep items per warp queue
+constexpr int kMaxBatchK = 256;
+constexpr float kRhoSlack = 1.00001f;
+
+struct BEntry {  // a query probing a bucket
+  int32_t q;
+  int32_t base;  // query-local pair index of the bucket's first tile
+};
+struct BItem {
+  int32_t bucket, e0, ne, pad;
+};
+// A T'-survivor (phase 2).  The chain kernel sorts a query's list by pair and
+// sets tafter = T^ after the pushes of that pair; the recompute pass sets
+// real = 1 on the survivors it confirms under T^.
+struct BSurv {
+  float dist;
+  int32_t pair;  // query-local pair index
+  int64_t id;
+  int32_t slot;
+  float tafter;
+  int32_t real;
+  int32_t pad;
+};
+struct DeepItem {
+  float acc;
+  int16_t j, slot;
+  float that;  // recompute pass: the pair's T^
+};
+
+// Per-call constants (kernel parameter; copied to shared memory where they
+// are indexed at run time).
+struct BParams {
+  int32_t d, d_pad, nsteps, hsteps, hdims, k, pruner, nseg;
+  int32_t nq, surv_cap;
+  uint32_t hmask;  // bit e: a head step ends after dim e
+  int32_t ends[kMaxSteps];
+  double ratio[kMaxSteps], band[kMaxSteps];
+  float invb[kMaxSteps];
+  int32_t wmin[kTile + 1];
+};
+
+struct BArgs {
+  const float* tiles;
+  const int64_t* tile_ids;
+  int64_t tile_stride;
+  const int64_t* bucket_block;
+  const int64_t* block_tile;
+  const int32_t* block_m;
+  const float* queries;
+  const int32_t* sel;  // [nq][nseg]
+  const float* resid;  // BSA [ntiles][nsteps][64]
+  const float* coef;   // BSA [nsteps]
+  // per query
+  float* tprime;
+  float* bounds;        // [nq][nsteps]  B_s(T')
+  float* bsaq;          // BSA [nq][2][nsteps]  rq_s, sqrt(rq_s)
+  const int64_t* qoff;  // [nq+1]
+  int32_t* flags;
+  int32_t* nsurv;
+  BSurv* surv;  // [nq][surv_cap]
+  // per pair
+  uint32_t* ptouched;
+  float* prho;
+  uint8_t* pcnt;  // [P][nsteps] (survivor traces only)
+  // work
+  const BItem* items;
+  const int32_t* nitems;
+  const BEntry* entries;
+  const int64_t* bnvec;  // vectors per bucket
+  // outputs
+  float* out_dist;
+  int64_t* out_ids;
+  int32_t* out_count;
+  int64_t* out_touched;
+  int64_t* out_total;
+  int32_t* trace;
+  int64_t trace_cap;
+  int64_t* trace_len;
+};
+
+__device__ __forceinline__ float l2upd(float acc, float q, float x) {
+  const float t = __fsub_rn(q, x);
+  return __fadd_rn(acc, __fmul_rn(t, t));
+}
+
+// BSA estimate (bsa_est in pdx_scan_spec.cuh, same association).
+__device__ __forceinline__ float bsa_est2(float acc, float rx, float rq, float sq, float coef) {
+  const float cx = __fmul_rn(coef, __fsqrt_rn(rx));
+  return __fsub_rn(__fadd_rn(__fadd_rn(acc, rx), rq), __fmul_rn(cx, sq));
+}
+
+// --------------------------------------------------------------- planning
+// One warp per query: first bucket, query-local pair bases of the other
+// selected buckets, the window's pair count, and the bucket histogram.
+__global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
+                             const int64_t* __restrict__ bucket_block,
+                             const int64_t* __restrict__ block_tile, int32_t* __restrict__ seg0,
+                             int64_t* __restrict__ wcount, int32_t* __restrict__ pbase,
+                             int32_t* __restrict__ bcnt) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const int32_t* sq = sel + (int64_t)q * nseg;
+  if (lane == 0) seg0[q] = sq[0];
+  int run = 0;
+  for (int s0 = 1; s0 < nseg; s0 += 32) {
+    const int s = s0 + lane;
+    int nt = 0;
+    if (s < nseg) {
+      const int c = sq[s];
+      nt = (int)(block_tile[bucket_block[c + 1]] - block_tile[bucket_block[c]]);
+      if (nt > 0) atomicAdd(&bcnt[c], 1);
+    }
+    int incl = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (s < nseg) pbase[(int64_t)q * nseg + s] = run + incl - nt;
+    run += __shfl_sync(kFull, incl, 31);
+  }
+  if (lane == 0) wcount[q] = run;
+}
+
+// Per bucket: work-item count and vector count.
+__global__ void bchunks_kernel(const int32_t* __restrict__ bcnt, int nb,
+                               const int64_t* __restrict__ bucket_block,
+                               const int32_t* __restrict__ block_m, int32_t* __restrict__ nch,
+                               int64_t* __restrict__ bnvec) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  if (c == nb) {
+    nch[c] = 0;
+    return;
+  }
+  nch[c] = (bcnt[c] + kQC - 1) / kQC;
+  int64_t v = 0;
+  for (int64_t b = bucket_block[c]; b < bucket_block[c + 1]; ++b) v += block_m[b];
+  bnvec[c] = v;
+}
+
+__global__ void bfill_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
+                             const int64_t* __restrict__ bucket_block,
+                             const int64_t* __restrict__ block_tile,
+                             const int32_t* __restrict__ pbase, const int32_t* __restrict__ boff,
+                             int32_t* __restrict__ bcur, BEntry* __restrict__ entries) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = nseg - 1;
+  if (i >= (int64_t)nq * per) return;
+  const int q = (int)(i / per), s = 1 + (int)(i % per);
+  const int c = sel[(int64_t)q * nseg + s];
+  if (block_tile[bucket_block[c + 1]] == block_tile[bucket_block[c]]) return;
+  const int pos = atomicAdd(&bcur[c], 1);
+  entries[boff[c] + pos] = BEntry{q, pbase[(int64_t)q * nseg + s]};
+}
+
+__global__ void bitems_kernel(const int32_t* __restrict__ bcnt, int nb,
+                              const int32_t* __restrict__ boff, const int32_t* __restrict__ choff,
+                              BItem* __restrict__ items, int32_t* __restrict__ nitems) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c == 0) *nitems = choff[nb];
+  if (c >= nb) return;
+  const int n = bcnt[c];
+  for (int i = 0, j = choff[c]; i < n; i += kQC, ++j)
+    items[j] = BItem{c, boff[c] + i, min(kQC, n - i), 0};
+}
+
+// T' per query (the phase-1 heap's k-th distance), the bounds B_s(T'), and
+// the BSA query residual energies (the scan kernel's prologue order).
+__global__ void btprime_kernel(const BParams P, BArgs A) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P.nq) return;
+  const int cnt = A.out_count[q];
+  const float T = cnt >= P.k ? A.out_dist[(int64_t)q * P.k + P.k - 1] : INFINITY;
+  float* tp = const_cast<float*>(A.tprime);
+  float* bd = const_cast<float*>(A.bounds);
+  tp[q] = T;
+  A.flags[q] = T == INFINITY ? 1 : 0;
+  A.nsurv[q] = 0;
+  for (int s = 0; s < P.nsteps; ++s)
+    bd[(int64_t)q * P.nsteps + s] =
+        T == INFINITY ? -INFINITY
+                      : (P.pruner == PDX_PRUNER_BSA ? T : ads_or_bond_bound(T, P.ratio[s], P.band[s]));
+  if (P.pruner == PDX_PRUNER_BSA) {
+    const float* qg = A.queries + (int64_t)q * P.d;
+    float* bq = const_cast<float*>(A.bsaq) + (int64_t)q * 2 * P.nsteps;
+    for (int s = 0; s < P.nsteps; ++s) {
+      float r = 0.f;
+      for (int j = P.ends[s]; j < P.d; ++j) r = __fadd_rn(r, __fmul_rn(qg[j], qg[j]));
+      bq[s] = r;
+      bq[P.nsteps + s] = __fsqrt_rn(r);
+    }
+  }
+}
+
+__device__ __forceinline__ void record_survivor(const BParams& P, const BArgs& A, int q,
+                                                int32_t pair, float dist, int64_t tile, int slot) {
+  const int i = atomicAdd(&A.nsurv[q], 1);
+  if (i < P.surv_cap)
+    A.surv[(int64_t)q * P.surv_cap + i] =
+        BSurv{dist, pair, __ldg(A.tile_ids + tile * kTile + slot), slot, 0.f, 0, 0};
+  else
+    A.flags[q] = 1;
+}
+
+// ------------------------------------------------------------ phase 2 scan
+// Head schedule known at compile time: initial_step IS, step s ends after
+// dim IS * (2^(s+1) - 1) (step_schedule, search.py:106-117) while <= 16.
+// IS = 0 is the run-time version (any schedule, d < 16).
+template <int IS>
+struct HeadSched {
+  static constexpr int n = IS == 0 ? 0
+                           : (15 * IS <= kHeadDims) ? 4
+                           : (7 * IS <= kHeadDims)  ? 3
+                           : (3 * IS <= kHeadDims)  ? 2
+                           : (IS <= kHeadDims)      ? 1
+                                                    : 0;
+  static constexpr int dims = n > 0 ? ((2 << (n - 1)) - 1) * IS : 0;
+  __host__ __device__ static constexpr int step_at(int e) {  // step ending after dim e
+    return (n >= 1 && e + 1 == IS)       ? 0
+           : (n >= 2 && e + 1 == 3 * IS) ? 1
+           : (n >= 3 && e + 1 == 7 * IS) ? 2
+           : (n >= 4 && e + 1 == 15 * IS) ? 3
+                                          : -1;
+  }
+};
+
+// A pair is uncertain (its decisions may differ between T' and T^) unless
+// T^ == T' or every (slot, step) surviving under T' has v_s < B_s(T^): rho
+// bounds v_s / beta_s and kRhoSlack covers the rounding of rho, beta_s and
+// B_s.
+__device__ __forceinline__ bool pair_uncertain(float that, float tp, float rho) {
+  return that < tp && !(that >= 1e-30f && __fmul_rn(rho, kRhoSlack) < that);
+}
+
+// T^ before pair `pl` of query q: tafter of the last survivor of an earlier
+// pair in the query's pair-sorted list, else T'.
+__device__ __forceinline__ float that_of(const BSurv* sv, int n, int pl, float tp) {
+  int lo = 0, hi = n;  // first entry with pair >= pl
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sv[mid].pair < pl) lo = mid + 1; else hi = mid;
+  }
+  return lo > 0 ? sv[lo - 1].tafter : tp;
+}
+
+__device__ __forceinline__ void confirm_survivor(const BParams& P, const BArgs& A, int q, int pl,
+                                                 int slot) {
+  BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
+  const int n = min(A.nsurv[q], P.surv_cap);
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sv[mid].pair < pl) lo = mid + 1; else hi = mid;
+  }
+  for (; lo < n && sv[lo].pair == pl; ++lo)
+    if (sv[lo].slot == slot) {
+      sv[lo].real = 1;
+      return;
+    }
+  A.flags[q] = 1;  // not a T'-survivor: cannot happen (T^ <= T'); fall back
+}
+
+__device__ __forceinline__ float bound_at(const BParams& P, float T, int s, const double* ratio,
+                                          const double* band) {
+  return P.pruner == PDX_PRUNER_BSA ? T : ads_or_bond_bound(T, ratio[s], band[s]);
+}
+
+// One CTA per work item (a bucket and up to kQC queries probing it).  Warp w
+// takes tiles w, w + kBW, ... of the bucket; per tile, lane l holds the head
+// dims of slots l and l + 32 in registers and loops over the queries.
+// Slots alive after the head become deep items, finished one per lane.
+// MODE 0: every pair under B_s(T').  MODE 1: only the uncertain pairs, under
+// B_s(T^_p) — their stats are overwritten and their real survivors confirmed.
+template <int IS, bool BSA, int MODE>
+__global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, const BArgs A) {
+  __shared__ __align__(16) float s_qh[kQC][kHeadDims];
+  __shared__ __align__(16) float s_bnd[kQC][kMaxSteps];
+  __shared__ float s_bq[BSA ? kQC : 1][2][kMaxHead];  // BSA head: rq_s, sqrt(rq_s)
+  __shared__ int32_t s_qid[kQC], s_base[kQC];
+  __shared__ int64_t s_qo[kQC];
+  __shared__ float s_tp[kQC];
+  __shared__ uint32_t s_hcnt[kBW][kQC];             // head-step counts, one byte per step
+  __shared__ uint32_t s_dcnt[kBW][kQC][kMaxSteps];  // deep-step counts
+  __shared__ uint32_t s_rho[kBW][kQC];
+  __shared__ float s_that[kBW][kQC];                // MODE 1: T^ of this tile's pairs
+  __shared__ DeepItem s_deep[kBW][kDeepCap];
+  __shared__ float s_rx[BSA ? kBW : 1][kMaxHead][kTile];
+  __shared__ int32_t s_ends[kMaxSteps], s_wmin[kTile + 1];
+  __shared__ float s_invb[kMaxSteps], s_coef[kMaxSteps];
+  __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
+
+  if ((int)blockIdx.x >= *A.nitems) return;
+  const BItem it = A.items[blockIdx.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ne = it.ne, nsteps = P.nsteps;
+  const int64_t b0 = A.bucket_block[it.bucket];
+  const int nt = (int)(A.bucket_block[it.bucket + 1] - b0);
+  const int64_t t0 = A.block_tile[b0];
+  for (int i = threadIdx.x; i < ne * kHeadDims; i += blockDim.x) {
+    const int j = i / kHeadDims, e = i % kHeadDims;
+    const int q = A.entries[it.e0 + j].q;
+    s_qh[j][e] = e < P.d ? A.queries[(int64_t)q * P.d + e] : 0.f;
+  }
+  if (MODE == 0)
+    for (int i = threadIdx.x; i < ne * nsteps; i += blockDim.x) {
+      const int j = i / nsteps, s = i % nsteps;
+      s_bnd[j][s] = A.bounds[(int64_t)A.entries[it.e0 + j].q * nsteps + s];
+    }
+  if (BSA)
+    for (int i = threadIdx.x; i < ne * P.hsteps; i += blockDim.x) {
+      const int j = i / P.hsteps, s = i % P.hsteps;
+      const float* bq = A.bsaq + (int64_t)A.entries[it.e0 + j].q * 2 * nsteps;
+      s_bq[j][0][s] = bq[s];
+      s_bq[j][1][s] = bq[nsteps + s];
+    }
+  for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+    const BEntry en = A.entries[it.e0 + j];
+    s_qid[j] = en.q;
+    s_base[j] = en.base;
+    s_qo[j] = A.qoff[en.q];
+    s_tp[j] = A.tprime[en.q];
+  }
+  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
+    s_ends[i] = P.ends[i];
+    s_invb[i] = P.invb[i];
+    s_ratio[i] = P.ratio[i];
+    s_band[i] = P.band[i];
+    s_coef[i] = (BSA && i < nsteps) ? A.coef[i] : 0.f;
+  }
+  for (int i = threadIdx.x; i <= kTile; i += blockDim.x) s_wmin[i] = P.wmin[i];
+  __syncthreads();
+
+  constexpr int HS = HeadSched<IS>::n, HD = HeadSched<IS>::dims;
+  const int hs = IS ? HS : P.hsteps, hd = IS ? HD : P.hdims;
+  const float ib0 = s_invb[0], ib1 = s_invb[1], ib2 = s_invb[2], ib3 = s_invb[3];
+  for (int ti = w; ti < nt; ti += kBW) {
+    const int64_t tile = t0 + ti;
+    // MODE 1: which queries of this tile are uncertain (bit j)
+    uint32_t todo = 0xffffffffu >> (32 - ne);
+    if (MODE == 1) {
+      bool unc = false;
+      if (lane < ne) {
+        const int q = s_qid[lane], pl = s_base[lane] + ti;
+        if (!A.flags[q]) {
+          const BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
+          const float that = that_of(sv, min(A.nsurv[q], P.surv_cap), pl, s_tp[lane]);
+          unc = pair_uncertain(that, s_tp[lane], A.prho[s_qo[lane] + pl]);
+          if (unc) s_that[w][lane] = that;
+        }
+      }
+      todo = __ballot_sync(kFull, unc);
+      if (!todo) continue;
+      __syncwarp();
+    }
+    const int m = A.block_m[b0 + ti];
+    const float* __restrict__ tb = A.tiles + tile * A.tile_stride;
+    float x0[kHeadDims], x1[kHeadDims];
+    ldg8(tb + lane * 8, *reinterpret_cast<float(*)[8]>(x0));
+    ldg8(tb + (32 + lane) * 8, *reinterpret_cast<float(*)[8]>(x1));
+    if ((IS ? HD : kHeadDims) > 8 && P.d_pad > 8) {
+      ldg8(tb + (kTile + lane) * 8, *reinterpret_cast<float(*)[8]>(x0 + 8));
+      ldg8(tb + (kTile + 32 + lane) * 8, *reinterpret_cast<float(*)[8]>(x1 + 8));
+    } else {
+#pragma unroll
+      for (int e = 8; e < kHeadDims; ++e) x0[e] = x1[e] = 0.f;
+    }
+    if (BSA) {
+      for (int s = 0; s < hs; ++s) {
+        s_rx[w][s][lane] = __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + lane);
+        s_rx[w][s][lane + 32] = __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + lane + 32);
+      }
+      __syncwarp();
+    }
+    const bool in0 = lane < m, in1 = lane + 32 < m;
+    int qn = 0;  // deep items queued by this warp for this tile
+
+    // finish the queued deep items, one per lane (all belong to this tile)
+    auto flush = [&]() {
+      __syncwarp();
+      for (int b = 0; b < qn; b += 32) {
+        bool act = b + lane < qn;
+        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f};
+        const int j = di.j, slot = di.slot;
+        const int q = s_qid[j];
+        const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
+        const bool q4 = (P.d & 3) == 0;
+        float acc = di.acc;
+        int s = hs, pos = hd;
+        while (act) {
+          const int g = pos >> 3;
+          float x[8], qv[8];
+          ldg8(tb + ((size_t)g * kTile + slot) * 8, x);
+          if (q4 && g * 8 + 8 <= P.d) {
+            const float4 a = ldg4(qg + g * 8), c = ldg4(qg + g * 8 + 4);
+            qv[0] = a.x; qv[1] = a.y; qv[2] = a.z; qv[3] = a.w;
+            qv[4] = c.x; qv[5] = c.y; qv[6] = c.z; qv[7] = c.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + g * 8 + e) : 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int dim = g * 8 + e;
+            if (act && dim >= pos) {
+              acc = l2upd(acc, qv[e], x[e]);
+              if (dim + 1 == s_ends[s]) {
+                float v = acc;
+                if (BSA) {
+                  const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
+                  v = bsa_est2(acc, __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + slot),
+                               bq[s], bq[nsteps + s], s_coef[s]);
+                }
+                const float B = MODE == 0 ? s_bnd[j][s] : bound_at(P, di.that, s, s_ratio, s_band);
+                const bool ok = v < B;
+                if (ok) {
+                  atomicAdd(&s_dcnt[w][j][s], 1u);
+                  if (MODE == 0)
+                    atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
+                }
+                ++s;
+                if (!ok) {
+                  act = false;
+                } else if (s == nsteps) {
+                  if (MODE == 0)
+                    record_survivor(P, A, q, s_base[j] + ti, acc, tile, slot);
+                  else
+                    confirm_survivor(P, A, q, s_base[j] + ti, slot);
+                  act = false;
+                }
+              }
+            }
+          }
+          pos = (g + 1) * 8;
+        }
+      }
+      __syncwarp();
+      qn = 0;
+    };
+
+    for (uint32_t tm = todo; tm; tm &= tm - 1) {
+      const int j = __ffs(tm) - 1;
+      if (lane >= hs && lane < nsteps) s_dcnt[w][j][lane] = 0u;
+      float bnd[kMaxHead];
+      float that = 0.f;
+      if (MODE == 0) {
+        const float4 b4 = *reinterpret_cast<const float4*>(s_bnd[j]);
+        bnd[0] = b4.x; bnd[1] = b4.y; bnd[2] = b4.z; bnd[3] = b4.w;
+        bnd[4] = s_bnd[j][4];
+      } else {
+        that = s_that[w][j];
+        const float bl = lane < nsteps ? bound_at(P, that, lane, s_ratio, s_band) : 0.f;
+#pragma unroll
+        for (int s = 0; s < kMaxHead; ++s) bnd[s] = __shfl_sync(kFull, bl, s);
+      }
+      float acc0 = 0.f, acc1 = 0.f, rho = 0.f;
+      bool al0 = in0, al1 = in1;
+      uint32_t packed = 0;
+      auto step = [&](int s, float ib) {
+        float v0 = acc0, v1 = acc1;
+        if (BSA) {
+          v0 = bsa_est2(acc0, s_rx[w][s][lane], s_bq[j][0][s], s_bq[j][1][s], s_coef[s]);
+          v1 = bsa_est2(acc1, s_rx[w][s][lane + 32], s_bq[j][0][s], s_bq[j][1][s], s_coef[s]);
+        }
+        const float B = bnd[s];
+        al0 = al0 && v0 < B;
+        al1 = al1 && v1 < B;
+        if (MODE == 0) {
+          if (al0) rho = fmaxf(rho, __fmul_rn(v0, ib));
+          if (al1) rho = fmaxf(rho, __fmul_rn(v1, ib));
+        }
+        const uint32_t c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
+        packed |= c << (8 * s);
+      };
+      if (IS > 0) {
+        float qv[HD > 0 ? HD : 1];
+#pragma unroll
+        for (int i = 0; i < (HD + 3) / 4; ++i) {
+          const float4 t = *reinterpret_cast<const float4*>(&s_qh[j][4 * i]);
+          if (4 * i < HD) qv[4 * i] = t.x;
+          if (4 * i + 1 < HD) qv[4 * i + 1] = t.y;
+          if (4 * i + 2 < HD) qv[4 * i + 2] = t.z;
+          if (4 * i + 3 < HD) qv[4 * i + 3] = t.w;
+        }
+#pragma unroll
+        for (int e = 0; e < HD; ++e) {
+          acc0 = l2upd(acc0, qv[e], x0[e]);
+          acc1 = l2upd(acc1, qv[e], x1[e]);
+          const int s = HeadSched<IS>::step_at(e);
+          if (s >= 0) step(s, s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3);
+        }
+      } else {
+        int s = 0;
+        const uint32_t hmask = P.hmask;
+#pragma unroll
+        for (int e = 0; e < kHeadDims; ++e) {
+          if (e < hd) {
+            const float qe = s_qh[j][e];
+            acc0 = l2upd(acc0, qe, x0[e]);
+            acc1 = l2upd(acc1, qe, x1[e]);
+            if ((hmask >> e) & 1u) {
+              step(s, s_invb[s]);
+              ++s;
+            }
+          }
+        }
+      }
+      if (lane == 0) s_hcnt[w][j] = packed;
+      if (MODE == 0) {
+        const uint32_t r = __reduce_max_sync(kFull, __float_as_uint(rho));
+        if (lane == 0) s_rho[w][j] = r;
+      }
+      const int pl = s_base[j] + ti;
+      if (hs == nsteps) {  // the whole schedule fits in the head (d <= 16)
+        if (MODE == 0) {
+          if (al0) record_survivor(P, A, s_qid[j], pl, acc0, tile, lane);
+          if (al1) record_survivor(P, A, s_qid[j], pl, acc1, tile, lane + 32);
+        } else {
+          if (al0) confirm_survivor(P, A, s_qid[j], pl, lane);
+          if (al1) confirm_survivor(P, A, s_qid[j], pl, lane + 32);
+        }
+      } else {
+        const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
+        const int n = __popc(m0) + __popc(m1);
+        if (n) {
+          if (qn + n > kDeepCap) flush();
+          const unsigned lt = (1u << lane) - 1u;
+          const int pre = qn + __popc(m0 & lt) + __popc(m1 & lt);
+          if (al0) s_deep[w][pre] = DeepItem{acc0, (int16_t)j, (int16_t)lane, that};
+          if (al1)
+            s_deep[w][pre + (al0 ? 1 : 0)] = DeepItem{acc1, (int16_t)j, (int16_t)(lane + 32), that};
+          qn += n;
+        }
+      }
+    }
+    flush();
+    // the pairs' stats: values_touched (search.py:148-169) and trace counts
+    for (int j = lane; j < ne; j += 32) {
+      if (!((todo >> j) & 1u)) continue;
+      const int64_t p = s_qo[j] + s_base[j] + ti;
+      const uint32_t hp = s_hcnt[w][j];
+      int64_t touched = 0, prev = m;
+      bool warm = true;
+      int a = 0;
+      for (int s = 0; s < nsteps; ++s) {
+        const int w_s = s_ends[s] - a;
+        a = s_ends[s];
+        if (warm && prev >= s_wmin[m]) {
+          touched += (int64_t)m * w_s;
+        } else {
+          warm = false;
+          touched += prev * w_s;
+        }
+        prev = s < hs ? (int)((hp >> (8 * s)) & 0xffu) : (int)s_dcnt[w][j][s];
+        if (A.pcnt) A.pcnt[p * nsteps + s] = (uint8_t)prev;
+      }
+      A.ptouched[p] = (uint32_t)touched;
+      if (MODE == 0) A.prho[p] = __uint_as_float(s_rho[w][j]);
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ chain
+// One warp per query: sort its T'-survivors by pair and record, per entry,
+// T^ after the pushes of its pair (the k-th smallest of H and the survivors
+// of pairs up to it).  Pushing a T'-survivor the exact chain prunes leaves
+// the k-th distance unchanged when its distance is >= T^ (bfinal_kernel
+// checks that every such survivor is), so this is the reference's chain.
+__global__ void bchain_kernel(const BParams P, const BArgs A) {
+  extern __shared__ float s_top[];  // [warps][k]
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int q = blockIdx.x * (blockDim.x >> 5) + wq;
+  if (q >= P.nq || A.flags[q]) return;
+  const int n = min(A.nsurv[q], P.surv_cap);
+  if (n == 0) return;
+  const int k = P.k;
+  float* top = s_top + (size_t)wq * k;
+  for (int i = lane; i < k; i += 32) top[i] = A.out_dist[(int64_t)q * k + i];
+  __syncwarp();
+  if (lane != 0) return;
+  BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
+  for (int i = 1; i < n; ++i) {  // insertion sort by pair (n is small: ~1-2 at C2)
+    const BSurv x = sv[i];
+    int j = i;
+    while (j > 0 && sv[j - 1].pair > x.pair) {
+      sv[j] = sv[j - 1];
+      --j;
+    }
+    sv[j] = x;
+  }
+  for (int i = 0; i < n;) {
+    int e = i;
+    for (; e < n && sv[e].pair == sv[i].pair; ++e) {
+      const float dv = sv[e].dist;
+      if (dv < top[k - 1]) {  // TopK.push, threshold value only
+        int j = k - 1;
+        while (j > 0 && top[j - 1] > dv) {
+          top[j] = top[j - 1];
+          --j;
+        }
+        top[j] = dv;
+      }
+    }
+    for (int j = i; j < e; ++j) sv[j].tafter = top[k - 1];
+    i = e;
+  }
+}
+
+// ------------------------------------------------------------------ final
+// One warp per unflagged query: survivors of uncertain pairs that the
+// recompute pass did not confirm are dropped (or, below T^, flag the query);
+// top-k of H and the real survivors; the stats.
+__global__ void bfinal_kernel(const BParams P, const BArgs A) {
+  extern __shared__ unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int q = blockIdx.x * (blockDim.x >> 5) + wq;
+  if (q >= P.nq || A.flags[q]) return;
+  const int k = P.k;
+  float* td = reinterpret_cast<float*>(s_raw) + (size_t)wq * k;
+  int64_t* ti = reinterpret_cast<int64_t*>(s_raw + (size_t)(blockDim.x >> 5) * k * 4 + 8) +
+                (size_t)wq * k;
+  const int n = min(A.nsurv[q], P.surv_cap);
+  BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
+  float* od = A.out_dist + (int64_t)q * k;
+  int64_t* oi = A.out_ids + (int64_t)q * k;
+  const int64_t p0 = A.qoff[q], p1 = A.qoff[q + 1];
+  const float tp = A.tprime[q];
+  // drop unconfirmed survivors of uncertain pairs (the list is pair-sorted)
+  bool bad = false;
+  for (int i = lane; i < n; i += 32) {
+    const float that = that_of(sv, n, sv[i].pair, tp);
+    if (pair_uncertain(that, tp, A.prho[p0 + sv[i].pair]) && !sv[i].real) {
+      if (sv[i].dist < that) bad = true;
+      sv[i].real = -1;
+    }
+  }
+  if (__any_sync(kFull, bad)) {
+    if (lane == 0) A.flags[q] = 1;
+    return;
+  }
+  __syncwarp();
+  if (n > 0) {
+    if (lane == 0) {
+      // real survivors ascending by (dist, id), then a merge with H (sorted)
+      int nr = 0;
+      for (int i = 0; i < n; ++i)
+        if (sv[i].real >= 0) sv[nr++] = sv[i];
+      for (int i = 1; i < nr; ++i) {
+        const BSurv x = sv[i];
+        int j = i;
+        while (j > 0 && pair_less(x.dist, x.id, sv[j - 1].dist, sv[j - 1].id)) {
+          sv[j] = sv[j - 1];
+          --j;
+        }
+        sv[j] = x;
+      }
+      int a = 0, b = 0;
+      for (int r = 0; r < k; ++r) {
+        const bool takeh = b >= nr || (a < k && pair_less(od[a], oi[a], sv[b].dist, sv[b].id));
+        if (takeh) {
+          td[r] = od[a];
+          ti[r] = oi[a];
+          ++a;
+        } else {
+          td[r] = sv[b].dist;
+          ti[r] = sv[b].id;
+          ++b;
+        }
+      }
+    }
+    __syncwarp();
+    for (int r = lane; r < k; r += 32) {
+      od[r] = td[r];
+      oi[r] = ti[r];
+    }
+  }
+  if (lane == 0 && A.out_count) A.out_count[q] = k;
+  if (A.out_touched) {
+    unsigned long long t = 0;
+    for (int64_t p = p0 + lane; p < p1; p += 32) t += A.ptouched[p];
+    t = __reduce_add_sync(kFull, (unsigned)(t & 0xffffffffu)) +
+        ((unsigned long long)__reduce_add_sync(kFull, (unsigned)(t >> 32)) << 32);
+    if (lane == 0) A.out_touched[q] += (int64_t)t;
+  }
+  if (A.out_total) {
+    int64_t v = 0;
+    for (int s = 1 + lane; s < P.nseg; s += 32) v += A.bnvec[A.sel[(int64_t)q * P.nseg + s]];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) A.out_total[q] += v * P.d;
+  }
+  if (A.trace) {
+    const int64_t tl = A.trace_len[q];
+    const int64_t np = p1 - p0, rec = 1 + P.nsteps;
+    const bool fits = tl >= 0 && tl + np * rec <= A.trace_cap;
+    if (fits) {
+      int32_t* tr = A.trace + (int64_t)q * A.trace_cap + tl;
+      for (int64_t p = lane; p < np; p += 32) {
+        tr[p * rec] = P.nsteps;
+        for (int s = 0; s < P.nsteps; ++s) tr[p * rec + 1 + s] = A.pcnt[(p0 + p) * P.nsteps + s];
+      }
+    }
+    if (lane == 0) A.trace_len[q] = fits ? tl + np * rec : -1;
+  }
+}
+
+int schedule(int d, int initial_step, int32_t* ends) {
+  int n = 0;
+  int64_t start = 0, width = initial_step;
+  while (start < d && n < kMaxSteps) {
+    start = start + width < d ? start + width : d;
+    ends[n++] = (int32_t)start;
+    width *= 2;
+  }
+  return start < d ? -1 : n;
+}
+
+int host_warm_min(int m, double sf) {  // warm_min_count (pdx_scan_kernel.cuh)
+  int p = (int)ceil(sf * (double)m);
+  p = p < 0 ? 0 : (p > m ? m : p);
+  while (p > 0 && (double)(p - 1) / (double)m >= sf) --p;
+  while (p < m && (double)p / (double)m < sf) ++p;
+  return p;
+}
+
+template <typename T>
+T* carve(unsigned char*& at, int64_t count) {
+  T* p = reinterpret_cast<T*>(at);
+  at += ((count * (int64_t)sizeof(T) + 255) / 256) * 256;
+  return p;
+}
+
+}  // namespace
+
+bool batched_eligible(const pdx_store* store, const pdx_search_params* prm, int64_t nq,
+                      const int32_t* d_seg_bucket, int32_t nseg, const uint16_t* d_orders,
+                      const pdx_search_out* out) {
+  if (prm->batched == 1) return false;
+  if (!d_seg_bucket || nseg < 2 || d_orders || store->group != 8) return false;
+  if (store->ntiles != store->nblocks) return false;  // every block one tile (64-blocks)
+  if (prm->pruner == PDX_PRUNER_NONE || prm->metric != PDX_METRIC_L2) return false;
+  if (prm->splits > 1 || out->d_debug || prm->k > kMaxBatchK) return false;
+  if (prm->initial_step > kHeadDims) return false;
+  if (prm->batched == 0 && nq < 32) return false;
+  if (nq > (1 << 24)) return false;
+  const int64_t pairs = nq * (int64_t)(nseg - 1) * store->max_bucket_tiles;
+  return pairs <= (int64_t)1 << 31;
+}
+
+int search_batched(const pdx_store* store, const pdx_search_params* prm, const float* d_queries,
+                   int64_t nq64, const int32_t* d_seg_bucket, int32_t nseg,
+                   const pdx_search_out* out, void* d_work, int64_t work_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int nq = (int)nq64, k = prm->k, nb = store->nbuckets;
+  BParams P;
+  memset(&P, 0, sizeof(P));
+  P.d = store->d;
+  P.d_pad = store->d_pad;
+  P.k = k;
+  P.pruner = prm->pruner;
+  P.nseg = nseg;
+  P.nq = nq;
+  P.nsteps = schedule(store->d, prm->initial_step, P.ends);
+  PDX_REQUIRE(P.nsteps > 0, "step schedule too long");
+  for (int s = P.nsteps; s < kMaxSteps; ++s) P.ends[s] = 0x7fffffff;
+  const int ads_d = (prm->ads_d >= 1 && prm->pruner != PDX_PRUNER_BSA) ? prm->ads_d : store->d;
+  for (int s = 0; s < P.nsteps; ++s) {  // bound_factors_kernel (pdx_scan.cu)
+    double ratio = 1.0, band = 1.0;
+    if (prm->pruner == PDX_PRUNER_ADS && P.ends[s] < ads_d) {
+      ratio = (double)P.ends[s] / (double)ads_d;
+      band = 1.0 + prm->ads_epsilon0 / sqrt((double)P.ends[s]);
+    }
+    P.ratio[s] = ratio;
+    P.band[s] = band;
+    P.invb[s] = (float)(1.0 / (ratio * band * band));
+    if (P.ends[s] <= kHeadDims && P.hsteps < kMaxHead) {
+      P.hsteps = s + 1;
+      P.hdims = P.ends[s];
+      P.hmask |= 1u << (P.ends[s] - 1);
+    }
+  }
+  PDX_REQUIRE(P.hsteps >= 1, "batched search needs initial_step <= %d", kHeadDims);
+  for (int m = 0; m <= kTile; ++m) P.wmin[m] = m > 0 ? host_warm_min(m, prm->selection_fraction) : 0;
+  P.surv_cap = 4 * k + 64;
+  const int64_t per = nseg - 1;
+  const int64_t pmax = nq64 * per * store->max_bucket_tiles;
+  const bool trace = out->d_trace != nullptr;
+  const int64_t nitems_max = nb + (nq64 * per + kQC - 1) / kQC + 1;
+
+  // cub scratch (three exclusive sums)
+  size_t cub1 = 0, cub2 = 0;
+  PDX_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, cub1, (int64_t*)nullptr, (int64_t*)nullptr,
+                                                nq + 1, st));
+  PDX_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, cub2, (int32_t*)nullptr, (int32_t*)nullptr,
+                                                nb + 1, st));
+  const size_t cubb = std::max(cub1, cub2);
+
+  int64_t bytes = 0;
+  {
+    unsigned char* z = nullptr;
+    unsigned char* at = z;
+    carve<int32_t>(at, nq);                    // seg0
+    carve<int64_t>(at, nq + 1);                // wcount
+    carve<int64_t>(at, nq + 1);                // qoff
+    carve<int32_t>(at, nq64 * nseg);           // pbase
+    carve<int32_t>(at, nb + 1);                // bcnt
+    carve<int32_t>(at, nb + 1);                // boff
+    carve<int32_t>(at, nb + 1);                // bcur
+    carve<int32_t>(at, nb + 1);                // nch
+    carve<int32_t>(at, nb + 1);                // choff
+    carve<int64_t>(at, nb + 1);                // bnvec
+    carve<BEntry>(at, nq64 * per + 1);         // entries
+    carve<BItem>(at, nitems_max);              // items
+    carve<int32_t>(at, 4);                     // nitems
+    carve<int32_t>(at, nq);                    // count scratch
+    carve<float>(at, nq);                      // tprime
+    carve<float>(at, nq64 * P.nsteps);         // bounds
+    carve<float>(at, nq64 * 2 * P.nsteps);     // bsaq
+    carve<int32_t>(at, nq);                    // flags
+    carve<int32_t>(at, nq);                    // nsurv
+    carve<BSurv>(at, nq64 * P.surv_cap);       // surv
+    carve<uint32_t>(at, pmax + 1);             // ptouched
+    carve<float>(at, pmax + 1);                // prho
+    carve<uint8_t>(at, trace ? pmax * P.nsteps + 1 : 1);  // pcnt
+    carve<unsigned char>(at, (int64_t)cubb + 16);
+    bytes = at - z;
+  }
+  unsigned char* base = nullptr;
+  PDX_CUDA_CHECK(cudaMallocAsync(&base, bytes, st));
+  unsigned char* at = base;
+  int32_t* seg0 = carve<int32_t>(at, nq);
+  int64_t* wcount = carve<int64_t>(at, nq + 1);
+  int64_t* qoff = carve<int64_t>(at, nq + 1);
+  int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
+  int32_t* bcnt = carve<int32_t>(at, nb + 1);
+  int32_t* boff = carve<int32_t>(at, nb + 1);
+  int32_t* bcur = carve<int32_t>(at, nb + 1);
+  int32_t* nch = carve<int32_t>(at, nb + 1);
+  int32_t* choff = carve<int32_t>(at, nb + 1);
+  int64_t* bnvec = carve<int64_t>(at, nb + 1);
+  BEntry* entries = carve<BEntry>(at, nq64 * per + 1);
+  BItem* items = carve<BItem>(at, nitems_max);
+  int32_t* ctr = carve<int32_t>(at, 4);
+  int32_t* cnt_scratch = carve<int32_t>(at, nq);
+  float* tprime = carve<float>(at, nq);
+  float* bounds = carve<float>(at, nq64 * P.nsteps);
+  float* bsaq = carve<float>(at, nq64 * 2 * P.nsteps);
+  int32_t* flags = carve<int32_t>(at, nq);
+  int32_t* nsurv = carve<int32_t>(at, nq);
+  BSurv* surv = carve<BSurv>(at, nq64 * P.surv_cap);
+  uint32_t* ptouched = carve<uint32_t>(at, pmax + 1);
+  float* prho = carve<float>(at, pmax + 1);
+  uint8_t* pcnt = carve<uint8_t>(at, trace ? pmax * P.nsteps + 1 : 1);
+  void* cubtmp = carve<unsigned char>(at, (int64_t)cubb + 16);
+
+  int rc = PDX_OK;
+  const bool dbg_sync = getenv("PDX_BATCH_SYNC") != nullptr;
+  auto phase = [&](const char* name) {
+    if (!dbg_sync) return;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[pdx batched] %s done: %s\n", name, cudaGetErrorString(e));
+  };
+  auto fail = [&](int r) {
+    cudaFreeAsync(base, st);
+    return r;
+  };
+#define PDX_B_CHECK(expr)                                                                    \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) {                                                                 \
+      ::pdx::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e));   \
+      return fail(PDX_ECUDA);                                                                \
+    }                                                                                        \
+  } while (0)
+
+  // ---- plan: per-query windows, bucket-major entries, work items
+  PDX_B_CHECK(cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), st));
+  PDX_B_CHECK(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (nb + 1), st));
+  PDX_B_CHECK(cudaMemsetAsync(wcount + nq, 0, sizeof(int64_t), st));
+  PDX_B_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 4, st));
+  bprep_kernel<<<(nq + 7) / 8, 256, 0, st>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
+                                             store->d_block_tile, seg0, wcount, pbase, bcnt);
+  PDX_B_CHECK(cudaGetLastError());
+  size_t cb = cubb;
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st));
+  cb = cubb;
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, bcnt, boff, nb + 1, st));
+  bchunks_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, store->d_bucket_block,
+                                                   store->d_block_m, nch, bnvec);
+  PDX_B_CHECK(cudaGetLastError());
+  cb = cubb;
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, nch, choff, nb + 1, st));
+  if (nq64 * per > 0) {
+    bfill_kernel<<<(unsigned)((nq64 * per + 255) / 256), 256, 0, st>>>(
+        d_seg_bucket, nq, nseg, store->d_bucket_block, store->d_block_tile, pbase, boff, bcur,
+        entries);
+    PDX_B_CHECK(cudaGetLastError());
+  }
+  bitems_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, boff, choff, items, ctr);
+  PDX_B_CHECK(cudaGetLastError());
+  phase("plan");
+
+  // ---- phase 1: the first selected bucket of every query, per-query scan
+  pdx_search_out o1 = *out;
+  if (!o1.d_count) o1.d_count = cnt_scratch;
+  o1.d_debug = nullptr;
+  rc = search_classic(store, prm, d_queries, nq64, seg0, 1, &o1, d_work, work_bytes, stream,
+                      nullptr);
+  if (rc != PDX_OK) return fail(rc);
+
+  phase("phase1");
+  BArgs A;
+  memset(&A, 0, sizeof(A));
+  A.tiles = store->d_tiles;
+  A.tile_ids = store->d_tile_ids;
+  A.tile_stride = (int64_t)store->d_pad * kTile;
+  A.bucket_block = store->d_bucket_block;
+  A.block_tile = store->d_block_tile;
+  A.block_m = store->d_block_m;
+  A.queries = d_queries;
+  A.sel = d_seg_bucket;
+  A.resid = store->d_resid;
+  A.coef = prm->bsa_coef;
+  A.tprime = tprime;
+  A.bounds = bounds;
+  A.bsaq = bsaq;
+  A.qoff = qoff;
+  A.flags = flags;
+  A.nsurv = nsurv;
+  A.surv = surv;
+  A.ptouched = ptouched;
+  A.prho = prho;
+  A.pcnt = trace ? pcnt : nullptr;
+  A.items = items;
+  A.nitems = ctr;
+  A.entries = entries;
+  A.bnvec = bnvec;
+  A.out_dist = out->d_dist;
+  A.out_ids = out->d_ids;
+  A.out_count = o1.d_count;
+  A.out_touched = out->d_touched;
+  A.out_total = out->d_total;
+  A.trace = out->d_trace;
+  A.trace_cap = out->trace_cap;
+  A.trace_len = out->d_trace_len;
+
+  const bool bsa = prm->pruner == PDX_PRUNER_BSA;
+  btprime_kernel<<<(nq + 127) / 128, 128, 0, st>>>(P, A);
+  PDX_B_CHECK(cudaGetLastError());
+  phase("tprime");
+  // ---- phase 2: every (query, tile) pair of the other buckets under T';
+  // chain; recompute of the uncertain pairs under T^ (same kernel, MODE 1)
+  const int is = (store->d >= kHeadDims) ? prm->initial_step : 0;
+  auto scan = [&](int mode) -> cudaError_t {
+    const dim3 g((unsigned)nitems_max), b(kBW * 32);
+#define PDX_B_LAUNCH(IS)                                                               \
+  if (bsa) {                                                                           \
+    if (mode == 0) bscan_kernel<IS, true, 0><<<g, b, 0, st>>>(P, A);                   \
+    else bscan_kernel<IS, true, 1><<<g, b, 0, st>>>(P, A);                             \
+  } else {                                                                             \
+    if (mode == 0) bscan_kernel<IS, false, 0><<<g, b, 0, st>>>(P, A);                  \
+    else bscan_kernel<IS, false, 1><<<g, b, 0, st>>>(P, A);                            \
+  }
+    switch (is) {
+      case 1: PDX_B_LAUNCH(1) break;
+      case 2: PDX_B_LAUNCH(2) break;
+      case 4: PDX_B_LAUNCH(4) break;
+      case 8: PDX_B_LAUNCH(8) break;
+      default: PDX_B_LAUNCH(0) break;
+    }
+#undef PDX_B_LAUNCH
+    return cudaGetLastError();
+  };
+  if (nitems_max > 0) PDX_B_CHECK(scan(0));
+  phase("scan");
+  bchain_kernel<<<(nq + 7) / 8, 256, 8 * k * sizeof(float), st>>>(P, A);
+  PDX_B_CHECK(cudaGetLastError());
+  phase("chain");
+  if (nitems_max > 0) PDX_B_CHECK(scan(1));
+  phase("recompute");
+  const size_t fsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t)) + 16;
+  if (fsm > 48 * 1024)
+    PDX_B_CHECK(cudaFuncSetAttribute(bfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fsm));
+  bfinal_kernel<<<(nq + 7) / 8, 256, fsm, st>>>(P, A);
+  PDX_B_CHECK(cudaGetLastError());
+  phase("final");
+  // ---- fallback: flagged queries through the per-query scan
+  rc = search_classic(store, prm, d_queries, nq64, d_seg_bucket, nseg, out, d_work, work_bytes,
+                      stream, flags);
+  if (rc != PDX_OK) return fail(rc);
+  phase("fallback");
+  if (getenv("PDX_BATCH_DEBUG")) {  // development aid: work items, uncertain pairs, fallbacks
+    int32_t h[1] = {0};
+    std::vector<int32_t> fl(nq);
+    cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(fl.data(), flags, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    int nf = 0;
+    for (int32_t f : fl) nf += f != 0;
+    fprintf(stderr, "[pdx batched] nq=%d items=%d fallback=%d\n", nq, h[0], nf);
+  }
+  PDX_B_CHECK(cudaFreeAsync(base, st));
+  return PDX_OK;
+#undef PDX_B_CHECK
+}
+
+}  // namespace pdx

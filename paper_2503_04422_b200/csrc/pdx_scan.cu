@@ -32,6 +32,7 @@
 
 #include "pdx_common.cuh"
 #include "pdx_scan_kernel.cuh"
+#include "pdx_batch.cuh"
 
 namespace pdx {
 
@@ -43,12 +44,13 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
     const int32_t* __restrict__ seg_bucket, int nseg, const int64_t* __restrict__ bucket_block,
     const int64_t* __restrict__ block_tile, const int32_t* __restrict__ block_m,
     const int32_t* __restrict__ tile_block, TileEntry* __restrict__ out, int64_t maxtiles,
-    int32_t* __restrict__ counts, int32_t* __restrict__ overflow) {
+    int32_t* __restrict__ counts, int32_t* __restrict__ overflow, const int32_t* __restrict__ only) {
   using Scan = cub::BlockScan<int64_t, 256>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t s_b0[256], s_t0[256], s_toff[256], s_boff[256];
   __shared__ int64_t run_t, run_b;
   const int q = blockIdx.x;
+  if (only && only[q] == 0) return;
   if (threadIdx.x == 0) run_t = run_b = 0;
   __syncthreads();
   for (int base = 0; base < nseg; base += 256) {
@@ -192,11 +194,11 @@ extern "C" int64_t pdx_search_workspace(const pdx_store* store, int64_t nq, int3
   return 512 + nq * (int64_t)sizeof(int32_t) + 256 + nq * maxvis * (int64_t)sizeof(TileEntry) + 256;
 }
 
-extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
-                          const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
-                          int32_t nseg, const uint16_t* d_orders, int64_t order_qstride,
-                          int64_t order_sstride, const pdx_search_out* out, void* d_work,
-                          int64_t work_bytes, void* stream) {
+static int search_impl(const pdx_store* store, const pdx_search_params* prm,
+                       const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
+                       int32_t nseg, const uint16_t* d_orders, int64_t order_qstride,
+                       int64_t order_sstride, const pdx_search_out* out, void* d_work,
+                       int64_t work_bytes, void* stream, const int32_t* only, bool allow_batched) {
   PDX_REQUIRE(store && prm && out, "pdx_search: null argument");
   PDX_REQUIRE(prm->k >= 1, "k must be >= 1");
   PDX_REQUIRE(prm->k <= 4096, "k = %d exceeds this build's limit of 4096", prm->k);
@@ -230,6 +232,10 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
                    store->resid_initial_step == prm->initial_step),
               "bsa needs the store's residual energies for this step schedule "
               "(pdx_bsa_residuals with initial_step %d)", prm->initial_step);
+
+  if (allow_batched && batched_eligible(store, prm, nq, d_seg_bucket, nseg, d_orders, out))
+    return search_batched(store, prm, d_queries, nq, d_seg_bucket, nseg, out, d_work, work_bytes,
+                          stream);
 
   int dev = 0, optin = 0;
   PDX_CUDA_CHECK(cudaGetDevice(&dev));
@@ -270,7 +276,7 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
     build_visits_kernel<<<(unsigned)nlists, 256, 0, st>>>(
         d_seg_bucket, nseg, store->d_bucket_block, store->d_block_tile, store->d_block_m,
         store->d_tile_block, d_vis,
-        maxvis, d_counts, d_overflow);
+        maxvis, d_counts, d_overflow, only);
   } else {
     PDX_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, nlists * sizeof(int32_t), st));
   }
@@ -311,6 +317,7 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
   A.trace_len = out->d_trace_len;
   A.debug = out->d_debug;
   A.sparse_max = kItemsPerWarp / tpw;
+  A.only = only;
   PDX_REQUIRE(A.out_dist && A.out_ids, "output buffers required");
 
   // split mode: CTA b scans range b / nq of query b % nq into row b of a
@@ -389,4 +396,21 @@ extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
     }
   }
   return PDX_OK;
+}
+
+int pdx::search_classic(const pdx_store* store, const pdx_search_params* prm,
+                        const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
+                        int32_t nseg, const pdx_search_out* out, void* d_work, int64_t work_bytes,
+                        void* stream, const int32_t* only) {
+  return search_impl(store, prm, d_queries, nq, d_seg_bucket, nseg, nullptr, 0, 0, out, d_work,
+                     work_bytes, stream, only, false);
+}
+
+extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,
+                          const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
+                          int32_t nseg, const uint16_t* d_orders, int64_t order_qstride,
+                          int64_t order_sstride, const pdx_search_out* out, void* d_work,
+                          int64_t work_bytes, void* stream) {
+  return search_impl(store, prm, d_queries, nq, d_seg_bucket, nseg, d_orders, order_qstride,
+                     order_sstride, out, d_work, work_bytes, stream, nullptr, true);
 }

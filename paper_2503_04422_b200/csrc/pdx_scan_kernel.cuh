@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
   extern __shared__ __align__(16) unsigned char smem[];
   // split mode: CTA b scans range b / nq of query b % nq and writes row b
   const int q = A.nsplit > 1 ? (int)(blockIdx.x % (unsigned)A.nq) : (int)blockIdx.x;
+  if (A.only && A.only[q] == 0) return;  // batched path's fallback: flagged queries only
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int RB = L.rb;  // a power of two
   const int RMASK = RB - 1;

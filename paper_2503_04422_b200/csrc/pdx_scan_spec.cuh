@@ -101,6 +101,7 @@ struct ScanArgs {
   int32_t nq, nsplit;     // split mode: CTA b scans range b / nq of query b % nq
   const float* resid;     // BSA: [ntiles][nsteps][64] residual energy per slot and step
   const float* bsa_coef;  // BSA: [nsteps]
+  const int32_t* only;    // optional [nq]: scan only queries with only[q] != 0
 };
 
 // Shared-memory views of one round slice (the tiles of one compute warp).

@@ -252,13 +252,15 @@ class IvfSearcher:
     (BOND with a query-aware criterion), K5/K6 scan."""
 
     def __init__(self, index: IvfIndex, params: SearchParams, nprobe: int,
-                 criteria=OrderCriteria.SEQUENTIAL, zone_width=None, warps: int = 0):
+                 criteria=OrderCriteria.SEQUENTIAL, zone_width=None, warps: int = 0,
+                 batched: int = 0):
         if not 1 <= nprobe <= index.nlist:
             raise ValueError(f"nprobe must be in [1, {index.nlist}], got {nprobe}")
         self.index, self.params, self.nprobe = index, params, nprobe
         self.criteria = OrderCriteria(criteria)
         self.zone_width = zone_width
         self.warps = warps
+        self.batched = int(batched)  # pdx_search_params.batched: 0 auto, 1 off, 2 forced
         self._buf = {}
         self._scratch = None
 
@@ -282,7 +284,7 @@ class IvfSearcher:
         res = run_search(self.index.store, Q, self.params, seg_bucket=sel, nseg=self.nprobe,
                          orders=orders, order_qstride=self.nprobe, order_sstride=oss,
                          stats=stats, trace_cap=trace_cap, warps=self.warps, out=self._buf,
-                         timed=timed)
+                         timed=timed, batched=self.batched)
         if scan_events is not None:
             scan_events[2].record()
         if ev:
@@ -316,14 +318,14 @@ def ivf_search(index: IvfIndex, query, params: SearchParams, nprobe: int,
 
 def ivf_search_batch(index: IvfIndex, queries, params: SearchParams, nprobe: int,
                      criteria=OrderCriteria.SEQUENTIAL, zone_width=None, stats=False,
-                     trace=False):
+                     trace=False, batched=0):
     """All queries in one launch per kernel; returns host arrays
     (dist, ids, count[, touched, total, survivors, selected])."""
     import torch
     Q = to_device(np.asarray(queries, np.float32), torch.float32)
     if Q.shape[1] != index.d:
         raise ValueError(f"query dimensionality {Q.shape[1]} != {index.d}")
-    s = IvfSearcher(index, params, nprobe, criteria, zone_width)
+    s = IvfSearcher(index, params, nprobe, criteria, zone_width, batched=batched)
     cap = _trace_cap(nprobe * max(1, index.store.max_bucket_blocks), index.d,
                      params.initial_step) if trace else 0
     res = s.run(Q, stats=stats or trace, trace_cap=cap)

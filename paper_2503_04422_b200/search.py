@@ -172,9 +172,10 @@ def decode_trace(buf, n):
 
 
 def make_params(params: SearchParams, d: int, warps=0, device=None,
-                splits: int = 0) -> _lib.PdxSearchParams:
+                splits: int = 0, batched: int = 0) -> _lib.PdxSearchParams:
     """``warps``: compute warps per query CTA, or (warps, tiles_per_warp[,
-    ring_slots]); 0 = auto."""
+    ring_slots]); 0 = auto.  ``batched``: 0 auto, 1 per-query scan only, 2
+    the bucket-major batched pipeline whenever eligible (pdx_b200.h)."""
     ads = params.ads if params.ads is not None else AdsPruner(d=d)
     w, tpw, rb = (tuple(warps) + (0, 0))[:3] if isinstance(warps, tuple) else (warps, 0, 0)
     coef = None
@@ -186,12 +187,12 @@ def make_params(params: SearchParams, d: int, warps=0, device=None,
                                 _lib.PRUNER[params.pruner], int(params.initial_step),
                                 float(params.selection_fraction), int(ads.d), int(w),
                                 float(ads.epsilon0), int(tpw), int(rb), _lib.ptr(coef),
-                                int(splits))
+                                int(splits), int(batched))
 
 
 def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None, orders=None,
                order_qstride=0, order_sstride=0, stats=False, trace_cap=0, warps=0, out=None,
-               timed=False, splits=0):
+               timed=False, splits=0, batched=0):
     """Launch pdx_search over ``store`` for a device batch ``queries`` (nq x d).
 
     seg_bucket: int32 [nq, nseg] bucket per visit segment (None: segment s
@@ -237,7 +238,7 @@ def run_search(store, queries, params: SearchParams, seg_bucket=None, nseg=None,
         out["work"] = work
     if params.pruner == "bsa":
         store.ensure_bsa_residuals(params.initial_step)
-    p = make_params(params, store.d, warps, dev, splits)
+    p = make_params(params, store.d, warps, dev, splits, batched)
     sb = None if seg_bucket is None else seg_bucket.contiguous()
     st = _lib.stream_handle()
     ev0 = ev1 = None

@@ -47,7 +47,7 @@ def test_library_is_sm100a(L):
 
 def test_abi_version_and_errors_without_gpu(L):
     from paper_2503_04422_b200 import _lib
-    assert L.pdx_abi_version() == 2
+    assert L.pdx_abi_version() == 3
     store = _lib.PdxStore(128, 128, 8, 1, 0, 0, None, None, None, None, None, 0, 0)
     prm = _lib.PdxSearchParams(0, 0, 0, 2, 0.2, 128, 0, 2.1)  # k = 0
     out = _lib.PdxSearchOut()

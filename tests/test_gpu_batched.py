@@ -1,0 +1,102 @@
+"""The bucket-major batched IVF pipeline (pdx_batch.cu) against the
+per-query scan and the C oracle: ids, float32 distances, values_touched /
+values_total and every survivor trace identical (no tolerance)."""
+import numpy as np
+import pytest
+
+import recipes
+from test_gpu_parity import P, _bsa_setup, _oracle_ivf  # noqa: F401 (P is a fixture)
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(P, index, q, params, nprobe, batched):
+    return P.ivf_search_batch(index, q, params, nprobe, trace=True, batched=batched)
+
+
+def _same(a, b):
+    np.testing.assert_array_equal(a["ids"], b["ids"])
+    np.testing.assert_array_equal(a["dist"], b["dist"])
+    np.testing.assert_array_equal(a["count"], b["count"])
+    np.testing.assert_array_equal(a["touched"], b["touched"])
+    np.testing.assert_array_equal(a["total"], b["total"])
+    assert a["survivors"] == b["survivors"]
+
+
+@pytest.fixture(scope="module")
+def rotated(P):
+    x = recipes.data("mixture", 200_000, 128, 7)
+    Q = recipes.queries("near", x, 96, 8)
+    T = P.generate_orthogonal(128, 0)
+    xr, qr = P.apply_transform(T, x), P.apply_transform(T, Q)
+    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=256, seed=0)
+    return xr, qr, index
+
+
+@pytest.mark.parametrize("eps,nprobe,k", [(2.1, 8, 10), (2.1, 32, 10), (0.7, 16, 10),
+                                          (0.3, 16, 10), (2.1, 16, 1), (2.1, 16, 100)])
+def test_batched_ads_equals_per_query_and_oracle(P, oracle, rotated, eps, nprobe, k):
+    xr, qr, index = rotated
+    params = P.SearchParams(k=k, pruner="ads", ads=P.AdsPruner(d=128, epsilon0=eps))
+    a = _run(P, index, qr, params, nprobe, 2)
+    b = _run(P, index, qr, params, nprobe, 1)
+    _same(a, b)
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, k, nprobe, pruner="ads",
+                                  eps0=eps, survivors_cap=1 << 18)
+    np.testing.assert_array_equal(a["ids"], ref["ids"])
+    np.testing.assert_array_equal(a["dist"], ref["dist"])
+    np.testing.assert_array_equal(a["touched"], ref["touched"])
+    assert a["survivors"] == ref["survivor_lists"]
+
+
+@pytest.mark.parametrize("initial_step,sf", [(1, 0.2), (2, 0.05), (8, 0.4), (16, 0.2)])
+def test_batched_schedules_bond(P, rotated, initial_step, sf):
+    _, qr, index = rotated
+    params = P.SearchParams(k=10, pruner="bond", initial_step=initial_step,
+                            selection_fraction=sf)
+    _same(_run(P, index, qr, params, 12, 2), _run(P, index, qr, params, 12, 1))
+
+
+@pytest.mark.parametrize("quantile,multiplier", [(0.99, 1.0), (0.5, 0.7)])
+def test_batched_bsa(P, oracle, quantile, multiplier):
+    import torch
+    x, Q, xr, qr = _bsa_setup(P)
+    bsa = P.fit_bsa(torch.from_numpy(xr).cuda(), quantile=quantile, multiplier=multiplier)
+    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=128, seed=0)
+    params = P.SearchParams(k=10, pruner="bsa", bsa=bsa)
+    a = _run(P, index, qr, params, 16, 2)
+    _same(a, _run(P, index, qr, params, 16, 1))
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, 10, 16, pruner="bsa",
+                                  bsa_coef=np.asarray(bsa.coef, np.float32),
+                                  survivors_cap=1 << 18)
+    np.testing.assert_array_equal(a["ids"], ref["ids"])
+    np.testing.assert_array_equal(a["touched"], ref["touched"])
+    assert a["survivors"] == ref["survivor_lists"]
+
+
+def test_batched_small_buckets_and_tiny_batches(P):
+    """Buckets smaller than k (phase-1 heap not full: fallback), a single
+    query, ragged bucket sizes, d not a multiple of 8 and d <= 16."""
+    for n, d, nlist, k, nq in [(3000, 37, 300, 20, 40), (5000, 12, 64, 10, 1),
+                               (20000, 16, 128, 5, 33), (4000, 9, 50, 10, 64)]:
+        rng = np.random.default_rng(n + d)
+        x = (rng.standard_normal((n, d)) * (1 + rng.integers(0, 4, (n, 1)))).astype(np.float32)
+        q = x[rng.choice(n, nq, replace=False)] + 0.1 * rng.standard_normal((nq, d)).astype(
+            np.float32)
+        index = P.ivf_build(P.VectorCollection.from_array(x), nlist=nlist, seed=0)
+        for pruner in ("ads", "bond"):
+            params = P.SearchParams(k=k, pruner=pruner)
+            _same(_run(P, index, q, params, min(nlist, 24), 2),
+                  _run(P, index, q, params, min(nlist, 24), 1))
+
+
+def test_batched_duplicates_and_ties(P):
+    """Exact duplicate vectors (distance ties, T^ = 0 chains) keep the lower id."""
+    rng = np.random.default_rng(5)
+    base = rng.standard_normal((500, 32)).astype(np.float32)
+    x = np.concatenate([base] * 20)
+    q = base[:40] + 0.0
+    index = P.ivf_build(P.VectorCollection.from_array(x), nlist=40, seed=0)
+    for pruner in ("ads", "bond"):
+        params = P.SearchParams(k=10, pruner=pruner)
+        _same(_run(P, index, q, params, 8, 2), _run(P, index, q, params, 8, 1))
