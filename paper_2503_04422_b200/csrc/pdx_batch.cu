@@ -145,6 +145,25 @@ __device__ __forceinline__ float l2upd(float acc, float q, float x) {
   return __fadd_rn(acc, __fmul_rn(t, t));
 }
 
+// (q - x0)^2 and (q - x1)^2 for a slot pair held as one 64-bit register:
+// FADD2 with q broadcast, FMUL2 — each lane of the pair rounded on its own,
+// exactly like __fsub_rn / __fmul_rn.  The accumulation stays scalar: ptxas
+// contracts an f32x2 multiply followed by an f32x2 add into FFMA2.
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 sqdiff2(float q, unsigned long long xx) {
+  unsigned long long qq, t, p;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(qq), "l"(xx));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(p) : "l"(t));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+
 // BSA estimate (bsa_est in pdx_scan_spec.cuh, same association).
 __device__ __forceinline__ float bsa_est2(float acc, float rx, float rq, float sq, float coef) {
   const float cx = __fmul_rn(coef, __fsqrt_rn(rx));
@@ -158,12 +177,15 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
                              const int64_t* __restrict__ bucket_block,
                              const int64_t* __restrict__ block_tile, int32_t* __restrict__ seg0,
                              int64_t* __restrict__ wcount, int32_t* __restrict__ pbase,
-                             int32_t* __restrict__ bcnt) {
+                             int32_t* __restrict__ bcnt, int64_t* __restrict__ w0count) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const int32_t* sq = sel + (int64_t)q * nseg;
-  if (lane == 0) seg0[q] = sq[0];
+  if (lane == 0) {
+    seg0[q] = sq[0];
+    w0count[q] = block_tile[bucket_block[sq[0] + 1]] - block_tile[bucket_block[sq[0]]];
+  }
   int run = 0;
   for (int s0 = 1; s0 < nseg; s0 += 32) {
     const int s = s0 + lane;
@@ -266,6 +288,296 @@ __device__ __forceinline__ void record_survivor(const BParams& P, const BArgs& A
     A.flags[q] = 1;
 }
 
+__device__ __forceinline__ float bound_at(const BParams& P, float T, int s, const double* ratio,
+                                          const double* band) {
+  return P.pruner == PDX_PRUNER_BSA ? T : ads_or_bond_bound(T, ratio[s], band[s]);
+}
+
+// ---------------------------------------------------------------- phase 1
+// The reference chain over each query's first selected bucket, in two
+// kernels.  bdense_kernel: every slot's partial (the BSA estimate for bsa)
+// at every step end, prune-free, one warp per (query, tile) — a dense,
+// throughput-bound pass with no dependence between tiles.  bchain1_kernel:
+// one warp per query walks the bucket's blocks in order with the exact
+// threshold chain (search.py:193-205), reading the recorded partials — the
+// linear first block, every prune decision, the top-k pushes, values_touched
+// and the survivor traces.  (A query's first bucket is where its threshold
+// moves at almost every block, so pruned speculation would be replayed
+// anyway after chasing long survivor tails one L2 round trip at a time.)
+// FIRST: tile 0 of each query's first bucket (its linear block), no pruning.
+// Otherwise tiles 1.. under the bounds B_s(T_0), T_0 the threshold after that
+// block (b0bnd, +inf while the heap is not full): T_0 >= every later T_b of
+// the chain, so a slot pruned under it is pruned by the chain too — its
+// partials past that step are recorded as +inf and never read from HBM.
+template <bool BSA, bool FIRST>
+__global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArgs A,
+                                                     const int32_t* __restrict__ seg0,
+                                                     const int64_t* __restrict__ p1off,
+                                                     float* __restrict__ part1,
+                                                     const float* __restrict__ b0bnd) {
+  extern __shared__ __align__(16) float s_q[];  // [d_pad] query, then [2][nsteps] BSA rq, sqrt
+  __shared__ int32_t s_ends[kMaxSteps];
+  __shared__ float s_coef[kMaxSteps];
+  const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = seg0[q];
+  const int64_t b0 = A.bucket_block[c];
+  const int nt = (int)(A.bucket_block[c + 1] - b0);
+  if (FIRST ? nt == 0 : (int)blockIdx.y * 4 + 1 >= nt) return;
+  const int nsteps = P.nsteps;
+  const float* qg = A.queries + (int64_t)q * P.d;
+  for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
+  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
+    s_ends[i] = P.ends[i];
+    s_coef[i] = (BSA && i < nsteps) ? A.coef[i] : 0.f;
+  }
+  __syncthreads();
+  float* s_bq = s_q + P.d_pad;
+  if (BSA) {  // the query's residual energies (pdx_scan_kernel's prologue order)
+    if (threadIdx.x < nsteps) {
+      float r = 0.f;
+      for (int j = s_ends[threadIdx.x]; j < P.d; ++j) r = __fadd_rn(r, __fmul_rn(s_q[j], s_q[j]));
+      s_bq[threadIdx.x] = r;
+      s_bq[nsteps + threadIdx.x] = __fsqrt_rn(r);
+    }
+    __syncthreads();
+  }
+  const int ti = FIRST ? 0 : blockIdx.y * 4 + w + 1;
+  if (ti >= nt || (FIRST && w > 0)) return;
+  const int64_t tile = A.block_tile[b0] + ti;
+  const int m = A.block_m[b0 + ti];
+  const float bl = (!FIRST && lane < nsteps) ? b0bnd[(int64_t)q * nsteps + lane] : INFINITY;
+  const float* __restrict__ tb = A.tiles + tile * A.tile_stride;
+  float* __restrict__ out = part1 + (p1off[q] + ti) * nsteps * kTile;
+  const int ng = P.d_pad >> 3;
+  float acc0 = 0.f, acc1 = 0.f;
+  bool al0 = lane < m, al1 = lane + 32 < m;
+  float n0[8], n1[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
+  if (FIRST || al0) ldg8(tb + lane * 8, n0);
+  if (FIRST || al1) ldg8(tb + (32 + lane) * 8, n1);
+  int s = 0;
+  for (int g = 0; g < ng && s < nsteps; ++g) {
+    if (!FIRST && !__any_sync(kFull, al0 || al1)) {  // every slot pruned under T_0
+      for (; s < nsteps; ++s) {
+        out[s * kTile + lane] = INFINITY;
+        out[s * kTile + 32 + lane] = INFINITY;
+      }
+      break;
+    }
+    float x0[8], x1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      x0[e] = n0[e];
+      x1[e] = n1[e];
+    }
+    if (g + 1 < ng) {
+      if (FIRST || al0) ldg8(tb + ((size_t)(g + 1) * kTile + lane) * 8, n0);
+      if (FIRST || al1) ldg8(tb + ((size_t)(g + 1) * kTile + 32 + lane) * 8, n1);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int dim = g * 8 + e;
+      if (dim < P.d) {
+        const float qe = s_q[dim];
+        acc0 = l2upd(acc0, qe, x0[e]);
+        acc1 = l2upd(acc1, qe, x1[e]);
+        if (dim + 1 == s_ends[s]) {
+          float v0 = acc0, v1 = acc1;
+          if (BSA) {
+            const float* rs = A.resid + ((size_t)tile * nsteps + s) * kTile;
+            v0 = bsa_est2(acc0, __ldg(rs + lane), s_bq[s], s_bq[nsteps + s], s_coef[s]);
+            v1 = bsa_est2(acc1, __ldg(rs + lane + 32), s_bq[s], s_bq[nsteps + s], s_coef[s]);
+          }
+          if (!FIRST) {
+            const float B = __shfl_sync(kFull, bl, s);
+            al0 = al0 && v0 < B;
+            al1 = al1 && v1 < B;
+          }
+          out[s * kTile + lane] = (FIRST || al0) ? v0 : INFINITY;
+          out[s * kTile + 32 + lane] = (FIRST || al1) ? v1 : INFINITY;
+          ++s;
+        }
+      }
+    }
+  }
+}
+
+// T_0 per query: the k-th smallest distance of its first block (the heap
+// after the linear block, search.py:125-135), +inf if that block has fewer
+// than k vectors; b0bnd = B_s(T_0).
+__global__ void bt0_kernel(const BParams P, const BArgs A, const int32_t* __restrict__ seg0,
+                           const int64_t* __restrict__ p1off, const float* __restrict__ part1,
+                           float* __restrict__ b0bnd) {
+  __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
+  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
+    s_ratio[i] = P.ratio[i];
+    s_band[i] = P.band[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= P.nq) return;
+  const int c = seg0[q];
+  const int64_t b0 = A.bucket_block[c];
+  const int m = A.bucket_block[c + 1] > b0 ? A.block_m[b0] : 0;
+  float T = INFINITY;
+  if (m >= P.k) {
+    const float* fin = part1 + p1off[q] * P.nsteps * kTile + (P.nsteps - 1) * kTile;
+    const float v0 = lane < m ? fin[lane] : INFINITY, v1 = lane + 32 < m ? fin[lane + 32] : INFINITY;
+    int l0 = 0, e0 = 0, l1 = 0, e1 = 0;  // values below / equal to mine
+    for (int j = 0; j < 32; ++j) {
+      const float a = __shfl_sync(kFull, v0, j), b = __shfl_sync(kFull, v1, j);
+      l0 += (a < v0) + (b < v0);
+      e0 += (a == v0) + (b == v0);
+      l1 += (a < v1) + (b < v1);
+      e1 += (a == v1) + (b == v1);
+    }
+    const int k = P.k;
+    const bool h0 = l0 <= k - 1 && l0 + e0 >= k, h1 = l1 <= k - 1 && l1 + e1 >= k;
+    const unsigned hm = __ballot_sync(kFull, h0 || h1);
+    const int src = __ffs(hm) - 1;
+    T = __shfl_sync(kFull, h0 ? v0 : v1, src);
+  }
+  if (lane < P.nsteps)
+    b0bnd[(int64_t)q * P.nsteps + lane] = T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
+}
+
+__global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
+                                                      const int32_t* __restrict__ seg0,
+                                                      const int64_t* __restrict__ p1off,
+                                                      const float* __restrict__ part1) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  __shared__ Control s_ctl[8];
+  __shared__ int32_t s_cnt[8][kMaxSteps];
+  __shared__ int32_t s_ends[kMaxSteps], s_wmin[kTile + 1];
+  __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
+  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
+    s_ends[i] = P.ends[i];
+    s_ratio[i] = P.ratio[i];
+    s_band[i] = P.band[i];
+  }
+  for (int i = threadIdx.x; i <= kTile; i += blockDim.x) s_wmin[i] = P.wmin[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int q = blockIdx.x * 8 + wq;
+  if (q >= P.nq) return;
+  const int k = P.k, nsteps = P.nsteps;
+  float* tkd = reinterpret_cast<float*>(s_raw) + (size_t)wq * k;
+  int64_t* tki = reinterpret_cast<int64_t*>(s_raw + (size_t)8 * k * sizeof(float)) + (size_t)wq * k;
+  Control& ctl = s_ctl[wq];
+  if (lane == 0) ctl.n = 0;
+  __syncwarp();
+  const int c = seg0[q];
+  const int64_t b0 = A.bucket_block[c];
+  const int nt = (int)(A.bucket_block[c + 1] - b0);
+  const int64_t t0 = A.block_tile[b0];
+  int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
+  int64_t touched = 0, total = 0, tlen = 0;  // lane 0
+  float T = INFINITY, Tb = -1.f, bl = 0.f;
+  // software pipeline: the next tile's partials, ids and size load while the
+  // current tile is decided (one L2 round trip per tile, hidden)
+  float u0[kMaxSteps], u1[kMaxSteps], n0[kMaxSteps], n1[kMaxSteps];
+  int64_t id0 = 0, id1 = 0, nid0 = 0, nid1 = 0;
+  int m = 0, nm = 0;
+  auto fetch = [&](int ti) {
+    if (ti >= nt) return;
+    const float* __restrict__ pp = part1 + (p1off[q] + ti) * nsteps * kTile;
+#pragma unroll
+    for (int s = 0; s < kMaxSteps; ++s) {
+      n0[s] = s < nsteps ? __ldg(pp + s * kTile + lane) : 0.f;
+      n1[s] = s < nsteps ? __ldg(pp + s * kTile + 32 + lane) : 0.f;
+    }
+    const int64_t* gid = A.tile_ids + (t0 + ti) * kTile;
+    nid0 = __ldg(gid + lane);
+    nid1 = __ldg(gid + lane + 32);
+    nm = A.block_m[b0 + ti];
+  };
+  fetch(0);
+  for (int ti = 0; ti < nt; ++ti) {
+#pragma unroll
+    for (int s = 0; s < kMaxSteps; ++s) {
+      u0[s] = n0[s];
+      u1[s] = n1[s];
+    }
+    id0 = nid0;
+    id1 = nid1;
+    m = nm;
+    fetch(ti + 1);
+    const bool linear = ti == 0 || T == INFINITY;  // search.py:201
+    bool c0 = lane < m, c1 = lane + 32 < m;
+    if (linear) {
+      if (lane == 0) {
+        touched += (int64_t)m * P.d;
+        if (tr) {
+          if (tlen >= 0 && tlen + 2 <= A.trace_cap) {
+            tr[tlen] = 1;
+            tr[tlen + 1] = m;
+            tlen += 2;
+          } else {
+            tlen = -1;
+          }
+        }
+      }
+    } else {
+      if (T != Tb) {  // the bounds move only with the threshold
+        bl = lane < nsteps ? bound_at(P, T, lane, s_ratio, s_band) : 0.f;
+        Tb = T;
+      }
+      int mycnt = 0;
+#pragma unroll
+      for (int s = 0; s < kMaxSteps; ++s) {
+        if (s >= nsteps) break;
+        const float B = __shfl_sync(kFull, bl, s);
+        c0 = c0 && u0[s] < B;
+        c1 = c1 && u1[s] < B;
+        const int cn = __popc(__ballot_sync(kFull, c0)) + __popc(__ballot_sync(kFull, c1));
+        if (lane == s) mycnt = cn;
+      }
+      if (lane < nsteps) s_cnt[wq][lane] = mycnt;
+      __syncwarp();
+      if (lane == 0) {
+        touched += block_touched(m, s_wmin[m], s_cnt[wq], s_ends, nsteps);
+        if (tr) {
+          if (tlen >= 0 && tlen + 1 + nsteps <= A.trace_cap) {
+            tr[tlen] = nsteps;
+            for (int s = 0; s < nsteps; ++s) tr[tlen + 1 + s] = s_cnt[wq][s];
+            tlen += 1 + nsteps;
+          } else {
+            tlen = -1;
+          }
+        }
+      }
+    }
+    if (lane == 0) total += (int64_t)m * P.d;
+    if (__any_sync(kFull, c0 || c1)) {  // push the block's survivors (search.py:173-174)
+      float f0 = 0.f, f1 = 0.f;  // the partial at the last step is the distance
+#pragma unroll
+      for (int s = 0; s < kMaxSteps; ++s)
+        if (s == nsteps - 1) {
+          f0 = u0[s];
+          f1 = u1[s];
+        }
+      topk_push_lanes(ctl, k, tkd, tki, c0, f0, id0, lane);
+      topk_push_lanes(ctl, k, tkd, tki, c1, f1, id1, lane);
+      __syncwarp();
+      T = topk_threshold(ctl, k, tkd);
+    }
+  }
+  __syncwarp();
+  const int n = ctl.n;
+  for (int i = lane; i < k; i += 32) {
+    A.out_dist[(int64_t)q * k + i] = i < n ? tkd[i] : INFINITY;
+    A.out_ids[(int64_t)q * k + i] = i < n ? tki[i] : -1;
+  }
+  if (lane == 0) {
+    A.out_count[q] = n;
+    if (A.out_touched) A.out_touched[q] = touched;
+    if (A.out_total) A.out_total[q] = total;
+    if (A.trace_len) A.trace_len[q] = tlen;
+  }
+}
+
 // ------------------------------------------------------------ phase 2 scan
 // Head schedule known at compile time: initial_step IS, step s ends after
 // dim IS * (2^(s+1) - 1) (step_schedule, search.py:106-117) while <= 16.
@@ -324,11 +636,6 @@ __device__ __forceinline__ void confirm_survivor(const BParams& P, const BArgs& 
   A.flags[q] = 1;  // not a T'-survivor: cannot happen (T^ <= T'); fall back
 }
 
-__device__ __forceinline__ float bound_at(const BParams& P, float T, int s, const double* ratio,
-                                          const double* band) {
-  return P.pruner == PDX_PRUNER_BSA ? T : ads_or_bond_bound(T, ratio[s], band[s]);
-}
-
 // One CTA per work item (a bucket and up to kQC queries probing it).  Warp w
 // takes tiles w, w + kBW, ... of the bucket; per tile, lane l holds the head
 // dims of slots l and l + 32 in registers and loops over the queries.
@@ -347,6 +654,8 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
   __shared__ uint32_t s_dcnt[kBW][kQC][kMaxSteps];  // deep-step counts
   __shared__ uint32_t s_rho[kBW][kQC];
   __shared__ float s_that[kBW][kQC];                // MODE 1: T^ of this tile's pairs
+  __shared__ float s_that0[kQC];                     // MODE 1: T^ at the bucket's first pair
+  __shared__ uint32_t s_jvar, s_jmay;                // MODE 1: T^ varies in the bucket / may be < T'
   __shared__ DeepItem s_deep[kBW][kDeepCap];
   __shared__ float s_rx[BSA ? kBW : 1][kMaxHead][kTile];
   __shared__ int32_t s_ends[kMaxSteps], s_wmin[kTile + 1];
@@ -384,6 +693,32 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
     s_qo[j] = A.qoff[en.q];
     s_tp[j] = A.tprime[en.q];
   }
+  if (MODE == 1) {
+    if (threadIdx.x < 32) {
+      const int j = threadIdx.x;
+      bool may = false, var = false;
+      if (j < ne) {
+        const BEntry en = A.entries[it.e0 + j];
+        if (!A.flags[en.q]) {
+          const BSurv* sv = A.surv + (int64_t)en.q * P.surv_cap;
+          const int n = min(A.nsurv[en.q], P.surv_cap);
+          const float tp = A.tprime[en.q];
+          const float t0 = that_of(sv, n, en.base, tp);
+          const float t1 = that_of(sv, n, en.base + nt - 1, tp);
+          s_that0[j] = t0;
+          var = t1 != t0;
+          may = t0 < tp || t1 < tp;
+        }
+      }
+      const unsigned mm = __ballot_sync(kFull, may), vv = __ballot_sync(kFull, var);
+      if (j == 0) {
+        s_jmay = mm;
+        s_jvar = vv;
+      }
+    }
+    __syncthreads();
+    if (s_jmay == 0) return;  // every pair of this item is certain
+  }
   for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
     s_ends[i] = P.ends[i];
     s_invb[i] = P.invb[i];
@@ -403,14 +738,15 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
     uint32_t todo = 0xffffffffu >> (32 - ne);
     if (MODE == 1) {
       bool unc = false;
-      if (lane < ne) {
+      if ((s_jmay >> lane) & 1u) {
         const int q = s_qid[lane], pl = s_base[lane] + ti;
-        if (!A.flags[q]) {
+        float that = s_that0[lane];
+        if ((s_jvar >> lane) & 1u) {
           const BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
-          const float that = that_of(sv, min(A.nsurv[q], P.surv_cap), pl, s_tp[lane]);
-          unc = pair_uncertain(that, s_tp[lane], A.prho[s_qo[lane] + pl]);
-          if (unc) s_that[w][lane] = that;
+          that = that_of(sv, min(A.nsurv[q], P.surv_cap), pl, s_tp[lane]);
         }
+        unc = pair_uncertain(that, s_tp[lane], A.prho[s_qo[lane] + pl]);
+        if (unc) s_that[w][lane] = that;
       }
       todo = __ballot_sync(kFull, unc);
       if (!todo) continue;
@@ -434,6 +770,11 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
         s_rx[w][s][lane + 32] = __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + lane + 32);
       }
       __syncwarp();
+    }
+    unsigned long long xx[IS > 0 ? HD : 1];
+    if (IS > 0) {
+#pragma unroll
+      for (int e = 0; e < (IS > 0 ? HD : 1); ++e) xx[e] = pack2(x0[e], x1[e]);
     }
     const bool in0 = lane < m, in1 = lane + 32 < m;
     int qn = 0;  // deep items queued by this warp for this tile
@@ -518,7 +859,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
       }
       float acc0 = 0.f, acc1 = 0.f, rho = 0.f;
       bool al0 = in0, al1 = in1;
-      uint32_t packed = 0;
+      uint32_t cntl = 0;  // this lane's survivors per head step, one byte per step
       auto step = [&](int s, float ib) {
         float v0 = acc0, v1 = acc1;
         if (BSA) {
@@ -532,8 +873,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
           if (al0) rho = fmaxf(rho, __fmul_rn(v0, ib));
           if (al1) rho = fmaxf(rho, __fmul_rn(v1, ib));
         }
-        const uint32_t c = __popc(__ballot_sync(kFull, al0)) + __popc(__ballot_sync(kFull, al1));
-        packed |= c << (8 * s);
+        cntl += (al0 ? 1u << (8 * s) : 0u) + (al1 ? 1u << (8 * s) : 0u);
       };
       if (IS > 0) {
         float qv[HD > 0 ? HD : 1];
@@ -547,8 +887,9 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
         }
 #pragma unroll
         for (int e = 0; e < HD; ++e) {
-          acc0 = l2upd(acc0, qv[e], x0[e]);
-          acc1 = l2upd(acc1, qv[e], x1[e]);
+          const float2 d2 = sqdiff2(qv[e], xx[e]);
+          acc0 = __fadd_rn(acc0, d2.x);
+          acc1 = __fadd_rn(acc1, d2.y);
           const int s = HeadSched<IS>::step_at(e);
           if (s >= 0) step(s, s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3);
         }
@@ -568,6 +909,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
           }
         }
       }
+      const uint32_t packed = __reduce_add_sync(kFull, cntl);  // counts <= 64: no carries
       if (lane == 0) s_hcnt[w][j] = packed;
       if (MODE == 0) {
         const uint32_t r = __reduce_max_sync(kFull, __float_as_uint(rho));
@@ -631,43 +973,48 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
 // the k-th distance unchanged when its distance is >= T^ (bfinal_kernel
 // checks that every such survivor is), so this is the reference's chain.
 __global__ void bchain_kernel(const BParams P, const BArgs A) {
-  extern __shared__ float s_top[];  // [warps][k]
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const int q = blockIdx.x * (blockDim.x >> 5) + wq;
+  extern __shared__ float s_top[];  // [warps][k] then [warps][surv_cap] BSurv
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q = blockIdx.x * nw + wq;
   if (q >= P.nq || A.flags[q]) return;
   const int n = min(A.nsurv[q], P.surv_cap);
   if (n == 0) return;
   const int k = P.k;
   float* top = s_top + (size_t)wq * k;
-  for (int i = lane; i < k; i += 32) top[i] = A.out_dist[(int64_t)q * k + i];
-  __syncwarp();
-  if (lane != 0) return;
+  BSurv* ls = reinterpret_cast<BSurv*>(s_top + (size_t)nw * k + 4) + (size_t)wq * P.surv_cap;
   BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
-  for (int i = 1; i < n; ++i) {  // insertion sort by pair (n is small: ~1-2 at C2)
-    const BSurv x = sv[i];
-    int j = i;
-    while (j > 0 && sv[j - 1].pair > x.pair) {
-      sv[j] = sv[j - 1];
-      --j;
-    }
-    sv[j] = x;
-  }
-  for (int i = 0; i < n;) {
-    int e = i;
-    for (; e < n && sv[e].pair == sv[i].pair; ++e) {
-      const float dv = sv[e].dist;
-      if (dv < top[k - 1]) {  // TopK.push, threshold value only
-        int j = k - 1;
-        while (j > 0 && top[j - 1] > dv) {
-          top[j] = top[j - 1];
-          --j;
-        }
-        top[j] = dv;
+  for (int i = lane; i < k; i += 32) top[i] = A.out_dist[(int64_t)q * k + i];
+  for (int i = lane; i < n; i += 32) ls[i] = sv[i];
+  __syncwarp();
+  if (lane == 0) {
+    for (int i = 1; i < n; ++i) {  // insertion sort by pair (n is small: ~1-2 at C2)
+      const BSurv x = ls[i];
+      int j = i;
+      while (j > 0 && ls[j - 1].pair > x.pair) {
+        ls[j] = ls[j - 1];
+        --j;
       }
+      ls[j] = x;
     }
-    for (int j = i; j < e; ++j) sv[j].tafter = top[k - 1];
-    i = e;
+    for (int i = 0; i < n;) {
+      int e = i;
+      for (; e < n && ls[e].pair == ls[i].pair; ++e) {
+        const float dv = ls[e].dist;
+        if (dv < top[k - 1]) {  // TopK.push, threshold value only
+          int j = k - 1;
+          while (j > 0 && top[j - 1] > dv) {
+            top[j] = top[j - 1];
+            --j;
+          }
+          top[j] = dv;
+        }
+      }
+      for (int j = i; j < e; ++j) ls[j].tafter = top[k - 1];
+      i = e;
+    }
   }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) sv[i] = ls[i];
 }
 
 // ------------------------------------------------------------------ final
@@ -803,7 +1150,7 @@ bool batched_eligible(const pdx_store* store, const pdx_search_params* prm, int6
   if (store->ntiles != store->nblocks) return false;  // every block one tile (64-blocks)
   if (prm->pruner == PDX_PRUNER_NONE || prm->metric != PDX_METRIC_L2) return false;
   if (prm->splits > 1 || out->d_debug || prm->k > kMaxBatchK) return false;
-  if (prm->initial_step > kHeadDims) return false;
+  if (prm->initial_step > kHeadDims || store->d_pad > 8192) return false;
   if (prm->batched == 0 && nq < 32) return false;
   if (nq > (1 << 24)) return false;
   const int64_t pairs = nq * (int64_t)(nseg - 1) * store->max_bucket_tiles;
@@ -865,6 +1212,10 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     carve<int32_t>(at, nq);                    // seg0
     carve<int64_t>(at, nq + 1);                // wcount
     carve<int64_t>(at, nq + 1);                // qoff
+    carve<int64_t>(at, nq + 1);                // w0count
+    carve<int64_t>(at, nq + 1);                // p1off
+    carve<float>(at, nq64 * store->max_bucket_tiles * P.nsteps * kTile);  // part1
+    carve<float>(at, nq64 * P.nsteps);                                     // b0bnd
     carve<int32_t>(at, nq64 * nseg);           // pbase
     carve<int32_t>(at, nb + 1);                // bcnt
     carve<int32_t>(at, nb + 1);                // boff
@@ -894,6 +1245,10 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   int32_t* seg0 = carve<int32_t>(at, nq);
   int64_t* wcount = carve<int64_t>(at, nq + 1);
   int64_t* qoff = carve<int64_t>(at, nq + 1);
+  int64_t* w0count = carve<int64_t>(at, nq + 1);
+  int64_t* p1off = carve<int64_t>(at, nq + 1);
+  float* part1 = carve<float>(at, nq64 * store->max_bucket_tiles * P.nsteps * kTile);
+  float* b0bnd = carve<float>(at, nq64 * P.nsteps);
   int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
   int32_t* bcnt = carve<int32_t>(at, nb + 1);
   int32_t* boff = carve<int32_t>(at, nb + 1);
@@ -940,12 +1295,16 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   PDX_B_CHECK(cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), st));
   PDX_B_CHECK(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (nb + 1), st));
   PDX_B_CHECK(cudaMemsetAsync(wcount + nq, 0, sizeof(int64_t), st));
+  PDX_B_CHECK(cudaMemsetAsync(w0count + nq, 0, sizeof(int64_t), st));
   PDX_B_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 4, st));
   bprep_kernel<<<(nq + 7) / 8, 256, 0, st>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
-                                             store->d_block_tile, seg0, wcount, pbase, bcnt);
+                                             store->d_block_tile, seg0, wcount, pbase, bcnt,
+                                             w0count);
   PDX_B_CHECK(cudaGetLastError());
   size_t cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st));
+  cb = cubb;
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, w0count, p1off, nq + 1, st));
   cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, bcnt, boff, nb + 1, st));
   bchunks_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, store->d_bucket_block,
@@ -963,15 +1322,8 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   PDX_B_CHECK(cudaGetLastError());
   phase("plan");
 
-  // ---- phase 1: the first selected bucket of every query, per-query scan
   pdx_search_out o1 = *out;
   if (!o1.d_count) o1.d_count = cnt_scratch;
-  o1.d_debug = nullptr;
-  rc = search_classic(store, prm, d_queries, nq64, seg0, 1, &o1, d_work, work_bytes, stream,
-                      nullptr);
-  if (rc != PDX_OK) return fail(rc);
-
-  phase("phase1");
   BArgs A;
   memset(&A, 0, sizeof(A));
   A.tiles = store->d_tiles;
@@ -1008,6 +1360,45 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   A.trace_len = out->d_trace_len;
 
   const bool bsa = prm->pruner == PDX_PRUNER_BSA;
+  // ---- phase 1: the first selected bucket of every query (exact chain)
+  {
+    const dim3 g((unsigned)nq, (unsigned)((store->max_bucket_tiles + 2) / 4));
+    const size_t sm = sizeof(float) * (store->d_pad + 2 * kMaxSteps);
+    if (sm > 48 * 1024) {
+      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
+    if (store->max_bucket_tiles > 0) {
+      const dim3 g1((unsigned)nq, 1);
+      if (bsa)
+        bdense_kernel<true, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
+      else
+        bdense_kernel<false, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
+      PDX_B_CHECK(cudaGetLastError());
+      bt0_kernel<<<(nq + 7) / 8, 256, 0, st>>>(P, A, seg0, p1off, part1, b0bnd);
+      PDX_B_CHECK(cudaGetLastError());
+      if (store->max_bucket_tiles > 1) {
+        if (bsa)
+          bdense_kernel<true, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
+        else
+          bdense_kernel<false, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
+        PDX_B_CHECK(cudaGetLastError());
+      }
+    }
+    const size_t hsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t));
+    if (hsm > 48 * 1024)
+      PDX_B_CHECK(cudaFuncSetAttribute(bchain1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)hsm));
+    bchain1_kernel<<<(nq + 7) / 8, 256, hsm, st>>>(P, A, seg0, p1off, part1);
+    PDX_B_CHECK(cudaGetLastError());
+  }
+  phase("phase1");
   btprime_kernel<<<(nq + 127) / 128, 128, 0, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("tprime");
@@ -1036,7 +1427,14 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   };
   if (nitems_max > 0) PDX_B_CHECK(scan(0));
   phase("scan");
-  bchain_kernel<<<(nq + 7) / 8, 256, 8 * k * sizeof(float), st>>>(P, A);
+  // one warp per query; its heap threshold and survivor list live in shared memory
+  const size_t cper = (size_t)k * sizeof(float) + (size_t)P.surv_cap * sizeof(BSurv);
+  const int cw = (int)std::max<size_t>(1, std::min<size_t>(8, (160u << 10) / cper));
+  const size_t csm = cw * cper + 16;
+  if (csm > 48 * 1024)
+    PDX_B_CHECK(cudaFuncSetAttribute(bchain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)csm));
+  bchain_kernel<<<(nq + cw - 1) / cw, cw * 32, csm, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("chain");
   if (nitems_max > 0) PDX_B_CHECK(scan(1));

@@ -198,7 +198,8 @@ static int search_impl(const pdx_store* store, const pdx_search_params* prm,
                        const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
                        int32_t nseg, const uint16_t* d_orders, int64_t order_qstride,
                        int64_t order_sstride, const pdx_search_out* out, void* d_work,
-                       int64_t work_bytes, void* stream, const int32_t* only, bool allow_batched) {
+                       int64_t work_bytes, void* stream, const int32_t* only, bool allow_batched,
+                       bool dense_spec = false) {
   PDX_REQUIRE(store && prm && out, "pdx_search: null argument");
   PDX_REQUIRE(prm->k >= 1, "k must be >= 1");
   PDX_REQUIRE(prm->k <= 4096, "k = %d exceeds this build's limit of 4096", prm->k);
@@ -318,6 +319,7 @@ static int search_impl(const pdx_store* store, const pdx_search_params* prm,
   A.debug = out->d_debug;
   A.sparse_max = kItemsPerWarp / tpw;
   A.only = only;
+  A.dense_spec = dense_spec ? 1 : 0;
   PDX_REQUIRE(A.out_dist && A.out_ids, "output buffers required");
 
   // split mode: CTA b scans range b / nq of query b % nq into row b of a
@@ -401,9 +403,9 @@ static int search_impl(const pdx_store* store, const pdx_search_params* prm,
 int pdx::search_classic(const pdx_store* store, const pdx_search_params* prm,
                         const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
                         int32_t nseg, const pdx_search_out* out, void* d_work, int64_t work_bytes,
-                        void* stream, const int32_t* only) {
+                        void* stream, const int32_t* only, bool dense_spec) {
   return search_impl(store, prm, d_queries, nq, d_seg_bucket, nseg, nullptr, 0, 0, out, d_work,
-                     work_bytes, stream, only, false);
+                     work_bytes, stream, only, false, dense_spec);
 }
 
 extern "C" int pdx_search(const pdx_store* store, const pdx_search_params* prm,

@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
         t.block_m = e.block_m;
         t.vis = e.vis;
         t.flags = e.flags;
-        if (A.pruner == PDX_PRUNER_NONE) {
+        if (A.pruner == PDX_PRUNER_NONE || A.dense_spec) {
           t.tspec = INFINITY;
         } else {
           const int first = n0 + lane - e.tib;  // the block's first tile

@@ -102,6 +102,8 @@ struct ScanArgs {
   const float* resid;     // BSA: [ntiles][nsteps][64] residual energy per slot and step
   const float* bsa_coef;  // BSA: [nsteps]
   const int32_t* only;    // optional [nq]: scan only queries with only[q] != 0
+  int32_t dense_spec;     // compute warps speculate with T' = +inf (prune-free scans; the
+                          // commit warp replays every decision from the partials)
 };
 
 // Shared-memory views of one round slice (the tiles of one compute warp).
