@@ -63,6 +63,7 @@ constexpr int kMaxHead = 5;     // steps inside the head (initial_step 1: 1,3,7,
 constexpr int kDeepCap = 64;    // deep items per warp queue
 constexpr int kMaxBatchK = 256;
 constexpr float kRhoSlack = 1.00001f;
+constexpr int kTodoCap = 256;   // recompute pass: per-tile masks for buckets up to this many tiles
 
 struct BEntry {  // a query probing a bucket
   int32_t q;
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
-  if (FIRST ? nt == 0 : (int)blockIdx.y * 4 + 1 >= nt) return;
+  if (FIRST ? nt == 0 : (int)blockIdx.y * 16 + 1 >= nt) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
@@ -341,8 +342,10 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
     }
     __syncthreads();
   }
-  const int ti = FIRST ? 0 : blockIdx.y * 4 + w + 1;
-  if (ti >= nt || (FIRST && w > 0)) return;
+  if (FIRST && w > 0) return;
+  for (int it4 = 0; it4 < (FIRST ? 1 : 4); ++it4) {
+  const int ti = FIRST ? 0 : blockIdx.y * 16 + it4 * 4 + w + 1;
+  if (ti >= nt) return;
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
   const float bl = (!FIRST && lane < nsteps) ? b0bnd[(int64_t)q * nsteps + lane] : INFINITY;
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   const int ng = P.d_pad >> 3;
   float acc0 = 0.f, acc1 = 0.f;
   bool al0 = lane < m, al1 = lane + 32 < m;
+  int nend = s_ends[0];  // end of the current step
   float n0[8], n1[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
@@ -375,14 +379,25 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
       if (FIRST || al0) ldg8(tb + ((size_t)(g + 1) * kTile + lane) * 8, n0);
       if (FIRST || al1) ldg8(tb + ((size_t)(g + 1) * kTile + 32 + lane) * 8, n1);
     }
+    const float4 qa = *reinterpret_cast<const float4*>(s_q + g * 8);
+    const float4 qb = *reinterpret_cast<const float4*>(s_q + g * 8 + 4);
+    const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+    if (g * 8 + 8 < nend) {  // no step ends in this group: straight-line arithmetic
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        acc0 = l2upd(acc0, qv[e], x0[e]);
+        acc1 = l2upd(acc1, qv[e], x1[e]);
+      }
+      continue;
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int dim = g * 8 + e;
-      if (dim < P.d) {
-        const float qe = s_q[dim];
+      if (s < nsteps) {  // (dims past d are never reached: the last step ends at d)
+        const float qe = qv[e];
         acc0 = l2upd(acc0, qe, x0[e]);
         acc1 = l2upd(acc1, qe, x1[e]);
-        if (dim + 1 == s_ends[s]) {
+        if (dim + 1 == nend) {
           float v0 = acc0, v1 = acc1;
           if (BSA) {
             const float* rs = A.resid + ((size_t)tile * nsteps + s) * kTile;
@@ -397,9 +412,11 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
           out[s * kTile + lane] = (FIRST || al0) ? v0 : INFINITY;
           out[s * kTile + 32 + lane] = (FIRST || al1) ? v1 : INFINITY;
           ++s;
+          nend = s < nsteps ? s_ends[s] : 0x7fffffff;
         }
       }
     }
+  }
   }
 }
 
@@ -524,20 +541,41 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
         bl = lane < nsteps ? bound_at(P, T, lane, s_ratio, s_band) : 0.f;
         Tb = T;
       }
-      int mycnt = 0;
+      // per step independently: bit s = partial below B_s; a slot survives
+      // steps 0 .. d-1 where d = the number of trailing ones (its chain)
+      uint32_t ok0 = 0, ok1 = 0;
 #pragma unroll
       for (int s = 0; s < kMaxSteps; ++s) {
         if (s >= nsteps) break;
         const float B = __shfl_sync(kFull, bl, s);
-        c0 = c0 && u0[s] < B;
-        c1 = c1 && u1[s] < B;
-        const int cn = __popc(__ballot_sync(kFull, c0)) + __popc(__ballot_sync(kFull, c1));
+        ok0 |= (u0[s] < B ? 1u : 0u) << s;
+        ok1 |= (u1[s] < B ? 1u : 0u) << s;
+      }
+      const int d0 = c0 ? __ffs(~ok0) - 1 : 0, d1 = c1 ? __ffs(~ok1) - 1 : 0;
+      int mycnt = 0;
+#pragma unroll
+      for (int s = 0; s < kMaxSteps; ++s) {
+        if (s >= nsteps) break;
+        const int cn = __popc(__ballot_sync(kFull, d0 > s)) + __popc(__ballot_sync(kFull, d1 > s));
         if (lane == s) mycnt = cn;
       }
-      if (lane < nsteps) s_cnt[wq][lane] = mycnt;
+      c0 = d0 >= nsteps;
+      c1 = d1 >= nsteps;
+      // values_touched (search.py:148-169): step s counts m * w_s while the
+      // entering count stays >= the WARMUP minimum (counts only fall, so the
+      // flag is just that test), entering * w_s after; one lane per step
+      const int enter = __shfl_up_sync(kFull, mycnt, 1);
+      int64_t tv = 0;
+      if (lane < nsteps) {
+        const int e_s = lane == 0 ? m : enter;
+        const int w_s = s_ends[lane] - (lane ? s_ends[lane - 1] : 0);
+        tv = (int64_t)(e_s >= s_wmin[m] ? m : e_s) * w_s;
+      }
+      const unsigned tsum = __reduce_add_sync(kFull, (unsigned)tv);  // <= 64 * d per block
+      if (tr && lane < nsteps) s_cnt[wq][lane] = mycnt;
       __syncwarp();
       if (lane == 0) {
-        touched += block_touched(m, s_wmin[m], s_cnt[wq], s_ends, nsteps);
+        touched += tsum;
         if (tr) {
           if (tlen >= 0 && tlen + 1 + nsteps <= A.trace_cap) {
             tr[tlen] = nsteps;
@@ -656,6 +694,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
   __shared__ float s_that[kBW][kQC];                // MODE 1: T^ of this tile's pairs
   __shared__ float s_that0[kQC];                     // MODE 1: T^ at the bucket's first pair
   __shared__ uint32_t s_jvar, s_jmay;                // MODE 1: T^ varies in the bucket / may be < T'
+  __shared__ uint32_t s_todo[MODE == 1 ? kTodoCap : 1];  // MODE 1: uncertain queries per tile
   __shared__ DeepItem s_deep[kBW][kDeepCap];
   __shared__ float s_rx[BSA ? kBW : 1][kMaxHead][kTile];
   __shared__ int32_t s_ends[kMaxSteps], s_wmin[kTile + 1];
@@ -729,6 +768,22 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
   for (int i = threadIdx.x; i <= kTile; i += blockDim.x) s_wmin[i] = P.wmin[i];
   __syncthreads();
 
+  if (MODE == 1 && nt <= kTodoCap) {  // which (query, tile) pairs are uncertain, all at once
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) s_todo[i] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ne * nt; i += blockDim.x) {
+      const int j = i / nt, ti = i - j * nt;
+      if (!((s_jmay >> j) & 1u)) continue;
+      const int pl = s_base[j] + ti;
+      float that = s_that0[j];
+      if ((s_jvar >> j) & 1u) {
+        const int q = s_qid[j];
+        that = that_of(A.surv + (int64_t)q * P.surv_cap, min(A.nsurv[q], P.surv_cap), pl, s_tp[j]);
+      }
+      if (pair_uncertain(that, s_tp[j], A.prho[s_qo[j] + pl])) atomicOr(&s_todo[ti], 1u << j);
+    }
+    __syncthreads();
+  }
   constexpr int HS = HeadSched<IS>::n, HD = HeadSched<IS>::dims;
   const int hs = IS ? HS : P.hsteps, hd = IS ? HD : P.hdims;
   const float ib0 = s_invb[0], ib1 = s_invb[1], ib2 = s_invb[2], ib3 = s_invb[3];
@@ -736,7 +791,20 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
     const int64_t tile = t0 + ti;
     // MODE 1: which queries of this tile are uncertain (bit j)
     uint32_t todo = 0xffffffffu >> (32 - ne);
-    if (MODE == 1) {
+    if (MODE == 1 && nt <= kTodoCap) {
+      todo = s_todo[ti];
+      if (!todo) continue;
+      if ((todo >> lane) & 1u) {
+        float that = s_that0[lane];
+        if ((s_jvar >> lane) & 1u) {
+          const int q = s_qid[lane];
+          that = that_of(A.surv + (int64_t)q * P.surv_cap, min(A.nsurv[q], P.surv_cap),
+                         s_base[lane] + ti, s_tp[lane]);
+        }
+        s_that[w][lane] = that;
+      }
+      __syncwarp();
+    } else if (MODE == 1) {
       bool unc = false;
       if ((s_jmay >> lane) & 1u) {
         const int q = s_qid[lane], pl = s_base[lane] + ti;
@@ -791,6 +859,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
         const bool q4 = (P.d & 3) == 0;
         float acc = di.acc;
         int s = hs, pos = hd;
+        int nend = s_ends[s];
         while (act) {
           const int g = pos >> 3;
           float x[8], qv[8];
@@ -808,7 +877,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
             const int dim = g * 8 + e;
             if (act && dim >= pos) {
               acc = l2upd(acc, qv[e], x[e]);
-              if (dim + 1 == s_ends[s]) {
+              if (dim + 1 == nend) {
                 float v = acc;
                 if (BSA) {
                   const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
@@ -823,6 +892,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
                     atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
                 }
                 ++s;
+                nend = s < nsteps ? s_ends[s] : 0x7fffffff;
                 if (!ok) {
                   act = false;
                 } else if (s == nsteps) {
@@ -850,7 +920,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
       if (MODE == 0) {
         const float4 b4 = *reinterpret_cast<const float4*>(s_bnd[j]);
         bnd[0] = b4.x; bnd[1] = b4.y; bnd[2] = b4.z; bnd[3] = b4.w;
-        bnd[4] = s_bnd[j][4];
+        bnd[4] = IS > 0 ? 0.f : s_bnd[j][4];
       } else {
         that = s_that[w][j];
         const float bl = lane < nsteps ? bound_at(P, that, lane, s_ratio, s_band) : 0.f;
@@ -858,6 +928,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
         for (int s = 0; s < kMaxHead; ++s) bnd[s] = __shfl_sync(kFull, bl, s);
       }
       float acc0 = 0.f, acc1 = 0.f, rho = 0.f;
+      float mx[kMaxHead] = {0.f, 0.f, 0.f, 0.f, 0.f};  // per head step: max surviving partial
       bool al0 = in0, al1 = in1;
       uint32_t cntl = 0;  // this lane's survivors per head step, one byte per step
       auto step = [&](int s, float ib) {
@@ -870,8 +941,13 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
         al0 = al0 && v0 < B;
         al1 = al1 && v1 < B;
         if (MODE == 0) {
-          if (al0) rho = fmaxf(rho, __fmul_rn(v0, ib));
-          if (al1) rho = fmaxf(rho, __fmul_rn(v1, ib));
+          if (IS > 0) {  // s is a compile-time constant here: v * ib is folded in once per pair
+            if (al0) mx[s] = fmaxf(mx[s], v0);
+            if (al1) mx[s] = fmaxf(mx[s], v1);
+          } else {
+            if (al0) rho = fmaxf(rho, __fmul_rn(v0, ib));
+            if (al1) rho = fmaxf(rho, __fmul_rn(v1, ib));
+          }
         }
         cntl += (al0 ? 1u << (8 * s) : 0u) + (al1 ? 1u << (8 * s) : 0u);
       };
@@ -912,6 +988,11 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
       const uint32_t packed = __reduce_add_sync(kFull, cntl);  // counts <= 64: no carries
       if (lane == 0) s_hcnt[w][j] = packed;
       if (MODE == 0) {
+        if (IS > 0) {  // max_s(max v_s * ib_s) = max over (slot, s) of v * ib: rounding is monotone
+#pragma unroll
+          for (int s = 0; s < HS; ++s)
+            rho = fmaxf(rho, __fmul_rn(mx[s], s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3));
+        }
         const uint32_t r = __reduce_max_sync(kFull, __float_as_uint(rho));
         if (lane == 0) s_rho[w][j] = r;
       }
@@ -1362,7 +1443,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   const bool bsa = prm->pruner == PDX_PRUNER_BSA;
   // ---- phase 1: the first selected bucket of every query (exact chain)
   {
-    const dim3 g((unsigned)nq, (unsigned)((store->max_bucket_tiles + 2) / 4));
+    const dim3 g((unsigned)nq, (unsigned)((store->max_bucket_tiles + 14) / 16));
     const size_t sm = sizeof(float) * (store->d_pad + 2 * kMaxSteps);
     if (sm > 48 * 1024) {
       PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, true>,

@@ -1,7 +1,8 @@
 """Per-CUDA-source-line instruction and stall totals from an ncu report."""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+flt = sys.argv[3].split() if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 cur_file, out = None, []
