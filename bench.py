@@ -343,7 +343,7 @@ def main():
     prof = ncu_traffic()
     traffic = None
     if prof and prof.get("workload") == config["workload"]:
-        traffic = prof.get("dram_bytes_per_launch")
+        traffic = prof.get("dram_bytes_per_search")
     line = {
         "metric": "queries/sec at recall@10", "value": qps, "unit": "queries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
@@ -353,8 +353,10 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic,
                      "traffic_source": (prof or {}).get("source"),
-                     "kernel": "pdx_scan_kernel<8,false,L2>",
-                     "time_share_ncu": (prof or {}).get("scan_time_share"),
+                     "kernel": "pdx_search (batched pipeline, pdx_batch.cu); achieved = "
+                               "algorithmic bytes / the whole search call",
+                     "dominant_kernel": (prof or {}).get("dominant_kernel"),
+                     "dominant_time_share_ncu": (prof or {}).get("dominant_time_share"),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "full_scan_bytes_per_launch": 4 * total,
                      "pruning_power": 1 - touched / total, "scan_ms": t_scan},
@@ -363,8 +365,8 @@ def main():
                 "d2h_bytes_per_step": int(args.nq * K * (4 + 8)),
                 "path": ("pdx_index_search (C-ABI handle, pinned host buffers)" if ws == 1 else
                          "pinned host queries -> sharded scan -> NCCL gather + merge -> host")},
-        # per step: project, centroid_dist, select, bound_factors, build_visits, scan
-        "gpu_launches": 6 * args.steps,
+        # per step: the projection + every launch of one search (ncu launch list)
+        "gpu_launches": (1 + int((prof or {}).get("launches_per_search") or 0)) * args.steps,
         "index_build_s": build_s,
     }
     line["clocks"] = clk.summary()
@@ -376,7 +378,7 @@ def main():
                 s2.run(Qr_dev)
             torch.cuda.synchronize()
             ts = []
-            for _ in range(5):
+            for _ in range(9):
                 flush.fill_(1)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
@@ -386,7 +388,8 @@ def main():
                 ts.append(e0.elapsed_time(e1))
             ids2 = r2.ids.cpu().numpy()
             rec2 = float(np.mean([P.recall_at_k(gt.ids[i], ids2[i], K) for i in range(args.nq)]))
-            extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.mean(ts) / 1e3), "recall_at_10": rec2}
+            extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": rec2,
+                                       "timing": "median of 9 L2-flushed searches"}
         # BSA (this build's restatement) on the same data and nprobe
         est = P.IvfNearestNeighbors(pruner="bsa", nlist=NLIST, nprobe=args.nprobe, seed=0).fit(X)
         sb = est.searcher(K)
@@ -397,7 +400,7 @@ def main():
             sb.run(Qb)
         torch.cuda.synchronize()
         ts = []
-        for _ in range(5):
+        for _ in range(9):
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -408,7 +411,7 @@ def main():
         idsb = rb.ids.cpu().numpy()
         recb = float(np.mean([P.recall_at_k(gt.ids[i], idsb[i], K) for i in range(args.nq)]))
         extras[f"bsa_nprobe_{args.nprobe}"] = {
-            "qps": args.nq / (np.mean(ts) / 1e3), "recall_at_10": recb,
+            "qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": recb,
             "pruning_power": pp_b, "coef": [round(c, 4) for c in est.bsa_.coef]}
         line["extras"] = extras
     if ws == 1:
