@@ -58,6 +58,7 @@ namespace {
 
 constexpr int kBW = 8;          // warps per work-item CTA
 constexpr int kQC = 32;         // queries per work item
+constexpr int kTC = 32;         // tiles per work item (long buckets are split: load balance)
 constexpr int kHeadDims = 16;   // dims every pair evaluates for all 64 slots
 constexpr int kMaxHead = 5;     // steps inside the head (initial_step 1: 1,3,7,15)
 constexpr int kDeepCap = 64;    // deep items per warp queue
@@ -69,8 +70,8 @@ struct BEntry {  // a query probing a bucket
   int32_t q;
   int32_t base;  // query-local pair index of the bucket's first tile
 };
-struct BItem {
-  int32_t bucket, e0, ne, pad;
+struct BItem {  // a work item: bucket, its entries [e0, e0 + ne), tiles [t0, t0 + kTC)
+  int32_t bucket, e0, ne, t0;
 };
 // A T'-survivor (phase 2).  The chain kernel sorts a query's list by pair and
 // sets tafter = T^ after the pushes of that pair; the recompute pass sets
@@ -219,7 +220,8 @@ __global__ void bchunks_kernel(const int32_t* __restrict__ bcnt, int nb,
     nch[c] = 0;
     return;
   }
-  nch[c] = (bcnt[c] + kQC - 1) / kQC;
+  const int ntc = (int)(bucket_block[c + 1] - bucket_block[c]);
+  nch[c] = ((bcnt[c] + kQC - 1) / kQC) * ((ntc + kTC - 1) / kTC);
   int64_t v = 0;
   for (int64_t b = bucket_block[c]; b < bucket_block[c + 1]; ++b) v += block_m[b];
   bnvec[c] = v;
@@ -242,13 +244,16 @@ __global__ void bfill_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
 
 __global__ void bitems_kernel(const int32_t* __restrict__ bcnt, int nb,
                               const int32_t* __restrict__ boff, const int32_t* __restrict__ choff,
-                              BItem* __restrict__ items, int32_t* __restrict__ nitems) {
+                              const int64_t* __restrict__ bucket_block, BItem* __restrict__ items,
+                              int32_t* __restrict__ nitems) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c == 0) *nitems = choff[nb];
   if (c >= nb) return;
   const int n = bcnt[c];
-  for (int i = 0, j = choff[c]; i < n; i += kQC, ++j)
-    items[j] = BItem{c, boff[c] + i, min(kQC, n - i), 0};
+  const int ntc = (int)(bucket_block[c + 1] - bucket_block[c]);
+  int j = choff[c];
+  for (int t = 0; t < ntc; t += kTC)
+    for (int i = 0; i < n; i += kQC) items[j++] = BItem{c, boff[c] + i, min(kQC, n - i), t};
 }
 
 // T' per query (the phase-1 heap's k-th distance), the bounds B_s(T'), and
@@ -705,8 +710,11 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
   const BItem it = A.items[blockIdx.x];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ne = it.ne, nsteps = P.nsteps;
-  const int64_t b0 = A.bucket_block[it.bucket];
-  const int nt = (int)(A.bucket_block[it.bucket + 1] - b0);
+  const int64_t bk0 = A.bucket_block[it.bucket];
+  const int tbeg = it.t0;  // this item's tiles of the bucket: [tbeg, tend); ti below is local
+  const int tend = min((int)(A.bucket_block[it.bucket + 1] - bk0), tbeg + kTC);
+  const int nt = tend - tbeg;
+  const int64_t b0 = bk0 + tbeg;  // block (= tile, 64-blocks) of local tile 0
   const int64_t t0 = A.block_tile[b0];
   for (int i = threadIdx.x; i < ne * kHeadDims; i += blockDim.x) {
     const int j = i / kHeadDims, e = i % kHeadDims;
@@ -728,7 +736,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
   for (int j = threadIdx.x; j < ne; j += blockDim.x) {
     const BEntry en = A.entries[it.e0 + j];
     s_qid[j] = en.q;
-    s_base[j] = en.base;
+    s_base[j] = en.base + tbeg;  // pair index of local tile 0
     s_qo[j] = A.qoff[en.q];
     s_tp[j] = A.tprime[en.q];
   }
@@ -742,8 +750,8 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
           const BSurv* sv = A.surv + (int64_t)en.q * P.surv_cap;
           const int n = min(A.nsurv[en.q], P.surv_cap);
           const float tp = A.tprime[en.q];
-          const float t0 = that_of(sv, n, en.base, tp);
-          const float t1 = that_of(sv, n, en.base + nt - 1, tp);
+          const float t0 = that_of(sv, n, en.base + tbeg, tp);
+          const float t1 = that_of(sv, n, en.base + tbeg + nt - 1, tp);
           s_that0[j] = t0;
           var = t1 != t0;
           may = t0 < tp || t1 < tp;
@@ -1276,7 +1284,8 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   const int64_t per = nseg - 1;
   const int64_t pmax = nq64 * per * store->max_bucket_tiles;
   const bool trace = out->d_trace != nullptr;
-  const int64_t nitems_max = nb + (nq64 * per + kQC - 1) / kQC + 1;
+  const int64_t nitems_max = (nb + (nq64 * per + kQC - 1) / kQC + 1) *
+                             ((store->max_bucket_tiles + kTC - 1) / kTC);
 
   // cub scratch (three exclusive sums)
   size_t cub1 = 0, cub2 = 0;
@@ -1399,7 +1408,8 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
         entries);
     PDX_B_CHECK(cudaGetLastError());
   }
-  bitems_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, boff, choff, items, ctr);
+  bitems_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, boff, choff, store->d_bucket_block,
+                                                  items, ctr);
   PDX_B_CHECK(cudaGetLastError());
   phase("plan");
 
