@@ -59,6 +59,7 @@ namespace {
 constexpr int kBW = 8;          // warps per work-item CTA
 constexpr int kQC = 32;         // queries per work item
 constexpr int kTC = 32;         // tiles per work item (long buckets are split: load balance)
+constexpr int kP1Cap = 64;      // phase 1 covers at most this many tiles of the first bucket
 constexpr int kHeadDims = 16;   // dims every pair evaluates for all 64 slots
 constexpr int kMaxHead = 5;     // steps inside the head (initial_step 1: 1,3,7,15)
 constexpr int kDeepCap = 64;    // deep items per warp queue
@@ -184,11 +185,17 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const int32_t* sq = sel + (int64_t)q * nseg;
+  // phase 1 takes the first min(nt0, kP1Cap) tiles of the first bucket; its
+  // tail (if any) opens the speculative window, pair indices from 0
+  const int nt0 = (int)(block_tile[bucket_block[sq[0] + 1]] - block_tile[bucket_block[sq[0]]]);
+  const int p1 = min(nt0, kP1Cap);
   if (lane == 0) {
     seg0[q] = sq[0];
-    w0count[q] = block_tile[bucket_block[sq[0] + 1]] - block_tile[bucket_block[sq[0]]];
+    w0count[q] = p1;
+    pbase[(int64_t)q * nseg] = -p1;
+    if (nt0 > p1) atomicAdd(&bcnt[sq[0]], 1);
   }
-  int run = 0;
+  int run = nt0 - p1;
   for (int s0 = 1; s0 < nseg; s0 += 32) {
     const int s = s0 + lane;
     int nt = 0;
@@ -233,11 +240,11 @@ __global__ void bfill_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
                              const int32_t* __restrict__ pbase, const int32_t* __restrict__ boff,
                              int32_t* __restrict__ bcur, BEntry* __restrict__ entries) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t per = nseg - 1;
-  if (i >= (int64_t)nq * per) return;
-  const int q = (int)(i / per), s = 1 + (int)(i % per);
+  if (i >= (int64_t)nq * nseg) return;
+  const int q = (int)(i / nseg), s = (int)(i % nseg);
   const int c = sel[(int64_t)q * nseg + s];
-  if (block_tile[bucket_block[c + 1]] == block_tile[bucket_block[c]]) return;
+  const int64_t ntc = block_tile[bucket_block[c + 1]] - block_tile[bucket_block[c]];
+  if (s == 0 ? ntc <= kP1Cap : ntc == 0) return;  // no tail of the first bucket / empty
   const int pos = atomicAdd(&bcur[c], 1);
   entries[boff[c] + pos] = BEntry{q, pbase[(int64_t)q * nseg + s]};
 }
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
-  if (FIRST ? nt == 0 : (int)blockIdx.y * 16 + 1 >= nt) return;
+  if (FIRST ? nt == 0 : (int)blockIdx.y * 16 + 1 >= min(nt, kP1Cap)) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   if (FIRST && w > 0) return;
   for (int it4 = 0; it4 < (FIRST ? 1 : 4); ++it4) {
   const int ti = FIRST ? 0 : blockIdx.y * 16 + it4 * 4 + w + 1;
-  if (ti >= nt) return;
+  if (ti >= min(nt, kP1Cap)) return;
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
   const float bl = (!FIRST && lane < nsteps) ? b0bnd[(int64_t)q * nsteps + lane] : INFINITY;
@@ -465,6 +472,7 @@ __global__ void bt0_kernel(const BParams P, const BArgs A, const int32_t* __rest
     b0bnd[(int64_t)q * P.nsteps + lane] = T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
 }
 
+template <int NSM>  // NSM >= nsteps: register arrays sized to the schedule
 __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
                                                       const int32_t* __restrict__ seg0,
                                                       const int64_t* __restrict__ p1off,
@@ -492,21 +500,21 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   __syncwarp();
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
-  const int nt = (int)(A.bucket_block[c + 1] - b0);
+  const int nt = min((int)(A.bucket_block[c + 1] - b0), kP1Cap);
   const int64_t t0 = A.block_tile[b0];
   int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
   int64_t touched = 0, total = 0, tlen = 0;  // lane 0
   float T = INFINITY, Tb = -1.f, bl = 0.f;
   // software pipeline: the next tile's partials, ids and size load while the
   // current tile is decided (one L2 round trip per tile, hidden)
-  float u0[kMaxSteps], u1[kMaxSteps], n0[kMaxSteps], n1[kMaxSteps];
+  float u0[NSM], u1[NSM], n0[NSM], n1[NSM];
   int64_t id0 = 0, id1 = 0, nid0 = 0, nid1 = 0;
   int m = 0, nm = 0;
   auto fetch = [&](int ti) {
     if (ti >= nt) return;
     const float* __restrict__ pp = part1 + (p1off[q] + ti) * nsteps * kTile;
 #pragma unroll
-    for (int s = 0; s < kMaxSteps; ++s) {
+    for (int s = 0; s < NSM; ++s) {
       n0[s] = s < nsteps ? __ldg(pp + s * kTile + lane) : 0.f;
       n1[s] = s < nsteps ? __ldg(pp + s * kTile + 32 + lane) : 0.f;
     }
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   fetch(0);
   for (int ti = 0; ti < nt; ++ti) {
 #pragma unroll
-    for (int s = 0; s < kMaxSteps; ++s) {
+    for (int s = 0; s < NSM; ++s) {
       u0[s] = n0[s];
       u1[s] = n1[s];
     }
@@ -550,7 +558,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
       // steps 0 .. d-1 where d = the number of trailing ones (its chain)
       uint32_t ok0 = 0, ok1 = 0;
 #pragma unroll
-      for (int s = 0; s < kMaxSteps; ++s) {
+      for (int s = 0; s < NSM; ++s) {
         if (s >= nsteps) break;
         const float B = __shfl_sync(kFull, bl, s);
         ok0 |= (u0[s] < B ? 1u : 0u) << s;
@@ -559,7 +567,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
       const int d0 = c0 ? __ffs(~ok0) - 1 : 0, d1 = c1 ? __ffs(~ok1) - 1 : 0;
       int mycnt = 0;
 #pragma unroll
-      for (int s = 0; s < kMaxSteps; ++s) {
+      for (int s = 0; s < NSM; ++s) {
         if (s >= nsteps) break;
         const int cn = __popc(__ballot_sync(kFull, d0 > s)) + __popc(__ballot_sync(kFull, d1 > s));
         if (lane == s) mycnt = cn;
@@ -593,10 +601,54 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
       }
     }
     if (lane == 0) total += (int64_t)m * P.d;
+    if (ti == 0 && k <= kTile) {
+      // the linear first block into an empty heap: the k smallest (dist, id)
+      // of its m vectors, by a warp bitonic sort of the 64 slots
+      float f0 = INFINITY, f1 = INFINITY;
+#pragma unroll
+      for (int s = 0; s < NSM; ++s)
+        if (s == nsteps - 1) {
+          f0 = c0 ? u0[s] : INFINITY;
+          f1 = c1 ? u1[s] : INFINITY;
+        }
+      int64_t i0 = c0 ? id0 : INT64_MAX, i1 = c1 ? id1 : INT64_MAX;
+      // element e = lane (f0) and e = lane + 32 (f1); ascending (dist, id)
+      for (int size = 2; size <= 64; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          if (stride == 32) {  // partners are f0/f1 of the same lane
+            const bool asc = true;  // size == 64: one ascending sequence
+            const bool sw = pair_less(f1, i1, f0, i0) == asc;
+            if (sw) {
+              const float tf = f0; f0 = f1; f1 = tf;
+              const int64_t tt = i0; i0 = i1; i1 = tt;
+            }
+          } else {
+            auto cx = [&](float& f, int64_t& id, int e) {
+              const float of = __shfl_xor_sync(kFull, f, stride);
+              const int64_t oi = __shfl_xor_sync(kFull, id, stride);
+              const bool lower = (e & stride) == 0;
+              const bool asc = (e & size) == 0;
+              const bool mine_less = pair_less(f, id, of, oi);
+              const bool keep = (lower == asc) ? mine_less : !mine_less;
+              if (!keep) { f = of; id = oi; }
+            };
+            cx(f0, i0, lane);
+            cx(f1, i1, lane + 32);
+          }
+        }
+      }
+      const int n = min(k, m);
+      if (lane < n) { tkd[lane] = f0; tki[lane] = i0; }
+      if (lane + 32 < n) { tkd[lane + 32] = f1; tki[lane + 32] = i1; }
+      if (lane == 0) ctl.n = n;
+      __syncwarp();
+      T = topk_threshold(ctl, k, tkd);
+      c0 = c1 = false;
+    }
     if (__any_sync(kFull, c0 || c1)) {  // push the block's survivors (search.py:173-174)
       float f0 = 0.f, f1 = 0.f;  // the partial at the last step is the distance
 #pragma unroll
-      for (int s = 0; s < kMaxSteps; ++s)
+      for (int s = 0; s < NSM; ++s)
         if (s == nsteps - 1) {
           f0 = u0[s];
           f1 = u1[s];
@@ -783,6 +835,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
       const int j = i / nt, ti = i - j * nt;
       if (!((s_jmay >> j) & 1u)) continue;
       const int pl = s_base[j] + ti;
+      if (pl < 0) continue;
       float that = s_that0[j];
       if ((s_jvar >> j) & 1u) {
         const int q = s_qid[j];
@@ -798,7 +851,8 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
   for (int ti = w; ti < nt; ti += kBW) {
     const int64_t tile = t0 + ti;
     // MODE 1: which queries of this tile are uncertain (bit j)
-    uint32_t todo = 0xffffffffu >> (32 - ne);
+    uint32_t todo = __ballot_sync(kFull, lane < ne && s_base[lane] + ti >= 0);
+    if (!todo) continue;  // (tiles of a first bucket that phase 1 covered)
     if (MODE == 1 && nt <= kTodoCap) {
       todo = s_todo[ti];
       if (!todo) continue;
@@ -814,7 +868,7 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
       __syncwarp();
     } else if (MODE == 1) {
       bool unc = false;
-      if ((s_jmay >> lane) & 1u) {
+      if (((s_jmay >> lane) & 1u) && s_base[lane] + ti >= 0) {
         const int q = s_qid[lane], pl = s_base[lane] + ti;
         float that = s_that0[lane];
         if ((s_jvar >> lane) & 1u) {
@@ -1185,6 +1239,9 @@ __global__ void bfinal_kernel(const BParams P, const BArgs A) {
   if (A.out_total) {
     int64_t v = 0;
     for (int s = 1 + lane; s < P.nseg; s += 32) v += A.bnvec[A.sel[(int64_t)q * P.nseg + s]];
+    const int64_t f0 = A.bucket_block[A.sel[(int64_t)q * P.nseg]];
+    const int nt0 = (int)(A.bucket_block[A.sel[(int64_t)q * P.nseg] + 1] - f0);
+    for (int ti = kP1Cap + lane; ti < nt0; ti += 32) v += A.block_m[f0 + ti];  // first-bucket tail
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     if (lane == 0) A.out_total[q] += v * P.d;
   }
@@ -1282,9 +1339,9 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   for (int m = 0; m <= kTile; ++m) P.wmin[m] = m > 0 ? host_warm_min(m, prm->selection_fraction) : 0;
   P.surv_cap = 4 * k + 64;
   const int64_t per = nseg - 1;
-  const int64_t pmax = nq64 * per * store->max_bucket_tiles;
+  const int64_t pmax = nq64 * nseg * store->max_bucket_tiles;
   const bool trace = out->d_trace != nullptr;
-  const int64_t nitems_max = (nb + (nq64 * per + kQC - 1) / kQC + 1) *
+  const int64_t nitems_max = (nb + (nq64 * nseg + kQC - 1) / kQC + 1) *
                              ((store->max_bucket_tiles + kTC - 1) / kTC);
 
   // cub scratch (three exclusive sums)
@@ -1304,7 +1361,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     carve<int64_t>(at, nq + 1);                // qoff
     carve<int64_t>(at, nq + 1);                // w0count
     carve<int64_t>(at, nq + 1);                // p1off
-    carve<float>(at, nq64 * store->max_bucket_tiles * P.nsteps * kTile);  // part1
+    carve<float>(at, nq64 * std::min(store->max_bucket_tiles, kP1Cap) * P.nsteps * kTile);  // part1
     carve<float>(at, nq64 * P.nsteps);                                     // b0bnd
     carve<int32_t>(at, nq64 * nseg);           // pbase
     carve<int32_t>(at, nb + 1);                // bcnt
@@ -1313,7 +1370,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     carve<int32_t>(at, nb + 1);                // nch
     carve<int32_t>(at, nb + 1);                // choff
     carve<int64_t>(at, nb + 1);                // bnvec
-    carve<BEntry>(at, nq64 * per + 1);         // entries
+    carve<BEntry>(at, nq64 * nseg + 1);        // entries
     carve<BItem>(at, nitems_max);              // items
     carve<int32_t>(at, 4);                     // nitems
     carve<int32_t>(at, nq);                    // count scratch
@@ -1337,7 +1394,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   int64_t* qoff = carve<int64_t>(at, nq + 1);
   int64_t* w0count = carve<int64_t>(at, nq + 1);
   int64_t* p1off = carve<int64_t>(at, nq + 1);
-  float* part1 = carve<float>(at, nq64 * store->max_bucket_tiles * P.nsteps * kTile);
+  float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, kP1Cap) * P.nsteps * kTile);
   float* b0bnd = carve<float>(at, nq64 * P.nsteps);
   int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
   int32_t* bcnt = carve<int32_t>(at, nb + 1);
@@ -1346,7 +1403,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   int32_t* nch = carve<int32_t>(at, nb + 1);
   int32_t* choff = carve<int32_t>(at, nb + 1);
   int64_t* bnvec = carve<int64_t>(at, nb + 1);
-  BEntry* entries = carve<BEntry>(at, nq64 * per + 1);
+  BEntry* entries = carve<BEntry>(at, nq64 * nseg + 1);
   BItem* items = carve<BItem>(at, nitems_max);
   int32_t* ctr = carve<int32_t>(at, 4);
   int32_t* cnt_scratch = carve<int32_t>(at, nq);
@@ -1402,8 +1459,8 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   PDX_B_CHECK(cudaGetLastError());
   cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, nch, choff, nb + 1, st));
-  if (nq64 * per > 0) {
-    bfill_kernel<<<(unsigned)((nq64 * per + 255) / 256), 256, 0, st>>>(
+  if (nq64 * nseg > 0) {
+    bfill_kernel<<<(unsigned)((nq64 * nseg + 255) / 256), 256, 0, st>>>(
         d_seg_bucket, nq, nseg, store->d_bucket_block, store->d_block_tile, pbase, boff, bcur,
         entries);
     PDX_B_CHECK(cudaGetLastError());
@@ -1453,7 +1510,8 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   const bool bsa = prm->pruner == PDX_PRUNER_BSA;
   // ---- phase 1: the first selected bucket of every query (exact chain)
   {
-    const dim3 g((unsigned)nq, (unsigned)((store->max_bucket_tiles + 14) / 16));
+    const int p1max = std::min(store->max_bucket_tiles, kP1Cap);
+    const dim3 g((unsigned)nq, (unsigned)((p1max + 14) / 16));
     const size_t sm = sizeof(float) * (store->d_pad + 2 * kMaxSteps);
     if (sm > 48 * 1024) {
       PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, true>,
@@ -1465,7 +1523,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
       PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
-    if (store->max_bucket_tiles > 0) {
+    if (p1max > 0) {
       const dim3 g1((unsigned)nq, 1);
       if (bsa)
         bdense_kernel<true, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
@@ -1474,7 +1532,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
       PDX_B_CHECK(cudaGetLastError());
       bt0_kernel<<<(nq + 7) / 8, 256, 0, st>>>(P, A, seg0, p1off, part1, b0bnd);
       PDX_B_CHECK(cudaGetLastError());
-      if (store->max_bucket_tiles > 1) {
+      if (p1max > 1) {
         if (bsa)
           bdense_kernel<true, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
         else
@@ -1483,11 +1541,21 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
       }
     }
     const size_t hsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t));
-    if (hsm > 48 * 1024)
-      PDX_B_CHECK(cudaFuncSetAttribute(bchain1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)hsm));
-    bchain1_kernel<<<(nq + 7) / 8, 256, hsm, st>>>(P, A, seg0, p1off, part1);
-    PDX_B_CHECK(cudaGetLastError());
+    auto chain1 = [&](auto kern) -> cudaError_t {
+      if (hsm > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<(nq + 7) / 8, 256, hsm, st>>>(P, A, seg0, p1off, part1);
+      return cudaGetLastError();
+    };
+    if (P.nsteps <= 8)
+      PDX_B_CHECK(chain1(bchain1_kernel<8>));
+    else if (P.nsteps <= 12)
+      PDX_B_CHECK(chain1(bchain1_kernel<12>));
+    else
+      PDX_B_CHECK(chain1(bchain1_kernel<kMaxSteps>));
   }
   phase("phase1");
   btprime_kernel<<<(nq + 127) / 128, 128, 0, st>>>(P, A);
