@@ -112,7 +112,8 @@ struct BArgs {
   const int64_t* block_tile;
   const int32_t* block_m;
   const float* queries;
-  const int32_t* sel;  // [nq][nseg]
+  const int32_t* sel;   // [nq][nseg]
+  const int32_t* fseg;  // [nq] first selected segment with blocks (phase 1's bucket)
   const float* resid;  // BSA [ntiles][nsteps][64]
   const float* coef;   // BSA [nsteps]
   // per query
@@ -180,23 +181,32 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
                              const int64_t* __restrict__ bucket_block,
                              const int64_t* __restrict__ block_tile, int32_t* __restrict__ seg0,
                              int64_t* __restrict__ wcount, int32_t* __restrict__ pbase,
-                             int32_t* __restrict__ bcnt, int64_t* __restrict__ w0count) {
+                             int32_t* __restrict__ bcnt, int64_t* __restrict__ w0count,
+                             int32_t* __restrict__ fseg) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const int32_t* sq = sel + (int64_t)q * nseg;
   // phase 1 takes the first min(nt0, kP1Cap) tiles of the first bucket; its
   // tail (if any) opens the speculative window, pair indices from 0
-  const int nt0 = (int)(block_tile[bucket_block[sq[0] + 1]] - block_tile[bucket_block[sq[0]]]);
+  // (the reference's block list skips empty buckets: phase 1 takes the first
+  // selected bucket that has blocks — on a bucket shard, often not segment 0)
+  int f = 0;
+  auto ntiles = [&](int c) {
+    return (int)(block_tile[bucket_block[c + 1]] - block_tile[bucket_block[c]]);
+  };
+  while (f < nseg - 1 && ntiles(sq[f]) == 0) ++f;
+  const int nt0 = ntiles(sq[f]);
   const int p1 = min(nt0, kP1Cap);
   if (lane == 0) {
-    seg0[q] = sq[0];
+    seg0[q] = sq[f];
+    fseg[q] = f;
     w0count[q] = p1;
-    pbase[(int64_t)q * nseg] = -p1;
-    if (nt0 > p1) atomicAdd(&bcnt[sq[0]], 1);
+    pbase[(int64_t)q * nseg + f] = -p1;
+    if (nt0 > p1) atomicAdd(&bcnt[sq[f]], 1);
   }
   int run = nt0 - p1;
-  for (int s0 = 1; s0 < nseg; s0 += 32) {
+  for (int s0 = f + 1; s0 < nseg; s0 += 32) {
     const int s = s0 + lane;
     int nt = 0;
     if (s < nseg) {
@@ -238,13 +248,15 @@ __global__ void bfill_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
                              const int64_t* __restrict__ bucket_block,
                              const int64_t* __restrict__ block_tile,
                              const int32_t* __restrict__ pbase, const int32_t* __restrict__ boff,
-                             int32_t* __restrict__ bcur, BEntry* __restrict__ entries) {
+                             int32_t* __restrict__ bcur, BEntry* __restrict__ entries,
+                             const int32_t* __restrict__ fseg) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)nq * nseg) return;
   const int q = (int)(i / nseg), s = (int)(i % nseg);
   const int c = sel[(int64_t)q * nseg + s];
   const int64_t ntc = block_tile[bucket_block[c + 1]] - block_tile[bucket_block[c]];
-  if (s == 0 ? ntc <= kP1Cap : ntc == 0) return;  // no tail of the first bucket / empty
+  const int f = fseg[q];
+  if (s < f || (s == f ? ntc <= kP1Cap : ntc == 0)) return;  // before / no tail of the first bucket
   const int pos = atomicAdd(&bcur[c], 1);
   entries[boff[c] + pos] = BEntry{q, pbase[(int64_t)q * nseg + s]};
 }
@@ -1238,9 +1250,10 @@ __global__ void bfinal_kernel(const BParams P, const BArgs A) {
   }
   if (A.out_total) {
     int64_t v = 0;
-    for (int s = 1 + lane; s < P.nseg; s += 32) v += A.bnvec[A.sel[(int64_t)q * P.nseg + s]];
-    const int64_t f0 = A.bucket_block[A.sel[(int64_t)q * P.nseg]];
-    const int nt0 = (int)(A.bucket_block[A.sel[(int64_t)q * P.nseg] + 1] - f0);
+    const int fs = A.fseg[q];
+    for (int s = fs + 1 + lane; s < P.nseg; s += 32) v += A.bnvec[A.sel[(int64_t)q * P.nseg + s]];
+    const int64_t f0 = A.bucket_block[A.sel[(int64_t)q * P.nseg + fs]];
+    const int nt0 = (int)(A.bucket_block[A.sel[(int64_t)q * P.nseg + fs] + 1] - f0);
     for (int ti = kP1Cap + lane; ti < nt0; ti += 32) v += A.block_m[f0 + ti];  // first-bucket tail
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     if (lane == 0) A.out_total[q] += v * P.d;
@@ -1357,6 +1370,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     unsigned char* z = nullptr;
     unsigned char* at = z;
     carve<int32_t>(at, nq);                    // seg0
+    carve<int32_t>(at, nq);                    // fseg
     carve<int64_t>(at, nq + 1);                // wcount
     carve<int64_t>(at, nq + 1);                // qoff
     carve<int64_t>(at, nq + 1);                // w0count
@@ -1390,6 +1404,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   PDX_CUDA_CHECK(cudaMallocAsync(&base, bytes, st));
   unsigned char* at = base;
   int32_t* seg0 = carve<int32_t>(at, nq);
+  int32_t* fseg = carve<int32_t>(at, nq);
   int64_t* wcount = carve<int64_t>(at, nq + 1);
   int64_t* qoff = carve<int64_t>(at, nq + 1);
   int64_t* w0count = carve<int64_t>(at, nq + 1);
@@ -1446,7 +1461,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   PDX_B_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 4, st));
   bprep_kernel<<<(nq + 7) / 8, 256, 0, st>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
                                              store->d_block_tile, seg0, wcount, pbase, bcnt,
-                                             w0count);
+                                             w0count, fseg);
   PDX_B_CHECK(cudaGetLastError());
   size_t cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st));
@@ -1462,7 +1477,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   if (nq64 * nseg > 0) {
     bfill_kernel<<<(unsigned)((nq64 * nseg + 255) / 256), 256, 0, st>>>(
         d_seg_bucket, nq, nseg, store->d_bucket_block, store->d_block_tile, pbase, boff, bcur,
-        entries);
+        entries, fseg);
     PDX_B_CHECK(cudaGetLastError());
   }
   bitems_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, boff, choff, store->d_bucket_block,
@@ -1482,6 +1497,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   A.block_m = store->d_block_m;
   A.queries = d_queries;
   A.sel = d_seg_bucket;
+  A.fseg = fseg;
   A.resid = store->d_resid;
   A.coef = prm->bsa_coef;
   A.tprime = tprime;

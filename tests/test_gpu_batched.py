@@ -100,3 +100,21 @@ def test_batched_duplicates_and_ties(P):
     for pruner in ("ads", "bond"):
         params = P.SearchParams(k=10, pruner=pruner)
         _same(_run(P, index, q, params, 8, 2), _run(P, index, q, params, 8, 1))
+
+
+def test_batched_bucket_shards_and_empty_buckets(P):
+    """Queries whose nearest selected buckets are empty (a bucket shard of a
+    multi-GPU index: the other ranks' buckets are empty here) — phase 1
+    takes the first selected bucket that has blocks."""
+    import torch
+    from paper_2503_04422_b200.sharded import shard_index
+    x = recipes.data("mixture", 60_000, 64, 11)
+    q = recipes.queries("near", x, 64, 12)
+    col = P.VectorCollection.from_array(x)
+    index = P.ivf_build(col, nlist=128, seed=0)
+    for rank in range(3):
+        sh = shard_index(index, col, rank, 3)
+        for pruner in ("ads", "bond"):
+            params = P.SearchParams(k=10, pruner=pruner)
+            _same(_run(P, sh, q, params, 24, 2), _run(P, sh, q, params, 24, 1))
+    del torch
