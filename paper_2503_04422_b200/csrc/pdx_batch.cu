@@ -1310,7 +1310,11 @@ bool batched_eligible(const pdx_store* store, const pdx_search_params* prm, int6
   if (prm->pruner == PDX_PRUNER_NONE || prm->metric != PDX_METRIC_L2) return false;
   if (prm->splits > 1 || out->d_debug || prm->k > kMaxBatchK) return false;
   if (prm->initial_step > kHeadDims || store->d_pad > 8192) return false;
-  if (prm->batched == 0 && nq < 32) return false;
+  // auto: batches of 32+ queries over d <= 256, where the 16-dim head decides
+  // most slots (C2: 2.1x the per-query scan).  For wide vectors most of the
+  // work is the survivors' long tails, which the per-query scan's dense
+  // groups handle better (C5-scaled, d = 768: 0.89x ADS, 0.67x BOND).
+  if (prm->batched == 0 && (nq < 32 || store->d > 256)) return false;
   if (nq > (1 << 24)) return false;
   const int64_t pairs = nq * (int64_t)(nseg - 1) * store->max_bucket_tiles;
   return pairs <= (int64_t)1 << 31;

@@ -23,6 +23,20 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2503_04422_b200 as P  # noqa: E402
 
+import os  # noqa: E402
+
+# pdx_search_params.batched for the IVF configs: 0 auto (the batched pipeline
+# for batches of 32+ queries), 1 the per-query scan, 2 batched whenever eligible
+BATCHED = int(os.environ.get("PDX_CFG_BATCHED", "0"))
+
+
+def same_as_per_query(ix, params, nprobe, q, r):
+    """The per-query scan on the same batch: identical ids, distances and
+    values_touched (the batched pipeline's exactness, at full size)."""
+    r1 = P.IvfSearcher(ix, params, nprobe, batched=1).run(q, stats=True)
+    return bool(torch.equal(r1.ids, r.ids) and torch.equal(r1.dist, r.dist)
+                and torch.equal(r1.touched, r.touched))
+
 
 def mixture(n, d, centres, seed, spread=1.0, centre_scale=2.0, sigma=None, normalize=False,
             device="cuda"):
@@ -72,11 +86,14 @@ def c3():
     t0 = time.perf_counter()
     ix = P.ivf_build(P.VectorCollection.from_array(x.cpu().numpy()), nlist=nlist, seed=0, x_dev=x)
     build_s = time.perf_counter() - t0
-    s = P.IvfSearcher(ix, P.SearchParams(k=k, pruner="ads", ads=P.AdsPruner(d=d)), nprobe)
+    prm = P.SearchParams(k=k, pruner="ads", ads=P.AdsPruner(d=d))
+    s = P.IvfSearcher(ix, prm, nprobe, batched=BATCHED)
     r = s.run(q, stats=True)
     pp = 1 - r.touched.sum().item() / r.total.sum().item()
     sec = timed(lambda: s.run(q))
-    out.append({"config": "C3", "pruner": "ads", "n": n, "d": d, "nlist": nlist, "nprobe": nprobe,
+    out.append({"config": "C3", "pruner": "ads", "batched": BATCHED,
+                "same_as_per_query": same_as_per_query(ix, prm, nprobe, q, r),
+                "n": n, "d": d, "nlist": nlist, "nprobe": nprobe,
                 "queries": nq, "k": k, "qps": nq / sec, "scan_batch_s": sec,
                 "recall_at_10": recall(gt, r.ids.cpu().numpy(), k), "pruning_power": pp,
                 "algorithmic_GBps": 4 * r.touched.sum().item() / sec / 1e9,
@@ -88,19 +105,23 @@ def c3():
     qp = P.apply_transform(T, q)
     ix = P.ivf_build(P.VectorCollection.from_array(xp.cpu().numpy()), nlist=nlist, seed=0, x_dev=xp)
     bsa = P.fit_bsa(xp)
-    s = P.IvfSearcher(ix, P.SearchParams(k=k, pruner="bsa", bsa=bsa), nprobe)
+    prm = P.SearchParams(k=k, pruner="bsa", bsa=bsa)
+    s = P.IvfSearcher(ix, prm, nprobe, batched=BATCHED)
     r = s.run(qp, stats=True)
     pp = 1 - r.touched.sum().item() / r.total.sum().item()
     sec = timed(lambda: s.run(qp))
-    out.append({"config": "C3", "pruner": "bsa", "n": n, "d": d, "nlist": nlist,
+    out.append({"config": "C3", "pruner": "bsa", "batched": BATCHED,
+                "same_as_per_query": same_as_per_query(ix, prm, nprobe, qp, r),
+                "n": n, "d": d, "nlist": nlist,
                 "nprobe": nprobe, "queries": nq, "k": k, "qps": nq / sec, "scan_batch_s": sec,
                 "recall_at_10": recall(gt, r.ids.cpu().numpy(), k), "pruning_power": pp,
                 "algorithmic_GBps": 4 * r.touched.sum().item() / sec / 1e9,
                 "bsa_cosine_quantiles": [round(c, 4) for c in bsa.cosines]})
-    s = P.IvfSearcher(ix, P.SearchParams(k=k, pruner="bond"), nprobe)
+    s = P.IvfSearcher(ix, P.SearchParams(k=k, pruner="bond"), nprobe, batched=BATCHED)
     r = s.run(qp, stats=True)
     sec = timed(lambda: s.run(qp))
-    out.append({"config": "C3", "pruner": "bond (same PCA index)", "qps": nq / sec,
+    out.append({"config": "C3", "pruner": "bond (same PCA index)", "batched": BATCHED,
+                "qps": nq / sec,
                 "recall_at_10": recall(gt, r.ids.cpu().numpy(), k),
                 "pruning_power": 1 - r.touched.sum().item() / r.total.sum().item()})
     return out
@@ -186,10 +207,13 @@ def c5(n=10_000_000, d=768, nlist=8192, nprobe=128, nq=10_000, k=10):
     gt = gt.cpu().numpy()
     out = []
     for pruner in ("ads", "bond"):
-        s = P.IvfSearcher(ix, P.SearchParams(k=k, pruner=pruner, ads=P.AdsPruner(d=d)), nprobe)
+        prm = P.SearchParams(k=k, pruner=pruner, ads=P.AdsPruner(d=d))
+        s = P.IvfSearcher(ix, prm, nprobe, batched=BATCHED)
         r = s.run(q, stats=True)
         sec = timed(lambda: s.run(q), reps=3, warm=1)
-        out.append({"config": "C5-scaled (1 GPU)", "n": n, "d": d, "nlist": nlist,
+        out.append({"config": "C5-scaled (1 GPU)", "batched": BATCHED,
+                    "same_as_per_query": same_as_per_query(ix, prm, nprobe, q, r),
+                    "n": n, "d": d, "nlist": nlist,
                     "nprobe": nprobe, "queries": nq, "k": k, "pruner": pruner,
                     "qps": nq / sec, "batch_s": sec,
                     "recall_at_10": recall(gt, r.ids.cpu().numpy(), k),
