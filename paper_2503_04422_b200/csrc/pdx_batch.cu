@@ -47,11 +47,16 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "pdx_batch.cuh"
 #include "pdx_common.cuh"
 #include "pdx_scan_kernel.cuh"
+
+#ifndef PDX_BSCAN_MIN_BLOCKS
+#define PDX_BSCAN_MIN_BLOCKS 3  // work-item CTAs per SM (80 registers)
+#endif
 
 namespace pdx {
 namespace {
@@ -750,7 +755,7 @@ __device__ __forceinline__ void confirm_survivor(const BParams& P, const BArgs& 
 // MODE 0: every pair under B_s(T').  MODE 1: only the uncertain pairs, under
 // B_s(T^_p) — their stats are overwritten and their real survivors confirmed.
 template <int IS, bool BSA, int MODE>
-__global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, const BArgs A) {
+__global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(const BParams P, const BArgs A) {
   __shared__ __align__(16) float s_qh[kQC][kHeadDims];
   __shared__ __align__(16) float s_bnd[kQC][kMaxSteps];
   __shared__ float s_bq[BSA ? kQC : 1][2][kMaxHead];  // BSA head: rq_s, sqrt(rq_s)
@@ -986,9 +991,11 @@ __global__ void __launch_bounds__(kBW * 32, 3) bscan_kernel(const BParams P, con
       qn = 0;
     };
 
+    for (int i = lane; i < ne * (nsteps - hs); i += 32)  // deep-step counters of this tile
+      s_dcnt[w][i / (nsteps - hs)][hs + i % (nsteps - hs)] = 0u;
+    __syncwarp();
     for (uint32_t tm = todo; tm; tm &= tm - 1) {
       const int j = __ffs(tm) - 1;
-      if (lane >= hs && lane < nsteps) s_dcnt[w][j][lane] = 0u;
       float bnd[kMaxHead];
       float that = 0.f;
       if (MODE == 0) {
@@ -1292,6 +1299,28 @@ int host_warm_min(int m, double sf) {  // warm_min_count (pdx_scan_kernel.cuh)
   return p;
 }
 
+// A per-device side stream and fork/join events for the planning kernels.
+// Calls on different streams may share it: each call records its own fork
+// before and its own join after its kernels, so stream order stays correct.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static std::mutex mu;
+  static SideStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& ss = per_dev[dev & 63];
+  if (!ss.s) {
+    cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+  }
+  return ss;
+}
+
 template <typename T>
 T* carve(unsigned char*& at, int64_t count) {
   T* p = reinterpret_cast<T*>(at);
@@ -1468,25 +1497,33 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
                                              w0count, fseg);
   PDX_B_CHECK(cudaGetLastError());
   size_t cb = cubb;
-  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st));
-  cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, w0count, p1off, nq + 1, st));
+  // The work lists (below) and phase 1 (after them) only share bprep's
+  // outputs: build the lists on a side stream while phase 1 runs; the main
+  // stream joins before phase 2.
+  SideStream& side = side_stream();
+  cudaStream_t st2 = side.s;
+  PDX_B_CHECK(cudaEventRecord(side.fork, st));
+  PDX_B_CHECK(cudaStreamWaitEvent(st2, side.fork, 0));
   cb = cubb;
-  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, bcnt, boff, nb + 1, st));
-  bchunks_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, store->d_bucket_block,
-                                                   store->d_block_m, nch, bnvec);
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st2));
+  cb = cubb;
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, bcnt, boff, nb + 1, st2));
+  bchunks_kernel<<<(nb + 256) / 256, 256, 0, st2>>>(bcnt, nb, store->d_bucket_block,
+                                                    store->d_block_m, nch, bnvec);
   PDX_B_CHECK(cudaGetLastError());
   cb = cubb;
-  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, nch, choff, nb + 1, st));
+  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, nch, choff, nb + 1, st2));
   if (nq64 * nseg > 0) {
-    bfill_kernel<<<(unsigned)((nq64 * nseg + 255) / 256), 256, 0, st>>>(
+    bfill_kernel<<<(unsigned)((nq64 * nseg + 255) / 256), 256, 0, st2>>>(
         d_seg_bucket, nq, nseg, store->d_bucket_block, store->d_block_tile, pbase, boff, bcur,
         entries, fseg);
     PDX_B_CHECK(cudaGetLastError());
   }
-  bitems_kernel<<<(nb + 256) / 256, 256, 0, st>>>(bcnt, nb, boff, choff, store->d_bucket_block,
-                                                  items, ctr);
+  bitems_kernel<<<(nb + 256) / 256, 256, 0, st2>>>(bcnt, nb, boff, choff, store->d_bucket_block,
+                                                   items, ctr);
   PDX_B_CHECK(cudaGetLastError());
+  PDX_B_CHECK(cudaEventRecord(side.join, st2));
   phase("plan");
 
   pdx_search_out o1 = *out;
@@ -1578,6 +1615,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
       PDX_B_CHECK(chain1(bchain1_kernel<kMaxSteps>));
   }
   phase("phase1");
+  PDX_B_CHECK(cudaStreamWaitEvent(st, side.join, 0));  // the work lists are ready
   btprime_kernel<<<(nq + 127) / 128, 128, 0, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("tprime");
