@@ -16,7 +16,21 @@
 
 namespace pdx {
 
-constexpr int kQT = 64, kCT = 64, kDC = 16;
+constexpr int kQT = 32, kCT = 64, kDC = 16;  // 2 x 4 outputs per thread (4 = two f32x2 pairs)
+
+// (q - c0)^2, (q - c1)^2 as one FADD2 (q broadcast) + FMUL2, each lane rounded
+// on its own; the accumulation stays scalar (an f32x2 add after an f32x2
+// multiply is contracted into FFMA2 by ptxas).
+__device__ __forceinline__ float2 sqdiff_pair(float q, float c0, float c1) {
+  unsigned long long cc, qq, t, p;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c0), "f"(c1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(qq), "l"(cc));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(p) : "l"(t));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
 
 template <int METRIC>
 __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restrict__ Q, int64_t nq,
@@ -24,12 +38,13 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
                                                             int d, float* __restrict__ out) {
   __shared__ float qs[kDC][kQT + 4];
   __shared__ float cs[kDC][kCT + 4];
+  constexpr int RI = kQT / 16;  // query rows per thread
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t q0 = (int64_t)blockIdx.y * kQT;
   const int c0 = blockIdx.x * kCT;
-  float acc[4][4];
+  float acc[RI][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < RI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   for (int j0 = 0; j0 < d; j0 += kDC) {
@@ -40,27 +55,44 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
       const int64_t qr = q0 + r;
       const int dj = j0 + c;
       qs[c][r] = (qr < nq && dj < d) ? Q[qr * d + dj] : 0.f;
+    }
+#pragma unroll
+    for (int it = 0; it < (kCT * kDC) / 256; ++it) {
+      const int e = threadIdx.x + 256 * it;
+      const int r = e / kDC, c = e % kDC;
+      const int dj = j0 + c;
       const int cr = c0 + r;
       cs[c][r] = (cr < nlist && dj < d) ? Cm[(int64_t)cr * d + dj] : 0.f;
     }
     __syncthreads();
     const int jn = min(kDC, d - j0);
     for (int jj = 0; jj < jn; ++jj) {
-      float qv[4], cv[4];
+      float qv[RI], cv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) qv[i] = qs[jj][ty * 4 + i];
+      for (int i = 0; i < RI; ++i) qv[i] = qs[jj][ty * RI + i];
 #pragma unroll
       for (int j = 0; j < 4; ++j) cv[j] = cs[jj][tx * 4 + j];
+      if (METRIC == PDX_METRIC_L2) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = upd<METRIC>(acc[i][j], qv[i], cv[j]);
+          for (int j = 0; j < 4; j += 2) {
+            const float2 p = sqdiff_pair(qv[i], cv[j], cv[j + 1]);
+            acc[i][j] = __fadd_rn(acc[i][j], p.x);
+            acc[i][j + 1] = __fadd_rn(acc[i][j + 1], p.y);
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = upd<METRIC>(acc[i][j], qv[i], cv[j]);
+      }
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t qr = q0 + ty * 4 + i;
+  for (int i = 0; i < RI; ++i) {
+    const int64_t qr = q0 + ty * RI + i;
     if (qr >= nq) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
