@@ -1146,18 +1146,18 @@ __global__ void bchain_kernel(const BParams P, const BArgs A) {
   BSurv* ls = reinterpret_cast<BSurv*>(s_top + (size_t)nw * k + 4) + (size_t)wq * P.surv_cap;
   BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
   for (int i = lane; i < k; i += 32) top[i] = A.out_dist[(int64_t)q * k + i];
-  for (int i = lane; i < n; i += 32) ls[i] = sv[i];
+  // rank sort by (pair, list position), lane-parallel: O(n^2 / 32)
+  for (int i = lane; i < n; i += 32) {
+    const int pi = sv[i].pair;
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const int pj = sv[j].pair;
+      r += pj < pi || (pj == pi && j < i);
+    }
+    ls[r] = sv[i];
+  }
   __syncwarp();
   if (lane == 0) {
-    for (int i = 1; i < n; ++i) {  // insertion sort by pair (n is small: ~1-2 at C2)
-      const BSurv x = ls[i];
-      int j = i;
-      while (j > 0 && ls[j - 1].pair > x.pair) {
-        ls[j] = ls[j - 1];
-        --j;
-      }
-      ls[j] = x;
-    }
     for (int i = 0; i < n;) {
       int e = i;
       for (; e < n && ls[e].pair == ls[i].pair; ++e) {
@@ -1184,14 +1184,19 @@ __global__ void bchain_kernel(const BParams P, const BArgs A) {
 // recompute pass did not confirm are dropped (or, below T^, flag the query);
 // top-k of H and the real survivors; the stats.
 __global__ void bfinal_kernel(const BParams P, const BArgs A) {
-  extern __shared__ unsigned char s_raw[];
+  extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const int q = blockIdx.x * (blockDim.x >> 5) + wq;
   if (q >= P.nq || A.flags[q]) return;
   const int k = P.k;
+  const int nwb = blockDim.x >> 5;  // smem: td | ti | tsi | ts, each 16-byte aligned
+  const size_t o_ti = ((size_t)nwb * k * 4 + 15) & ~(size_t)15;
+  const size_t o_tsi = o_ti + (size_t)nwb * k * 8;
+  const size_t o_ts = o_tsi + (size_t)nwb * P.surv_cap * 8;
   float* td = reinterpret_cast<float*>(s_raw) + (size_t)wq * k;
-  int64_t* ti = reinterpret_cast<int64_t*>(s_raw + (size_t)(blockDim.x >> 5) * k * 4 + 8) +
-                (size_t)wq * k;
+  int64_t* ti = reinterpret_cast<int64_t*>(s_raw + o_ti) + (size_t)wq * k;
+  int64_t* tsi = reinterpret_cast<int64_t*>(s_raw + o_tsi) + (size_t)wq * P.surv_cap;
+  float* ts = reinterpret_cast<float*>(s_raw + o_ts) + (size_t)wq * P.surv_cap;
   const int n = min(A.nsurv[q], P.surv_cap);
   BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
   float* od = A.out_dist + (int64_t)q * k;
@@ -1213,30 +1218,33 @@ __global__ void bfinal_kernel(const BParams P, const BArgs A) {
   }
   __syncwarp();
   if (n > 0) {
+    // real survivors ascending by (dist, id): lane-parallel rank sort (ids are
+    // distinct), into the first nr entries of this warp's smem buffers
+    int nr = 0;
+    for (int i = lane; i < n; i += 32) {
+      if (sv[i].real < 0) continue;
+      const float di = sv[i].dist;
+      const int64_t ii = sv[i].id;
+      int r = 0;
+      for (int j = 0; j < n; ++j)
+        r += sv[j].real >= 0 && pair_less(sv[j].dist, sv[j].id, di, ii);
+      ts[r] = di;
+      tsi[r] = ii;
+    }
+    for (int i = lane; i < n; i += 32) nr += sv[i].real >= 0;
+    nr = __reduce_add_sync(kFull, nr);
+    __syncwarp();
     if (lane == 0) {
-      // real survivors ascending by (dist, id), then a merge with H (sorted)
-      int nr = 0;
-      for (int i = 0; i < n; ++i)
-        if (sv[i].real >= 0) sv[nr++] = sv[i];
-      for (int i = 1; i < nr; ++i) {
-        const BSurv x = sv[i];
-        int j = i;
-        while (j > 0 && pair_less(x.dist, x.id, sv[j - 1].dist, sv[j - 1].id)) {
-          sv[j] = sv[j - 1];
-          --j;
-        }
-        sv[j] = x;
-      }
       int a = 0, b = 0;
       for (int r = 0; r < k; ++r) {
-        const bool takeh = b >= nr || (a < k && pair_less(od[a], oi[a], sv[b].dist, sv[b].id));
+        const bool takeh = b >= nr || (a < k && pair_less(od[a], oi[a], ts[b], tsi[b]));
         if (takeh) {
           td[r] = od[a];
           ti[r] = oi[a];
           ++a;
         } else {
-          td[r] = sv[b].dist;
-          ti[r] = sv[b].id;
+          td[r] = ts[b];
+          ti[r] = tsi[b];
           ++b;
         }
       }
@@ -1656,11 +1664,14 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   phase("chain");
   if (nitems_max > 0) PDX_B_CHECK(scan(1));
   phase("recompute");
-  const size_t fsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t)) + 16;
+  const size_t fper = (size_t)k * (sizeof(float) + sizeof(int64_t)) +
+                      (size_t)P.surv_cap * (sizeof(float) + sizeof(int64_t));
+  const int fw = (int)std::max<size_t>(1, std::min<size_t>(8, (160u << 10) / fper));
+  const size_t fsm = fw * fper + 32;
   if (fsm > 48 * 1024)
     PDX_B_CHECK(cudaFuncSetAttribute(bfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)fsm));
-  bfinal_kernel<<<(nq + 7) / 8, 256, fsm, st>>>(P, A);
+  bfinal_kernel<<<(nq + fw - 1) / fw, fw * 32, fsm, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("final");
   // ---- fallback: flagged queries through the per-query scan
