@@ -785,30 +785,6 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
   const int nt = tend - tbeg;
   const int64_t b0 = bk0 + tbeg;  // block (= tile, 64-blocks) of local tile 0
   const int64_t t0 = A.block_tile[b0];
-  for (int i = threadIdx.x; i < ne * kHeadDims; i += blockDim.x) {
-    const int j = i / kHeadDims, e = i % kHeadDims;
-    const int q = A.entries[it.e0 + j].q;
-    s_qh[j][e] = e < P.d ? A.queries[(int64_t)q * P.d + e] : 0.f;
-  }
-  if (MODE == 0)
-    for (int i = threadIdx.x; i < ne * nsteps; i += blockDim.x) {
-      const int j = i / nsteps, s = i % nsteps;
-      s_bnd[j][s] = A.bounds[(int64_t)A.entries[it.e0 + j].q * nsteps + s];
-    }
-  if (BSA)
-    for (int i = threadIdx.x; i < ne * P.hsteps; i += blockDim.x) {
-      const int j = i / P.hsteps, s = i % P.hsteps;
-      const float* bq = A.bsaq + (int64_t)A.entries[it.e0 + j].q * 2 * nsteps;
-      s_bq[j][0][s] = bq[s];
-      s_bq[j][1][s] = bq[nsteps + s];
-    }
-  for (int j = threadIdx.x; j < ne; j += blockDim.x) {
-    const BEntry en = A.entries[it.e0 + j];
-    s_qid[j] = en.q;
-    s_base[j] = en.base + tbeg;  // pair index of local tile 0
-    s_qo[j] = A.qoff[en.q];
-    s_tp[j] = A.tprime[en.q];
-  }
   if (MODE == 1) {
     if (threadIdx.x < 32) {
       const int j = threadIdx.x;
@@ -834,6 +810,30 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
     }
     __syncthreads();
     if (s_jmay == 0) return;  // every pair of this item is certain
+  }
+  for (int i = threadIdx.x; i < ne * kHeadDims; i += blockDim.x) {
+    const int j = i / kHeadDims, e = i % kHeadDims;
+    const int q = A.entries[it.e0 + j].q;
+    s_qh[j][e] = e < P.d ? A.queries[(int64_t)q * P.d + e] : 0.f;
+  }
+  if (MODE == 0)
+    for (int i = threadIdx.x; i < ne * nsteps; i += blockDim.x) {
+      const int j = i / nsteps, s = i % nsteps;
+      s_bnd[j][s] = A.bounds[(int64_t)A.entries[it.e0 + j].q * nsteps + s];
+    }
+  if (BSA)
+    for (int i = threadIdx.x; i < ne * P.hsteps; i += blockDim.x) {
+      const int j = i / P.hsteps, s = i % P.hsteps;
+      const float* bq = A.bsaq + (int64_t)A.entries[it.e0 + j].q * 2 * nsteps;
+      s_bq[j][0][s] = bq[s];
+      s_bq[j][1][s] = bq[nsteps + s];
+    }
+  for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+    const BEntry en = A.entries[it.e0 + j];
+    s_qid[j] = en.q;
+    s_base[j] = en.base + tbeg;  // pair index of local tile 0
+    s_qo[j] = A.qoff[en.q];
+    s_tp[j] = A.tprime[en.q];
   }
   for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
     s_ends[i] = P.ends[i];
