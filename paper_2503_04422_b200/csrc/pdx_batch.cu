@@ -582,12 +582,18 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
         ok1 |= (u1[s] < B ? 1u : 0u) << s;
       }
       const int d0 = c0 ? __ffs(~ok0) - 1 : 0, d1 = c1 ? __ffs(~ok1) - 1 : 0;
+      // survivors after step s = #slots with d > s: byte s of a unary code
+      // (one byte per step, <= 64 per byte), summed over the warp per 4 steps
       int mycnt = 0;
 #pragma unroll
-      for (int s = 0; s < NSM; ++s) {
-        if (s >= nsteps) break;
-        const int cn = __popc(__ballot_sync(kFull, d0 > s)) + __popc(__ballot_sync(kFull, d1 > s));
-        if (lane == s) mycnt = cn;
+      for (int g = 0; g < (NSM + 3) / 4; ++g) {
+        if (4 * g >= nsteps) break;
+        auto unary = [&](int dd) -> unsigned {
+          const int u = min(max(dd - 4 * g, 0), 4);
+          return u == 4 ? 0x01010101u : ((1u << (8 * u)) - 1u) & 0x01010101u;
+        };
+        const unsigned w = __reduce_add_sync(kFull, unary(d0) + unary(d1));
+        if ((lane >> 2) == g) mycnt = (int)((w >> (8 * (lane & 3))) & 0xffu);
       }
       c0 = d0 >= nsteps;
       c1 = d1 >= nsteps;
