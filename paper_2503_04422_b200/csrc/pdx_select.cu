@@ -11,6 +11,8 @@
 // (or -dist for IP) — numpy's stable argsort followed by [:nprobe].
 #include <cub/block/block_radix_sort.cuh>
 
+#include <algorithm>
+
 #include "pdx_common.cuh"
 #include "pdx_sort.cuh"
 
@@ -104,6 +106,86 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
 
 constexpr int kSelChunk = 2048;
 
+// nprobe <= 32, nlist <= 1024: one warp per query.  Keys are (order-preserving
+// key << 32 | bucket), so ties go to the lower bucket (numpy's stable
+// argsort).  The nprobe-th smallest of the 32 lane minima bounds the answer
+// from above (those minima are nprobe real keys); the keys at or below it
+// (~3 nprobe for typical data) are sorted by a warp bitonic sort in shared
+// memory.  A query with more than kWarpSelCap candidates is flagged for the
+// block radix sort below.
+constexpr int kWarpSelCap = 256;
+
+__global__ void __launch_bounds__(256) select_warp_kernel(const float* __restrict__ dists,
+                                                          int64_t nq, int nlist, int nprobe,
+                                                          int negate,
+                                                          int32_t* __restrict__ sel,
+                                                          int32_t* __restrict__ retry) {
+  __shared__ uint64_t s_c[8][kWarpSelCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * 8 + w;
+  if (q >= nq) return;
+  uint64_t* c = s_c[w];
+  const float* row = dists + q * nlist;
+  constexpr int PER = 1024 / 32;
+  uint64_t key[PER];
+  uint64_t mn = ~0ull;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = j * 32 + lane;
+    key[j] = ~0ull;
+    if (i < nlist) {
+      const float f = row[i];
+      key[j] = ((uint64_t)float_key(negate ? -f : f) << 32) | (uint32_t)i;
+    }
+    mn = key[j] < mn ? key[j] : mn;
+  }
+  // bitonic sort of the 32 lane minima (ascending across lanes)
+  uint64_t v = mn;
+  for (int size = 2; size <= 32; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, v, stride);
+      const bool lower = (lane & stride) == 0, asc = (lane & size) == 0;
+      v = (lower == asc) ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  const uint64_t U = __shfl_sync(0xffffffffu, v, nprobe - 1);
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) cnt += key[j] <= U;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total > kWarpSelCap) {
+    if (lane == 0) retry[q] = 1;
+    return;
+  }
+  if (lane == 0) retry[q] = 0;
+  int at = incl - cnt;
+#pragma unroll
+  for (int j = 0; j < PER; ++j)
+    if (key[j] <= U) c[at++] = key[j];
+  int n2 = 32;
+  while (n2 < total) n2 <<= 1;
+  for (int i = total + lane; i < n2; i += 32) c[i] = ~0ull;
+  __syncwarp();
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < n2 / 2; t += 32) {
+        const int i = (t / stride) * stride * 2 + (t % stride), jn = i + stride;
+        const bool asc = (i & size) == 0;
+        const uint64_t a = c[i], b = c[jn];
+        if ((a > b) == asc) {
+          c[i] = b;
+          c[jn] = a;
+        }
+      }
+      __syncwarp();
+    }
+  if (lane < nprobe) sel[q * nprobe + lane] = (int32_t)(uint32_t)c[lane];
+}
+
 __global__ void __launch_bounds__(512) select_kernel(const float* __restrict__ dists, int nlist,
                                                      int nprobe, int negate,
                                                      int32_t* __restrict__ sel) {
@@ -128,10 +210,16 @@ __global__ void __launch_bounds__(512) select_kernel(const float* __restrict__ d
 template <int IPT>
 __global__ void __launch_bounds__(256) select_radix_kernel(const float* __restrict__ dists,
                                                            int nlist, int nprobe, int negate,
-                                                           int32_t* __restrict__ sel) {
+                                                           int32_t* __restrict__ sel,
+                                                           const int32_t* __restrict__ only,
+                                                           int64_t nq) {
   using Sort = cub::BlockRadixSort<uint32_t, 256, IPT, int32_t>;
   __shared__ typename Sort::TempStorage tmp;
-  const float* row = dists + (int64_t)blockIdx.x * nlist;
+  // one query per CTA, or (with `only`) a grid-stride loop over the flagged ones
+  for (int64_t qb = blockIdx.x; qb < nq; qb += gridDim.x) {
+  if (only && !only[qb]) continue;
+  __syncthreads();  // tmp is reused across iterations
+  const float* row = dists + qb * nlist;
   uint32_t key[IPT];
   int32_t val[IPT];
 #pragma unroll
@@ -145,7 +233,8 @@ __global__ void __launch_bounds__(256) select_radix_kernel(const float* __restri
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
     const int r = threadIdx.x * IPT + j;
-    if (r < nprobe) sel[(int64_t)blockIdx.x * nprobe + r] = val[j];
+    if (r < nprobe) sel[qb * nprobe + r] = val[j];
+  }
   }
 }
 
@@ -177,13 +266,29 @@ extern "C" int pdx_select_buckets(const float* d_queries, int64_t nq, int32_t d,
   }
   PDX_LAUNCH_CHECK();
   const int neg = metric == PDX_METRIC_IP;
+  if (nlist <= 1024 && nprobe <= 32) {
+    int32_t* retry = nullptr;  // queries with too many candidates: block radix sort
+    PDX_CUDA_CHECK(cudaMallocAsync(&retry, sizeof(int32_t) * nq, st));
+    select_warp_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(d_scratch, nq, nlist, nprobe,
+                                                                 neg, d_sel, retry);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    select_radix_kernel<4><<<(unsigned)std::min<int64_t>(nq, nsm), 256, 0, st>>>(
+        d_scratch, nlist, nprobe, neg, d_sel, retry, nq);
+    cudaFreeAsync(retry, st);
+    PDX_LAUNCH_CHECK();
+    return PDX_OK;
+  }
   if (nlist <= 256 * 4) {
-    select_radix_kernel<4><<<(unsigned)nq, 256, 0, st>>>(d_scratch, nlist, nprobe, neg, d_sel);
+    select_radix_kernel<4><<<(unsigned)nq, 256, 0, st>>>(d_scratch, nlist, nprobe, neg, d_sel,
+                                                         nullptr, nq);
     PDX_LAUNCH_CHECK();
     return PDX_OK;
   }
   if (nlist <= 256 * 8) {
-    select_radix_kernel<8><<<(unsigned)nq, 256, 0, st>>>(d_scratch, nlist, nprobe, neg, d_sel);
+    select_radix_kernel<8><<<(unsigned)nq, 256, 0, st>>>(d_scratch, nlist, nprobe, neg, d_sel,
+                                                         nullptr, nq);
     PDX_LAUNCH_CHECK();
     return PDX_OK;
   }

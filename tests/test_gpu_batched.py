@@ -118,3 +118,26 @@ def test_batched_bucket_shards_and_empty_buckets(P):
             params = P.SearchParams(k=10, pruner=pruner)
             _same(_run(P, sh, q, params, 24, 2), _run(P, sh, q, params, 24, 1))
     del torch
+
+
+def test_warp_bucket_selection_vs_oracle(P, oracle):
+    """K2's warp top-k path (nlist <= 1024, nprobe <= 32): the nprobe smallest
+    (distance, bucket) pairs in stable-argsort order, ties included (zero
+    queries under IP: every distance equal), a query count that is not a
+    multiple of 8, nlist below and at 1024's lane layout."""
+    from test_gpu_parity import _oracle_ivf
+    x = recipes.data("mixture", 20_000, 48, 43)
+    col = P.VectorCollection.from_array(x)
+    index = P.ivf_build(col, nlist=500, seed=0)
+    index2 = P.ivf_build(col, nlist=1000, seed=0)
+    for ix in (index, index2):
+        Q = np.concatenate([recipes.queries("near", x, 13, 44),
+                            np.zeros((2, 48), np.float32)])
+        view = _oracle_ivf(oracle, ix, x)
+        for metric in ("l2", "ip", "l1"):
+            for nprobe in (1, 7, 32):
+                got = P.index.select_buckets_device(ix, P.store.to_device(Q), nprobe, metric)
+                got = (got[0] if isinstance(got, tuple) else got).cpu().numpy()
+                for i, q in enumerate(Q):
+                    ref = oracle.select_buckets(view.cent, ix.nlist, q, metric, nprobe)
+                    np.testing.assert_array_equal(got[i], ref)
