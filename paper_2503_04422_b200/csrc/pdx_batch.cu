@@ -14,11 +14,18 @@
 // are monotone in T, and the top-k after a set of pushes does not depend on
 // their order (TopK keeps the k smallest (dist, id) pairs, search.py:44-51).
 //
-//  Phase 1  the per-query scan over each query's FIRST selected bucket only:
-//           heap H (exact), T' = its k-th distance.  Every later block has
-//           T_b <= T'.
-//  Phase 2  (bscan_kernel) every (query, tile) pair of the remaining buckets
-//           under the fixed bound B_s(T'): per-step survivor counts, the
+//  Phase 1  each query's first selected bucket that has blocks (at most its
+//           first kP1Cap tiles), exactly: bdense_kernel records every
+//           slot's partial at every step end (the linear first block dense,
+//           the rest pruned under T_0, the threshold after that block, which
+//           bounds every later T_b), then bchain1_kernel (one warp per query)
+//           replays the reference chain over those partials.  Heap H, T' =
+//           its k-th distance; every later block has T_b <= T'.  The rest of
+//           the selected blocks (the bucket's tail first) form the window.
+//  Phase 2  (bscan_kernel MODE 0) every (query, tile) pair of the window,
+//           tile-major (work items: a bucket's tile range x up to 32 of the
+//           queries probing it), under the fixed bound B_s(T'): per-step
+//           survivor counts, the
 //           pair's certainty margin rho = max over (slot, step) surviving
 //           under T' of v_s / beta_s (beta_s: the bound's factor, B_s(T) ~
 //           T beta_s), and the T'-survivors with their distances.
@@ -37,6 +44,8 @@
 //           values_touched / values_total / survivor traces summed per pair.
 //  Fallback flagged queries (and any whose phase-1 heap is not full, or
 //           whose buffers overflowed) are re-run by the per-query scan.
+//  The work-list kernels (bucket histogram, scans, entries, items) run on a
+//  side stream while phase 1 runs.
 //
 // Certain pairs: for T in [T^_p, T'] a slot pruned under T' is pruned under
 // T (monotone), and a slot surviving step s under T' has v_s < B_s(T^_p) <=

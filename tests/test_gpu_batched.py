@@ -141,3 +141,16 @@ def test_warp_bucket_selection_vs_oracle(P, oracle):
                 for i, q in enumerate(Q):
                     ref = oracle.select_buckets(view.cent, ix.nlist, q, metric, nprobe)
                     np.testing.assert_array_equal(got[i], ref)
+
+
+def test_batched_stats_without_traces(P, rotated):
+    """The bench's mode: values_touched / values_total with no survivor
+    traces (the pipeline then keeps no per-step counts) equal the per-query
+    scan's, for ADS and BOND at several nprobe."""
+    _, qr, index = rotated
+    for pruner, nprobe in (("ads", 32), ("ads", 8), ("bond", 16)):
+        params = P.SearchParams(k=10, pruner=pruner)
+        a = P.ivf_search_batch(index, qr, params, nprobe, stats=True, batched=2)
+        b = P.ivf_search_batch(index, qr, params, nprobe, stats=True, batched=1)
+        for key in ("ids", "dist", "count", "touched", "total"):
+            np.testing.assert_array_equal(a[key], b[key])
