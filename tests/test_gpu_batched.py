@@ -154,3 +154,30 @@ def test_batched_stats_without_traces(P, rotated):
         b = P.ivf_search_batch(index, qr, params, nprobe, stats=True, batched=1)
         for key in ("ids", "dist", "count", "touched", "total"):
             np.testing.assert_array_equal(a[key], b[key])
+
+
+@pytest.mark.parametrize("d", [300, 392])
+def test_batched_dense_continuation_wide(P, oracle, d):
+    """d > 256: the dense-continuation variant (every live query of a tile
+    advances group by group together, then one lane per survivor) — results,
+    decisions, values_touched and traces equal the per-query scan's and the
+    oracle's, for ADS, BOND and BSA."""
+    import torch
+    x = recipes.data("mixture", 30_000, d, 51)
+    q = recipes.queries("near", x, 40, 52)
+    T = P.generate_orthogonal(d, 3)
+    xr, qr = P.apply_transform(T, x), P.apply_transform(T, q)
+    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=48, seed=0)
+    for params in (P.SearchParams(k=10, pruner="ads"), P.SearchParams(k=10, pruner="bond"),
+                   P.SearchParams(k=5, pruner="ads", ads=P.AdsPruner(d=d, epsilon0=0.8))):
+        a = _run(P, index, qr, params, 12, 2)
+        _same(a, _run(P, index, qr, params, 12, 1))
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, 10, 12, pruner="ads",
+                                  survivors_cap=1 << 18)
+    a = _run(P, index, qr, P.SearchParams(k=10, pruner="ads"), 12, 2)
+    np.testing.assert_array_equal(a["ids"], ref["ids"])
+    np.testing.assert_array_equal(a["touched"], ref["touched"])
+    assert a["survivors"] == ref["survivor_lists"]
+    bsa = P.fit_bsa(torch.from_numpy(xr).cuda())
+    pb = P.SearchParams(k=10, pruner="bsa", bsa=bsa)
+    _same(_run(P, index, qr, pb, 12, 2), _run(P, index, qr, pb, 12, 1))
