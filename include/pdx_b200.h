@@ -131,7 +131,7 @@ typedef struct pdx_search_params {
   /* IVF query batches (per-query bucket selection, 64-vector blocks, G = 8
    * tiles, natural dimension order, pruner ads / bond / bsa, no split):
    *   0 = auto: the bucket-major batched pipeline when the batch has at
-   *       least 32 queries and d <= 256, else the per-query scan;
+   *       least 32 queries, else the per-query scan;
    *   1 = always the per-query scan;  2 = batched whenever eligible.
    * Both give the reference's results, decisions and stats bit for bit
    * (DESIGN.md §3.2); the batched one evaluates each tile once for every

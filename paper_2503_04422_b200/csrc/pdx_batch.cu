@@ -104,7 +104,8 @@ struct BSurv {
 struct DeepItem {
   float acc;
   int16_t j, slot;
-  float that;  // recompute pass: the pair's T^
+  float that;     // recompute pass: the pair's T^
+  int16_t s, pos;  // where the item resumes: next step, next dim
 };
 
 // Per-call constants (kernel parameter; copied to shared memory where they
@@ -947,13 +948,13 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
       __syncwarp();
       for (int b = 0; b < qn; b += 32) {
         bool act = b + lane < qn;
-        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f};
+        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f, 0, 0};
         const int j = di.j, slot = di.slot;
         const int q = s_qid[j];
         const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
         const bool q4 = (P.d & 3) == 0;
         float acc = di.acc;
-        int s = hs, pos = hd;
+        int s = di.s, pos = di.pos;
         int nend = s_ends[s];
         while (act) {
           const int g = pos >> 3;
@@ -1109,9 +1110,11 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
           if (qn + n > kDeepCap) flush();
           const unsigned lt = (1u << lane) - 1u;
           const int pre = qn + __popc(m0 & lt) + __popc(m1 & lt);
-          if (al0) s_deep[w][pre] = DeepItem{acc0, (int16_t)j, (int16_t)lane, that};
+          if (al0)
+            s_deep[w][pre] = DeepItem{acc0, (int16_t)j, (int16_t)lane, that, (int16_t)hs, (int16_t)hd};
           if (al1)
-            s_deep[w][pre + (al0 ? 1 : 0)] = DeepItem{acc1, (int16_t)j, (int16_t)(lane + 32), that};
+            s_deep[w][pre + (al0 ? 1 : 0)] =
+                DeepItem{acc1, (int16_t)j, (int16_t)(lane + 32), that, (int16_t)hs, (int16_t)hd};
           qn += n;
         }
       }
@@ -1317,7 +1320,6 @@ __global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, c
     }
     const bool in0 = lane < m, in1 = lane + 32 < m;
     int qn = 0;  // deep items queued by this warp for this tile
-    int fs0 = hs, fpos0 = hd;  // where queued items resume (the continuation parks later)
     uint32_t live = 0;         // queries with live slots after the head
     int nlive = 0;             // live (query, slot) pairs
 
@@ -1326,13 +1328,13 @@ __global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, c
       __syncwarp();
       for (int b = 0; b < qn; b += 32) {
         bool act = b + lane < qn;
-        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f};
+        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f, 0, 0};
         const int j = di.j, slot = di.slot;
         const int q = s_qid[j];
         const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
         const bool q4 = (P.d & 3) == 0;
         float acc = di.acc;
-        int s = fs0, pos = fpos0;
+        int s = di.s, pos = di.pos;
         int nend = s_ends[s];
         while (act) {
           const int g = pos >> 3;
@@ -1502,7 +1504,7 @@ __global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, c
       __syncwarp();
       while (live) {
         if (nlive <= 32) {  // few left: one lane per survivor from here (flush)
-          qn = 0;
+          if (qn + nlive > kDeepCap) flush();
           for (uint32_t tm = live; tm; tm &= tm - 1) {
             const int j = __ffs(tm) - 1;
             const unsigned m0 = s_alm[w][j][0], m1 = s_alm[w][j][1];
@@ -1510,14 +1512,15 @@ __global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, c
             const unsigned lt = (1u << lane) - 1u;
             const int pre = qn + __popc(m0 & lt) + __popc(m1 & lt);
             const float th = MODE == 1 ? s_that[w][j] : 0.f;
-            if (a0) s_deep[w][pre] = DeepItem{s_accd[(w * kQC + j) * kTile + lane], (int16_t)j, (int16_t)lane, th};
+            if (a0)
+              s_deep[w][pre] = DeepItem{s_accd[(w * kQC + j) * kTile + lane], (int16_t)j,
+                                        (int16_t)lane, th, (int16_t)s, (int16_t)pos};
             if (a1)
               s_deep[w][pre + (a0 ? 1 : 0)] =
-                  DeepItem{s_accd[(w * kQC + j) * kTile + lane + 32], (int16_t)j, (int16_t)(lane + 32), th};
+                  DeepItem{s_accd[(w * kQC + j) * kTile + lane + 32], (int16_t)j,
+                           (int16_t)(lane + 32), th, (int16_t)s, (int16_t)pos};
             qn += __popc(m0) + __popc(m1);
           }
-          fs0 = s;
-          fpos0 = pos;
           flush();
           live = 0;
           break;
@@ -1550,6 +1553,19 @@ __global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, c
             for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + e) : 0.f;
           }
           float a0 = s_accd[(w * kQC + j) * kTile + lane], a1 = s_accd[(w * kQC + j) * kTile + lane + 32];
+          if (bm == 0) {  // no step ends in this group: the alive masks stay
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if (e >= e0) {
+                const float2 d2 = sqdiff2(qv[e], xx2[e]);
+                a0 = __fadd_rn(a0, d2.x);
+                a1 = __fadd_rn(a1, d2.y);
+              }
+            }
+            s_accd[(w * kQC + j) * kTile + lane] = a0;
+            s_accd[(w * kQC + j) * kTile + lane + 32] = a1;
+            continue;
+          }
           const unsigned o0 = s_alm[w][j][0], o1 = s_alm[w][j][1];
           bool l0 = (o0 >> lane) & 1u, l1 = (o1 >> lane) & 1u;
           int se = sg;
@@ -1611,6 +1627,7 @@ __global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, c
         s = sg + __popc(bm);
         pos = (g + 1) * 8;
       }
+      if (qn) flush();
     }
     // the pairs' stats: values_touched (search.py:148-169) and trace counts
     for (int j = lane; j < ne; j += 32) {
@@ -1858,11 +1875,10 @@ bool batched_eligible(const pdx_store* store, const pdx_search_params* prm, int6
   if (prm->pruner == PDX_PRUNER_NONE || prm->metric != PDX_METRIC_L2) return false;
   if (prm->splits > 1 || out->d_debug || prm->k > kMaxBatchK) return false;
   if (prm->initial_step > kHeadDims || store->d_pad > 8192) return false;
-  // auto: batches of 32+ queries over d <= 256, where the 16-dim head decides
-  // most slots (C2: 2.1x the per-query scan).  For wide vectors most of the
-  // work is the survivors' long tails, which the per-query scan's dense
-  // groups handle better (C5-scaled, d = 768: 0.89x ADS, 0.67x BOND).
-  if (prm->batched == 0 && (nq < 32 || store->d > 256)) return false;
+  // auto: batches of 32+ queries (C2 d = 128: 2.2x the per-query scan; with
+  // the dense continuation for d > 256, C3 d = 960: 1.2-1.5x, C5-scaled
+  // d = 768: BOND 1.34x, ADS 0.97x)
+  if (prm->batched == 0 && nq < 32) return false;
   if (nq > (1 << 24)) return false;
   const int64_t pairs = nq * (int64_t)(nseg - 1) * store->max_bucket_tiles;
   return pairs <= (int64_t)1 << 31;
