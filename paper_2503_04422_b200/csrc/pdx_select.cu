@@ -111,15 +111,14 @@ constexpr int kSelChunk = 2048;
 // argsort).  The nprobe-th smallest of the 32 lane minima bounds the answer
 // from above (those minima are nprobe real keys); the keys at or below it
 // (~3 nprobe for typical data) are sorted by a warp bitonic sort in shared
-// memory.  A query with more than kWarpSelCap candidates is flagged for the
-// block radix sort below.
+// memory.  A query with more than kWarpSelCap candidates takes nprobe rounds
+// of a warp-wide minimum instead.
 constexpr int kWarpSelCap = 256;
 
 __global__ void __launch_bounds__(256) select_warp_kernel(const float* __restrict__ dists,
                                                           int64_t nq, int nlist, int nprobe,
                                                           int negate,
-                                                          int32_t* __restrict__ sel,
-                                                          int32_t* __restrict__ retry) {
+                                                          int32_t* __restrict__ sel) {
   __shared__ uint64_t s_c[8][kWarpSelCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t q = (int64_t)blockIdx.x * 8 + w;
@@ -158,10 +157,24 @@ __global__ void __launch_bounds__(256) select_warp_kernel(const float* __restric
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   if (total > kWarpSelCap) {
-    if (lane == 0) retry[q] = 1;
+    // rare (skewed rows): nprobe rounds of a warp-wide minimum, each taken
+    // out of its lane's registers (the keys are distinct: bucket in the low bits)
+    for (int r = 0; r < nprobe; ++r) {
+      uint64_t lm = ~0ull;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) lm = key[j] < lm ? key[j] : lm;
+      uint64_t gm = lm;
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(0xffffffffu, gm, o);
+        gm = t < gm ? t : gm;
+      }
+#pragma unroll
+      for (int j = 0; j < PER; ++j)
+        if (key[j] == gm) key[j] = ~0ull;
+      if (lane == 0) sel[q * nprobe + r] = (int32_t)(uint32_t)gm;
+    }
     return;
   }
-  if (lane == 0) retry[q] = 0;
   int at = incl - cnt;
 #pragma unroll
   for (int j = 0; j < PER; ++j)
@@ -267,16 +280,8 @@ extern "C" int pdx_select_buckets(const float* d_queries, int64_t nq, int32_t d,
   PDX_LAUNCH_CHECK();
   const int neg = metric == PDX_METRIC_IP;
   if (nlist <= 1024 && nprobe <= 32) {
-    int32_t* retry = nullptr;  // queries with too many candidates: block radix sort
-    PDX_CUDA_CHECK(cudaMallocAsync(&retry, sizeof(int32_t) * nq, st));
     select_warp_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(d_scratch, nq, nlist, nprobe,
-                                                                 neg, d_sel, retry);
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    select_radix_kernel<4><<<(unsigned)std::min<int64_t>(nq, nsm), 256, 0, st>>>(
-        d_scratch, nlist, nprobe, neg, d_sel, retry, nq);
-    cudaFreeAsync(retry, st);
+                                                                 neg, d_sel);
     PDX_LAUNCH_CHECK();
     return PDX_OK;
   }

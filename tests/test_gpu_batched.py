@@ -181,3 +181,37 @@ def test_batched_dense_continuation_wide(P, oracle, d):
     bsa = P.fit_bsa(torch.from_numpy(xr).cuda())
     pb = P.SearchParams(k=10, pruner="bsa", bsa=bsa)
     _same(_run(P, index, qr, pb, 12, 2), _run(P, index, qr, pb, 12, 1))
+
+
+def test_warp_bucket_selection_overflow(P):
+    """Rows whose lane minima bound admits > 256 candidates (every 32nd
+    bucket far away) take the warp kernel's round-by-round minimum: same
+    stable-argsort selection as numpy on the per-op-rounded distances."""
+    import torch
+    from paper_2503_04422_b200 import _lib
+    rng = np.random.default_rng(7)
+    nlist, d = 1024, 16
+    cent = rng.standard_normal((nlist, d)).astype(np.float32)
+    cent[31::32] += 50.0
+    cent[5] = cent[9]  # a tie: the lower bucket first
+    Q = np.concatenate([np.zeros((3, d), np.float32),
+                        rng.standard_normal((6, d)).astype(np.float32)])
+    for metric, code in (("l2", 0), ("ip", 2)):
+        for nprobe in (1, 17, 32):
+            qd, cd = P.store.to_device(Q), P.store.to_device(cent)
+            scratch = torch.empty((Q.shape[0] * nlist,), dtype=torch.float32, device="cuda")
+            sel = torch.empty((Q.shape[0], nprobe), dtype=torch.int32, device="cuda")
+            _lib.check(_lib.lib().pdx_select_buckets(_lib.ptr(qd), Q.shape[0], d, _lib.ptr(cd),
+                                                     nlist, code, nprobe, _lib.ptr(scratch),
+                                                     _lib.ptr(sel), _lib.stream_handle()))
+            for i, q in enumerate(Q):
+                acc = np.zeros(nlist, np.float32)
+                for j in range(d):  # kernels.py:55-61 order and rounding
+                    if metric == "l2":
+                        t = (q[j] - cent[:, j]).astype(np.float32)
+                        acc = (acc + (t * t).astype(np.float32)).astype(np.float32)
+                    else:
+                        acc = (acc + (q[j] * cent[:, j]).astype(np.float32)).astype(np.float32)
+                key = -acc if metric == "ip" else acc
+                ref = np.argsort(key, kind="stable")[:nprobe]
+                np.testing.assert_array_equal(sel[i].cpu().numpy(), ref)
