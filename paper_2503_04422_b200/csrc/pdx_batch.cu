@@ -771,23 +771,31 @@ __device__ __forceinline__ void confirm_survivor(const BParams& P, const BArgs& 
 // Slots alive after the head become deep items, finished one per lane.
 // MODE 0: every pair under B_s(T').  MODE 1: only the uncertain pairs, under
 // B_s(T^_p) — their stats are overwritten and their real survivors confirmed.
-template <int IS, bool BSA, int MODE>
-__global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(const BParams P, const BArgs A) {
+// DENSE (d > 256): after the head, every live query of a tile advances
+// together group by group (the group loaded once per warp, per-query
+// accumulators in shared memory) until few live slots remain; otherwise
+// the head's survivors go straight to the one-lane-per-survivor queue.
+template <int IS, bool BSA, int MODE, bool DENSE>
+__global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSCAN_MIN_BLOCKS)
+    bscan_kernel(const BParams P, const BArgs A) {
+  constexpr int BW = DENSE ? kBWD : kBW;  // warps per CTA
   __shared__ __align__(16) float s_qh[kQC][kHeadDims];
   __shared__ __align__(16) float s_bnd[kQC][kMaxSteps];
   __shared__ float s_bq[BSA ? kQC : 1][2][kMaxHead];  // BSA head: rq_s, sqrt(rq_s)
   __shared__ int32_t s_qid[kQC], s_base[kQC];
   __shared__ int64_t s_qo[kQC];
   __shared__ float s_tp[kQC];
-  __shared__ uint32_t s_hcnt[kBW][kQC];             // head-step counts, one byte per step
-  __shared__ uint32_t s_dcnt[kBW][kQC][kMaxSteps];  // deep-step counts
-  __shared__ uint32_t s_rho[kBW][kQC];
-  __shared__ float s_that[kBW][kQC];                // MODE 1: T^ of this tile's pairs
+  __shared__ uint32_t s_hcnt[BW][kQC];             // head-step counts, one byte per step
+  __shared__ uint32_t s_dcnt[BW][kQC][kMaxSteps];  // deep-step counts
+  __shared__ uint32_t s_rho[BW][kQC];
+  __shared__ float s_that[BW][kQC];                // MODE 1: T^ of this tile's pairs
   __shared__ float s_that0[kQC];                     // MODE 1: T^ at the bucket's first pair
   __shared__ uint32_t s_jvar, s_jmay;                // MODE 1: T^ varies in the bucket / may be < T'
   __shared__ uint32_t s_todo[MODE == 1 ? kTodoCap : 1];  // MODE 1: uncertain queries per tile
-  __shared__ DeepItem s_deep[kBW][kDeepCap];
-  __shared__ float s_rx[BSA ? kBW : 1][kMaxHead][kTile];
+  __shared__ DeepItem s_deep[BW][kDeepCap];
+  extern __shared__ __align__(16) float s_accd[];  // DENSE: [BW][kQC][kTile] partials of live slots
+  __shared__ uint32_t s_alm[DENSE ? BW : 1][kQC][2];  // DENSE: their alive masks (slot l, l + 32)
+  __shared__ float s_rx[BSA ? BW : 1][kMaxHead][kTile];
   __shared__ int32_t s_ends[kMaxSteps], s_wmin[kTile + 1];
   __shared__ float s_invb[kMaxSteps], s_coef[kMaxSteps];
   __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
@@ -882,7 +890,7 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
   constexpr int HS = HeadSched<IS>::n, HD = HeadSched<IS>::dims;
   const int hs = IS ? HS : P.hsteps, hd = IS ? HD : P.hdims;
   const float ib0 = s_invb[0], ib1 = s_invb[1], ib2 = s_invb[2], ib3 = s_invb[3];
-  for (int ti = w; ti < nt; ti += kBW) {
+  for (int ti = w; ti < nt; ti += BW) {
     const int64_t tile = t0 + ti;
     // MODE 1: which queries of this tile are uncertain (bit j)
     uint32_t todo = __ballot_sync(kFull, lane < ne && s_base[lane] + ti >= 0);
@@ -942,6 +950,8 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
     }
     const bool in0 = lane < m, in1 = lane + 32 < m;
     int qn = 0;  // deep items queued by this warp for this tile
+    uint32_t live = 0;  // DENSE: queries with live slots after the head
+    int nlive = 0;      // DENSE: live (query, slot) pairs
 
     // finish the queued deep items, one per lane (all belong to this tile)
     auto flush = [&]() {
@@ -1103,6 +1113,16 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
           if (al0) confirm_survivor(P, A, s_qid[j], pl, lane);
           if (al1) confirm_survivor(P, A, s_qid[j], pl, lane + 32);
         }
+      } else if (DENSE) {
+        const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
+        s_accd[(w * kQC + j) * kTile + lane] = acc0;
+        s_accd[(w * kQC + j) * kTile + lane + 32] = acc1;
+        if (lane == 0) {
+          s_alm[w][j][0] = m0;
+          s_alm[w][j][1] = m1;
+        }
+        if (m0 | m1) live |= 1u << j;
+        nlive += __popc(m0) + __popc(m1);
       } else {
         const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
         const int n = __popc(m0) + __popc(m1);
@@ -1119,515 +1139,142 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS) bscan_kernel(c
         }
       }
     }
-    flush();
-    // the pairs' stats: values_touched (search.py:148-169) and trace counts
-    for (int j = lane; j < ne; j += 32) {
-      if (!((todo >> j) & 1u)) continue;
-      const int64_t p = s_qo[j] + s_base[j] + ti;
-      const uint32_t hp = s_hcnt[w][j];
-      int64_t touched = 0, prev = m;
-      bool warm = true;
-      int a = 0;
-      for (int s = 0; s < nsteps; ++s) {
-        const int w_s = s_ends[s] - a;
-        a = s_ends[s];
-        if (warm && prev >= s_wmin[m]) {
-          touched += (int64_t)m * w_s;
-        } else {
-          warm = false;
-          touched += prev * w_s;
-        }
-        prev = s < hs ? (int)((hp >> (8 * s)) & 0xffu) : (int)s_dcnt[w][j][s];
-        if (A.pcnt) A.pcnt[p * nsteps + s] = (uint8_t)prev;
-      }
-      A.ptouched[p] = (uint32_t)touched;
-      if (MODE == 0) A.prho[p] = __uint_as_float(s_rho[w][j]);
-    }
-    __syncwarp();
-  }
-}
-
-template <int IS, bool BSA, int MODE>
-__global__ void __launch_bounds__(kBWD * 32, 4) bdscan_kernel(const BParams P, const BArgs A) {
-  __shared__ __align__(16) float s_qh[kQC][kHeadDims];
-  __shared__ __align__(16) float s_bnd[kQC][kMaxSteps];
-  __shared__ float s_bq[BSA ? kQC : 1][2][kMaxHead];  // BSA head: rq_s, sqrt(rq_s)
-  __shared__ int32_t s_qid[kQC], s_base[kQC];
-  __shared__ int64_t s_qo[kQC];
-  __shared__ float s_tp[kQC];
-  __shared__ uint32_t s_hcnt[kBWD][kQC];             // head-step counts, one byte per step
-  __shared__ uint32_t s_dcnt[kBWD][kQC][kMaxSteps];  // deep-step counts
-  __shared__ uint32_t s_rho[kBWD][kQC];
-  __shared__ float s_that[kBWD][kQC];                // MODE 1: T^ of this tile's pairs
-  __shared__ float s_that0[kQC];                     // MODE 1: T^ at the bucket's first pair
-  __shared__ uint32_t s_jvar, s_jmay;                // MODE 1: T^ varies in the bucket / may be < T'
-  __shared__ uint32_t s_todo[MODE == 1 ? kTodoCap : 1];  // MODE 1: uncertain queries per tile
-  __shared__ DeepItem s_deep[kBWD][kDeepCap];
-  extern __shared__ __align__(16) float s_accd[];  // [kBWD][kQC][kTile] partials of live slots
-  __shared__ uint32_t s_alm[kBWD][kQC][2];        // and their alive masks (slot l, l + 32)
-  __shared__ float s_rx[BSA ? kBWD : 1][kMaxHead][kTile];
-  __shared__ int32_t s_ends[kMaxSteps], s_wmin[kTile + 1];
-  __shared__ float s_invb[kMaxSteps], s_coef[kMaxSteps];
-  __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
-
-  if ((int)blockIdx.x >= *A.nitems) return;
-  const BItem it = A.items[blockIdx.x];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int ne = it.ne, nsteps = P.nsteps;
-  const int64_t bk0 = A.bucket_block[it.bucket];
-  const int tbeg = it.t0;  // this item's tiles of the bucket: [tbeg, tend); ti below is local
-  const int tend = min((int)(A.bucket_block[it.bucket + 1] - bk0), tbeg + kTC);
-  const int nt = tend - tbeg;
-  const int64_t b0 = bk0 + tbeg;  // block (= tile, 64-blocks) of local tile 0
-  const int64_t t0 = A.block_tile[b0];
-  if (MODE == 1) {
-    if (threadIdx.x < 32) {
-      const int j = threadIdx.x;
-      bool may = false, var = false;
-      if (j < ne) {
-        const BEntry en = A.entries[it.e0 + j];
-        if (!A.flags[en.q]) {
-          const BSurv* sv = A.surv + (int64_t)en.q * P.surv_cap;
-          const int n = min(A.nsurv[en.q], P.surv_cap);
-          const float tp = A.tprime[en.q];
-          const float t0 = that_of(sv, n, en.base + tbeg, tp);
-          const float t1 = that_of(sv, n, en.base + tbeg + nt - 1, tp);
-          s_that0[j] = t0;
-          var = t1 != t0;
-          may = t0 < tp || t1 < tp;
-        }
-      }
-      const unsigned mm = __ballot_sync(kFull, may), vv = __ballot_sync(kFull, var);
-      if (j == 0) {
-        s_jmay = mm;
-        s_jvar = vv;
-      }
-    }
-    __syncthreads();
-    if (s_jmay == 0) return;  // every pair of this item is certain
-  }
-  for (int i = threadIdx.x; i < ne * kHeadDims; i += blockDim.x) {
-    const int j = i / kHeadDims, e = i % kHeadDims;
-    const int q = A.entries[it.e0 + j].q;
-    s_qh[j][e] = e < P.d ? A.queries[(int64_t)q * P.d + e] : 0.f;
-  }
-  if (MODE == 0)
-    for (int i = threadIdx.x; i < ne * nsteps; i += blockDim.x) {
-      const int j = i / nsteps, s = i % nsteps;
-      s_bnd[j][s] = A.bounds[(int64_t)A.entries[it.e0 + j].q * nsteps + s];
-    }
-  if (BSA)
-    for (int i = threadIdx.x; i < ne * P.hsteps; i += blockDim.x) {
-      const int j = i / P.hsteps, s = i % P.hsteps;
-      const float* bq = A.bsaq + (int64_t)A.entries[it.e0 + j].q * 2 * nsteps;
-      s_bq[j][0][s] = bq[s];
-      s_bq[j][1][s] = bq[nsteps + s];
-    }
-  for (int j = threadIdx.x; j < ne; j += blockDim.x) {
-    const BEntry en = A.entries[it.e0 + j];
-    s_qid[j] = en.q;
-    s_base[j] = en.base + tbeg;  // pair index of local tile 0
-    s_qo[j] = A.qoff[en.q];
-    s_tp[j] = A.tprime[en.q];
-  }
-  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
-    s_ends[i] = P.ends[i];
-    s_invb[i] = P.invb[i];
-    s_ratio[i] = P.ratio[i];
-    s_band[i] = P.band[i];
-    s_coef[i] = (BSA && i < nsteps) ? A.coef[i] : 0.f;
-  }
-  for (int i = threadIdx.x; i <= kTile; i += blockDim.x) s_wmin[i] = P.wmin[i];
-  __syncthreads();
-
-  if (MODE == 1 && nt <= kTodoCap) {  // which (query, tile) pairs are uncertain, all at once
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) s_todo[i] = 0u;
-    __syncthreads();
-    for (int i = threadIdx.x; i < ne * nt; i += blockDim.x) {
-      const int j = i / nt, ti = i - j * nt;
-      if (!((s_jmay >> j) & 1u)) continue;
-      const int pl = s_base[j] + ti;
-      if (pl < 0) continue;
-      float that = s_that0[j];
-      if ((s_jvar >> j) & 1u) {
-        const int q = s_qid[j];
-        that = that_of(A.surv + (int64_t)q * P.surv_cap, min(A.nsurv[q], P.surv_cap), pl, s_tp[j]);
-      }
-      if (pair_uncertain(that, s_tp[j], A.prho[s_qo[j] + pl])) atomicOr(&s_todo[ti], 1u << j);
-    }
-    __syncthreads();
-  }
-  constexpr int HS = HeadSched<IS>::n, HD = HeadSched<IS>::dims;
-  const int hs = IS ? HS : P.hsteps, hd = IS ? HD : P.hdims;
-  const float ib0 = s_invb[0], ib1 = s_invb[1], ib2 = s_invb[2], ib3 = s_invb[3];
-  for (int ti = w; ti < nt; ti += kBWD) {
-    const int64_t tile = t0 + ti;
-    // MODE 1: which queries of this tile are uncertain (bit j)
-    uint32_t todo = __ballot_sync(kFull, lane < ne && s_base[lane] + ti >= 0);
-    if (!todo) continue;  // (tiles of a first bucket that phase 1 covered)
-    if (MODE == 1 && nt <= kTodoCap) {
-      todo = s_todo[ti];
-      if (!todo) continue;
-      if ((todo >> lane) & 1u) {
-        float that = s_that0[lane];
-        if ((s_jvar >> lane) & 1u) {
-          const int q = s_qid[lane];
-          that = that_of(A.surv + (int64_t)q * P.surv_cap, min(A.nsurv[q], P.surv_cap),
-                         s_base[lane] + ti, s_tp[lane]);
-        }
-        s_that[w][lane] = that;
-      }
-      __syncwarp();
-    } else if (MODE == 1) {
-      bool unc = false;
-      if (((s_jmay >> lane) & 1u) && s_base[lane] + ti >= 0) {
-        const int q = s_qid[lane], pl = s_base[lane] + ti;
-        float that = s_that0[lane];
-        if ((s_jvar >> lane) & 1u) {
-          const BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
-          that = that_of(sv, min(A.nsurv[q], P.surv_cap), pl, s_tp[lane]);
-        }
-        unc = pair_uncertain(that, s_tp[lane], A.prho[s_qo[lane] + pl]);
-        if (unc) s_that[w][lane] = that;
-      }
-      todo = __ballot_sync(kFull, unc);
-      if (!todo) continue;
-      __syncwarp();
-    }
-    const int m = A.block_m[b0 + ti];
-    const float* __restrict__ tb = A.tiles + tile * A.tile_stride;
-    float x0[kHeadDims], x1[kHeadDims];
-    ldg8(tb + lane * 8, *reinterpret_cast<float(*)[8]>(x0));
-    ldg8(tb + (32 + lane) * 8, *reinterpret_cast<float(*)[8]>(x1));
-    if ((IS ? HD : kHeadDims) > 8 && P.d_pad > 8) {
-      ldg8(tb + (kTile + lane) * 8, *reinterpret_cast<float(*)[8]>(x0 + 8));
-      ldg8(tb + (kTile + 32 + lane) * 8, *reinterpret_cast<float(*)[8]>(x1 + 8));
-    } else {
-#pragma unroll
-      for (int e = 8; e < kHeadDims; ++e) x0[e] = x1[e] = 0.f;
-    }
-    if (BSA) {
-      for (int s = 0; s < hs; ++s) {
-        s_rx[w][s][lane] = __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + lane);
-        s_rx[w][s][lane + 32] = __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + lane + 32);
-      }
-      __syncwarp();
-    }
-    unsigned long long xx[IS > 0 ? HD : 1];
-    if (IS > 0) {
-#pragma unroll
-      for (int e = 0; e < (IS > 0 ? HD : 1); ++e) xx[e] = pack2(x0[e], x1[e]);
-    }
-    const bool in0 = lane < m, in1 = lane + 32 < m;
-    int qn = 0;  // deep items queued by this warp for this tile
-    uint32_t live = 0;         // queries with live slots after the head
-    int nlive = 0;             // live (query, slot) pairs
-
-    // finish the queued deep items, one per lane (all belong to this tile)
-    auto flush = [&]() {
-      __syncwarp();
-      for (int b = 0; b < qn; b += 32) {
-        bool act = b + lane < qn;
-        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f, 0, 0};
-        const int j = di.j, slot = di.slot;
-        const int q = s_qid[j];
-        const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
-        const bool q4 = (P.d & 3) == 0;
-        float acc = di.acc;
-        int s = di.s, pos = di.pos;
-        int nend = s_ends[s];
-        while (act) {
+    if constexpr (DENSE) {
+      // ---- dense continuation: every live query advances together, group by
+      // group (all share the schedule position), the tile's group loaded once
+      {
+        int s = hs, pos = hd;
+        const int ngr = P.d_pad >> 3;
+        __syncwarp();
+        while (live) {
+          if (nlive <= 32) {  // few left: one lane per survivor from here (flush)
+            if (qn + nlive > kDeepCap) flush();
+            for (uint32_t tm = live; tm; tm &= tm - 1) {
+              const int j = __ffs(tm) - 1;
+              const unsigned m0 = s_alm[w][j][0], m1 = s_alm[w][j][1];
+              const bool a0 = (m0 >> lane) & 1u, a1 = (m1 >> lane) & 1u;
+              const unsigned lt = (1u << lane) - 1u;
+              const int pre = qn + __popc(m0 & lt) + __popc(m1 & lt);
+              const float th = MODE == 1 ? s_that[w][j] : 0.f;
+              if (a0)
+                s_deep[w][pre] = DeepItem{s_accd[(w * kQC + j) * kTile + lane], (int16_t)j,
+                                          (int16_t)lane, th, (int16_t)s, (int16_t)pos};
+              if (a1)
+                s_deep[w][pre + (a0 ? 1 : 0)] =
+                    DeepItem{s_accd[(w * kQC + j) * kTile + lane + 32], (int16_t)j,
+                             (int16_t)(lane + 32), th, (int16_t)s, (int16_t)pos};
+              qn += __popc(m0) + __popc(m1);
+            }
+            flush();
+            live = 0;
+            break;
+          }
           const int g = pos >> 3;
-          float x[8], qv[8];
-          ldg8(tb + ((size_t)g * kTile + slot) * 8, x);
-          if (q4 && g * 8 + 8 <= P.d) {
-            const float4 a = ldg4(qg + g * 8), c = ldg4(qg + g * 8 + 4);
-            qv[0] = a.x; qv[1] = a.y; qv[2] = a.z; qv[3] = a.w;
-            qv[4] = c.x; qv[5] = c.y; qv[6] = c.z; qv[7] = c.w;
-          } else {
+          if (g >= ngr) break;
+          float xa[8], xb[8];
+          ldg8(tb + ((size_t)g * kTile + lane) * 8, xa);
+          ldg8(tb + ((size_t)g * kTile + 32 + lane) * 8, xb);
+          unsigned long long xx2[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + g * 8 + e) : 0.f;
-          }
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int dim = g * 8 + e;
-            if (act && dim >= pos) {
-              acc = l2upd(acc, qv[e], x[e]);
-              if (dim + 1 == nend) {
-                float v = acc;
-                if (BSA) {
-                  const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
-                  v = bsa_est2(acc, __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + slot),
-                               bq[s], bq[nsteps + s], s_coef[s]);
-                }
-                const float B = MODE == 0 ? s_bnd[j][s] : bound_at(P, di.that, s, s_ratio, s_band);
-                const bool ok = v < B;
-                if (ok) {
-                  atomicAdd(&s_dcnt[w][j][s], 1u);
-                  if (MODE == 0)
-                    atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
-                }
-                ++s;
-                nend = s < nsteps ? s_ends[s] : 0x7fffffff;
-                if (!ok) {
-                  act = false;
-                } else if (s == nsteps) {
-                  if (MODE == 0)
-                    record_survivor(P, A, q, s_base[j] + ti, acc, tile, slot);
-                  else
-                    confirm_survivor(P, A, q, s_base[j] + ti, slot);
-                  act = false;
-                }
-              }
-            }
-          }
-          pos = (g + 1) * 8;
-        }
-      }
-      __syncwarp();
-      qn = 0;
-    };
-
-    for (int i = lane; i < ne * (nsteps - hs); i += 32)  // deep-step counters of this tile
-      s_dcnt[w][i / (nsteps - hs)][hs + i % (nsteps - hs)] = 0u;
-    __syncwarp();
-    for (uint32_t tm = todo; tm; tm &= tm - 1) {
-      const int j = __ffs(tm) - 1;
-      float bnd[kMaxHead];
-      float that = 0.f;
-      if (MODE == 0) {
-        const float4 b4 = *reinterpret_cast<const float4*>(s_bnd[j]);
-        bnd[0] = b4.x; bnd[1] = b4.y; bnd[2] = b4.z; bnd[3] = b4.w;
-        bnd[4] = IS > 0 ? 0.f : s_bnd[j][4];
-      } else {
-        that = s_that[w][j];
-        const float bl = lane < nsteps ? bound_at(P, that, lane, s_ratio, s_band) : 0.f;
-#pragma unroll
-        for (int s = 0; s < kMaxHead; ++s) bnd[s] = __shfl_sync(kFull, bl, s);
-      }
-      float acc0 = 0.f, acc1 = 0.f, rho = 0.f;
-      float mx[kMaxHead] = {0.f, 0.f, 0.f, 0.f, 0.f};  // per head step: max surviving partial
-      bool al0 = in0, al1 = in1;
-      uint32_t cntl = 0;  // this lane's survivors per head step, one byte per step
-      auto step = [&](int s, float ib) {
-        float v0 = acc0, v1 = acc1;
-        if (BSA) {
-          v0 = bsa_est2(acc0, s_rx[w][s][lane], s_bq[j][0][s], s_bq[j][1][s], s_coef[s]);
-          v1 = bsa_est2(acc1, s_rx[w][s][lane + 32], s_bq[j][0][s], s_bq[j][1][s], s_coef[s]);
-        }
-        const float B = bnd[s];
-        al0 = al0 && v0 < B;
-        al1 = al1 && v1 < B;
-        if (MODE == 0) {
-          if (IS > 0) {  // s is a compile-time constant here: v * ib is folded in once per pair
-            if (al0) mx[s] = fmaxf(mx[s], v0);
-            if (al1) mx[s] = fmaxf(mx[s], v1);
-          } else {
-            if (al0) rho = fmaxf(rho, __fmul_rn(v0, ib));
-            if (al1) rho = fmaxf(rho, __fmul_rn(v1, ib));
-          }
-        }
-        cntl += (al0 ? 1u << (8 * s) : 0u) + (al1 ? 1u << (8 * s) : 0u);
-      };
-      if (IS > 0) {
-        float qv[HD > 0 ? HD : 1];
-#pragma unroll
-        for (int i = 0; i < (HD + 3) / 4; ++i) {
-          const float4 t = *reinterpret_cast<const float4*>(&s_qh[j][4 * i]);
-          if (4 * i < HD) qv[4 * i] = t.x;
-          if (4 * i + 1 < HD) qv[4 * i + 1] = t.y;
-          if (4 * i + 2 < HD) qv[4 * i + 2] = t.z;
-          if (4 * i + 3 < HD) qv[4 * i + 3] = t.w;
-        }
-#pragma unroll
-        for (int e = 0; e < HD; ++e) {
-          const float2 d2 = sqdiff2(qv[e], xx[e]);
-          acc0 = __fadd_rn(acc0, d2.x);
-          acc1 = __fadd_rn(acc1, d2.y);
-          const int s = HeadSched<IS>::step_at(e);
-          if (s >= 0) step(s, s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3);
-        }
-      } else {
-        int s = 0;
-        const uint32_t hmask = P.hmask;
-#pragma unroll
-        for (int e = 0; e < kHeadDims; ++e) {
-          if (e < hd) {
-            const float qe = s_qh[j][e];
-            acc0 = l2upd(acc0, qe, x0[e]);
-            acc1 = l2upd(acc1, qe, x1[e]);
-            if ((hmask >> e) & 1u) {
-              step(s, s_invb[s]);
-              ++s;
-            }
-          }
-        }
-      }
-      const uint32_t packed = __reduce_add_sync(kFull, cntl);  // counts <= 64: no carries
-      if (lane == 0) s_hcnt[w][j] = packed;
-      if (MODE == 0) {
-        if (IS > 0) {  // max_s(max v_s * ib_s) = max over (slot, s) of v * ib: rounding is monotone
-#pragma unroll
-          for (int s = 0; s < HS; ++s)
-            rho = fmaxf(rho, __fmul_rn(mx[s], s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3));
-        }
-        const uint32_t r = __reduce_max_sync(kFull, __float_as_uint(rho));
-        if (lane == 0) s_rho[w][j] = r;
-      }
-      const int pl = s_base[j] + ti;
-      if (hs == nsteps) {  // the whole schedule fits in the head (d <= 16)
-        if (MODE == 0) {
-          if (al0) record_survivor(P, A, s_qid[j], pl, acc0, tile, lane);
-          if (al1) record_survivor(P, A, s_qid[j], pl, acc1, tile, lane + 32);
-        } else {
-          if (al0) confirm_survivor(P, A, s_qid[j], pl, lane);
-          if (al1) confirm_survivor(P, A, s_qid[j], pl, lane + 32);
-        }
-      } else {
-        const unsigned m0 = __ballot_sync(kFull, al0), m1 = __ballot_sync(kFull, al1);
-        s_accd[(w * kQC + j) * kTile + lane] = acc0;
-        s_accd[(w * kQC + j) * kTile + lane + 32] = acc1;
-        if (lane == 0) {
-          s_alm[w][j][0] = m0;
-          s_alm[w][j][1] = m1;
-        }
-        if (m0 | m1) live |= 1u << j;
-        nlive += __popc(m0) + __popc(m1);
-        (void)that;
-      }
-    }
-    // ---- dense continuation: every live query advances together, group by
-    // group (all share the schedule position), the tile's group loaded once
-    {
-      int s = hs, pos = hd;
-      const int ngr = P.d_pad >> 3;
-      __syncwarp();
-      while (live) {
-        if (nlive <= 32) {  // few left: one lane per survivor from here (flush)
-          if (qn + nlive > kDeepCap) flush();
+          for (int e = 0; e < 8; ++e) xx2[e] = pack2(xa[e], xb[e]);
+          // step ends inside this group (the same for every query)
+          uint32_t bm = 0;
+          const int sg = s;
+          for (int ss = s; ss < nsteps && s_ends[ss] <= g * 8 + 8; ++ss)
+            bm |= 1u << (s_ends[ss] - 1 - g * 8);
+          const int e0 = pos - g * 8;
           for (uint32_t tm = live; tm; tm &= tm - 1) {
             const int j = __ffs(tm) - 1;
-            const unsigned m0 = s_alm[w][j][0], m1 = s_alm[w][j][1];
-            const bool a0 = (m0 >> lane) & 1u, a1 = (m1 >> lane) & 1u;
-            const unsigned lt = (1u << lane) - 1u;
-            const int pre = qn + __popc(m0 & lt) + __popc(m1 & lt);
-            const float th = MODE == 1 ? s_that[w][j] : 0.f;
-            if (a0)
-              s_deep[w][pre] = DeepItem{s_accd[(w * kQC + j) * kTile + lane], (int16_t)j,
-                                        (int16_t)lane, th, (int16_t)s, (int16_t)pos};
-            if (a1)
-              s_deep[w][pre + (a0 ? 1 : 0)] =
-                  DeepItem{s_accd[(w * kQC + j) * kTile + lane + 32], (int16_t)j,
-                           (int16_t)(lane + 32), th, (int16_t)s, (int16_t)pos};
-            qn += __popc(m0) + __popc(m1);
-          }
-          flush();
-          live = 0;
-          break;
-        }
-        const int g = pos >> 3;
-        if (g >= ngr) break;
-        float xa[8], xb[8];
-        ldg8(tb + ((size_t)g * kTile + lane) * 8, xa);
-        ldg8(tb + ((size_t)g * kTile + 32 + lane) * 8, xb);
-        unsigned long long xx2[8];
+            const int q = s_qid[j];
+            const float* __restrict__ qg = A.queries + (int64_t)q * P.d + g * 8;
+            float qv[8];
+            if ((P.d & 3) == 0 && g * 8 + 8 <= P.d) {
+              const float4 u = ldg4(qg), v = ldg4(qg + 4);
+              qv[0] = u.x; qv[1] = u.y; qv[2] = u.z; qv[3] = u.w;
+              qv[4] = v.x; qv[5] = v.y; qv[6] = v.z; qv[7] = v.w;
+            } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) xx2[e] = pack2(xa[e], xb[e]);
-        // step ends inside this group (the same for every query)
-        uint32_t bm = 0;
-        const int sg = s;
-        for (int ss = s; ss < nsteps && s_ends[ss] <= g * 8 + 8; ++ss)
-          bm |= 1u << (s_ends[ss] - 1 - g * 8);
-        const int e0 = pos - g * 8;
-        for (uint32_t tm = live; tm; tm &= tm - 1) {
-          const int j = __ffs(tm) - 1;
-          const int q = s_qid[j];
-          const float* __restrict__ qg = A.queries + (int64_t)q * P.d + g * 8;
-          float qv[8];
-          if ((P.d & 3) == 0 && g * 8 + 8 <= P.d) {
-            const float4 u = ldg4(qg), v = ldg4(qg + 4);
-            qv[0] = u.x; qv[1] = u.y; qv[2] = u.z; qv[3] = u.w;
-            qv[4] = v.x; qv[5] = v.y; qv[6] = v.z; qv[7] = v.w;
-          } else {
+              for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + e) : 0.f;
+            }
+            float a0 = s_accd[(w * kQC + j) * kTile + lane], a1 = s_accd[(w * kQC + j) * kTile + lane + 32];
+            if (bm == 0) {  // no step ends in this group: the alive masks stay
 #pragma unroll
-            for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + e) : 0.f;
-          }
-          float a0 = s_accd[(w * kQC + j) * kTile + lane], a1 = s_accd[(w * kQC + j) * kTile + lane + 32];
-          if (bm == 0) {  // no step ends in this group: the alive masks stay
+              for (int e = 0; e < 8; ++e) {
+                if (e >= e0) {
+                  const float2 d2 = sqdiff2(qv[e], xx2[e]);
+                  a0 = __fadd_rn(a0, d2.x);
+                  a1 = __fadd_rn(a1, d2.y);
+                }
+              }
+              s_accd[(w * kQC + j) * kTile + lane] = a0;
+              s_accd[(w * kQC + j) * kTile + lane + 32] = a1;
+              continue;
+            }
+            const unsigned o0 = s_alm[w][j][0], o1 = s_alm[w][j][1];
+            bool l0 = (o0 >> lane) & 1u, l1 = (o1 >> lane) & 1u;
+            int se = sg;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               if (e >= e0) {
                 const float2 d2 = sqdiff2(qv[e], xx2[e]);
                 a0 = __fadd_rn(a0, d2.x);
                 a1 = __fadd_rn(a1, d2.y);
+                if ((bm >> e) & 1u) {  // step se ends after this dim (warp-uniform)
+                  float v0 = a0, v1 = a1;
+                  if (BSA) {
+                    const float* rs = A.resid + ((size_t)tile * nsteps + se) * kTile;
+                    const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
+                    v0 = bsa_est2(a0, l0 ? __ldg(rs + lane) : 0.f, bq[se], bq[nsteps + se],
+                                  s_coef[se]);
+                    v1 = bsa_est2(a1, l1 ? __ldg(rs + lane + 32) : 0.f, bq[se], bq[nsteps + se],
+                                  s_coef[se]);
+                  }
+                  const float B =
+                      MODE == 0 ? s_bnd[j][se] : bound_at(P, s_that[w][j], se, s_ratio, s_band);
+                  l0 = l0 && v0 < B;
+                  l1 = l1 && v1 < B;
+                  const int c = __popc(__ballot_sync(kFull, l0)) + __popc(__ballot_sync(kFull, l1));
+                  if (MODE == 0) {
+                    float r = 0.f;
+                    if (l0) r = fmaxf(r, __fmul_rn(v0, s_invb[se]));
+                    if (l1) r = fmaxf(r, __fmul_rn(v1, s_invb[se]));
+                    const uint32_t rm = __reduce_max_sync(kFull, __float_as_uint(r));
+                    if (lane == 0 && rm > s_rho[w][j]) s_rho[w][j] = rm;
+                  }
+                  if (lane == 0) s_dcnt[w][j][se] = (uint32_t)c;
+                  if (se == nsteps - 1) {  // the last step: survivors
+                    if (MODE == 0) {
+                      if (l0) record_survivor(P, A, q, s_base[j] + ti, a0, tile, lane);
+                      if (l1) record_survivor(P, A, q, s_base[j] + ti, a1, tile, lane + 32);
+                    } else {
+                      if (l0) confirm_survivor(P, A, q, s_base[j] + ti, lane);
+                      if (l1) confirm_survivor(P, A, q, s_base[j] + ti, lane + 32);
+                    }
+                    l0 = l1 = false;
+                  }
+                  ++se;
+                }
               }
             }
+            const unsigned m0 = __ballot_sync(kFull, l0), m1 = __ballot_sync(kFull, l1);
+            nlive += (int)(__popc(m0) + __popc(m1)) - (int)(__popc(o0) + __popc(o1));
+            __syncwarp();
             s_accd[(w * kQC + j) * kTile + lane] = a0;
             s_accd[(w * kQC + j) * kTile + lane + 32] = a1;
-            continue;
-          }
-          const unsigned o0 = s_alm[w][j][0], o1 = s_alm[w][j][1];
-          bool l0 = (o0 >> lane) & 1u, l1 = (o1 >> lane) & 1u;
-          int se = sg;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            if (e >= e0) {
-              const float2 d2 = sqdiff2(qv[e], xx2[e]);
-              a0 = __fadd_rn(a0, d2.x);
-              a1 = __fadd_rn(a1, d2.y);
-              if ((bm >> e) & 1u) {  // step se ends after this dim (warp-uniform)
-                float v0 = a0, v1 = a1;
-                if (BSA) {
-                  const float* rs = A.resid + ((size_t)tile * nsteps + se) * kTile;
-                  const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
-                  v0 = bsa_est2(a0, l0 ? __ldg(rs + lane) : 0.f, bq[se], bq[nsteps + se],
-                                s_coef[se]);
-                  v1 = bsa_est2(a1, l1 ? __ldg(rs + lane + 32) : 0.f, bq[se], bq[nsteps + se],
-                                s_coef[se]);
-                }
-                const float B =
-                    MODE == 0 ? s_bnd[j][se] : bound_at(P, s_that[w][j], se, s_ratio, s_band);
-                l0 = l0 && v0 < B;
-                l1 = l1 && v1 < B;
-                const int c = __popc(__ballot_sync(kFull, l0)) + __popc(__ballot_sync(kFull, l1));
-                if (MODE == 0) {
-                  float r = 0.f;
-                  if (l0) r = fmaxf(r, __fmul_rn(v0, s_invb[se]));
-                  if (l1) r = fmaxf(r, __fmul_rn(v1, s_invb[se]));
-                  const uint32_t rm = __reduce_max_sync(kFull, __float_as_uint(r));
-                  if (lane == 0 && rm > s_rho[w][j]) s_rho[w][j] = rm;
-                }
-                if (lane == 0) s_dcnt[w][j][se] = (uint32_t)c;
-                if (se == nsteps - 1) {  // the last step: survivors
-                  if (MODE == 0) {
-                    if (l0) record_survivor(P, A, q, s_base[j] + ti, a0, tile, lane);
-                    if (l1) record_survivor(P, A, q, s_base[j] + ti, a1, tile, lane + 32);
-                  } else {
-                    if (l0) confirm_survivor(P, A, q, s_base[j] + ti, lane);
-                    if (l1) confirm_survivor(P, A, q, s_base[j] + ti, lane + 32);
-                  }
-                  l0 = l1 = false;
-                }
-                ++se;
-              }
+            if (lane == 0) {
+              s_alm[w][j][0] = m0;
+              s_alm[w][j][1] = m1;
             }
+            if (!(m0 | m1)) live &= ~(1u << j);
+            __syncwarp();
           }
-          const unsigned m0 = __ballot_sync(kFull, l0), m1 = __ballot_sync(kFull, l1);
-          nlive += (int)(__popc(m0) + __popc(m1)) - (int)(__popc(o0) + __popc(o1));
-          __syncwarp();
-          s_accd[(w * kQC + j) * kTile + lane] = a0;
-          s_accd[(w * kQC + j) * kTile + lane + 32] = a1;
-          if (lane == 0) {
-            s_alm[w][j][0] = m0;
-            s_alm[w][j][1] = m1;
-          }
-          if (!(m0 | m1)) live &= ~(1u << j);
-          __syncwarp();
+          s = sg + __popc(bm);
+          pos = (g + 1) * 8;
         }
-        s = sg + __popc(bm);
-        pos = (g + 1) * 8;
+        if (qn) flush();
       }
-      if (qn) flush();
+    } else {
+      flush();
     }
     // the pairs' stats: values_touched (search.py:148-169) and trace counts
     for (int j = lane; j < ne; j += 32) {
@@ -2165,7 +1812,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     const int dsm = (int)(sizeof(float) * kBWD * kQC * kTile);
 #define PDX_B_DENSE(IS, B, M)                                                          \
   {                                                                                    \
-    auto fn = bdscan_kernel<IS, B, M>;                                                 \
+    auto fn = bscan_kernel<IS, B, M, true>;                                            \
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);        \
     fn<<<g, bd, dsm, st>>>(P, A);                                                      \
   }
@@ -2177,11 +1824,11 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
       if (mode == 0) PDX_B_DENSE(IS, false, 0) else PDX_B_DENSE(IS, false, 1)          \
     }                                                                                  \
   } else if (bsa) {                                                                    \
-    if (mode == 0) bscan_kernel<IS, true, 0><<<g, b, 0, st>>>(P, A);                   \
-    else bscan_kernel<IS, true, 1><<<g, b, 0, st>>>(P, A);                             \
+    if (mode == 0) bscan_kernel<IS, true, 0, false><<<g, b, 0, st>>>(P, A);            \
+    else bscan_kernel<IS, true, 1, false><<<g, b, 0, st>>>(P, A);                      \
   } else {                                                                             \
-    if (mode == 0) bscan_kernel<IS, false, 0><<<g, b, 0, st>>>(P, A);                  \
-    else bscan_kernel<IS, false, 1><<<g, b, 0, st>>>(P, A);                            \
+    if (mode == 0) bscan_kernel<IS, false, 0, false><<<g, b, 0, st>>>(P, A);           \
+    else bscan_kernel<IS, false, 1, false><<<g, b, 0, st>>>(P, A);                     \
   }
     switch (is) {
       case 1: PDX_B_LAUNCH(1) break;
