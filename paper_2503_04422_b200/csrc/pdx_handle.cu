@@ -95,7 +95,23 @@ struct pdx_index {
   DevBuf<int64_t> cand;
   DevBuf<int32_t> ccount;
   cublasHandle_t blas = nullptr;
+  // CUDA graph of the last repeated search call (pdx_index_search)
+  struct GraphKey {
+    const void* q;
+    const void* outs[4];
+    int64_t nq;
+    void* stream;
+    pdx_query_params prm;
+  };
+  GraphKey gkey{}, gseen{};
+  bool gseen_valid = false;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gs = nullptr;
+  cudaEvent_t gev = nullptr;
   ~pdx_index() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (gs) cudaStreamDestroy(gs);
+    if (gev) cudaEventDestroy(gev);
     if (blas) cublasDestroy(blas);
   }
 };
@@ -367,9 +383,12 @@ extern "C" int pdx_index_destroy(pdx_index* index) {
   return PDX_OK;
 }
 
-extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const float* Q,
+// Enqueue one search on `st` (blocking only on the K8 path); host outputs
+// are copied back asynchronously — the caller synchronizes.
+static int index_search_enqueue(pdx_index* I, const pdx_query_params* P, const float* Q,
                                 int64_t nq, float* out_dist, int64_t* out_ids,
-                                int64_t* out_touched, int64_t* out_total, void* stream) {
+                                int64_t* out_touched, int64_t* out_total, cudaStream_t st) {
+  void* stream = st;
   PDX_REQUIRE(I && P, "pdx_index_search: null argument");
   PDX_REQUIRE(nq >= 0, "bad query count");
   if (nq == 0) return PDX_OK;
@@ -377,7 +396,6 @@ extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const f
   PDX_REQUIRE(P->k >= 1, "k must be >= 1");
   PDX_REQUIRE(!P->rotate || I->has_rotation, "the index carries no rotation matrix");
   const int64_t d = I->d, k = P->k;
-  cudaStream_t st = as_stream(stream);
   const bool ivf = I->nlist > 0;
   if (ivf) PDX_REQUIRE(P->nprobe >= 1 && P->nprobe <= I->nlist, "nprobe must be in [1, %d], got %d",
                        I->nlist, P->nprobe);
@@ -498,7 +516,88 @@ extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const f
       PDX_CUDA_CHECK(cudaMemcpyAsync(out_touched, touched, 8 * nq, cudaMemcpyDeviceToHost, st));
     if (out_total)
       PDX_CUDA_CHECK(cudaMemcpyAsync(out_total, total, 8 * nq, cudaMemcpyDeviceToHost, st));
-    PDX_CUDA_CHECK(cudaStreamSynchronize(st));
   }
+  (void)stream;
+  return PDX_OK;
+}
+
+static bool page_locked(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// A repeated call (same buffers, batch size, parameters and stream) is
+// captured once into a CUDA graph and replayed: the ~30 launches and copies
+// of a search leave no host gaps.  Only for IVF searches from page-locked
+// host buffers whose path has no host synchronization or host-side uploads
+// (no K8, no BSA); anything else, or a failed capture, runs directly.
+extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const float* Q,
+                                int64_t nq, float* out_dist, int64_t* out_ids,
+                                int64_t* out_touched, int64_t* out_total, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const bool graphable = I && P && nq > 0 && I->nlist > 0 && !P->queries_on_device &&
+                         !P->outputs_on_device && P->pruner != PDX_PRUNER_BSA &&
+                         !getenv("PDX_NO_GRAPHS") && page_locked(Q) && page_locked(out_dist) &&
+                         page_locked(out_ids) && page_locked(out_touched) &&
+                         page_locked(out_total);
+  if (graphable) {
+    pdx_index::GraphKey key;
+    memset(&key, 0, sizeof(key));
+    key.q = Q;
+    key.outs[0] = out_dist;
+    key.outs[1] = out_ids;
+    key.outs[2] = out_touched;
+    key.outs[3] = out_total;
+    key.nq = nq;
+    key.stream = stream;
+    key.prm = *P;
+    if (!I->gs) {
+      PDX_CUDA_CHECK(cudaStreamCreateWithFlags(&I->gs, cudaStreamNonBlocking));
+      PDX_CUDA_CHECK(cudaEventCreateWithFlags(&I->gev, cudaEventDisableTiming));
+    }
+    auto after_caller = [&]() -> int {  // the graph stream follows the caller's stream
+      PDX_CUDA_CHECK(cudaEventRecord(I->gev, st));
+      PDX_CUDA_CHECK(cudaStreamWaitEvent(I->gs, I->gev, 0));
+      return PDX_OK;
+    };
+    if (I->gexec && memcmp(&key, &I->gkey, sizeof(key)) == 0) {
+      PDX_TRY(after_caller());
+      PDX_CUDA_CHECK(cudaGraphLaunch(I->gexec, I->gs));
+      PDX_CUDA_CHECK(cudaStreamSynchronize(I->gs));
+      return PDX_OK;
+    }
+    if (I->gseen_valid && memcmp(&key, &I->gseen, sizeof(key)) == 0) {
+      PDX_TRY(after_caller());
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ex = nullptr;
+      bool ok = cudaStreamBeginCapture(I->gs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        const int rc = index_search_enqueue(I, P, Q, nq, out_dist, out_ids, out_touched,
+                                            out_total, I->gs);
+        ok = cudaStreamEndCapture(I->gs, &g) == cudaSuccess && rc == PDX_OK && g;
+        ok = ok && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+      }
+      if (g) cudaGraphDestroy(g);
+      if (ok) {
+        if (I->gexec) cudaGraphExecDestroy(I->gexec);
+        I->gexec = ex;
+        I->gkey = key;
+        PDX_CUDA_CHECK(cudaGraphLaunch(I->gexec, I->gs));
+        PDX_CUDA_CHECK(cudaStreamSynchronize(I->gs));
+        return PDX_OK;
+      }
+      if (ex) cudaGraphExecDestroy(ex);
+      cudaGetLastError();  // a failed capture leaves no sticky error: run directly
+    }
+    I->gseen = key;
+    I->gseen_valid = true;
+  }
+  PDX_TRY(index_search_enqueue(I, P, Q, nq, out_dist, out_ids, out_touched, out_total, st));
+  if (!P->outputs_on_device) PDX_CUDA_CHECK(cudaStreamSynchronize(st));
   return PDX_OK;
 }

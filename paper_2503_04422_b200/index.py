@@ -264,6 +264,26 @@ class IvfSearcher:
         self._buf = {}
         self._scratch = None
 
+    def select(self, Q):
+        """K2 only: int32 [nq, nprobe] selected buckets (ivf_select_buckets)."""
+        return select_buckets_device(self.index, Q, self.nprobe, self.params.metric,
+                                     self._scratch)
+
+    def search(self, Q, sel, stats=False, trace_cap=0, timed=False):
+        """The scan for a given selection (device buffers in and out: the call
+        a CUDA graph of a fixed batch captures, see bench.py)."""
+        orders, oss = None, 0
+        if self.params.pruner == "bond" and self.criteria is not OrderCriteria.SEQUENTIAL:
+            orders = dimension_orders_device(Q, self.index.means_dev, self.criteria,
+                                             self.zone_width, mean_index=sel, nsets=self.nprobe)
+            oss = 1
+        res = run_search(self.index.store, Q, self.params, seg_bucket=sel, nseg=self.nprobe,
+                         orders=orders, order_qstride=self.nprobe, order_sstride=oss,
+                         stats=stats, trace_cap=trace_cap, warps=self.warps, out=self._buf,
+                         timed=timed, batched=self.batched)
+        res.selected = sel
+        return res
+
     def run(self, Q, stats=False, trace_cap=0, timed=False, phase_times=None, scan_events=None):
         import torch
         ev = None

@@ -102,3 +102,35 @@ def test_handle_tensor_core_path_identical(metric):
     hb = P.PdxIndex.from_index(flat)  # borrowed store, same path
     c = hb.search(Q, k=20, metric=metric, tensor_cores=True)
     np.testing.assert_array_equal(c["ids"].numpy(), b["ids"].numpy())
+
+
+@pytest.mark.gpu
+def test_handle_graph_replay_identical():
+    """Repeated calls with the same page-locked buffers are captured into a
+    CUDA graph and replayed (pdx_index_search): every call's ids, distances
+    and stats equal the first (direct) call's, across a parameter change."""
+    import torch
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((30_000, 32)).astype(np.float32)
+    idx = P.ivf_build(P.VectorCollection.from_array(x), nlist=64, seed=0)
+    h = P.PdxIndex.from_index(idx)
+    Q = torch.from_numpy(x[:64] + 0.1 * rng.standard_normal((64, 32)).astype(np.float32))
+    Q = Q.pin_memory()
+    out = {"dist": torch.empty((64, 10), dtype=torch.float32).pin_memory(),
+           "ids": torch.empty((64, 10), dtype=torch.int64).pin_memory(),
+           "touched": torch.empty((64,), dtype=torch.int64).pin_memory(),
+           "total": torch.empty((64,), dtype=torch.int64).pin_memory()}
+    for nprobe, pruner in ((12, "ads"), (6, "bond"), (12, "ads")):
+        first = None
+        for _ in range(4):  # direct, capture, replay, replay
+            h.search(Q, k=10, pruner=pruner, nprobe=nprobe, stats=True, out=out)
+            got = {key: v.clone() for key, v in out.items()}
+            if first is None:
+                first = got
+                ref = P.ivf_search_batch(idx, Q.numpy(), P.SearchParams(k=10, pruner=pruner),
+                                         nprobe, stats=True)
+                np.testing.assert_array_equal(got["ids"].numpy(), ref["ids"])
+                np.testing.assert_array_equal(got["touched"].numpy(), ref["touched"])
+            for key in first:
+                assert torch.equal(got[key], first[key]), key
+    h.close()
