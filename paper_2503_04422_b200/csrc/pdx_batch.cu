@@ -147,6 +147,7 @@ struct BArgs {
   // work
   const BItem* items;
   const int32_t* nitems;
+  int32_t* wctr;  // [2]: work items handed out by MODE 0 / MODE 1
   const BEntry* entries;
   const int64_t* bnvec;  // vectors per bucket
   // outputs
@@ -800,8 +801,10 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
   __shared__ float s_invb[kMaxSteps], s_coef[kMaxSteps];
   __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
 
-  if ((int)blockIdx.x >= *A.nitems) return;
-  const BItem it = A.items[blockIdx.x];
+  __shared__ int s_itx;
+  // one work item (the body returns early for an item with nothing to do)
+  auto run_item = [&](const int itx) {
+  const BItem it = A.items[itx];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ne = it.ne, nsteps = P.nsteps;
   const int64_t bk0 = A.bucket_block[it.bucket];
@@ -1018,8 +1021,9 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
       qn = 0;
     };
 
-    for (int i = lane; i < ne * (nsteps - hs); i += 32)  // deep-step counters of this tile
-      s_dcnt[w][i / (nsteps - hs)][hs + i % (nsteps - hs)] = 0u;
+    for (int j = lane; j < ne; j += 32)  // deep-step counters of this tile's pairs
+      if ((todo >> j) & 1u)
+        for (int t = hs; t < nsteps; ++t) s_dcnt[w][j][t] = 0u;
     __syncwarp();
     for (uint32_t tm = todo; tm; tm &= tm - 1) {
       const int j = __ffs(tm) - 1;
@@ -1300,6 +1304,17 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
       if (MODE == 0) A.prho[p] = __uint_as_float(s_rho[w][j]);
     }
     __syncwarp();
+  }
+  };
+  // persistent CTAs pull work items from a counter (no empty CTAs: the
+  // item count is only known on the device)
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_itx = atomicAdd(A.wctr + MODE, 1);
+    __syncthreads();
+    const int itx = s_itx;
+    if (itx >= *A.nitems) return;
+    run_item(itx);
   }
 }
 
@@ -1735,6 +1750,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   A.pcnt = trace ? pcnt : nullptr;
   A.items = items;
   A.nitems = ctr;
+  A.wctr = ctr + 2;
   A.entries = entries;
   A.bnvec = bnvec;
   A.out_dist = out->d_dist;
@@ -1808,7 +1824,12 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     // wide vectors: survivors of the head are many and long — the dense
     // continuation variant (all live queries of a tile advance together)
     const bool dense = store->d > 256;
-    const dim3 g((unsigned)nitems_max), b(kBW * 32), bd(kBWD * 32);
+    int nsm = 148, dv = 0;
+    cudaGetDevice(&dv);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
+    // persistent grids: about two CTAs per SM slot pull the work items
+    const dim3 g((unsigned)std::min<int64_t>(nitems_max, (int64_t)nsm * (dense ? 8 : 6)));
+    const dim3 b(kBW * 32), bd(kBWD * 32);
     const int dsm = (int)(sizeof(float) * kBWD * kQC * kTile);
 #define PDX_B_DENSE(IS, B, M)                                                          \
   {                                                                                    \
