@@ -56,7 +56,6 @@
 
 #include <algorithm>
 #include <cstdlib>
-#include <mutex>
 #include <vector>
 
 #include "pdx_batch.cuh"
@@ -1497,19 +1496,18 @@ int host_warm_min(int m, double sf) {  // warm_min_count (pdx_scan_kernel.cuh)
   return p;
 }
 
-// A per-device side stream and fork/join events for the planning kernels.
-// Calls on different streams may share it: each call records its own fork
-// before and its own join after its kernels, so stream order stays correct.
+// A side stream and fork/join events for the planning kernels, per host
+// thread and device: a call's record-then-wait on its fork event must not
+// interleave with another thread's (the ABI allows concurrent calls on
+// different streams); calls of one thread are ordered by the thread itself.
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_stream() {
-  static std::mutex mu;
-  static SideStream per_dev[64];
+  thread_local SideStream per_dev[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(mu);
   SideStream& ss = per_dev[dev & 63];
   if (!ss.s) {
     cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
