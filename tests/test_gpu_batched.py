@@ -215,3 +215,36 @@ def test_warp_bucket_selection_overflow(P):
                 key = -acc if metric == "ip" else acc
                 ref = np.argsort(key, kind="stable")[:nprobe]
                 np.testing.assert_array_equal(sel[i].cpu().numpy(), ref)
+
+
+def test_batched_concurrent_threads(P, rotated):
+    """Two host threads searching on their own streams (the C-ABI allows it;
+    ctypes drops the GIL): each result equals the serial search's."""
+    import threading
+
+    import torch
+    _, qr, index = rotated
+    params = P.SearchParams(k=10, pruner="ads")
+    serial = [P.ivf_search_batch(index, qr[i::2], params, 16, stats=True, batched=2)
+              for i in range(2)]
+    got = [None, None]
+
+    def work(i):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            s = P.IvfSearcher(index, params, 16, batched=2)
+            q = P.store.to_device(qr[i::2])
+            for _ in range(3):
+                r = s.run(q, stats=True)
+            st.synchronize()
+            got[i] = (r.ids.cpu().numpy(), r.dist.cpu().numpy(), r.touched.cpu().numpy())
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(2):
+        np.testing.assert_array_equal(got[i][0], serial[i]["ids"])
+        np.testing.assert_array_equal(got[i][1], serial[i]["dist"])
+        np.testing.assert_array_equal(got[i][2], serial[i]["touched"])
