@@ -184,6 +184,27 @@ __device__ __forceinline__ float2 sqdiff2(float q, unsigned long long xx) {
   return r;
 }
 
+// acc + (q - x)^2 for a slot pair, all three steps f32x2: FADD2 (q
+// broadcast), the square as FFMA2 with a +0 addend — the exact square
+// rounded once, bit-identical to mul.rn (a square is never -0) — and FADD2.
+// ptxas does not contract FFMA2 + FADD2, so each op stays separately rounded
+// (the reference's per-op rounding) at 3 instructions per dim per pair.
+__device__ __forceinline__ unsigned long long sqacc2(unsigned long long acc, float q,
+                                                     unsigned long long xx) {
+  unsigned long long qq, z, t, p, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(z) : "f"(0.0f));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(qq), "l"(xx));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(p) : "l"(t), "l"(z));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(acc), "l"(p));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
 // BSA estimate (bsa_est in pdx_scan_spec.cuh, same association).
 __device__ __forceinline__ float bsa_est2(float acc, float rx, float rq, float sq, float coef) {
   const float cx = __fmul_rn(coef, __fsqrt_rn(rx));
@@ -1072,13 +1093,17 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
           if (4 * i + 2 < HD) qv[4 * i + 2] = t.z;
           if (4 * i + 3 < HD) qv[4 * i + 3] = t.w;
         }
+        unsigned long long acc2 = pack2(0.f, 0.f);
 #pragma unroll
         for (int e = 0; e < HD; ++e) {
-          const float2 d2 = sqdiff2(qv[e], xx[e]);
-          acc0 = __fadd_rn(acc0, d2.x);
-          acc1 = __fadd_rn(acc1, d2.y);
+          acc2 = sqacc2(acc2, qv[e], xx[e]);
           const int s = HeadSched<IS>::step_at(e);
-          if (s >= 0) step(s, s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3);
+          if (s >= 0) {
+            const float2 a = unpack2(acc2);
+            acc0 = a.x;
+            acc1 = a.y;
+            step(s, s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3);
+          }
         }
       } else {
         int s = 0;
@@ -1201,14 +1226,13 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
             }
             float a0 = s_accd[(w * kQC + j) * kTile + lane], a1 = s_accd[(w * kQC + j) * kTile + lane + 32];
             if (bm == 0) {  // no step ends in this group: the alive masks stay
+              unsigned long long a2 = pack2(a0, a1);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                if (e >= e0) {
-                  const float2 d2 = sqdiff2(qv[e], xx2[e]);
-                  a0 = __fadd_rn(a0, d2.x);
-                  a1 = __fadd_rn(a1, d2.y);
-                }
-              }
+              for (int e = 0; e < 8; ++e)
+                if (e >= e0) a2 = sqacc2(a2, qv[e], xx2[e]);
+              const float2 af = unpack2(a2);
+              a0 = af.x;
+              a1 = af.y;
               s_accd[(w * kQC + j) * kTile + lane] = a0;
               s_accd[(w * kQC + j) * kTile + lane + 32] = a1;
               continue;
