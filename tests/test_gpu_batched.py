@@ -248,3 +248,30 @@ def test_batched_concurrent_threads(P, rotated):
         np.testing.assert_array_equal(got[i][0], serial[i]["ids"])
         np.testing.assert_array_equal(got[i][1], serial[i]["dist"])
         np.testing.assert_array_equal(got[i][2], serial[i]["touched"])
+
+
+def test_batched_limits_and_trace_overflow(P, rotated):
+    """k = 256 (the batched path's limit), 33 queries, selection_fraction
+    1.0 and a survivor-trace buffer too small for the visit list (trace_len
+    = -1, the per-query scan's convention): identical to the per-query scan."""
+    from paper_2503_04422_b200.search import run_search
+    from paper_2503_04422_b200.index import select_buckets_device
+    _, qr, index = rotated
+    q = qr[:33]
+    for params in (P.SearchParams(k=256, pruner="ads"),
+                   P.SearchParams(k=10, pruner="bond", selection_fraction=1.0)):
+        _same(_run(P, index, q, params, 16, 2), _run(P, index, q, params, 16, 1))
+    Qd = P.store.to_device(q)
+    sel = select_buckets_device(index, Qd, 16, "l2")
+    sel = sel[0] if isinstance(sel, tuple) else sel
+    params = P.SearchParams(k=10, pruner="ads")
+    outs = []
+    for batched in (2, 1):
+        r = run_search(index.store, Qd, params, seg_bucket=sel.contiguous(), nseg=16,
+                       trace_cap=100, batched=batched)
+        outs.append((r.ids.cpu().numpy(), r.trace_len.cpu().numpy(),
+                     r.touched.cpu().numpy()))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[0][2], outs[1][2])
+    assert (outs[0][1] == -1).all()
