@@ -1329,8 +1329,12 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     __syncwarp();
   }
   };
-  // persistent CTAs pull work items from a counter (no empty CTAs: the
-  // item count is only known on the device)
+  if (MODE == 0) {  // one item per CTA: CTAs retire independently (no item barrier)
+    if ((int)blockIdx.x < *A.nitems) run_item(blockIdx.x);
+    return;
+  }
+  // MODE 1 (most items need little work): persistent CTAs pull work items
+  // from a counter instead of launching the item-count upper bound
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_itx = atomicAdd(A.wctr + MODE, 1);
@@ -1849,8 +1853,10 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     int nsm = 148, dv = 0;
     cudaGetDevice(&dv);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
-    // persistent grids: about two CTAs per SM slot pull the work items
-    const dim3 g((unsigned)std::min<int64_t>(nitems_max, (int64_t)nsm * (dense ? 8 : 6)));
+    // MODE 0: one CTA per work item (upper bound; the extra CTAs exit);
+    // MODE 1: persistent, about two CTAs per SM slot pull the items
+    const dim3 g(mode == 0 ? (unsigned)nitems_max
+                           : (unsigned)std::min<int64_t>(nitems_max, (int64_t)nsm * (dense ? 8 : 6)));
     const dim3 b(kBW * 32), bd(kBWD * 32);
     const int dsm = (int)(sizeof(float) * kBWD * kQC * kTile);
 #define PDX_B_DENSE(IS, B, M)                                                          \
