@@ -199,6 +199,15 @@ __device__ __forceinline__ unsigned long long sqacc2(unsigned long long acc, flo
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(acc), "l"(p));
   return r;
 }
+// (a, b) as a register pair computed once: x + (-0) is exact for every x
+// (-0 included), and as a real FADD2 ptxas keeps the pair instead of
+// rebuilding it from the two loads' registers at every use.
+__device__ __forceinline__ unsigned long long pack2_hold(float a, float b) {
+  unsigned long long r, nz;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(nz) : "f"(-0.0f));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pack2(a, b)), "l"(nz));
+  return r;
+}
 __device__ __forceinline__ float2 unpack2(unsigned long long v) {
   float2 r;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
@@ -969,7 +978,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     unsigned long long xx[IS > 0 ? HD : 1];
     if (IS > 0) {
 #pragma unroll
-      for (int e = 0; e < (IS > 0 ? HD : 1); ++e) xx[e] = pack2(x0[e], x1[e]);
+      for (int e = 0; e < (IS > 0 ? HD : 1); ++e) xx[e] = pack2_hold(x0[e], x1[e]);
     }
     const bool in0 = lane < m, in1 = lane + 32 < m;
     int qn = 0;  // deep items queued by this warp for this tile
@@ -1204,7 +1213,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
           ldg8(tb + ((size_t)g * kTile + 32 + lane) * 8, xb);
           unsigned long long xx2[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) xx2[e] = pack2(xa[e], xb[e]);
+          for (int e = 0; e < 8; ++e) xx2[e] = pack2_hold(xa[e], xb[e]);
           // step ends inside this group (the same for every query)
           uint32_t bm = 0;
           const int sg = s;
