@@ -1010,6 +1010,12 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
 #pragma unroll
             for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + g * 8 + e) : 0.f;
           }
+          if (pos == g * 8 && g * 8 + 8 < nend) {  // no step ends in this group
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = l2upd(acc, qv[e], x[e]);
+            pos += 8;
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int dim = g * 8 + e;
