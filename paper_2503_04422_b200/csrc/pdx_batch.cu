@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
-  if (FIRST ? nt == 0 : (int)blockIdx.y * 16 + 1 >= min(nt, kP1Cap)) return;
+  if (FIRST ? nt == 0 : (int)blockIdx.y * 4 + 1 >= min(nt, kP1Cap)) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
     __syncthreads();
   }
   if (FIRST && w > 0) return;
-  for (int it4 = 0; it4 < (FIRST ? 1 : 4); ++it4) {
-  const int ti = FIRST ? 0 : blockIdx.y * 16 + it4 * 4 + w + 1;
+  {  // one tile per warp (latency-bound: many tiles in flight)
+  const int ti = FIRST ? 0 : blockIdx.y * 4 + w + 1;
   if (ti >= min(nt, kP1Cap)) return;
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
@@ -1807,7 +1807,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   // ---- phase 1: the first selected bucket of every query (exact chain)
   {
     const int p1max = std::min(store->max_bucket_tiles, kP1Cap);
-    const dim3 g((unsigned)nq, (unsigned)((p1max + 14) / 16));
+    const dim3 g((unsigned)nq, (unsigned)((p1max + 2) / 4));
     const size_t sm = sizeof(float) * (store->d_pad + 2 * kMaxSteps);
     if (sm > 48 * 1024) {
       PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, true>,
