@@ -530,7 +530,9 @@ __global__ void bt0_kernel(const BParams P, const BArgs A, const int32_t* __rest
     b0bnd[(int64_t)q * P.nsteps + lane] = T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
 }
 
-template <int NSM>  // NSM >= nsteps: register arrays sized to the schedule
+// NSM >= nsteps: register arrays sized to the schedule.  RK (k <= 32): the
+// heap lives in registers, lane i holding the i-th smallest (dist, id).
+template <int NSM, bool RK>
 __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
                                                       const int32_t* __restrict__ seg0,
                                                       const int64_t* __restrict__ p1off,
@@ -556,6 +558,33 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   Control& ctl = s_ctl[wq];
   if (lane == 0) ctl.n = 0;
   __syncwarp();
+  float rd = INFINITY;  // RK heap
+  int64_t ri = INT64_MAX;
+  int rn = 0;
+  // TopK.push (search.py:44-51) of the lanes' candidates, in lane order
+  auto rk_push = [&](bool cand, float dv, int64_t iv) {
+    unsigned mask = __ballot_sync(kFull, cand);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const float d = __shfl_sync(kFull, dv, src);
+      const int64_t i = __shfl_sync(kFull, iv, src);
+      if (rn == k && !pair_less(d, i, __shfl_sync(kFull, rd, k - 1), __shfl_sync(kFull, ri, k - 1)))
+        continue;
+      const int pos = __popc(__ballot_sync(kFull, lane < rn && pair_less(rd, ri, d, i)));
+      const float pd = __shfl_up_sync(kFull, rd, 1);
+      const int64_t pi = __shfl_up_sync(kFull, ri, 1);
+      if (lane > pos) {
+        rd = pd;
+        ri = pi;
+      } else if (lane == pos) {
+        rd = d;
+        ri = i;
+      }
+      rn = rn < k ? rn + 1 : k;
+    }
+  };
+  auto rk_threshold = [&]() { return rn < k ? INFINITY : __shfl_sync(kFull, rd, k - 1); };
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = min((int)(A.bucket_block[c + 1] - b0), kP1Cap);
@@ -702,11 +731,18 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
         }
       }
       const int n = min(k, m);
-      if (lane < n) { tkd[lane] = f0; tki[lane] = i0; }
-      if (lane + 32 < n) { tkd[lane + 32] = f1; tki[lane + 32] = i1; }
-      if (lane == 0) ctl.n = n;
-      __syncwarp();
-      T = topk_threshold(ctl, k, tkd);
+      if (RK) {
+        rd = f0;
+        ri = i0;
+        rn = n;
+        T = rk_threshold();
+      } else {
+        if (lane < n) { tkd[lane] = f0; tki[lane] = i0; }
+        if (lane + 32 < n) { tkd[lane + 32] = f1; tki[lane + 32] = i1; }
+        if (lane == 0) ctl.n = n;
+        __syncwarp();
+        T = topk_threshold(ctl, k, tkd);
+      }
       c0 = c1 = false;
     }
     if (__any_sync(kFull, c0 || c1)) {  // push the block's survivors (search.py:173-174)
@@ -717,13 +753,32 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
           f0 = u0[s];
           f1 = u1[s];
         }
-      topk_push_lanes(ctl, k, tkd, tki, c0, f0, id0, lane);
-      topk_push_lanes(ctl, k, tkd, tki, c1, f1, id1, lane);
-      __syncwarp();
-      T = topk_threshold(ctl, k, tkd);
+      if (RK) {
+        rk_push(c0, f0, id0);
+        rk_push(c1, f1, id1);
+        T = rk_threshold();
+      } else {
+        topk_push_lanes(ctl, k, tkd, tki, c0, f0, id0, lane);
+        topk_push_lanes(ctl, k, tkd, tki, c1, f1, id1, lane);
+        __syncwarp();
+        T = topk_threshold(ctl, k, tkd);
+      }
     }
   }
   __syncwarp();
+  if (RK) {
+    if (lane < k) {
+      A.out_dist[(int64_t)q * k + lane] = lane < rn ? rd : INFINITY;
+      A.out_ids[(int64_t)q * k + lane] = lane < rn ? ri : -1;
+    }
+    if (lane == 0) {
+      A.out_count[q] = rn;
+      if (A.out_touched) A.out_touched[q] = touched;
+      if (A.out_total) A.out_total[q] = total;
+      if (A.trace_len) A.trace_len[q] = tlen;
+    }
+    return;
+  }
   const int n = ctl.n;
   for (int i = lane; i < k; i += 32) {
     A.out_dist[(int64_t)q * k + i] = i < n ? tkd[i] : INFINITY;
@@ -1846,12 +1901,14 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
       kern<<<(nq + 7) / 8, 256, hsm, st>>>(P, A, seg0, p1off, part1);
       return cudaGetLastError();
     };
+    const bool rk = k <= 32;  // the heap in registers
     if (P.nsteps <= 8)
-      PDX_B_CHECK(chain1(bchain1_kernel<8>));
+      PDX_B_CHECK(rk ? chain1(bchain1_kernel<8, true>) : chain1(bchain1_kernel<8, false>));
     else if (P.nsteps <= 12)
-      PDX_B_CHECK(chain1(bchain1_kernel<12>));
+      PDX_B_CHECK(rk ? chain1(bchain1_kernel<12, true>) : chain1(bchain1_kernel<12, false>));
     else
-      PDX_B_CHECK(chain1(bchain1_kernel<kMaxSteps>));
+      PDX_B_CHECK(rk ? chain1(bchain1_kernel<kMaxSteps, true>)
+                     : chain1(bchain1_kernel<kMaxSteps, false>));
   }
   phase("phase1");
   PDX_B_CHECK(cudaStreamWaitEvent(st, side.join, 0));  // the work lists are ready
