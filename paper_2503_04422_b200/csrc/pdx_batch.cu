@@ -592,14 +592,16 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
   int64_t touched = 0, total = 0, tlen = 0;  // lane 0
   float T = INFINITY, Tb = -1.f, bl = 0.f;
+  float bs[NSM];  // B_s(T) of every step, in every lane
   // software pipeline: the next tile's partials, ids and size load while the
   // current tile is decided (one L2 round trip per tile, hidden)
   float u0[NSM], u1[NSM], n0[NSM], n1[NSM];
   int64_t id0 = 0, id1 = 0, nid0 = 0, nid1 = 0;
   int m = 0, nm = 0;
+  const float* __restrict__ pq = part1 + p1off[q] * nsteps * kTile;
   auto fetch = [&](int ti) {
     if (ti >= nt) return;
-    const float* __restrict__ pp = part1 + (p1off[q] + ti) * nsteps * kTile;
+    const float* __restrict__ pp = pq + (int64_t)ti * nsteps * kTile;
 #pragma unroll
     for (int s = 0; s < NSM; ++s) {
       n0[s] = s < nsteps ? __ldg(pp + s * kTile + lane) : 0.f;
@@ -639,6 +641,8 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
     } else {
       if (T != Tb) {  // the bounds move only with the threshold
         bl = lane < nsteps ? bound_at(P, T, lane, s_ratio, s_band) : 0.f;
+#pragma unroll
+        for (int s = 0; s < NSM; ++s) bs[s] = __shfl_sync(kFull, bl, s);
         Tb = T;
       }
       // per step independently: bit s = partial below B_s; a slot survives
@@ -647,7 +651,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
 #pragma unroll
       for (int s = 0; s < NSM; ++s) {
         if (s >= nsteps) break;
-        const float B = __shfl_sync(kFull, bl, s);
+        const float B = bs[s];
         ok0 |= (u0[s] < B ? 1u : 0u) << s;
         ok1 |= (u1[s] < B ? 1u : 0u) << s;
       }
