@@ -385,21 +385,30 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
                                                      const int32_t* __restrict__ seg0,
                                                      const int64_t* __restrict__ p1off,
                                                      float* __restrict__ part1,
-                                                     const float* __restrict__ b0bnd) {
+                                                     float* __restrict__ b0bnd) {
   extern __shared__ __align__(16) float s_q[];  // [d_pad] query, then [2][nsteps] BSA rq, sqrt
   __shared__ int32_t s_ends[kMaxSteps];
   __shared__ float s_coef[kMaxSteps];
+  __shared__ double s_ratio[FIRST ? kMaxSteps : 1], s_band[FIRST ? kMaxSteps : 1];
   const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
-  if (FIRST ? nt == 0 : (int)blockIdx.y * 4 + 1 >= min(nt, kP1Cap)) return;
+  if (FIRST && nt == 0) {  // no first block: T_0 = +inf
+    if (threadIdx.x < P.nsteps) b0bnd[(int64_t)q * P.nsteps + threadIdx.x] = INFINITY;
+    return;
+  }
+  if (!FIRST && (int)blockIdx.y * 4 + 1 >= min(nt, kP1Cap)) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
   for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
     s_ends[i] = P.ends[i];
     s_coef[i] = (BSA && i < nsteps) ? A.coef[i] : 0.f;
+    if (FIRST) {
+      s_ratio[i] = P.ratio[i];
+      s_band[i] = P.band[i];
+    }
   }
   __syncthreads();
   float* s_bq = s_q + P.d_pad;
@@ -487,48 +496,34 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
       }
     }
   }
+  if (FIRST) {
+    // T_0: the k-th smallest distance of the first block (the heap after the
+    // linear block, search.py:125-135), +inf below k vectors; b0bnd = B_s(T_0)
+    float T = INFINITY;
+    const int k = P.k;
+    if (m >= k) {
+      const float* fin = out + (nsteps - 1) * kTile;  // this lane's own writes
+      const float v0 = lane < m ? fin[lane] : INFINITY, v1 = lane + 32 < m ? fin[lane + 32] : INFINITY;
+      int l0 = 0, e0 = 0, l1 = 0, e1 = 0;  // values below / equal to mine
+      for (int j = 0; j < 32; ++j) {
+        const float a = __shfl_sync(kFull, v0, j), b = __shfl_sync(kFull, v1, j);
+        l0 += (a < v0) + (b < v0);
+        e0 += (a == v0) + (b == v0);
+        l1 += (a < v1) + (b < v1);
+        e1 += (a == v1) + (b == v1);
+      }
+      const bool h0 = l0 <= k - 1 && l0 + e0 >= k, h1 = l1 <= k - 1 && l1 + e1 >= k;
+      const unsigned hm = __ballot_sync(kFull, h0 || h1);
+      const int src = __ffs(hm) - 1;
+      T = __shfl_sync(kFull, h0 ? v0 : v1, src);
+    }
+    if (lane < nsteps)
+      b0bnd[(int64_t)q * nsteps + lane] =
+          T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
+  }
   }
 }
 
-// T_0 per query: the k-th smallest distance of its first block (the heap
-// after the linear block, search.py:125-135), +inf if that block has fewer
-// than k vectors; b0bnd = B_s(T_0).
-__global__ void bt0_kernel(const BParams P, const BArgs A, const int32_t* __restrict__ seg0,
-                           const int64_t* __restrict__ p1off, const float* __restrict__ part1,
-                           float* __restrict__ b0bnd) {
-  __shared__ double s_ratio[kMaxSteps], s_band[kMaxSteps];
-  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
-    s_ratio[i] = P.ratio[i];
-    s_band[i] = P.band[i];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (q >= P.nq) return;
-  const int c = seg0[q];
-  const int64_t b0 = A.bucket_block[c];
-  const int m = A.bucket_block[c + 1] > b0 ? A.block_m[b0] : 0;
-  float T = INFINITY;
-  if (m >= P.k) {
-    const float* fin = part1 + p1off[q] * P.nsteps * kTile + (P.nsteps - 1) * kTile;
-    const float v0 = lane < m ? fin[lane] : INFINITY, v1 = lane + 32 < m ? fin[lane + 32] : INFINITY;
-    int l0 = 0, e0 = 0, l1 = 0, e1 = 0;  // values below / equal to mine
-    for (int j = 0; j < 32; ++j) {
-      const float a = __shfl_sync(kFull, v0, j), b = __shfl_sync(kFull, v1, j);
-      l0 += (a < v0) + (b < v0);
-      e0 += (a == v0) + (b == v0);
-      l1 += (a < v1) + (b < v1);
-      e1 += (a == v1) + (b == v1);
-    }
-    const int k = P.k;
-    const bool h0 = l0 <= k - 1 && l0 + e0 >= k, h1 = l1 <= k - 1 && l1 + e1 >= k;
-    const unsigned hm = __ballot_sync(kFull, h0 || h1);
-    const int src = __ffs(hm) - 1;
-    T = __shfl_sync(kFull, h0 ? v0 : v1, src);
-  }
-  if (lane < P.nsteps)
-    b0bnd[(int64_t)q * P.nsteps + lane] = T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
-}
 
 // NSM >= nsteps: register arrays sized to the schedule.  RK (k <= 32): the
 // heap lives in registers, lane i holding the i-th smallest (dist, id).
@@ -1884,8 +1879,6 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
         bdense_kernel<true, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
       else
         bdense_kernel<false, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
-      PDX_B_CHECK(cudaGetLastError());
-      bt0_kernel<<<(nq + 7) / 8, 256, 0, st>>>(P, A, seg0, p1off, part1, b0bnd);
       PDX_B_CHECK(cudaGetLastError());
       if (p1max > 1) {
         if (bsa)
