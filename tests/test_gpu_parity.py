@@ -242,6 +242,24 @@ def test_select_buckets_vs_oracle(P, oracle):
                 np.testing.assert_array_equal(got[i], ref)
 
 
+@pytest.mark.parametrize("nlist", [1024, 700, 40])
+def test_select_buckets_warp_path_vs_oracle(P, oracle, nlist):
+    """nlist <= 1024, nprobe <= 32: the one-warp-per-query selection (lane
+    minima threshold, candidates ranked), incl. nprobe == nlist."""
+    x = recipes.data("mixture", 20_000, 32, 43)
+    col = P.VectorCollection.from_array(x)
+    index = P.ivf_build(col, nlist=nlist, seed=0)
+    Q = np.concatenate([recipes.queries("near", x, 96, 44), recipes.queries("skewed", x, 32, 45)])
+    view = _oracle_ivf(oracle, index, x)
+    for metric in ("l2", "ip", "l1"):
+        for nprobe in sorted({1, 7, 32, min(32, nlist)}):
+            got = P.index.select_buckets_device(index, P.store.to_device(Q), nprobe, metric)
+            got = got.cpu().numpy()
+            for i, q in enumerate(Q):
+                ref = oracle.select_buckets(view.cent, index.nlist, q, metric, nprobe)
+                np.testing.assert_array_equal(got[i], ref)
+
+
 def test_merge_topk_matches_host(P):
     import torch
     from paper_2503_04422_b200 import _lib
