@@ -8,13 +8,24 @@ seeded orthogonal projection, 1,024 k-means buckets, epsilon0 = 2.1, K = 10,
 extras).  Synthetic data of the paper-dataset shape (the real datasets are
 not in the container).  A step = one pass of the whole query batch through
 the search hot path: query projection (K3), bucket selection (K2), pruned
-PDX scan + top-k (K5/K6).
+PDX scan + top-k (the batched pipeline, csrc/pdx_batch.cu).
+
+The index is the REFERENCE's: ``tests/golden/c2_ivf_reference.npz`` holds
+the centroids and assignment that ``dimscan.index.lloyd_kmeans`` produced
+for this data (tools/make_c2_index.py, run once in the build container).
+Both arms pack it themselves — the GPU arm with K1
+(``IvfIndex.from_assignment``), the reference arm in numpy — so neither arm
+runs this repo's k-means and both search the identical index.
 
 Arms:
   default            our sm_100a path.  `value`: inputs resident in HBM;
-                     `e2e`: IvfNearestNeighbors.kneighbors on host arrays.
+                     `e2e`: one pdx_index_search call (C-ABI) per batch with
+                     page-locked host buffers.  `parity`: ids, distances,
+                     values_touched of all 1000 queries at nprobe 8/32/128
+                     against the C oracle on the same index and queries.
   --impl reference   the reference algorithm on the host CPU (the C oracle
-                     port of dimscan, all host threads), same index/queries.
+                     port of dimscan, all host threads), same index/queries;
+                     never loads libpdx_b200.so.
 Multi-GPU (torchrun): buckets are sharded over ranks (LPT by size), each
 rank scans its buckets of the globally selected probes, per-rank top-k are
 all-gathered over NCCL and merged on device (K7).
@@ -22,9 +33,10 @@ all-gathered over NCCL and merged on device (K7).
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
-import subprocess
+import platform
 import sys
 import threading
 import time
@@ -36,6 +48,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_DEFAULT, D, NCENT, NLIST, NQ, K, EPS = 1_000_000, 128, 1000, 1024, 1000, 10, 2.1
+FIXTURE = ROOT / "tests" / "golden" / "c2_ivf_reference.npz"
 
 
 def make_data(n, nq, seed=0):
@@ -50,9 +63,40 @@ def make_data(n, nq, seed=0):
     return X, Q
 
 
+def rotation(d, seed=0):
+    """generate_orthogonal (pruning.py:36-45): seeded Gaussian, QR, sign fix."""
+    g = np.random.default_rng(seed).standard_normal((d, d))
+    q, r = np.linalg.qr(g)
+    return (q * np.sign(np.diag(r))).astype(np.float32)
+
+
+def load_fixture(XR):
+    """(centroids, assignment, data fingerprint matches) of the reference
+    k-means index, or None when the fixture does not fit the data."""
+    if not FIXTURE.exists():
+        return None
+    f = np.load(FIXTURE)
+    if f["assign"].shape[0] != XR.shape[0]:
+        return None
+    same = hashlib.sha256(XR.tobytes()).digest() == f["xr_sha"].tobytes()
+    return f["centroids"], f["assign"].astype(np.int64), bool(same)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 class Clocks:
-    """SM clock and clock-event reasons sampled through NVML every 10 ms
-    during the timed region (the same counters nvidia-smi reports)."""
+    """SM clock and clock-event reasons sampled through NVML during the
+    timed region (the counters nvidia-smi reports).  NVML is initialised
+    before the region; one sample is taken synchronously at its start and
+    one at its end, and a thread samples every 2 ms in between."""
 
     REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
                "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -60,28 +104,36 @@ class Clocks:
                "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, gpu=0):
-        self.samples, self.gpu, self._stop = [], gpu, threading.Event()
-        self.max_mhz = None
-
-    def _run(self):
+        self.samples, self._stop = [], threading.Event()
+        self.max_mhz, self.h, self.N, self.err = None, None, None, None
         try:
             import pynvml as N
             N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-        except Exception:
+            self.N = N
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[0].isdigit() else gpu
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001 - reported in the line
+            self.err = repr(e)
+
+    def sample(self):
+        if self.h is None:
             return
-        while not self._stop.is_set():
-            try:
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, [n for n, a in self.REASONS.items()
-                                          if rs & getattr(N, a)]))
-            except Exception:
-                pass
-            self._stop.wait(0.01)
+        N = self.N
+        try:
+            sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+            rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.samples.append((sm, [n for n, a in self.REASONS.items() if rs & getattr(N, a)]))
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+
+    def _run(self):
+        while not self._stop.wait(0.002):
+            self.sample()
 
     def __enter__(self):
+        self.sample()
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
         return self
@@ -89,21 +141,23 @@ class Clocks:
     def __exit__(self, *a):
         self._stop.set()
         self.t.join(timeout=6)
+        self.sample()
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "error": self.err}
         sm = [s[0] for s in self.samples]
         reasons = sorted({r for s in self.samples for r in s[1]})
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML"}
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the scan kernel from the committed ncu
-    capture summary (profiles/ncu_scan.json, written by tools/ncu_summary.py)."""
+def ncu_profile():
+    """Per-kernel DRAM bytes / issue activity of one search from the
+    committed ncu capture (profiles/r02_kernels.json, tools/ncu_kernels.py)."""
     try:
-        return json.loads((ROOT / "profiles" / "ncu_scan.json").read_text())
+        return json.loads((ROOT / "profiles" / "r02_kernels.json").read_text())
     except Exception:
         return None
 
@@ -115,39 +169,58 @@ def dist_env():
     return ws, rank, local
 
 
-def build_index(X, nlist, seed=0):
-    import torch
-    import paper_2503_04422_b200 as P
-    T = P.generate_orthogonal(D, seed)
-    xr = P.apply_transform(T, P.store.to_device(X))
-    col = P.VectorCollection(data=np.empty((0, D), np.float32), ids=np.empty(0, np.int64))
-    # the collection's host copy is only needed for the oracle views
-    col = P.VectorCollection.from_array(xr.cpu().numpy())
-    t0 = time.perf_counter()
-    index = P.ivf_build(col, nlist=nlist, seed=seed, x_dev=xr)
-    torch.cuda.synchronize()
-    return T, col, index, time.perf_counter() - t0
-
-
-def cpu_oracle_qps(index, Qr, nprobe, budget_s=12.0, max_q=None, threads=None):
-    """The C oracle (dimscan restated) over a bounded prefix of the queries."""
+def oracle_qps(view, Qr, nprobe, budget_s, threads):
+    """The C oracle (dimscan restated) in passes over the queries until the
+    time budget is spent (one untimed warm query first, cli.py:171-172)."""
     from oracle import oracle as O
-    O.build()
-    view = O.IvfView(index.centroid_blocks, index.buckets, index.means_dev.cpu().numpy())
-    threads = threads or os.cpu_count() or 1
-    done, t_total, chunk = 0, 0.0, max(4 * threads, 64)
-    limit = Qr.shape[0] if max_q is None else min(max_q, Qr.shape[0])
-    # untimed warm query (cli.py:171-172)
     O.ivf_search_batch(view, Qr[:1], K, nprobe, pruner="ads", eps0=EPS, nthreads=1)
-    # passes over the query set (wrapping around) until the time budget is spent
+    done, t_total, chunk = 0, 0.0, max(4 * threads, 16)
     while t_total < budget_s:
-        s = done % limit
-        q = Qr[s:min(limit, s + chunk)]
+        s = done % Qr.shape[0]
+        q = Qr[s:min(Qr.shape[0], s + chunk)]
         t0 = time.perf_counter()
         O.ivf_search_batch(view, q, K, nprobe, pruner="ads", eps0=EPS, nthreads=threads)
         t_total += time.perf_counter() - t0
         done += q.shape[0]
-    return done / t_total, done, t_total, threads, view
+    return done / t_total, done, t_total
+
+
+def reference_arm(args, config):
+    """The reference algorithm (C oracle port of dimscan) on the host cores,
+    on the reference k-means index; no GPU code is loaded."""
+    from oracle import oracle as O
+    X, Q = make_data(args.n, args.nq)
+    T = rotation(D)
+    XR, QR = X @ T.T, Q @ T.T  # apply_transform (pruning.py:48-53)
+    fx = load_fixture(XR)
+    if fx is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no reference k-means fixture for n={args.n} (tools/make_c2_index.py)"}))
+        return
+    cent, assign, _ = fx
+    O.build()
+    view = O.IvfView.from_assignment(XR, cent, assign, NLIST)
+    threads = os.cpu_count() or 1
+    O.ivf_search_batch(view, QR[:1], K, args.nprobe, pruner="ads", eps0=EPS, nthreads=1)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.ivf_search_batch(view, QR, K, args.nprobe, pruner="ads", eps0=EPS, nthreads=threads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    qps = args.nq * len(times) / sum(times)
+    print(json.dumps({
+        "impl": "reference", "metric": "queries/sec at recall@10", "value": qps,
+        "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config,
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
+                         "sample": f"all {args.nq} queries per step, {args.steps} timed steps; "
+                                   "the reference's k-means index (fixture), packed in numpy"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}))
 
 
 def main():
@@ -161,8 +234,8 @@ def main():
     ap.add_argument("--nprobe", type=int, default=32)
     ap.add_argument("--warps", default="0", help="compute warps per query CTA, or W,tiles_per_warp")
     ap.add_argument("--no-extras", action="store_true")
-    ap.add_argument("--debug", action="store_true", help="print kernel diagnostics to stderr")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--batched", type=int, default=0,
                     help="pdx_search_params.batched: 0 auto, 1 per-query scan, 2 batched")
     args = ap.parse_args()
@@ -170,61 +243,49 @@ def main():
     args.warps = tuple(int(v) for v in str(args.warps).split(",")) if "," in str(args.warps) else int(args.warps)
 
     ws, rank, local = dist_env()
+    config = {"workload": f"ivf-ads N={args.n} D={D} nlist={NLIST} nprobe={args.nprobe} "
+                          f"nq={args.nq} K={K} eps0={EPS}",
+              "n": args.n, "d": D, "nlist": NLIST, "nprobe": args.nprobe, "queries": args.nq,
+              "k": K, "epsilon0": EPS, "pruner": "ads", "layout": "tiles [D/8][64][8] f32",
+              "index": "reference lloyd_kmeans (tests/golden/c2_ivf_reference.npz)",
+              "l2_flush": "256 MiB write between timed steps", "parallelism": f"buckets x{ws}"}
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, config)
+        return
+
     import torch
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    X, Q = make_data(args.n, args.nq)
-    config = {"workload": f"ivf-ads N={args.n} D={D} nlist={NLIST} nprobe={args.nprobe} "
-                          f"nq={args.nq} K={K} eps0={EPS}",
-              "n": args.n, "d": D, "nlist": NLIST, "nprobe": args.nprobe, "queries": args.nq,
-              "k": K, "epsilon0": EPS, "pruner": "ads", "layout": "tiles [D/8][64][8] f32",
-              "l2_flush": "256 MiB write between timed steps", "parallelism": f"buckets x{ws}"}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        import paper_2503_04422_b200 as P
-        T, col, index, _ = build_index(X, NLIST)
-        Qr = Q @ T.matrix.T
-        threads = os.cpu_count() or 1
-        from oracle import oracle as O
-        O.build()
-        view = O.IvfView(index.centroid_blocks, index.buckets, index.means_dev.cpu().numpy())
-        sample = min(args.nq, 100)
-        O.ivf_search_batch(view, Qr[:1], K, args.nprobe, pruner="ads", eps0=EPS, nthreads=1)
-        times = []
-        for s in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            O.ivf_search_batch(view, Qr[:sample], K, args.nprobe, pruner="ads", eps0=EPS,
-                               nthreads=threads)
-            if s >= args.warmup:
-                times.append(time.perf_counter() - t0)
-        qps = sample * len(times) / sum(times)
-        print(json.dumps({
-            "impl": "reference", "metric": "queries/sec at recall@10", "value": qps,
-            "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": config,
-            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
-                             "sample": f"first {sample} queries per step; index built once "
-                                       "(build not timed)"},
-            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}))
-        return
-
     import paper_2503_04422_b200 as P
     from paper_2503_04422_b200 import _lib
     _lib.lib()
     dev = torch.device("cuda", local)
-    T, col, index, build_s = build_index(X, NLIST)
+
+    X, Q = make_data(args.n, args.nq)
+    T = P.generate_orthogonal(D, 0)
+    XR = X @ T.matrix.T  # the index data: apply_transform on the host, as the reference
+    x_dev = P.store.to_device(XR)
+    col = P.VectorCollection.from_array(XR)
+    fx = load_fixture(XR)
+    t0 = time.perf_counter()
+    if fx is not None:
+        cent, assign, same = fx
+        index = P.IvfIndex.from_assignment(col, cent, assign, nlist=NLIST, x_dev=x_dev)
+        config["index_data_fingerprint_match"] = same
+    else:  # other sizes: this repo's GPU k-means (same algorithm, index.py:27-64)
+        index = P.ivf_build(col, nlist=NLIST, seed=0, x_dev=x_dev)
+        config["index"] = "GPU lloyd_kmeans (no reference fixture for this n)"
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
     if ws > 1:
         from paper_2503_04422_b200.sharded import shard_index
-        index = shard_index(index, col, rank, ws)
+        index = shard_index(index, col, rank, ws, x_dev=x_dev)
+    del x_dev
     params = P.SearchParams(k=K, pruner="ads", ads=P.AdsPruner(d=D, epsilon0=EPS))
     searcher = P.IvfSearcher(index, params, args.nprobe, warps=args.warps, batched=args.batched)
     Qd = P.store.to_device(Q)
@@ -247,25 +308,12 @@ def main():
     touched = int(st_res.touched.sum().item())
     total = int(st_res.total.sum().item())
     alg_bytes = 4 * touched
-    if args.debug:
-        dbg = torch.zeros((args.nq, 16), dtype=torch.int64, device=dev)
-        searcher._buf["debug_buf"] = dbg
-        searcher.run(Qr_dev)
-        torch.cuda.synchronize()
-        del searcher._buf["debug_buf"]
-        d = dbg.cpu().numpy().astype(np.float64)
-        names = ["cycles", "tiles", "fast", "serial", "replay", "commit_idle", "ring_waits",
-                 "sparse_items", "cw_wait", "cw_dense", "cw_sparse", "cw_rest", "commit_busy"]
-        print("DEBUG per-query mean:", {n: round(float(d[:, i].mean()), 1)
-                                        for i, n in enumerate(names)},
-              "max cycles", int(d[:, 0].max()), file=sys.stderr)
 
     for _ in range(args.warmup):
         step(Qd)
     torch.cuda.synchronize()
     if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+        torch.distributed.barrier()
     # One GPU: the step as two CUDA graphs (fixed device buffers, inputs
     # resident) — projection + bucket selection, then the search — so the
     # ~30 launches of a step leave no host gaps; events between the replays
@@ -320,11 +368,29 @@ def main():
     t_step = float(np.mean(step_ms))
     t_scan = float(np.mean(scan_ms))
     if ws > 1:
-        import torch.distributed as dist
         tt = torch.tensor([t_step, t_scan], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_step, t_scan = float(tt[0]), float(tt[1])
     qps = args.nq / (t_step / 1e3)
+
+    # live per-phase device time of the search (CUDA events on the search
+    # stream inside the library; same L2 flush; direct launches)
+    phase_names = ["plan", "phase1_bdense_bchain1", "tprime_join", "bscan_mode0", "chain",
+                   "bscan_mode1", "final", "fallback"]
+    phases = None
+    if ws == 1:
+        import ctypes as C
+        L = _lib.lib()
+        L.pdx_batch_profile(1, None, 0, None)
+        for _ in range(20):
+            flush.fill_(1)
+            searcher.run(Qr_dev)
+        torch.cuda.synchronize()
+        acc = (C.c_double * 8)()
+        calls = C.c_int64()
+        L.pdx_batch_profile(0, C.cast(acc, C.c_void_p), 8, C.cast(C.pointer(calls), C.c_void_p))
+        if calls.value:
+            phases = {n: acc[i] / calls.value for i, n in enumerate(phase_names)}
 
     # e2e through the C-ABI handle with HOST buffers: one pdx_index_search
     # call per batch (H2D of the queries, projection, selection, scan, D2H
@@ -362,8 +428,7 @@ def main():
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_mean = float(tt[0])
     e2e_qps = args.nq / (e2e_mean / 1e3)
-    # results for recall: the e2e call's output (merged over ranks when sharded)
-    i_h = hout["ids"].numpy()
+    i_h = hout["ids"].numpy().copy()
 
     if rank != 0:
         if ws > 1:
@@ -372,98 +437,186 @@ def main():
     # recall@10 against float64 brute force on the unrotated data
     gt = P.compute_ground_truth(P.VectorCollection.from_array(X), Q, K)
     recall = float(np.mean([P.recall_at_k(gt.ids[i], i_h[i], K) for i in range(args.nq)]))
-    peak = 6556.2
+    peaks = {}
     try:
-        peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
-        peak_src = "measured"
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        peak, peak_src = peaks["hbm_gbs"], "measured"
     except Exception:
-        peak_src = "fallback"
-    achieved = alg_bytes / (t_scan / 1e3) / 1e9
-    prof = ncu_traffic()
-    traffic = None
-    if prof and prof.get("workload") == config["workload"]:
-        traffic = prof.get("dram_bytes_per_search")
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    prof = ncu_profile()
+    if prof and prof.get("workload") != config["workload"]:
+        prof = None
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # FADD/FMUL lane ops per s (no FMA: 1 op)
+    fp32_ops = 3.0 * touched  # sub, mul, add per value touched (search.py:132, :169)
+    kernels = []
+    if prof:
+        live = {"bscan_mode0": "bscan_mode0", "bscan_mode1": "bscan_mode1",
+                "bdense": "phase1_bdense_bchain1", "bchain1": "phase1_bdense_bchain1"}
+        for kk in prof.get("kernels", []):
+            e = dict(kk)
+            ph = live.get(kk.get("role", ""))
+            if phases and ph and kk.get("role") in ("bscan_mode0", "bscan_mode1"):
+                e["live_ms"] = phases[ph]
+                e["dram_gbs_live"] = kk["dram_bytes"] / (phases[ph] / 1e3) / 1e9
+                e["dram_frac_live"] = e["dram_gbs_live"] / peak
+            kernels.append(e)
+    dram = (prof or {}).get("dram_bytes_per_search")
     line = {
         "metric": "queries/sec at recall@10", "value": qps, "unit": "queries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Gaussian mixture, BASELINE configs[1] recipe)",
         "config": config, "recall_at_10": recall,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic,
-                     "traffic_source": (prof or {}).get("source"),
-                     "kernel": "pdx_search (batched pipeline, pdx_batch.cu); achieved = "
-                               "algorithmic bytes / the whole search call",
-                     "dominant_kernel": (prof or {}).get("dominant_kernel"),
-                     "dominant_time_share_ncu": (prof or {}).get("dominant_time_share"),
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "full_scan_bytes_per_launch": 4 * total,
-                     "pruning_power": 1 - touched / total, "scan_ms": t_scan},
+        "roofline": {
+            "bound": "issue",
+            "achieved": fp32_ops / (t_scan / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": fp32_ops / (t_scan / 1e3) / 1e12 / fp32_peak,
+            "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FADD/FMUL, computed)",
+            "what": "the whole search (25 launches, pdx_batch.cu): 3 FP32 ops per value touched "
+                    "(the reference's values_touched) / search time; the pipeline is "
+                    "instruction-issue bound (decisions + bookkeeping), not HBM- or tensor-bound",
+            "traffic": dram, "traffic_source": (prof or {}).get("source"),
+            "algorithmic_bytes_per_launch": alg_bytes, "full_scan_bytes_per_launch": 4 * total,
+            "pruning_power": 1 - touched / total, "scan_ms": t_scan,
+            "hbm": {"peak_gbs": peak, "peak_source": peak_src,
+                    "bytes_touched_gbs": alg_bytes / (t_scan / 1e3) / 1e9,
+                    "bytes_touched_frac": alg_bytes / (t_scan / 1e3) / 1e9 / peak,
+                    "bytes_touched_note": "north_star's 'bytes touched / time': a tile is read "
+                                          "once per work item and shared by ~31 queries, so this "
+                                          "is not DRAM traffic",
+                    "dram_gbs": dram / (t_scan / 1e3) / 1e9 if dram else None,
+                    "dram_frac": dram / (t_scan / 1e3) / 1e9 / peak if dram else None},
+            "phases_ms_live": phases,
+            "kernels": kernels,
+            "dominant_kernel": (prof or {}).get("dominant_kernel")},
         "e2e": {"value": e2e_qps, "unit": "queries/s",
                 "h2d_bytes_per_step": int(Q.nbytes),
                 "d2h_bytes_per_step": int(args.nq * K * (4 + 8)),
                 "path": ("pdx_index_search (C-ABI handle, pinned host buffers)" if ws == 1 else
                          "pinned host queries -> sharded scan -> NCCL gather + merge -> host")},
         # per step: the projection + every launch of one search (ncu launch list)
-        "gpu_launches": (1 + int((prof or {}).get("launches_per_search") or 0)) * args.steps,
-        "index_build_s": build_s,
+        "gpu_launches": (1 + int((prof or {}).get("launches_per_search") or 25)) * args.steps,
+        "index_pack_s": build_s,
     }
     line["clocks"] = clk.summary()
+    view = None
+    if ws == 1:  # the oracle's view of the very index the GPU searched
+        from oracle import oracle as O
+        O.build()
+        view = O.IvfView.from_assignment(index._host_data, index.centroids, index_assign(index),
+                                         index.nlist)
+    if ws == 1 and not args.no_parity:
+        line["parity"] = parity_block(P, view, index, params, Qr_dev, args, i_h)
     if not args.no_extras:
-        extras = {}
-        for npb in (8, 128):
-            s2 = P.IvfSearcher(index, params, npb, warps=args.warps)
-            for _ in range(3):
-                s2.run(Qr_dev)
-            torch.cuda.synchronize()
-            ts = []
-            for _ in range(9):
-                flush.fill_(1)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                r2 = s2.run(Qr_dev)
-                e1.record()
-                torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1))
-            ids2 = r2.ids.cpu().numpy()
-            rec2 = float(np.mean([P.recall_at_k(gt.ids[i], ids2[i], K) for i in range(args.nq)]))
-            extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": rec2,
-                                       "timing": "median of 9 L2-flushed searches"}
-        # BSA (this build's restatement) on the same data and nprobe
-        est = P.IvfNearestNeighbors(pruner="bsa", nlist=NLIST, nprobe=args.nprobe, seed=0).fit(X)
-        sb = est.searcher(K)
-        Qb = P.apply_transform(est.transform_, Qd)
-        rs = sb.run(Qb, stats=True)
-        pp_b = 1 - int(rs.touched.sum().item()) / int(rs.total.sum().item())
+        line["extras"] = extras_block(P, index, params, Qr_dev, Qd, X, args, gt, flush)
+    if ws == 1:
+        Qh = Qr_dev.cpu().numpy()
+        threads = os.cpu_count() or 1
+        cq, done, secs = oracle_qps(view, Qh, args.nprobe, args.cpu_budget, threads)
+        c1, done1, secs1 = oracle_qps(view, Qh, args.nprobe, args.cpu_budget / 2, 1)
+        line["cpu_baseline"] = {
+            "value": cq, "unit": "queries/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"{done} query searches ({secs:.1f} s) in passes over the {args.nq} "
+                      "queries of the same workload and index; C oracle of the reference, one "
+                      "query per host thread",
+            "single_thread": {"value": c1, "cores": 1,
+                              "sample": f"{done1} query searches ({secs1:.1f} s), 1 thread "
+                                        "(the reference's single-threaded semantics)"}}
+    print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.barrier()
+
+
+def index_assign(index):
+    """Row -> bucket of a GPU-built index (for the oracle view)."""
+    a = np.empty(int(np.sum(index._counts)), dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(index._counts)])
+    for c in range(index.nlist):
+        a[index._order[off[c]:off[c + 1]]] = c
+    return a
+
+
+def parity_block(P, view, index, params, Qr_dev, args, i_h):
+    """Headline-config parity: ids, f32 distances and values_touched of all
+    queries against the C oracle on the same index and the same (device-
+    projected) queries, at nprobe 8 / 32 / 128; plus the e2e call's output
+    against the device path."""
+    import torch
+    from oracle import oracle as O
+    Qh = Qr_dev.cpu().numpy()
+    out = {"queries": int(Qh.shape[0]), "reference": "C oracle (oracle/pdx_oracle.c), pinned "
+                                                       "to the reference by tests/golden"}
+    ok = True
+    for npb in (8, 32, 128):
+        s = P.IvfSearcher(index, params, npb)
+        r = s.run(Qr_dev, stats=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ref = O.ivf_search_batch(view, Qh, K, npb, pruner="ads", eps0=EPS,
+                                 nthreads=os.cpu_count() or 1)
+        e = {"ids_equal": bool(np.array_equal(r.ids.cpu().numpy(), ref["ids"])),
+             "dist_equal": bool(np.array_equal(r.dist.cpu().numpy(), ref["dist"])),
+             "touched_equal": bool(np.array_equal(r.touched.cpu().numpy(), ref["touched"])),
+             "total_equal": bool(np.array_equal(r.total.cpu().numpy(), ref["total"])),
+             "selection_equal": bool(np.array_equal(r.selected.cpu().numpy(), ref["selected"])),
+             "oracle_s": round(time.perf_counter() - t0, 2)}
+        e["queries_differing"] = int(np.sum(np.any(r.ids.cpu().numpy() != ref["ids"], axis=1)))
+        ok = ok and e["ids_equal"] and e["dist_equal"] and e["touched_equal"]
+        out[f"nprobe_{npb}"] = e
+        if npb == args.nprobe:  # the e2e handle's answer (host rotation path) vs device path
+            out["e2e_ids_equal_device"] = bool(np.array_equal(i_h, r.ids.cpu().numpy()))
+    out["ids_equal"] = out["dist_equal"] = out["touched_equal"] = ok
+    return out
+
+
+def extras_block(P, index, params, Qr_dev, Qd, X, args, gt, flush):
+    import torch
+    extras = {}
+    for npb in (8, 128):
+        s2 = P.IvfSearcher(index, params, npb, warps=args.warps)
         for _ in range(3):
-            sb.run(Qb)
+            s2.run(Qr_dev)
         torch.cuda.synchronize()
         ts = []
         for _ in range(9):
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            rb = sb.run(Qb)
+            r2 = s2.run(Qr_dev)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
-        idsb = rb.ids.cpu().numpy()
-        recb = float(np.mean([P.recall_at_k(gt.ids[i], idsb[i], K) for i in range(args.nq)]))
-        extras[f"bsa_nprobe_{args.nprobe}"] = {
-            "qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": recb,
-            "pruning_power": pp_b, "coef": [round(c, 4) for c in est.bsa_.coef]}
-        line["extras"] = extras
-    if ws == 1:
-        cq, done, secs, threads, _ = cpu_oracle_qps(index, Qr_dev.cpu().numpy(), args.nprobe,
-                                                    budget_s=args.cpu_budget)
-        line["cpu_baseline"] = {"value": cq, "unit": "queries/s", "cores": threads, "kind": "port",
-                                "sample": f"{done} query searches ({secs:.1f} s wall; passes over "
-                                          f"the {args.nq} queries) of the same workload and "
-                                          "index, C oracle of the reference, one query per "
-                                          "host thread"}
-    print(json.dumps(line))
-    if ws > 1:
-        torch.distributed.barrier()
+        ids2 = r2.ids.cpu().numpy()
+        rec2 = float(np.mean([P.recall_at_k(gt.ids[i], ids2[i], K) for i in range(args.nq)]))
+        extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": rec2,
+                                   "timing": "median of 9 L2-flushed searches"}
+    # BSA (this build's restatement, DESIGN.md §3.1) on the same data and nprobe
+    est = P.IvfNearestNeighbors(pruner="bsa", nlist=NLIST, nprobe=args.nprobe, seed=0).fit(X)
+    sb = est.searcher(K)
+    Qb = P.apply_transform(est.transform_, Qd)
+    rs = sb.run(Qb, stats=True)
+    pp_b = 1 - int(rs.touched.sum().item()) / int(rs.total.sum().item())
+    for _ in range(3):
+        sb.run(Qb)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(9):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rb = sb.run(Qb)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    idsb = rb.ids.cpu().numpy()
+    recb = float(np.mean([P.recall_at_k(gt.ids[i], idsb[i], K) for i in range(args.nq)]))
+    extras[f"bsa_nprobe_{args.nprobe}"] = {
+        "qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": recb,
+        "pruning_power": pp_b, "coef": [round(c, 4) for c in est.bsa_.coef],
+        "index": "GPU k-means of this repo (BSA needs its PCA-space index)"}
+    return extras
 
 
 if __name__ == "__main__":

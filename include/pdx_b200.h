@@ -250,6 +250,34 @@ int pdx_search(const pdx_store* store, const pdx_search_params* params, const fl
                void* d_work, int64_t work_bytes, void* stream);
 
 /*
+ * The vertical kernels as standalone ops: vertical_accumulate
+ * (kernels.py:41-62; d_positions NULL: every one of the mp slots) and
+ * vertical_accumulate_selected (kernels.py:65-91; the npos listed slots,
+ * distinct, others untouched).  d_block f32 [d][mp] (a Block's data),
+ * d_query f32 [d], dims [a, b) of the natural order or of d_order (int64
+ * permutation of 0..d-1), d_acc f32 [mp] updated in place, each op rounded
+ * separately (no FMA), in visit order.  The search kernels fuse the same
+ * arithmetic (pdx_search).
+ */
+int pdx_vertical_accumulate(const float* d_block, int32_t d, int32_t mp, const float* d_query,
+                            int32_t a, int32_t b, const int64_t* d_order,
+                            const int64_t* d_positions, int32_t npos, int32_t metric,
+                            float* d_acc, void* stream);
+
+/*
+ * Phase timing of the batched IVF pipeline (pdx_search with per-query bucket
+ * selections): with enable = 1 every later batched call records CUDA events
+ * on its stream at the phase boundaries (not while the stream is being
+ * captured), waits for them at its end and accumulates the device time per
+ * phase: [0] plan, [1] phase 1 (bdense + bchain1), [2] T' (incl. the join of
+ * the work-list stream), [3] bscan MODE 0, [4] chain, [5] bscan MODE 1,
+ * [6] final, [7] fallback.  Copies up to cap accumulated values (ms) to
+ * out_ms and the call count to out_calls (either may be NULL); enable >= 0
+ * then resets the accumulators and sets the mode, enable < 0 only reads.
+ */
+int pdx_batch_profile(int32_t enable, double* out_ms, int32_t cap, int64_t* out_calls);
+
+/*
  * K7 — merge of per-shard top-k lists (multi-GPU; no reference counterpart:
  * the reference is single-process).  d_dist/d_ids: [nparts][nq][k] sorted
  * lists (+inf/-1 padded) → the k smallest (dist, id) pairs per query, the

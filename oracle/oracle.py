@@ -129,6 +129,45 @@ class BlockList:
                          _p(self.mp), _p(self.ids), _p(self.id_off))
 
 
+class PackedBlocks:
+    """A packed block sequence built straight from arrays (no per-block
+    objects): ``data`` float32 [nblocks][d][mp] (dimension-major, padding
+    slots zero), ``m`` int [nblocks], ``ids`` int64 [sum(m)] in block order."""
+
+    def __init__(self, data, m, ids):
+        data = np.ascontiguousarray(data, dtype=np.float32)
+        nb, d, mp = data.shape
+        self.d, self.nblocks = int(d), int(nb)
+        self.data = data.reshape(-1) if nb else np.zeros(1, np.float32)
+        self.m = np.ascontiguousarray(m, dtype=np.int32) if nb else np.zeros(1, np.int32)
+        self.mp = np.full(max(1, nb), mp, dtype=np.int32)
+        self.data_off = np.arange(max(1, nb), dtype=np.int64) * (d * mp)
+        self.id_off = np.zeros(max(1, nb), dtype=np.int64)
+        if nb:
+            self.id_off[1:] = np.cumsum(self.m.astype(np.int64))[:-1]
+        self.ids = np.ascontiguousarray(ids, dtype=np.int64) if nb else np.zeros(1, np.int64)
+        self.c = _Blocks(self.d, self.nblocks, _p(self.data), _p(self.data_off), _p(self.m),
+                         _p(self.mp), _p(self.ids), _p(self.id_off))
+
+
+def pack_rows(x, rows, block_size=64):
+    """to_blocks (layout.py:93-110) of x[rows] in numpy: consecutive
+    block_size-row chunks, transposed to [d][block_size], zero padded.
+    Returns (data [nb][d][bs], m [nb], ids = rows)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    n, d = rows.shape[0], x.shape[1]
+    nb = (n + block_size - 1) // block_size
+    src = np.full(nb * block_size, -1, dtype=np.int64)
+    src[:n] = rows
+    g = x[np.maximum(src, 0)].astype(np.float32, copy=True)
+    g[src < 0] = 0.0
+    data = np.ascontiguousarray(g.reshape(nb, block_size, d).transpose(0, 2, 1))
+    m = np.full(nb, block_size, dtype=np.int32)
+    if nb and n % block_size:
+        m[-1] = n % block_size
+    return data, m, rows
+
+
 def _params(k, metric, pruner, selection_fraction, initial_step, ads_d, eps0, bsa_coef=None):
     beta = None
     if str(pruner) == "bsa":
@@ -261,6 +300,48 @@ class IvfView:
         self.nlist = len(bucket_chains)
         self.c = _Ivf(self.nlist, 0, C.addressof(self.cent.c), C.addressof(self.buckets.c),
                       _p(self.bucket_off), _p(self.means))
+
+
+    @classmethod
+    def from_assignment(cls, x, centroids, assign, nlist=None, block_size=64):
+        """The reference's ivf_build packing (index.py:98-108) of given
+        centroids and assignments, in numpy: members of each bucket in
+        ascending row order, block_size blocks, float64 means
+        (layout.py:126-138; an empty bucket takes its centroid)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        centroids = np.ascontiguousarray(centroids, dtype=np.float32)
+        nlist = centroids.shape[0] if nlist is None else int(nlist)
+        assign = np.asarray(assign, dtype=np.int64)
+        order = np.argsort(assign, kind="stable")
+        counts = np.bincount(assign, minlength=nlist)
+        off = np.concatenate([[0], np.cumsum(counts)])
+        nblk = (counts + block_size - 1) // block_size
+        # per-slot source row of every bucket's chain, back to back
+        slot = np.full(int(nblk.sum()) * block_size, -1, dtype=np.int64)
+        boff = np.concatenate([[0], np.cumsum(nblk)]) * block_size
+        for c in np.flatnonzero(counts):
+            slot[boff[c]:boff[c] + counts[c]] = order[off[c]:off[c + 1]]
+        nb = int(nblk.sum())
+        g = x[np.maximum(slot, 0)]
+        g[slot < 0] = 0.0
+        data = g.reshape(nb, block_size, x.shape[1]).transpose(0, 2, 1)
+        m = np.full(nb, block_size, dtype=np.int32)
+        last = boff[1:] // block_size - 1
+        rem = counts % block_size
+        m[last[(counts > 0) & (rem > 0)]] = rem[(counts > 0) & (rem > 0)]
+        means = centroids.astype(np.float64).copy()
+        for c in np.flatnonzero(counts):
+            means[c] = x[order[off[c]:off[c + 1]]].astype(np.float64).sum(axis=0) / counts[c]
+        self = cls.__new__(cls)
+        cd, cm, cids = pack_rows(centroids, np.arange(nlist), block_size)
+        self.cent = PackedBlocks(cd, cm, cids)
+        self.buckets = PackedBlocks(data, m, order)
+        self.bucket_off = np.concatenate([[0], np.cumsum(nblk)]).astype(np.int64)
+        self.means = np.ascontiguousarray(means)
+        self.nlist = nlist
+        self.c = _Ivf(self.nlist, 0, C.addressof(self.cent.c), C.addressof(self.buckets.c),
+                      _p(self.bucket_off), _p(self.means))
+        return self
 
 
 def _batch(nq, k, nprobe, surv_cap):

@@ -27,7 +27,8 @@ EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_til
            "pdx_search", "pdx_merge_topk", "pdx_segment_means", "pdx_ground_truth",
            "pdx_bsa_residuals", "pdx_file_probe", "pdx_file_load", "pdx_file_save",
            "pdx_index_create", "pdx_index_open", "pdx_index_destroy", "pdx_index_search",
-           "pdx_k8_norms", "pdx_k8_margin", "pdx_k8_filter", "pdx_k8_rescore")
+           "pdx_k8_norms", "pdx_k8_margin", "pdx_k8_filter", "pdx_k8_rescore",
+           "pdx_vertical_accumulate", "pdx_batch_profile")
 
 
 class PdxStore(C.Structure):
@@ -134,6 +135,9 @@ def lib():
         L.pdx_file_load.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.pdx_file_save.argtypes = [C.c_char_p, vp, i32, vp, vp, vp, C.c_uint64, i32,
                                     C.c_uint64, vp, vp, vp, vp]
+        L.pdx_vertical_accumulate.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp,
+                                              vp]
+        L.pdx_batch_profile.argtypes = [i32, vp, i32, vp]
         for name in EXPORTS:
             getattr(L, name).restype = getattr(L, name).restype or C.c_int
         if L.pdx_abi_version() != 3:

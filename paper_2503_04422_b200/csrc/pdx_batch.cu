@@ -1614,6 +1614,31 @@ SideStream& side_stream() {
   return ss;
 }
 
+// Phase timing of the batched pipeline (pdx_batch_profile): plan, phase 1,
+// T', MODE 0, chain, MODE 1, final, fallback.
+struct BatchProfile {
+  static constexpr int kEv = 9;
+  bool enabled = false;
+  cudaEvent_t ev[kEv] = {};
+  double ms[kEv] = {};
+  int64_t calls = 0;
+};
+BatchProfile& batch_profile() {
+  static BatchProfile p;
+  return p;
+}
+
+// Device scratch one batched call may take (PDX_BATCH_SCRATCH_MB overrides;
+// default 4 GiB, well inside 180 GB next to the largest store).
+int64_t batch_scratch_budget() {
+  static const int64_t b = [] {
+    const char* e = getenv("PDX_BATCH_SCRATCH_MB");
+    const long long mb = e ? atoll(e) : 0;
+    return mb > 0 ? (int64_t)mb << 20 : (int64_t)4 << 30;
+  }();
+  return b;
+}
+
 template <typename T>
 T* carve(unsigned char*& at, int64_t count) {
   T* p = reinterpret_cast<T*>(at);
@@ -1725,6 +1750,25 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     carve<unsigned char>(at, (int64_t)cubb + 16);
     bytes = at - z;
   }
+  // Scratch grows linearly with the batch (part1 alone is nq x 64 tiles x
+  // nsteps x 64 floats): a batch whose scratch exceeds the budget is answered
+  // as two halves, each its own pipeline over the same store (results are
+  // per query, so the split is invisible).  Traces index one flat buffer per
+  // call and are not split.
+  if (bytes > batch_scratch_budget() && nq64 >= 64 && !trace) {
+    const int64_t h = nq64 / 2;
+    pdx_search_out lo = *out, hi = *out;
+    hi.d_dist = out->d_dist + h * k;
+    hi.d_ids = out->d_ids + h * k;
+    if (out->d_count) hi.d_count = out->d_count + h;
+    if (out->d_touched) hi.d_touched = out->d_touched + h;
+    if (out->d_total) hi.d_total = out->d_total + h;
+    const int r0 = search_batched(store, prm, d_queries, h, d_seg_bucket, nseg, &lo, d_work,
+                                  work_bytes, stream);
+    if (r0 != PDX_OK) return r0;
+    return search_batched(store, prm, d_queries + h * store->d, nq64 - h,
+                          d_seg_bucket + h * nseg, nseg, &hi, d_work, work_bytes, stream);
+  }
   unsigned char* base = nullptr;
   PDX_CUDA_CHECK(cudaMallocAsync(&base, bytes, st));
   unsigned char* at = base;
@@ -1760,12 +1804,26 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
 
   int rc = PDX_OK;
   const bool dbg_sync = getenv("PDX_BATCH_SYNC") != nullptr;
+  // live phase timing (pdx_batch_profile): events on the main stream at
+  // each phase boundary; not while the stream is being captured
+  BatchProfile& prof = batch_profile();
+  cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap_st);
+  const bool timing = prof.enabled && cap_st == cudaStreamCaptureStatusNone;
+  int nev = 0;
+  if (timing) cudaEventRecord(prof.ev[nev++], st);
   auto phase = [&](const char* name) {
+    if (timing && nev < BatchProfile::kEv) cudaEventRecord(prof.ev[nev++], st);
     if (!dbg_sync) return;
     const cudaError_t e = cudaStreamSynchronize(st);
     fprintf(stderr, "[pdx batched] %s done: %s\n", name, cudaGetErrorString(e));
   };
+  // after the fork the side stream may still write into base: join it
+  // before the free
+  SideStream* forked = nullptr;
   auto fail = [&](int r) {
+    if (forked && cudaEventRecord(forked->join, forked->s) == cudaSuccess)
+      cudaStreamWaitEvent(st, forked->join, 0);
     cudaFreeAsync(base, st);
     return r;
   };
@@ -1797,6 +1855,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   cudaStream_t st2 = side.s;
   PDX_B_CHECK(cudaEventRecord(side.fork, st));
   PDX_B_CHECK(cudaStreamWaitEvent(st2, side.fork, 0));
+  forked = &side;
   cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st2));
   cb = cubb;
@@ -1909,6 +1968,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   }
   phase("phase1");
   PDX_B_CHECK(cudaStreamWaitEvent(st, side.join, 0));  // the work lists are ready
+  forked = nullptr;
   btprime_kernel<<<(nq + 127) / 128, 128, 0, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("tprime");
@@ -1999,8 +2059,34 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     fprintf(stderr, "[pdx batched] nq=%d items=%d fallback=%d\n", nq, h[0], nf);
   }
   PDX_B_CHECK(cudaFreeAsync(base, st));
+  if (timing) {
+    PDX_CUDA_CHECK(cudaEventSynchronize(prof.ev[nev - 1]));
+    for (int i = 1; i < nev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prof.ev[i - 1], prof.ev[i]);
+      prof.ms[i - 1] += ms;
+    }
+    prof.calls += 1;
+  }
   return PDX_OK;
 #undef PDX_B_CHECK
 }
 
 }  // namespace pdx
+
+// Accumulated per-phase device time of batched searches since the last
+// enable (CUDA events on the search stream; see include/pdx_b200.h).
+extern "C" int pdx_batch_profile(int32_t enable, double* out_ms, int32_t cap, int64_t* out_calls) {
+  pdx::BatchProfile& p = pdx::batch_profile();
+  if (out_ms)
+    for (int i = 0; i < cap && i < pdx::BatchProfile::kEv - 1; ++i) out_ms[i] = p.ms[i];
+  if (out_calls) *out_calls = p.calls;
+  if (enable >= 0) {
+    if (enable && !p.ev[0])
+      for (auto& e : p.ev) PDX_CUDA_CHECK(cudaEventCreate(&e));
+    p.enabled = enable != 0;
+    for (double& v : p.ms) v = 0.0;
+    p.calls = 0;
+  }
+  return PDX_OK;
+}

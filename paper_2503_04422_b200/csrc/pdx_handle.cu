@@ -9,6 +9,7 @@
 // pays one C call per batch.
 #include <cublas_v2.h>
 
+#include <atomic>
 #include <cmath>
 #include <vector>
 
@@ -17,6 +18,12 @@
 
 namespace pdx {
 namespace {
+
+// Bumped whenever any handle buffer is (re)allocated.  A captured search
+// graph holds raw device pointers, so its key records the generation it was
+// captured at: a reallocation in between makes the key miss (no replay on
+// freed memory).
+std::atomic<uint64_t> g_buf_generation{1};
 
 template <typename T>
 struct DevBuf {
@@ -27,6 +34,7 @@ struct DevBuf {
   }
   int need(size_t count) {
     if (count <= n) return PDX_OK;
+    g_buf_generation.fetch_add(1, std::memory_order_relaxed);
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -101,6 +109,7 @@ struct pdx_index {
     const void* outs[4];
     int64_t nq;
     void* stream;
+    uint64_t generation;  // g_buf_generation when captured
     pdx_query_params prm;
   };
   GraphKey gkey{}, gseen{};
@@ -555,6 +564,7 @@ extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const f
     key.outs[3] = out_total;
     key.nq = nq;
     key.stream = stream;
+    key.generation = g_buf_generation.load(std::memory_order_relaxed);
     key.prm = *P;
     if (!I->gs) {
       PDX_CUDA_CHECK(cudaStreamCreateWithFlags(&I->gs, cudaStreamNonBlocking));

@@ -387,6 +387,51 @@ extern "C" int pdx_project(const float* d_x, int64_t n, int32_t d, const float* 
   return PDX_OK;
 }
 
+// The reference's vertical kernels as a standalone op (kernels.py:41-91):
+// one thread per slot (or per listed position), dims [a, b) of the natural
+// order or of d_order, each float32 op rounded on its own.
+template <int METRIC>
+__global__ void __launch_bounds__(128) vacc_kernel(const float* __restrict__ block, int mp,
+                                                   const float* __restrict__ q, int a, int b,
+                                                   const int64_t* __restrict__ order,
+                                                   const int64_t* __restrict__ pos, int npos,
+                                                   float* __restrict__ acc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npos) return;
+  const int64_t slot = pos ? pos[t] : t;
+  float v = acc[slot];
+  for (int i = a; i < b; ++i) {
+    const int64_t j = order ? order[i] : i;
+    v = upd<METRIC>(v, q[j], block[j * mp + slot]);
+  }
+  acc[slot] = v;
+}
+
+extern "C" int pdx_vertical_accumulate(const float* d_block, int32_t d, int32_t mp,
+                                       const float* d_query, int32_t a, int32_t b,
+                                       const int64_t* d_order, const int64_t* d_positions,
+                                       int32_t npos, int32_t metric, float* d_acc, void* stream) {
+  PDX_REQUIRE(d >= 1 && mp >= 0, "bad block shape");
+  PDX_REQUIRE(0 <= a && a <= b && b <= d, "dimension range [%d, %d) out of bounds for d=%d", a, b,
+              d);
+  PDX_REQUIRE(metric >= 0 && metric <= 2, "unknown metric %d", metric);
+  const int n = d_positions ? npos : mp;
+  if (n <= 0 || a == b) return PDX_OK;
+  cudaStream_t st = as_stream(stream);
+  const unsigned g = (unsigned)((n + 127) / 128);
+  if (metric == PDX_METRIC_L2)
+    vacc_kernel<PDX_METRIC_L2><<<g, 128, 0, st>>>(d_block, mp, d_query, a, b, d_order, d_positions,
+                                                  n, d_acc);
+  else if (metric == PDX_METRIC_L1)
+    vacc_kernel<PDX_METRIC_L1><<<g, 128, 0, st>>>(d_block, mp, d_query, a, b, d_order, d_positions,
+                                                  n, d_acc);
+  else
+    vacc_kernel<PDX_METRIC_IP><<<g, 128, 0, st>>>(d_block, mp, d_query, a, b, d_order, d_positions,
+                                                  n, d_acc);
+  PDX_LAUNCH_CHECK();
+  return PDX_OK;
+}
+
 extern "C" int pdx_merge_topk(const float* d_dist, const int64_t* d_ids, int32_t nparts, int64_t nq,
                               int32_t k, float* d_out_dist, int64_t* d_out_ids, void* stream) {
   PDX_REQUIRE(nparts >= 1 && k >= 1, "bad merge sizes");

@@ -242,17 +242,18 @@ def test_select_buckets_vs_oracle(P, oracle):
                 np.testing.assert_array_equal(got[i], ref)
 
 
-@pytest.mark.parametrize("nlist", [1024, 700, 40])
+@pytest.mark.parametrize("nlist", [1024, 700, 40, 32, 20])
 def test_select_buckets_warp_path_vs_oracle(P, oracle, nlist):
     """nlist <= 1024, nprobe <= 32: the one-warp-per-query selection (lane
-    minima threshold, candidates ranked), incl. nprobe == nlist."""
+    minima threshold, candidates ranked), incl. nprobe == nlist (nlist 32,
+    20) and nlist < 32, where some lanes hold no keys."""
     x = recipes.data("mixture", 20_000, 32, 43)
     col = P.VectorCollection.from_array(x)
     index = P.ivf_build(col, nlist=nlist, seed=0)
     Q = np.concatenate([recipes.queries("near", x, 96, 44), recipes.queries("skewed", x, 32, 45)])
     view = _oracle_ivf(oracle, index, x)
     for metric in ("l2", "ip", "l1"):
-        for nprobe in sorted({1, 7, 32, min(32, nlist)}):
+        for nprobe in sorted(p for p in {1, 7, 32, min(32, nlist)} if p <= nlist):
             got = P.index.select_buckets_device(index, P.store.to_device(Q), nprobe, metric)
             got = got.cpu().numpy()
             for i, q in enumerate(Q):
@@ -488,3 +489,50 @@ def test_exact_estimator_tensor_core_auto(P):
     db, ib = b.kneighbors(Q, 10)
     np.testing.assert_array_equal(ia, ib)
     np.testing.assert_array_equal(da, db)
+
+
+def _np_vertical(data, q, a, b, metric, acc, positions=None, order=None):
+    """kernels.py:41-91 restated with numpy float32 ufuncs (each op rounded)."""
+    dims = range(a, b) if order is None else order[a:b]
+    sl = slice(None) if positions is None else np.unique(positions)
+    for j in dims:
+        col = data[j, sl]
+        if metric == "l2":
+            t = q[j] - col
+            acc[sl] += t * t
+        elif metric == "l1":
+            acc[sl] += np.abs(q[j] - col)
+        else:
+            acc[sl] += q[j] * col
+    return acc
+
+
+@pytest.mark.parametrize("metric", ["l2", "l1", "ip"])
+def test_vertical_accumulate_ops(P, metric):
+    """The exported vertical kernels (pdx_vertical_accumulate) = numpy's
+    per-op rounding, natural and permuted orders, selected slots with
+    duplicates, and bit-exact range additivity (tests/test_kernels.py:54-65
+    of the reference)."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((50, 37)).astype(np.float32) * 3
+    blk = P.to_blocks(P.VectorCollection.from_array(x), 64)[0]
+    q = rng.standard_normal(37).astype(np.float32)
+    order = rng.permutation(37)
+    for o in (None, order):
+        acc = P.new_accumulator(64)
+        P.vertical_accumulate(blk, q, (0, 37), metric, acc, order=o)
+        ref = _np_vertical(blk.data, q, 0, 37, metric, P.new_accumulator(64), order=o)
+        np.testing.assert_array_equal(acc, ref)
+        split = P.new_accumulator(64)
+        P.vertical_accumulate(blk, q, (0, 11), metric, split, order=o)
+        P.vertical_accumulate(blk, q, (11, 37), metric, split, order=o)
+        np.testing.assert_array_equal(split, acc)
+        pos = np.array([3, 9, 9, 0, 49])
+        sel = np.full(64, 0.5, np.float32)
+        P.vertical_accumulate_selected(blk, q, (2, 30), metric, sel, pos, order=o)
+        ref = _np_vertical(blk.data, q, 2, 30, metric, np.full(64, 0.5, np.float32), pos, o)
+        np.testing.assert_array_equal(sel, ref)
+    with pytest.raises(ValueError):
+        P.vertical_accumulate(blk, q, (5, 38), metric, P.new_accumulator(64))
+    with pytest.raises(ValueError):
+        P.vertical_accumulate_selected(blk, q, (0, 3), metric, P.new_accumulator(64), [50])

@@ -134,3 +134,36 @@ def test_handle_graph_replay_identical():
             for key in first:
                 assert torch.equal(got[key], first[key]), key
     h.close()
+
+
+@pytest.mark.gpu
+def test_handle_graph_not_replayed_after_realloc():
+    """A, A (captured), a larger B (the handle's scratch buffers are
+    reallocated), then A again: the captured graph of A holds the old
+    buffers' pointers, so it must not be replayed (the graph key carries the
+    buffer generation); every A answer equals the first."""
+    import torch
+    rng = np.random.default_rng(22)
+    x = rng.standard_normal((40_000, 48)).astype(np.float32)
+    idx = P.ivf_build(P.VectorCollection.from_array(x), nlist=100, seed=0)
+    h = P.PdxIndex.from_index(idx)
+
+    def bufs(nq, k):
+        Q = torch.from_numpy(x[:nq] + 0.1 * rng.standard_normal((nq, 48)).astype(np.float32))
+        return Q.pin_memory(), {"dist": torch.empty((nq, k), dtype=torch.float32).pin_memory(),
+                                "ids": torch.empty((nq, k), dtype=torch.int64).pin_memory()}
+    qa, oa = bufs(64, 10)
+    qb, ob = bufs(1024, 100)
+    first = None
+    for call in ("A", "A", "A", "B", "A", "A", "A", "B", "B", "A"):
+        if call == "B":
+            h.search(qb, k=100, pruner="ads", nprobe=40, out=ob)
+            continue
+        h.search(qa, k=10, pruner="ads", nprobe=12, out=oa)
+        got = (oa["ids"].clone(), oa["dist"].clone())
+        if first is None:
+            first = got
+        assert torch.equal(got[0], first[0]) and torch.equal(got[1], first[1])
+    ref = P.ivf_search_batch(idx, qa.numpy(), P.SearchParams(k=10, pruner="ads"), 12)
+    np.testing.assert_array_equal(first[0].numpy(), ref["ids"])
+    h.close()

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import recipes
-from conftest import decode_survivors, host_means
+from conftest import GOLDEN, decode_survivors, host_means
 from paper_2503_04422_b200.layout import VectorCollection, to_blocks
 
 
@@ -218,3 +218,55 @@ def test_oracle_bsa_matches_host_restatement(oracle):
     assert a == b and sa["values_touched"] <= sb["values_touched"]
     with pytest.raises(ValueError):
         oracle.search(blocks, q, 5, pruner="bsa")
+
+
+def test_oracle_c2_headline_prefix_equals_reference():
+    """The bench's headline config (C2, BASELINE configs[1]) on the
+    reference-k-means index: the C oracle equals the real reference's
+    ivf_search (tests/golden/c2_reference_prefix.npz) bit for bit on the
+    query prefix at nprobe 8 / 32 / 128 — the oracle is pinned at full size,
+    not only on the small golden cases."""
+    import bench
+    from oracle import oracle as O
+    g = np.load(GOLDEN / "c2_reference_prefix.npz")
+    X, _ = bench.make_data(1_000_000, 1000)
+    T = bench.rotation(128)
+    XR = X @ T.T
+    cent, assign, same = bench.load_fixture(XR)
+    if not same:
+        pytest.skip("this host's BLAS rotated the data differently from the fixture's")
+    view = O.IvfView.from_assignment(XR, cent, assign, 1024)
+    for npb in (8, 32, 128):
+        ref = O.ivf_search_batch(view, g["queries"], 10, npb, pruner="ads", eps0=2.1)
+        np.testing.assert_array_equal(ref["ids"], g[f"ids_{npb}"])
+        np.testing.assert_array_equal(ref["dist"], g[f"dist_{npb}"])
+        np.testing.assert_array_equal(ref["touched"], g[f"touched_{npb}"])
+        np.testing.assert_array_equal(ref["total"], g[f"total_{npb}"])
+
+
+def test_packed_ivf_view_equals_block_list_view():
+    """oracle.IvfView.from_assignment (numpy packing, used by the bench's
+    reference arm) = the view built from per-bucket to_blocks chains."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(1)
+    n, d, nl = 5000, 24, 37
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    c = rng.standard_normal((nl, d)).astype(np.float32)
+    a = rng.integers(0, nl - 3, n)  # the last buckets stay empty
+    chains, means = [], []
+    for b in range(nl):
+        mem = np.flatnonzero(a == b)
+        chains.append(to_blocks(VectorCollection(data=x[mem], ids=mem.astype(np.int64)), 64)
+                      if len(mem) else [])
+        means.append(x[mem].astype(np.float64).sum(0) / len(mem) if len(mem)
+                     else c[b].astype(np.float64))
+    v1 = O.IvfView(to_blocks(VectorCollection.from_array(c), 64), chains, means)
+    v2 = O.IvfView.from_assignment(x, c, a, nl)
+    np.testing.assert_array_equal(v1.means, v2.means)
+    q = rng.standard_normal((50, d)).astype(np.float32)
+    for pr, cr in (("ads", "sequential"), ("bond", "dmeans"), ("none", "sequential")):
+        r1 = O.ivf_search_batch(v1, q, 10, 8, pruner=pr, criteria=cr, survivors_cap=1 << 14)
+        r2 = O.ivf_search_batch(v2, q, 10, 8, pruner=pr, criteria=cr, survivors_cap=1 << 14)
+        for key in ("ids", "dist", "touched", "total", "selected"):
+            np.testing.assert_array_equal(r1[key], r2[key])
+        assert r1["survivor_lists"] == r2["survivor_lists"]
