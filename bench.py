@@ -592,6 +592,24 @@ def extras_block(P, index, params, Qr_dev, Qd, X, args, gt, flush):
         rec2 = float(np.mean([P.recall_at_k(gt.ids[i], ids2[i], K) for i in range(args.nq)]))
         extras[f"nprobe_{npb}"] = {"qps": args.nq / (np.median(ts) / 1e3), "recall_at_10": rec2,
                                    "timing": "median of 9 L2-flushed searches"}
+    # the GPU IVF build (csrc/pdx_build.cu) of the same data vs the
+    # reference's k-means (the fixture: 252 s on one host core)
+    fx = load_fixture(index._host_data)
+    if fx is not None:
+        xr = P.store.to_device(index._host_data)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cent_g, assign_g = P.index.lloyd_kmeans_device(xr, NLIST, 0)
+        torch.cuda.synchronize()
+        tb = time.perf_counter() - t0
+        a_g = assign_g.cpu().numpy()
+        extras["gpu_ivf_build"] = {
+            "kmeans_s": tb, "reference_kmeans_s": float(np.load(FIXTURE)["kmeans_seconds"]),
+            "assignment_agreement_with_reference": float(np.mean(a_g == fx[1])),
+            "max_centroid_abs_diff": float(np.abs(cent_g.cpu().numpy() - fx[0]).max()),
+            "what": "lloyd_kmeans_device (fused f32 distance+argmin, radix bucket layout, f64 "
+                    "means, 20 iterations max) on the C2 data"}
+        del xr
     # BSA (this build's restatement) on the same data and nprobe
     est = P.IvfNearestNeighbors(pruner="bsa", nlist=NLIST, nprobe=args.nprobe, seed=0).fit(X)
     sb = est.searcher(K)

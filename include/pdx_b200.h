@@ -250,6 +250,49 @@ int pdx_search(const pdx_store* store, const pdx_search_params* params, const fl
                void* d_work, int64_t work_bytes, void* stream);
 
 /*
+ * GPU IVF build (next #1): the reference's Lloyd k-means (index.py:27-64)
+ * and bucket layout (index.py:98-100) — SIMT float32 kernels and a CUB
+ * radix sort, no cuBLAS.
+ *   pdx_row_norms: out[i] = sum_j x[i][j]^2 (float32; einsum, index.py:70).
+ *   pdx_kmeans_assign: for row i (d_rows[i] when d_rows is not NULL) the
+ *     centroid c minimising max(xnorm + cnorm[c] - 2 x.c, 0) (_pairwise_l2,
+ *     index.py:67-72), the lowest c among equal minima (np.argmin);
+ *     d_min_dist (optional) gets that distance.  d_xnorm is indexed by i.
+ *   pdx_bucket_layout: d_order = rows sorted by (bucket, row) (members of
+ *     each bucket ascending, np.flatnonzero), d_counts [nlist], d_offsets
+ *     [nlist+1] (exclusive sums); call with d_work = NULL for *work_bytes.
+ *   pdx_kmeans_update: new[c] = f32(means[c]) if counts[c] > 0 else old[c]
+ *     (index.py:45-48, means from pdx_segment_means in float64).
+ *   pdx_kmeans_farthest: the member of `bucket` farthest from d_centroid by
+ *     the same distance (index.py:52-54); *d_out_key = (gap bits << 32) |
+ *     (0xffffffff - row), the largest gap and then the lowest row.
+ *   pdx_kmeans_shift: *d_out = max_c ||new_c - old_c|| / (||old_c|| + 1e-30)
+ *     in float32 (index.py:57-61).
+ *   pdx_gather_rows: d_out[i] = d_x[d_rows[i]] (the sample init, :38-39).
+ *   pdx_pack_rows: a chunk of m rows written straight into their slots of
+ *     a store (d_dest[i] = tile * 64 + slot, -1 = skip) with their ids: the
+ *     chunked build packs without a full copy of the collection.
+ */
+int pdx_row_norms(const float* d_x, int64_t n, int32_t d, float* d_out, void* stream);
+int pdx_kmeans_assign(const float* d_x, const int64_t* d_rows, int64_t n, int32_t d,
+                      const float* d_xnorm, const float* d_centroids, const float* d_cnorm,
+                      int32_t nlist, int32_t* d_assign, float* d_min_dist, void* stream);
+int pdx_bucket_layout(const int32_t* d_assign, int64_t n, int32_t nlist, int64_t* d_order,
+                      int64_t* d_counts, int64_t* d_offsets, void* d_work, int64_t* work_bytes,
+                      void* stream);
+int pdx_kmeans_update(const double* d_means, const int64_t* d_counts, const float* d_old,
+                      int32_t nlist, int32_t d, float* d_new, void* stream);
+int pdx_kmeans_shift(const float* d_new, const float* d_old, int32_t nlist, int32_t d,
+                     float* d_out, void* stream);
+int pdx_kmeans_farthest(const float* d_x, int64_t n, int32_t d, const int32_t* d_assign,
+                        int32_t bucket, const float* d_centroid, float cnorm, int64_t* d_out_key,
+                        void* stream);
+int pdx_gather_rows(const float* d_x, int32_t d, const int64_t* d_rows, int64_t m, float* d_out,
+                    void* stream);
+int pdx_pack_rows(const float* d_x, int64_t m, int32_t d, const int64_t* d_dest,
+                  const int64_t* d_ids, const pdx_store* store, void* stream);
+
+/*
  * The vertical kernels as standalone ops: vertical_accumulate
  * (kernels.py:41-62; d_positions NULL: every one of the mp slots) and
  * vertical_accumulate_selected (kernels.py:65-91; the npos listed slots,

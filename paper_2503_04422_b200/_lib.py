@@ -28,7 +28,9 @@ EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_til
            "pdx_bsa_residuals", "pdx_file_probe", "pdx_file_load", "pdx_file_save",
            "pdx_index_create", "pdx_index_open", "pdx_index_destroy", "pdx_index_search",
            "pdx_k8_norms", "pdx_k8_margin", "pdx_k8_filter", "pdx_k8_rescore",
-           "pdx_vertical_accumulate", "pdx_batch_profile")
+           "pdx_vertical_accumulate", "pdx_batch_profile", "pdx_row_norms",
+           "pdx_kmeans_assign", "pdx_bucket_layout", "pdx_kmeans_update", "pdx_kmeans_shift",
+           "pdx_kmeans_farthest", "pdx_gather_rows", "pdx_pack_rows")
 
 
 class PdxStore(C.Structure):
@@ -138,6 +140,14 @@ def lib():
         L.pdx_vertical_accumulate.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp,
                                               vp]
         L.pdx_batch_profile.argtypes = [i32, vp, i32, vp]
+        L.pdx_row_norms.argtypes = [vp, i64, i32, vp, vp]
+        L.pdx_kmeans_assign.argtypes = [vp, vp, i64, i32, vp, vp, vp, i32, vp, vp, vp]
+        L.pdx_bucket_layout.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp]
+        L.pdx_kmeans_update.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+        L.pdx_kmeans_shift.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.pdx_kmeans_farthest.argtypes = [vp, i64, i32, vp, i32, vp, C.c_float, vp, vp]
+        L.pdx_gather_rows.argtypes = [vp, i32, vp, i64, vp, vp]
+        L.pdx_pack_rows.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         for name in EXPORTS:
             getattr(L, name).restype = getattr(L, name).restype or C.c_int
         if L.pdx_abi_version() != 3:

@@ -540,6 +540,23 @@ static bool page_locked(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+static pdx_index::GraphKey gkey_of(const float* Q, float* out_dist, int64_t* out_ids,
+                                   int64_t* out_touched, int64_t* out_total, int64_t nq,
+                                   void* stream, const pdx_query_params* P) {
+  pdx_index::GraphKey key;
+  memset(&key, 0, sizeof(key));
+  key.q = Q;
+  key.outs[0] = out_dist;
+  key.outs[1] = out_ids;
+  key.outs[2] = out_touched;
+  key.outs[3] = out_total;
+  key.nq = nq;
+  key.stream = stream;
+  key.generation = g_buf_generation.load(std::memory_order_relaxed);
+  key.prm = *P;
+  return key;
+}
+
 // A repeated call (same buffers, batch size, parameters and stream) is
 // captured once into a CUDA graph and replayed: the ~30 launches and copies
 // of a search leave no host gaps.  Only for IVF searches from page-locked
@@ -555,17 +572,8 @@ extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const f
                          page_locked(out_ids) && page_locked(out_touched) &&
                          page_locked(out_total);
   if (graphable) {
-    pdx_index::GraphKey key;
-    memset(&key, 0, sizeof(key));
-    key.q = Q;
-    key.outs[0] = out_dist;
-    key.outs[1] = out_ids;
-    key.outs[2] = out_touched;
-    key.outs[3] = out_total;
-    key.nq = nq;
-    key.stream = stream;
-    key.generation = g_buf_generation.load(std::memory_order_relaxed);
-    key.prm = *P;
+    const pdx_index::GraphKey key =
+        gkey_of(Q, out_dist, out_ids, out_touched, out_total, nq, stream, P);
     if (!I->gs) {
       PDX_CUDA_CHECK(cudaStreamCreateWithFlags(&I->gs, cudaStreamNonBlocking));
       PDX_CUDA_CHECK(cudaEventCreateWithFlags(&I->gev, cudaEventDisableTiming));
@@ -604,10 +612,12 @@ extern "C" int pdx_index_search(pdx_index* I, const pdx_query_params* P, const f
       if (ex) cudaGraphExecDestroy(ex);
       cudaGetLastError();  // a failed capture leaves no sticky error: run directly
     }
-    I->gseen = key;
-    I->gseen_valid = true;
   }
   PDX_TRY(index_search_enqueue(I, P, Q, nq, out_dist, out_ids, out_touched, out_total, st));
+  if (graphable) {  // the next identical call (buffers as this call left them) is captured
+    I->gseen = gkey_of(Q, out_dist, out_ids, out_touched, out_total, nq, stream, P);
+    I->gseen_valid = true;
+  }
   if (!P->outputs_on_device) PDX_CUDA_CHECK(cudaStreamSynchronize(st));
   return PDX_OK;
 }

@@ -1,9 +1,10 @@
 """IVF bucket index and flat partitioning over the HBM store (index.py:1-191).
 
-Build (``lloyd_kmeans``/``ivf_build``/``flat_build``) runs on the GPU:
-k-means distances are a cuBLAS fp32 GEMM in the reference's expansion form
-(index.py:67-72), the centroid update and every mean use the float64
-segment-mean kernel (numpy's order), bucket packing is kernel K1.  Search
+Build (``lloyd_kmeans``/``ivf_build``/``flat_build``) runs on the GPU in
+this library's kernels (csrc/pdx_build.cu): a fused float32 distance +
+argmin in the reference's expansion form (index.py:67-72), a stable radix
+bucket layout, the float64 segment-mean kernel (numpy's order) for every
+mean, and kernel K1 for the packing.  Search
 (``ivf_search``/``exact_search`` and their batched forms) runs kernels
 K2 (bucket selection), K4 (orders) and K5/K6 (pruned scan + top-k).
 """
@@ -28,80 +29,137 @@ KMEANS_SHIFT_TOL = 1e-4
 
 
 # ------------------------------------------------------------------ k-means
-def _pairwise_l2_dev(x, c):
-    """max(|x|^2 + |c|^2 - 2 x.c, 0) in float32 (index.py:67-72), cuBLAS fp32."""
+def _empty(shape, dtype, dev):
     import torch
-    xx = (x * x).sum(1, keepdim=True)
-    cc = (c * c).sum(1)[None, :]
-    return torch.clamp(xx + cc - 2.0 * (x @ c.T), min=0.0)
+    return torch.empty(shape, dtype=dtype, device=dev)
 
 
-def _argmin_chunked(x, c, chunk=1 << 17):
+def row_norms(x):
+    """||x_i||^2, float32 (pdx_row_norms; the einsum of index.py:70)."""
     import torch
-    out = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
-    for s in range(0, x.shape[0], chunk):
-        out[s:s + chunk] = torch.argmin(_pairwise_l2_dev(x[s:s + chunk], c), dim=1)
+    out = _empty((x.shape[0],), torch.float32, x.device)
+    _lib.check(_lib.lib().pdx_row_norms(_lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(out),
+                                        _lib.stream_handle()))
     return out
 
 
-def _bucket_layout(assign, nlist):
-    """Members of every bucket in ascending original index (index.py:100)."""
+def kmeans_assign(x, centroids, xnorm=None, cnorm=None, rows=None, min_dist=False):
+    """Nearest centroid of every row (pdx_kmeans_assign: fused float32
+    distance max(xx + cc - 2 x.c, 0) of index.py:67-72 + argmin, lowest
+    index on ties as np.argmin).  Returns int32 assignments [, distances]."""
     import torch
-    order = torch.sort(assign, stable=True).indices
-    counts = torch.bincount(assign, minlength=nlist)
-    off = torch.zeros(nlist + 1, dtype=torch.int64, device=assign.device)
-    off[1:] = torch.cumsum(counts, 0)
+    n = x.shape[0] if rows is None else rows.shape[0]
+    xnorm = row_norms(x) if xnorm is None else xnorm
+    if rows is not None and xnorm.shape[0] != n:
+        xnorm = xnorm[rows]
+    cnorm = row_norms(centroids) if cnorm is None else cnorm
+    a = _empty((n,), torch.int32, x.device)
+    md = _empty((n,), torch.float32, x.device) if min_dist else None
+    _lib.check(_lib.lib().pdx_kmeans_assign(_lib.ptr(x), _lib.ptr(rows), n, x.shape[1],
+                                            _lib.ptr(xnorm), _lib.ptr(centroids),
+                                            _lib.ptr(cnorm), centroids.shape[0], _lib.ptr(a),
+                                            _lib.ptr(md), _lib.stream_handle()))
+    return (a, md) if min_dist else a
+
+
+def bucket_layout(assign, nlist):
+    """Members of every bucket in ascending original index (index.py:100):
+    (order int64 [n], counts int64 [nlist], offsets int64 [nlist+1]) from a
+    stable radix sort (pdx_bucket_layout)."""
+    import ctypes as C
+
+    import torch
+    if assign.dtype != torch.int32:
+        assign = assign.to(torch.int32)
+    n, dev = assign.shape[0], assign.device
+    wb = C.c_int64(0)
+    L = _lib.lib()
+    _lib.check(L.pdx_bucket_layout(_lib.ptr(assign), n, nlist, None, None, None, None,
+                                   C.cast(C.pointer(wb), C.c_void_p), _lib.stream_handle()))
+    work = _empty((max(1, wb.value),), torch.uint8, dev)
+    order = _empty((n,), torch.int64, dev)
+    counts = _empty((nlist,), torch.int64, dev)
+    off = _empty((nlist + 1,), torch.int64, dev)
+    _lib.check(L.pdx_bucket_layout(_lib.ptr(assign), n, nlist, _lib.ptr(order), _lib.ptr(counts),
+                                   _lib.ptr(off), _lib.ptr(work),
+                                   C.cast(C.pointer(wb), C.c_void_p), _lib.stream_handle()))
     return order, counts, off
 
 
-def lloyd_kmeans_device(x, nlist: int, seed: int, max_iters: int = DEFAULT_KMEANS_ITERS):
-    """Lloyd iterations of index.py:27-64 on device tensors.
-
-    Same seeded sample init, float64 member means (pdx_segment_means, the
-    reference's summation order), largest-cluster split for empty clusters
-    and relative-shift stop.  Returns (centroids f32 [nlist,d], assign i64)."""
+def _argmin_chunked(x, c, chunk=None):
+    """Nearest centroid of every row, int64 (tools' helper; one fused launch)."""
     import torch
-    n = x.shape[0]
+    return kmeans_assign(x, c).to(torch.int64)
+
+
+def _segment_means(x, order, off, nlist, init=None):
+    import torch
+    means = (init.clone() if init is not None else
+             torch.zeros((nlist, x.shape[1]), dtype=torch.float64, device=x.device))
+    _lib.check(_lib.lib().pdx_segment_means(_lib.ptr(x), x.shape[1], _lib.ptr(order),
+                                            _lib.ptr(off), nlist, _lib.ptr(means),
+                                            _lib.stream_handle()))
+    return means
+
+
+def _farthest(x, assign, bucket, centroid):
+    """index.py:52-54: members of `bucket`, the one farthest from centroid
+    (first on ties).  pdx_kmeans_farthest."""
+    import torch
+    key = _empty((1,), torch.int64, x.device)
+    cn = float(row_norms(centroid[None, :]).item())
+    _lib.check(_lib.lib().pdx_kmeans_farthest(_lib.ptr(x), x.shape[0], x.shape[1],
+                                              _lib.ptr(assign), int(bucket), _lib.ptr(centroid),
+                                              cn, _lib.ptr(key), _lib.stream_handle()))
+    k = int(key.item()) & 0xFFFFFFFF
+    return 0xFFFFFFFF - k
+
+
+def lloyd_kmeans_device(x, nlist: int, seed: int, max_iters: int = DEFAULT_KMEANS_ITERS):
+    """Lloyd iterations of index.py:27-64 on a device tensor, every step a
+    kernel of this library (no cuBLAS / ATen compute): seeded sample init
+    (pdx_gather_rows), fused distance + argmin (pdx_kmeans_assign), stable
+    bucket layout (pdx_bucket_layout), float64 member means in the
+    reference's summation order (pdx_segment_means), centroid update
+    (pdx_kmeans_update), largest-cluster split for empty clusters
+    (pdx_kmeans_farthest) and the relative-shift stop (pdx_kmeans_shift).
+    Returns (centroids f32 [nlist, d], assign int32 [n])."""
+    import torch
+    n, d = x.shape
     if not 1 <= nlist <= n:
         raise ValueError(f"nlist must be in [1, {n}], got {nlist}")
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        rng = np.random.default_rng(seed)
-        init = rng.choice(n, size=nlist, replace=False)
-        centroids = x[torch.from_numpy(init).to(x.device)].clone()
-        for _ in range(max_iters):
-            assign = _argmin_chunked(x, centroids)
-            order, counts, off = _bucket_layout(assign, nlist)
-            means = torch.zeros((nlist, x.shape[1]), dtype=torch.float64, device=x.device)
-            _lib.check(_lib.lib().pdx_segment_means(_lib.ptr(x), x.shape[1], _lib.ptr(order),
-                                                    _lib.ptr(off), nlist, _lib.ptr(means),
-                                                    _lib.stream_handle()))
-            nonempty = counts > 0
-            new_centroids = centroids.clone()
-            new_centroids[nonempty] = means[nonempty].to(torch.float32)
-            empties = torch.nonzero(~nonempty).flatten().tolist()
-            if empties:
-                counts_h = counts.cpu().numpy().copy()
-                for c in empties:
-                    if counts_h[c] > 0:
-                        continue
-                    largest = int(np.argmax(counts_h))
-                    members = torch.nonzero(assign == largest).flatten()
-                    gaps = _pairwise_l2_dev(x[members], new_centroids[largest][None, :])[:, 0]
-                    stray = int(members[int(torch.argmax(gaps).item())].item())
-                    new_centroids[c] = x[stray]
-                    assign[stray] = c
-                    counts_h[largest] -= 1
-                    counts_h[c] += 1
-            shift = torch.linalg.norm(new_centroids - centroids, dim=1)
-            scale = torch.linalg.norm(centroids, dim=1) + 1e-30
-            centroids = new_centroids
-            if float(torch.max(shift / scale).item()) < KMEANS_SHIFT_TOL:
-                break
-        assign = _argmin_chunked(x, centroids)
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+    dev = x.device
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    rng = np.random.default_rng(seed)
+    init = torch.from_numpy(rng.choice(n, size=nlist, replace=False).astype(np.int64)).to(dev)
+    centroids = _empty((nlist, d), torch.float32, dev)
+    _lib.check(L.pdx_gather_rows(_lib.ptr(x), d, _lib.ptr(init), nlist, _lib.ptr(centroids), st))
+    xnorm = row_norms(x)
+    shift = _empty((1,), torch.float32, dev)
+    for _ in range(max_iters):
+        assign = kmeans_assign(x, centroids, xnorm=xnorm)
+        order, counts, off = bucket_layout(assign, nlist)
+        means = _segment_means(x, order, off, nlist)
+        new = _empty((nlist, d), torch.float32, dev)
+        _lib.check(L.pdx_kmeans_update(_lib.ptr(means), _lib.ptr(counts), _lib.ptr(centroids),
+                                       nlist, d, _lib.ptr(new), st))
+        counts_h = counts.cpu().numpy().copy()
+        for c in np.flatnonzero(counts_h == 0):  # index.py:49-56, in bucket order
+            if counts_h[c] > 0:
+                continue
+            largest = int(np.argmax(counts_h))
+            stray = _farthest(x, assign, largest, new[largest].contiguous())
+            new[c] = x[stray]
+            assign[stray] = int(c)
+            counts_h[largest] -= 1
+            counts_h[c] += 1
+        _lib.check(L.pdx_kmeans_shift(_lib.ptr(new), _lib.ptr(centroids), nlist, d,
+                                      _lib.ptr(shift), st))
+        centroids = new
+        if float(shift.item()) < KMEANS_SHIFT_TOL:
+            break
+    assign = kmeans_assign(x, centroids, xnorm=xnorm)
     return centroids, assign
 
 
@@ -180,13 +238,10 @@ class IvfIndex:
         centroids = np.asarray(centroids, dtype=np.float32)
         nlist = centroids.shape[0] if nlist is None else nlist
         x = x_dev if x_dev is not None else to_device(collection.data, torch.float32)
-        a = to_device(assign if isinstance(assign, torch.Tensor) else np.asarray(assign, np.int64),
-                      torch.int64)
-        order, counts, off = _bucket_layout(a, nlist)
-        means = to_device(centroids, torch.float64).clone()
-        _lib.check(_lib.lib().pdx_segment_means(_lib.ptr(x), x.shape[1], _lib.ptr(order),
-                                                _lib.ptr(off), nlist, _lib.ptr(means),
-                                                _lib.stream_handle()))
+        a = to_device(assign if isinstance(assign, torch.Tensor) else np.asarray(assign, np.int32),
+                      torch.int32)
+        order, counts, off = bucket_layout(a, nlist)
+        means = _segment_means(x, order, off, nlist, init=to_device(centroids, torch.float64))
         counts_h = counts.cpu().numpy()
         nblk = (counts_h + block_size - 1) // block_size
         # vectors per logical block, bucket by bucket

@@ -41,9 +41,11 @@ def main(src, dst):
         unit = r.get("Metric Unit", "")
         m = r["Metric Name"]
         if m == "gpu__time_duration.sum":
-            e["time_us"] = v / 1e3 if unit == "nsecond" else (v if unit == "usecond" else v * 1e3)
+            e["time_us"] = v * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0,
+                                "ms": 1e3, "msecond": 1e3}.get(unit, 1e-3)
         elif m.startswith("dram__bytes"):
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3,
+                     "MB": 1e6, "GB": 1e9}.get(unit, 1)
             e["dram_bytes"] = e.get("dram_bytes", 0.0) + v * scale
         elif m == "smsp__issue_active.avg.pct_of_peak_sustained_active":
             e["issue_active_pct"] = v
