@@ -405,9 +405,10 @@ int pdx_file_save(const char* path, const pdx_store* store, int32_t block_size,
 
 /*
  * K8 — batched exact search with tensor-core candidate generation (L2, IP;
- * pruner none), for batches where Q X^T is a real dense GEMM (C4).  The
- * caller runs S = Q X^T chunk by chunk on the tensor cores (TF32 GEMM) and
- * passes each chunk to pdx_k8_filter; pdx_k8_rescore then recomputes the
+ * pruner none), for batches where Q X^T is a real dense GEMM (C4).
+ * pdx_k8_candidates runs the whole candidate pass on the tensor cores;
+ * pdx_k8_filter is its dense-chunk step (S from the tcgen05 kernel's dense
+ * mode, or from any GEMM); pdx_k8_rescore then recomputes the
  * candidates exactly as the scan does.  Results equal pdx_search's (the
  * candidate set provably contains the exact top-k: |S - ref| <= margin *
  * |q| |x|, pdx_k8_margin); a query whose candidates overflow C is reported
@@ -422,6 +423,24 @@ int pdx_file_save(const char* path, const pdx_store* store, int32_t block_size,
  *       row r = vector r of block r / part_size; outputs as pdx_search.
  */
 int pdx_k8_norms(const float* d_x, int64_t n, int32_t d, float* d_n2, void* stream);
+/* pdx_k8_norms over the first d floats of rows ld floats apart. */
+int pdx_k8_norms_ld(const float* d_x, int64_t n, int32_t d, int64_t ld, float* d_n2, void* stream);
+/*
+ * pdx_k8_candidates: the candidate pass on the 5th-generation tensor cores
+ * (csrc/pdx_k8tc.cu: tcgen05.mma kind::tf32 with TMEM accumulators, TMA
+ * operand staging, the interval filter fused into the TMEM epilogue — the
+ * score matrix is never written to HBM except for the first chunk of
+ * min(n, 65536) rows, whose k smallest upper bounds seed tau).
+ * d_x f32 [n][ld], d_q f32 [nq][ld] (ld a multiple of 4 >= d, 16-B aligned
+ * rows, the floats beyond d zero), d_xn2 = pdx_k8_norms_ld of d_x.  Writes
+ * d_cand [nq][C] row indices and d_ccount [nq] (> C: overflow, answer that
+ * query with pdx_search) — a superset of the exact top-k for
+ * pdx_k8_rescore.  d_work NULL: *work_bytes gets the scratch size.
+ */
+int pdx_k8_candidates(const float* d_x, int64_t n, int32_t d, int64_t ld, const float* d_xn2,
+                      const float* d_q, int64_t nq, int32_t metric, int32_t k, int64_t* d_cand,
+                      int32_t* d_ccount, int32_t C, void* d_work, int64_t* work_bytes,
+                      void* stream);
 float pdx_k8_margin(int32_t d, int32_t metric);
 int pdx_k8_filter(const float* d_S, int64_t ldS, int64_t nq, int32_t R, int64_t row0,
                   const float* d_xn2, const float* d_qn2, int32_t metric, int32_t d, int32_t k,

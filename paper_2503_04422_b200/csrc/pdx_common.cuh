@@ -35,6 +35,11 @@ void set_error(const char* fmt, ...);
   } while (0)
 
 #define PDX_LAUNCH_CHECK() PDX_CUDA_CHECK(cudaGetLastError())
+#define PDX_TRY(expr)              \
+  do {                             \
+    const int _rc = (expr);        \
+    if (_rc != PDX_OK) return _rc; \
+  } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -7,8 +7,6 @@
 // launches — K3 projection, K2 bucket selection, K4 orders, K5/K6 scan —
 // with the host<->device copies at its ends, so a caller with host buffers
 // pays one C call per batch.
-#include <cublas_v2.h>
-
 #include <atomic>
 #include <cmath>
 #include <vector>
@@ -52,7 +50,8 @@ struct DevBuf {
 
 // row r of a flat index = vector r % part of block r / part, row-major
 __global__ void __launch_bounds__(256) tiles_to_rows_kernel(const float* __restrict__ tiles,
-                                                            int64_t tile_stride, int d, int group,
+                                                            int64_t tile_stride, int d, int64_t ld,
+                                                            int group,
                                                             const int64_t* __restrict__ block_tile,
                                                             int64_t part, int64_t n,
                                                             float* __restrict__ rows) {
@@ -61,9 +60,10 @@ __global__ void __launch_bounds__(256) tiles_to_rows_kernel(const float* __restr
   const int64_t b = r / part, w = r - b * part;
   const float* tb = tiles + (block_tile[b] + w / kTile) * tile_stride;
   const int slot = (int)(w % kTile);
-  for (int j = threadIdx.x & 31; j < d; j += 32)
-    rows[r * d + j] = group == 8 ? tb[((j >> 3) * kTile + slot) * 8 + (j & 7)]
-                                 : tb[(int64_t)j * kTile + slot];
+  for (int j = threadIdx.x & 31; j < ld; j += 32)
+    rows[r * ld + j] = j >= d        ? 0.f
+                       : group == 8 ? tb[((j >> 3) * kTile + slot) * 8 + (j & 7)]
+                                    : tb[(int64_t)j * kTile + slot];
 }
 
 int schedule_len(int d, int initial_step) {
@@ -99,10 +99,10 @@ struct pdx_index {
   DevBuf<unsigned char> work;
   // K8 (flat indexes whose blocks hold part_size vectors, the last fewer)
   int64_t part_size = 0, nrows = 0;
-  DevBuf<float> rows, rn2, qn2, kprev, knext, S;
+  DevBuf<float> rows, rn2, qpad;
   DevBuf<int64_t> cand;
   DevBuf<int32_t> ccount;
-  cublasHandle_t blas = nullptr;
+  DevBuf<unsigned char> k8work;
   // CUDA graph of the last repeated search call (pdx_index_search)
   struct GraphKey {
     const void* q;
@@ -121,7 +121,6 @@ struct pdx_index {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (gs) cudaStreamDestroy(gs);
     if (gev) cudaEventDestroy(gev);
-    if (blas) cublasDestroy(blas);
   }
 };
 
@@ -201,54 +200,34 @@ namespace {
 int k8_search(pdx_index* I, const pdx_query_params* P, const float* dq, int64_t nq,
               float* out_dist, int64_t* out_ids, cudaStream_t st) {
   const int d = I->d, k = P->k;
-  const int64_t n = I->nrows;
+  const int64_t n = I->nrows, ld = (d + 3) / 4 * 4;
   constexpr int C = 4096;
   PDX_REQUIRE(k <= C, "k too large for the tensor-core path");
-  if (!I->blas) {
-    if (cublasCreate(&I->blas) != CUBLAS_STATUS_SUCCESS) {
-      set_error("cublasCreate failed");
-      return PDX_ECUDA;
-    }
-    cublasSetMathMode(I->blas, CUBLAS_TF32_TENSOR_OP_MATH);
-  }
-  cublasSetStream(I->blas, st);
-  if (I->rows.n < (size_t)(n * d)) {  // row-major copy of the vectors, once
-    PDX_TRY(I->rows.need((size_t)(n * d)));
+  if (I->rows.n < (size_t)(n * ld)) {  // row-major copy of the vectors (TMA rows), once
+    PDX_TRY(I->rows.need((size_t)(n * ld)));
     PDX_TRY(I->rn2.need((size_t)n));
     tiles_to_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
-        I->st.d_tiles, (int64_t)I->st.d_pad * kTile, d, I->st.group, I->st.d_block_tile,
+        I->st.d_tiles, (int64_t)I->st.d_pad * kTile, d, ld, I->st.group, I->st.d_block_tile,
         I->part_size, n, I->rows.p);
     PDX_LAUNCH_CHECK();
-    PDX_TRY(pdx_k8_norms(I->rows.p, n, d, I->rn2.p, st));
+    PDX_TRY(pdx_k8_norms_ld(I->rows.p, n, d, ld, I->rn2.p, st));
   }
-  const int64_t R = 65536;
-  PDX_TRY(I->qn2.need((size_t)nq));
-  PDX_TRY(I->kprev.need((size_t)(nq * k)));
-  PDX_TRY(I->knext.need((size_t)(nq * k)));
+  const float* qrows = dq;
+  if (ld != d) {  // queries as zero-padded TMA rows
+    PDX_TRY(I->qpad.need((size_t)(nq * ld)));
+    PDX_CUDA_CHECK(cudaMemsetAsync(I->qpad.p, 0, 4 * nq * ld, st));
+    PDX_CUDA_CHECK(cudaMemcpy2DAsync(I->qpad.p, 4 * ld, dq, 4 * d, 4 * d, nq,
+                                     cudaMemcpyDeviceToDevice, st));
+    qrows = I->qpad.p;
+  }
   PDX_TRY(I->cand.need((size_t)(nq * C)));
   PDX_TRY(I->ccount.need((size_t)nq));
-  PDX_TRY(I->S.need((size_t)(nq * R)));
-  PDX_TRY(pdx_k8_norms(dq, nq, d, I->qn2.p, st));
-  std::vector<float> inf((size_t)(nq * k), INFINITY);
-  PDX_CUDA_CHECK(cudaMemcpyAsync(I->kprev.p, inf.data(), 4 * nq * k, cudaMemcpyHostToDevice, st));
-  PDX_CUDA_CHECK(cudaMemsetAsync(I->ccount.p, 0, 4 * nq, st));
-  float* prev = I->kprev.p;
-  float* next = I->knext.p;
-  const float one = 1.f, zero = 0.f;
-  for (int64_t r0 = 0; r0 < n; r0 += R) {
-    const int rr = (int)(n - r0 < R ? n - r0 : R);
-    // S^T (rr x nq, column-major) = X_c (rr x d) * Q^T: S [nq][rr] row-major
-    if (cublasSgemm(I->blas, CUBLAS_OP_T, CUBLAS_OP_N, rr, (int)nq, d, &one, I->rows.p + r0 * d,
-                    d, dq, d, &zero, I->S.p, rr) != CUBLAS_STATUS_SUCCESS) {
-      set_error("cublasSgemm failed");
-      return PDX_ECUDA;
-    }
-    PDX_TRY(pdx_k8_filter(I->S.p, rr, nq, rr, r0, I->rn2.p + r0, I->qn2.p, P->metric, d, k, prev,
-                          next, I->cand.p, I->ccount.p, C, st));
-    float* t = prev;
-    prev = next;
-    next = t;
-  }
+  int64_t wb = 0;
+  PDX_TRY(pdx_k8_candidates(I->rows.p, n, d, ld, I->rn2.p, qrows, nq, P->metric, k, nullptr,
+                            nullptr, C, nullptr, &wb, st));
+  PDX_TRY(I->k8work.need((size_t)wb));
+  PDX_TRY(pdx_k8_candidates(I->rows.p, n, d, ld, I->rn2.p, qrows, nq, P->metric, k, I->cand.p,
+                            I->ccount.p, C, I->k8work.p, &wb, st));
   std::vector<int32_t> cc((size_t)nq);
   PDX_CUDA_CHECK(cudaMemcpyAsync(cc.data(), I->ccount.p, 4 * nq, cudaMemcpyDeviceToHost, st));
   PDX_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -13,12 +13,6 @@ namespace {
 constexpr int64_t kChunkBytes = 64ll << 20;
 constexpr int64_t kChunkTiles = 1 << 16;
 
-#define PDX_TRY(expr)         \
-  do {                        \
-    const int _rc = (expr);   \
-    if (_rc != PDX_OK) return _rc; \
-  } while (0)
-
 // One 64-slot tile of a block image in the staging buffer.
 struct TileSrc {
   int64_t raw_off;  // float offset of the block image [d][mp] in staging

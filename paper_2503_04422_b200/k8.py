@@ -1,20 +1,21 @@
 """K8 — batched exact search with tensor-core candidate generation.
 
 For a batch of queries over a flat store (exact_search, index.py:182-191,
-pruner "none", L2 or IP) the dense part Q X^T runs as a TF32 GEMM on the
-tensor cores (cuBLAS — a plain library GEMM, chunk by chunk); everything
-that decides the result is this package's CUDA: an error bound turns each
-approximate score into an interval around the reference's key,
-pdx_k8_filter keeps every vector that could still be in the top-k, and
-pdx_k8_rescore recomputes those candidates with the scan's exact arithmetic.
-The results therefore equal the scan's (and the reference's) bit for bit;
-queries whose candidates overflow fall back to the scan.
+pruner "none", L2 or IP) the dense part Q X^T runs on the 5th-generation
+tensor cores in this library's own kernel (csrc/pdx_k8tc.cu: tcgen05.mma
+kind::tf32, TMEM accumulators, TMA-staged operands) with the candidate
+filter fused into the TMEM epilogue: an error bound turns each approximate
+score into an interval around the reference's key, and a vector stays a
+candidate only while its interval can still reach the top-k
+(pdx_k8_candidates); pdx_k8_rescore recomputes the candidates with the
+scan's exact arithmetic.  The results therefore equal the scan's (and the
+reference's) bit for bit; queries whose candidates overflow fall back to
+the scan.
 """
 from __future__ import annotations
 
 import ctypes as C
 
-import numpy as np
 
 from . import _lib
 from .index import ExactSearcher, FlatPartitioning
@@ -25,8 +26,7 @@ from .search import SearchParams, SearchResult
 class TensorCoreExactSearcher:
     """Exact top-k for query batches over ``part`` via the tensor cores."""
 
-    def __init__(self, part: FlatPartitioning, params: SearchParams, chunk: int = 65536,
-                 candidates: int = 4096):
+    def __init__(self, part: FlatPartitioning, params: SearchParams, candidates: int = 4096):
         import torch
         metric = Metric(params.metric)
         if params.pruner != "none" or metric not in (Metric.L2, Metric.IP):
@@ -34,17 +34,23 @@ class TensorCoreExactSearcher:
         st = part.store
         self.part, self.params, self.metric = part, params, metric
         self.k = int(params.k)
-        self.chunk = int(chunk)
         self.cap = max(int(candidates), self.k)
+        self.d = st.d
+        self.ld = (st.d + 3) // 4 * 4  # TMA rows: 16-byte multiples, zero padded
         # row r = vector r of partition r // partition_size, as pdx_k8_rescore maps it
         t = st.tiles
-        rows = t.permute(0, 2, 1, 3).reshape(-1, t.shape[1] * t.shape[3])[:, :st.d]
-        self.X = rows[st.tile_ids.reshape(-1) >= 0].contiguous()
+        rows = t.permute(0, 2, 1, 3).reshape(-1, t.shape[1] * t.shape[3])[:, :self.ld]
+        X = rows[st.tile_ids.reshape(-1) >= 0]
+        if X.shape[1] < self.ld:
+            X = torch.nn.functional.pad(X, (0, self.ld - X.shape[1]))
+        X[:, st.d:] = 0
+        self.X = X.contiguous()
         self.n = int(self.X.shape[0])
         self.xn2 = torch.empty(self.n, dtype=torch.float32, device=t.device)
-        _lib.check(_lib.lib().pdx_k8_norms(_lib.ptr(self.X), self.n, st.d, _lib.ptr(self.xn2),
-                                           _lib.stream_handle()))
+        _lib.check(_lib.lib().pdx_k8_norms_ld(_lib.ptr(self.X), self.n, st.d, self.ld,
+                                              _lib.ptr(self.xn2), _lib.stream_handle()))
         self._fallback = ExactSearcher(part, params)
+        self._work = None
 
     def run(self, Q, stats=False):
         import torch
@@ -53,27 +59,20 @@ class TensorCoreExactSearcher:
         dev = Q.device
         Q = Q.contiguous()
         nq, k, cap = int(Q.shape[0]), self.k, self.cap
-        qn2 = torch.empty(nq, dtype=torch.float32, device=dev)
-        _lib.check(L.pdx_k8_norms(_lib.ptr(Q), nq, st.d, _lib.ptr(qn2), _lib.stream_handle()))
-        prev = torch.full((nq, k), float("inf"), dtype=torch.float32, device=dev)
-        nxt = torch.empty_like(prev)
+        Qp = Q if self.ld == self.d else torch.nn.functional.pad(Q, (0, self.ld - self.d))
+        Qp = Qp.contiguous()
         cand = torch.empty((nq, cap), dtype=torch.int64, device=dev)
         ccount = torch.zeros(nq, dtype=torch.int32, device=dev)
         met = _lib.METRIC[self.metric.value]
-        old = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = True
-        try:
-            for r0 in range(0, self.n, self.chunk):
-                Xc = self.X[r0:r0 + self.chunk]
-                S = Q @ Xc.T  # TF32 tensor cores, fp32 out
-                _lib.check(L.pdx_k8_filter(_lib.ptr(S), S.shape[1], nq, int(S.shape[1]), r0,
-                                           _lib.ptr(self.xn2[r0:r0 + Xc.shape[0]]),
-                                           _lib.ptr(qn2), met, st.d, k, _lib.ptr(prev),
-                                           _lib.ptr(nxt), _lib.ptr(cand), _lib.ptr(ccount), cap,
-                                           _lib.stream_handle()))
-                prev, nxt = nxt, prev
-        finally:
-            torch.backends.cuda.matmul.allow_tf32 = old
+        wb = C.c_int64(0)
+        args = (_lib.ptr(self.X), self.n, self.d, self.ld, _lib.ptr(self.xn2), _lib.ptr(Qp), nq,
+                met, k, _lib.ptr(cand), _lib.ptr(ccount), cap)
+        _lib.check(L.pdx_k8_candidates(*args, None, C.cast(C.pointer(wb), C.c_void_p),
+                                       _lib.stream_handle()))
+        if self._work is None or self._work.numel() < wb.value:
+            self._work = torch.empty(max(1, wb.value), dtype=torch.uint8, device=dev)
+        _lib.check(L.pdx_k8_candidates(*args, _lib.ptr(self._work),
+                                       C.cast(C.pointer(wb), C.c_void_p), _lib.stream_handle()))
         dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
         ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
         _lib.check(L.pdx_k8_rescore(st.ref, int(self.part.partition_size), _lib.ptr(Q), nq, met,

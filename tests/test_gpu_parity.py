@@ -451,17 +451,23 @@ def test_split_mode_exact(P, metric, pruner, k, splits):
 
 
 # ------------------------------------------------------- K8 tensor cores
-@pytest.mark.parametrize("metric,k,normalize", [("ip", 100, True), ("l2", 10, False),
-                                                 ("l2", 100, True), ("ip", 7, False)])
-def test_tensor_core_exact_equals_scan(P, metric, k, normalize):
-    """TF32 candidate generation + exact rescoring returns the scan's exact
-    top-k bit for bit (ids, float32 keys, counts), also across chunk edges
-    and with partitions that are not multiples of 64."""
+@pytest.mark.parametrize("metric,k,normalize,n,d,nq", [
+    ("ip", 100, True, 30_000, 96, 200), ("l2", 10, False, 30_000, 96, 200),
+    ("l2", 100, True, 30_000, 96, 200), ("ip", 7, False, 30_000, 96, 200),
+    ("l2", 10, False, 600_000, 40, 300), ("ip", 50, True, 300_000, 100, 129),
+    ("l2", 100, False, 140_000, 37, 64)])
+def test_tensor_core_exact_equals_scan(P, metric, k, normalize, n, d, nq):
+    """tcgen05 candidate generation (dense first chunk, then the fused
+    filter waves with tau tightening) + exact rescoring returns the scan's
+    exact top-k bit for bit (ids, float32 keys, counts): across the first
+    chunk (65,536 rows) and wave (262,144 rows) edges, partial query tiles
+    (nq not a multiple of 128), d not a multiple of 32 or of 4 (zero-padded
+    TMA rows), partitions that are not multiples of 64."""
     import torch
-    rng = np.random.default_rng(61)
-    c = rng.standard_normal((64, 96)).astype(np.float32)
-    x = c[rng.integers(0, 64, 30_000)] + 0.5 * rng.standard_normal((30_000, 96)).astype(np.float32)
-    q = c[rng.integers(0, 64, 200)] + 0.5 * rng.standard_normal((200, 96)).astype(np.float32)
+    rng = np.random.default_rng(61 + n + d)
+    c = rng.standard_normal((64, d)).astype(np.float32)
+    x = c[rng.integers(0, 64, n)] + 0.5 * rng.standard_normal((n, d)).astype(np.float32)
+    q = c[rng.integers(0, 64, nq)] + 0.5 * rng.standard_normal((nq, d)).astype(np.float32)
     if normalize:
         x /= np.linalg.norm(x, axis=1, keepdims=True)
         q /= np.linalg.norm(q, axis=1, keepdims=True)
@@ -471,13 +477,32 @@ def test_tensor_core_exact_equals_scan(P, metric, k, normalize):
         params = P.SearchParams(k=k, metric=metric)
         Qd = torch.from_numpy(q).cuda()
         ref = P.ExactSearcher(flat, params).run(Qd)
-        tc = P.TensorCoreExactSearcher(flat, params, chunk=7_000)
+        tc = P.TensorCoreExactSearcher(flat, params)
         out = tc.run(Qd)
         assert tc.overflow == 0
         np.testing.assert_array_equal(out.ids.cpu().numpy(), ref.ids.cpu().numpy())
         np.testing.assert_array_equal(out.dist.cpu().numpy(), ref.dist.cpu().numpy())
         np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
         assert int(tc.candidates.max()) < 4096
+        if n > 65_536:
+            break  # the 1000-wide partitions repeat the same rows
+
+
+def test_tensor_core_dense_mode_scores(P):
+    """The tcgen05 kernel's dense mode alone (n < 65,536: the first chunk's
+    S = Q X^T and pdx_k8_filter decide every candidate), up to k = n."""
+    import torch
+    rng = np.random.default_rng(5)
+    for n, d, nq, k in ((5000, 64, 130, 500), (3000, 37, 20, 3000)):
+        x = rng.standard_normal((n, d)).astype(np.float32)
+        q = rng.standard_normal((nq, d)).astype(np.float32)
+        flat = P.flat_build(P.VectorCollection.from_array(x), 64)
+        tc = P.TensorCoreExactSearcher(flat, P.SearchParams(k=k, metric="ip"),
+                                       candidates=max(4096 if k < n else n, k))
+        out = tc.run(torch.from_numpy(q).cuda())
+        assert tc.overflow == 0
+        ref = P.ExactSearcher(flat, P.SearchParams(k=k, metric="ip")).run(torch.from_numpy(q).cuda())
+        np.testing.assert_array_equal(out.ids.cpu().numpy(), ref.ids.cpu().numpy())
 
 
 def test_exact_estimator_tensor_core_auto(P):
