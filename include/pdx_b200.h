@@ -430,13 +430,21 @@ int pdx_k8_norms_ld(const float* d_x, int64_t n, int32_t d, int64_t ld, float* d
  * (csrc/pdx_k8tc.cu: tcgen05.mma kind::tf32 with TMEM accumulators, TMA
  * operand staging, the interval filter fused into the TMEM epilogue — the
  * score matrix is never written to HBM except for the first chunk of
- * min(n, 65536) rows, whose k smallest upper bounds seed tau).
+ * min(n, 8192) rows, whose k smallest upper bounds seed tau).
  * d_x f32 [n][ld], d_q f32 [nq][ld] (ld a multiple of 4 >= d, 16-B aligned
  * rows, the floats beyond d zero), d_xn2 = pdx_k8_norms_ld of d_x.  Writes
  * d_cand [nq][C] row indices and d_ccount [nq] (> C: overflow, answer that
  * query with pdx_search) — a superset of the exact top-k for
  * pdx_k8_rescore.  d_work NULL: *work_bytes gets the scratch size.
  */
+/* pdx_k8_rescore_rows: pdx_k8_rescore from the row-major copy d_x [n][ld]
+ * (d_rowids [n]: the id of each row) and ld-strided queries; cmax bounds
+ * every query's candidate count (the caller reads d_ccount; larger counts
+ * are truncated, so pass the maximum). */
+int pdx_k8_rescore_rows(const float* d_x, int64_t ld, int32_t d, const int64_t* d_rowids,
+                        const float* d_q, int64_t nq, int32_t metric, int32_t k,
+                        const int64_t* d_cand, const int32_t* d_ccount, int32_t C, int32_t cmax,
+                        float* d_dist, int64_t* d_ids, void* stream);
 int pdx_k8_candidates(const float* d_x, int64_t n, int32_t d, int64_t ld, const float* d_xn2,
                       const float* d_q, int64_t nq, int32_t metric, int32_t k, int64_t* d_cand,
                       int32_t* d_ccount, int32_t C, void* d_work, int64_t* work_bytes,

@@ -53,13 +53,16 @@ __global__ void __launch_bounds__(256) tiles_to_rows_kernel(const float* __restr
                                                             int64_t tile_stride, int d, int64_t ld,
                                                             int group,
                                                             const int64_t* __restrict__ block_tile,
+                                                            const int64_t* __restrict__ tile_ids,
                                                             int64_t part, int64_t n,
-                                                            float* __restrict__ rows) {
+                                                            float* __restrict__ rows,
+                                                            int64_t* __restrict__ rowids) {
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (r >= n) return;
   const int64_t b = r / part, w = r - b * part;
   const float* tb = tiles + (block_tile[b] + w / kTile) * tile_stride;
   const int slot = (int)(w % kTile);
+  if ((threadIdx.x & 31) == 0) rowids[r] = tile_ids[(block_tile[b] + w / kTile) * kTile + slot];
   for (int j = threadIdx.x & 31; j < ld; j += 32)
     rows[r * ld + j] = j >= d        ? 0.f
                        : group == 8 ? tb[((j >> 3) * kTile + slot) * 8 + (j & 7)]
@@ -100,7 +103,7 @@ struct pdx_index {
   // K8 (flat indexes whose blocks hold part_size vectors, the last fewer)
   int64_t part_size = 0, nrows = 0;
   DevBuf<float> rows, rn2, qpad;
-  DevBuf<int64_t> cand;
+  DevBuf<int64_t> cand, rowids;
   DevBuf<int32_t> ccount;
   DevBuf<unsigned char> k8work;
   // CUDA graph of the last repeated search call (pdx_index_search)
@@ -206,9 +209,10 @@ int k8_search(pdx_index* I, const pdx_query_params* P, const float* dq, int64_t 
   if (I->rows.n < (size_t)(n * ld)) {  // row-major copy of the vectors (TMA rows), once
     PDX_TRY(I->rows.need((size_t)(n * ld)));
     PDX_TRY(I->rn2.need((size_t)n));
+    PDX_TRY(I->rowids.need((size_t)n));
     tiles_to_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
         I->st.d_tiles, (int64_t)I->st.d_pad * kTile, d, ld, I->st.group, I->st.d_block_tile,
-        I->part_size, n, I->rows.p);
+        I->st.d_tile_ids, I->part_size, n, I->rows.p, I->rowids.p);
     PDX_LAUNCH_CHECK();
     PDX_TRY(pdx_k8_norms_ld(I->rows.p, n, d, ld, I->rn2.p, st));
   }
@@ -231,8 +235,11 @@ int k8_search(pdx_index* I, const pdx_query_params* P, const float* dq, int64_t 
   std::vector<int32_t> cc((size_t)nq);
   PDX_CUDA_CHECK(cudaMemcpyAsync(cc.data(), I->ccount.p, 4 * nq, cudaMemcpyDeviceToHost, st));
   PDX_CUDA_CHECK(cudaStreamSynchronize(st));
-  for (int32_t c : cc)
+  int32_t cmax = 1;
+  for (int32_t c : cc) {
     if (c > C) return PDX_ENOSUPPORT;
+    cmax = c > cmax ? c : cmax;
+  }
   float* dist = out_dist;
   int64_t* ids = out_ids;
   if (!P->outputs_on_device) {
@@ -241,8 +248,8 @@ int k8_search(pdx_index* I, const pdx_query_params* P, const float* dq, int64_t 
     dist = I->dist.p;
     ids = I->ids.p;
   }
-  PDX_TRY(pdx_k8_rescore(&I->st, I->part_size, dq, nq, P->metric, k, I->cand.p, I->ccount.p, C,
-                         dist, ids, st));
+  PDX_TRY(pdx_k8_rescore_rows(I->rows.p, ld, d, I->rowids.p, qrows, nq, P->metric, k, I->cand.p,
+                              I->ccount.p, C, cmax, dist, ids, st));
   if (!P->outputs_on_device) {
     PDX_CUDA_CHECK(cudaMemcpyAsync(out_dist, dist, 4 * nq * k, cudaMemcpyDeviceToHost, st));
     PDX_CUDA_CHECK(cudaMemcpyAsync(out_ids, ids, 8 * nq * k, cudaMemcpyDeviceToHost, st));

@@ -40,7 +40,9 @@ class TensorCoreExactSearcher:
         # row r = vector r of partition r // partition_size, as pdx_k8_rescore maps it
         t = st.tiles
         rows = t.permute(0, 2, 1, 3).reshape(-1, t.shape[1] * t.shape[3])[:, :self.ld]
-        X = rows[st.tile_ids.reshape(-1) >= 0]
+        valid = st.tile_ids.reshape(-1) >= 0
+        X = rows[valid]
+        self.rowids = st.tile_ids.reshape(-1)[valid].contiguous()
         if X.shape[1] < self.ld:
             X = torch.nn.functional.pad(X, (0, self.ld - X.shape[1]))
         X[:, st.d:] = 0
@@ -75,9 +77,11 @@ class TensorCoreExactSearcher:
                                        C.cast(C.pointer(wb), C.c_void_p), _lib.stream_handle()))
         dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
         ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
-        _lib.check(L.pdx_k8_rescore(st.ref, int(self.part.partition_size), _lib.ptr(Q), nq, met,
-                                    k, _lib.ptr(cand), _lib.ptr(ccount), cap, _lib.ptr(dist),
-                                    _lib.ptr(ids), _lib.stream_handle()))
+        cmax = min(int(ccount.max().item()) if nq else 0, cap)
+        _lib.check(L.pdx_k8_rescore_rows(_lib.ptr(self.X), self.ld, self.d, _lib.ptr(self.rowids),
+                                         _lib.ptr(Qp), nq, met, k, _lib.ptr(cand),
+                                         _lib.ptr(ccount), cap, max(cmax, 1), _lib.ptr(dist),
+                                         _lib.ptr(ids), _lib.stream_handle()))
         over = torch.nonzero(ccount > cap).flatten()
         self.overflow = int(over.numel())
         if self.overflow:

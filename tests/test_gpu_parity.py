@@ -460,7 +460,7 @@ def test_tensor_core_exact_equals_scan(P, metric, k, normalize, n, d, nq):
     """tcgen05 candidate generation (dense first chunk, then the fused
     filter waves with tau tightening) + exact rescoring returns the scan's
     exact top-k bit for bit (ids, float32 keys, counts): across the first
-    chunk (65,536 rows) and wave (262,144 rows) edges, partial query tiles
+    chunk (8,192 rows) and wave (32K doubling to 256K rows) edges, partial query tiles
     (nq not a multiple of 128), d not a multiple of 32 or of 4 (zero-padded
     TMA rows), partitions that are not multiples of 64."""
     import torch
@@ -484,13 +484,14 @@ def test_tensor_core_exact_equals_scan(P, metric, k, normalize, n, d, nq):
         np.testing.assert_array_equal(out.dist.cpu().numpy(), ref.dist.cpu().numpy())
         np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
         assert int(tc.candidates.max()) < 4096
-        if n > 65_536:
+        if n > 100_000:
             break  # the 1000-wide partitions repeat the same rows
 
 
 def test_tensor_core_dense_mode_scores(P):
-    """The tcgen05 kernel's dense mode alone (n < 65,536: the first chunk's
-    S = Q X^T and pdx_k8_filter decide every candidate), up to k = n."""
+    """Small collections (n = 3,000 < 8,192: the tcgen05 kernel's dense
+    mode and pdx_k8_filter decide every candidate; n = 5,000: one fused
+    wave), up to k = n."""
     import torch
     rng = np.random.default_rng(5)
     for n, d, nq, k in ((5000, 64, 130, 500), (3000, 37, 20, 3000)):
