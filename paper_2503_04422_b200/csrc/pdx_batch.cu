@@ -1601,11 +1601,13 @@ struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-SideStream& side_stream() {
-  thread_local SideStream per_dev[64];
+// slot 0..3: the work-list stream of one pipeline instance; slots 4..7: the
+// streams the query chunks of an overlapped batch run on
+SideStream& side_stream(int slot = 0) {
+  thread_local SideStream per_dev[16][8];
   int dev = 0;
   cudaGetDevice(&dev);
-  SideStream& ss = per_dev[dev & 63];
+  SideStream& ss = per_dev[dev & 15][slot & 7];
   if (!ss.s) {
     cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
@@ -1666,9 +1668,14 @@ bool batched_eligible(const pdx_store* store, const pdx_search_params* prm, int6
   return pairs <= (int64_t)1 << 31;
 }
 
-int search_batched(const pdx_store* store, const pdx_search_params* prm, const float* d_queries,
-                   int64_t nq64, const int32_t* d_seg_bucket, int32_t nseg,
-                   const pdx_search_out* out, void* d_work, int64_t work_bytes, void* stream) {
+// One pipeline instance over queries [0, nq64) of the given arrays.  With
+// flags_out the flagged queries are copied there (the caller runs the
+// fallback once for all instances) instead of answered here; side_slot picks
+// the work-list stream.
+int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
+                        const float* d_queries, int64_t nq64, const int32_t* d_seg_bucket,
+                        int32_t nseg, const pdx_search_out* out, void* d_work, int64_t work_bytes,
+                        void* stream, int32_t* flags_out, int side_slot) {
   cudaStream_t st = as_stream(stream);
   const int nq = (int)nq64, k = prm->k, nb = store->nbuckets;
   BParams P;
@@ -1763,11 +1770,12 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
     if (out->d_count) hi.d_count = out->d_count + h;
     if (out->d_touched) hi.d_touched = out->d_touched + h;
     if (out->d_total) hi.d_total = out->d_total + h;
-    const int r0 = search_batched(store, prm, d_queries, h, d_seg_bucket, nseg, &lo, d_work,
-                                  work_bytes, stream);
+    const int r0 = search_batched_core(store, prm, d_queries, h, d_seg_bucket, nseg, &lo, d_work,
+                                       work_bytes, stream, flags_out, side_slot);
     if (r0 != PDX_OK) return r0;
-    return search_batched(store, prm, d_queries + h * store->d, nq64 - h,
-                          d_seg_bucket + h * nseg, nseg, &hi, d_work, work_bytes, stream);
+    return search_batched_core(store, prm, d_queries + h * store->d, nq64 - h,
+                               d_seg_bucket + h * nseg, nseg, &hi, d_work, work_bytes, stream,
+                               flags_out ? flags_out + h : nullptr, side_slot);
   }
   unsigned char* base = nullptr;
   PDX_CUDA_CHECK(cudaMallocAsync(&base, bytes, st));
@@ -1809,7 +1817,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   BatchProfile& prof = batch_profile();
   cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap_st);
-  const bool timing = prof.enabled && cap_st == cudaStreamCaptureStatusNone;
+  const bool timing = prof.enabled && cap_st == cudaStreamCaptureStatusNone && !flags_out;
   int nev = 0;
   if (timing) cudaEventRecord(prof.ev[nev++], st);
   auto phase = [&](const char* name) {
@@ -1851,7 +1859,7 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   // The work lists (below) and phase 1 (after them) only share bprep's
   // outputs: build the lists on a side stream while phase 1 runs; the main
   // stream joins before phase 2.
-  SideStream& side = side_stream();
+  SideStream& side = side_stream(side_slot);
   cudaStream_t st2 = side.s;
   PDX_B_CHECK(cudaEventRecord(side.fork, st));
   PDX_B_CHECK(cudaStreamWaitEvent(st2, side.fork, 0));
@@ -2044,9 +2052,14 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   PDX_B_CHECK(cudaGetLastError());
   phase("final");
   // ---- fallback: flagged queries through the per-query scan
-  rc = search_classic(store, prm, d_queries, nq64, d_seg_bucket, nseg, out, d_work, work_bytes,
-                      stream, flags);
-  if (rc != PDX_OK) return fail(rc);
+  if (flags_out) {
+    PDX_B_CHECK(cudaMemcpyAsync(flags_out, flags, sizeof(int32_t) * nq, cudaMemcpyDeviceToDevice,
+                                st));
+  } else {
+    rc = search_classic(store, prm, d_queries, nq64, d_seg_bucket, nseg, out, d_work, work_bytes,
+                        stream, flags);
+    if (rc != PDX_OK) return fail(rc);
+  }
   phase("fallback");
   if (getenv("PDX_BATCH_DEBUG")) {  // development aid: work items, uncertain pairs, fallbacks
     int32_t h[1] = {0};
@@ -2070,6 +2083,57 @@ int search_batched(const pdx_store* store, const pdx_search_params* prm, const f
   }
   return PDX_OK;
 #undef PDX_B_CHECK
+}
+
+
+// The batch as `parts` query chunks, each its own pipeline instance on its
+// own stream, forked from and joined back to the caller's: one chunk's
+// latency-bound phases (phase 1, the chain) overlap another's issue-bound
+// scan.  The fallback for every flagged query runs once after the join.
+// PDX_BATCH_SPLIT=n sets the number of chunks (default 1: one instance).
+int search_batched(const pdx_store* store, const pdx_search_params* prm, const float* d_queries,
+                   int64_t nq64, const int32_t* d_seg_bucket, int32_t nseg,
+                   const pdx_search_out* out, void* d_work, int64_t work_bytes, void* stream) {
+  static const int split = [] {
+    const char* e = getenv("PDX_BATCH_SPLIT");
+    const int v = e ? atoi(e) : 1;
+    return v < 1 ? 1 : (v > 4 ? 4 : v);
+  }();
+  const int parts = (int)std::min<int64_t>(split, nq64 / 128);
+  if (parts <= 1 || out->d_trace || !out->d_count)
+    return search_batched_core(store, prm, d_queries, nq64, d_seg_bucket, nseg, out, d_work,
+                               work_bytes, stream, nullptr, 0);
+  cudaStream_t st = as_stream(stream);
+  const int k = prm->k;
+  int32_t* flags_all = nullptr;
+  PDX_CUDA_CHECK(cudaMallocAsync(&flags_all, sizeof(int32_t) * nq64, st));
+  SideStream& root = side_stream(4);
+  PDX_CUDA_CHECK(cudaEventRecord(root.fork, st));
+  int rc = PDX_OK;
+  for (int pi = 0; pi < parts && rc == PDX_OK; ++pi) {
+    const int64_t q0 = nq64 * pi / parts, q1 = nq64 * (pi + 1) / parts;
+    SideStream& ps = side_stream(4 + pi);
+    PDX_CUDA_CHECK(cudaStreamWaitEvent(ps.s, root.fork, 0));
+    pdx_search_out o = *out;
+    o.d_dist = out->d_dist + q0 * k;
+    o.d_ids = out->d_ids + q0 * k;
+    o.d_count = out->d_count + q0;
+    if (out->d_touched) o.d_touched = out->d_touched + q0;
+    if (out->d_total) o.d_total = out->d_total + q0;
+    rc = search_batched_core(store, prm, d_queries + q0 * store->d, q1 - q0,
+                             d_seg_bucket + q0 * nseg, nseg, &o, d_work, work_bytes, ps.s,
+                             flags_all + q0, pi);
+    PDX_CUDA_CHECK(cudaEventRecord(ps.join, ps.s));
+  }
+  for (int pi = 0; pi < parts; ++pi) PDX_CUDA_CHECK(cudaStreamWaitEvent(st, side_stream(4 + pi).join, 0));
+  if (rc != PDX_OK) {
+    cudaFreeAsync(flags_all, st);
+    return rc;
+  }
+  rc = search_classic(store, prm, d_queries, nq64, d_seg_bucket, nseg, out, d_work, work_bytes,
+                      stream, flags_all);
+  cudaFreeAsync(flags_all, st);
+  return rc;
 }
 
 }  // namespace pdx
