@@ -102,3 +102,80 @@ def test_sharded_search_equals_single_process(oracle, pruner, criteria):
                                   q, 10, 40, pruner=pruner, criteria=criteria)
     np.testing.assert_array_equal(got_i, ref["ids"])
     np.testing.assert_array_equal(got_d, ref["dist"])
+
+
+# ------------------------------------------ row-chunk shards (C5 layout)
+def _c5_problem():
+    """A small chunk-seeded mixture with C5's spectrum: 12 chunks of 700."""
+    from paper_2503_04422_b200.synthetic import c5_sigma, mixture_centres
+    d, nchunks, rows = 32, 12, 700
+    centres = mixture_centres(7, 40, d)
+    sig = c5_sigma(d)
+    return d, nchunks, rows, centres, sig
+
+
+def _c5_chunk(c, centres, rows, sig):
+    from paper_2503_04422_b200.synthetic import mixture_chunk
+    return mixture_chunk(7, c, rows, centres, sig)
+
+
+def _c5_worker(rank, world, port, pruner, ret):
+    """Rank r generates ONLY its chunks c = r, r + world, ... (chunk-seeded),
+    assigns them to the replicated centroids, scans its rows (the oracle
+    stands in for the GPU scan on this CPU box) and joins the single packed
+    all-gather + merge."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    d, nchunks, rows, centres, sig = _c5_problem()
+    cents = np.ascontiguousarray(_c5_chunk(0, centres, rows, sig)[:24])  # rank 0's sample
+    t = torch.from_numpy(cents)
+    dist.broadcast(t, src=0)  # the replicated centroids, as build_rank_index does
+    cents = t.numpy()
+    mine = list(range(rank, nchunks, world))
+    xs = [_c5_chunk(c, centres, rows, sig) for c in mine]
+    x = np.concatenate(xs)
+    gid = np.concatenate([np.arange(c * rows, (c + 1) * rows) for c in mine]).astype(np.int64)
+    assign = np.argmin(((x[:, None, :] - cents[None]) ** 2).sum(-1), axis=1)
+    view = O.IvfView.from_assignment(x, cents, assign, cents.shape[0])
+    view.buckets.ids[:] = gid[view.buckets.ids]  # global row ids
+    q = np.ascontiguousarray(_c5_chunk(99, centres, 16, sig))
+    local = O.ivf_search_batch(view, q, 10, 8, pruner=pruner)
+    d_, i_ = gather_merge(torch.from_numpy(local["dist"]), torch.from_numpy(local["ids"]), 10,
+                          merge=merge_host)
+    ret[rank] = (d_.numpy(), i_.numpy(), len(mine) * rows)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pruner", ["bond", "none"])
+def test_row_chunk_shards_world4_equal_single_process(oracle, pruner):
+    """World size 4: no rank generates or holds another rank's chunks; the
+    merged top-k (one packed all_gather) equals the single-process search
+    on the whole collection for the exact pruners, on every rank."""
+    port = _free_port()
+    world = 4
+    with mp.Manager() as mgr:
+        ret = mgr.dict()
+        mp.spawn(_c5_worker, args=(world, port, pruner, ret), nprocs=world, join=True)
+        res = dict(ret)
+    d, nchunks, rows, centres, sig = _c5_problem()
+    assert sum(res[r][2] for r in range(world)) == nchunks * rows
+    x = np.concatenate([_c5_chunk(c, centres, rows, sig) for c in range(nchunks)])
+    cents = np.ascontiguousarray(x[:24])
+    assign = np.argmin(((x[:, None, :] - cents[None]) ** 2).sum(-1), axis=1)
+    q = np.ascontiguousarray(_c5_chunk(99, centres, 16, sig))
+    ref = oracle.ivf_search_batch(oracle.IvfView.from_assignment(x, cents, assign, 24), q, 10, 8,
+                                  pruner=pruner)
+    for r in range(world):
+        np.testing.assert_array_equal(res[r][1], ref["ids"])
+        np.testing.assert_array_equal(res[r][0], ref["dist"])
+
+
+def test_pack_unpack_topk_roundtrip():
+    from paper_2503_04422_b200.sharded import pack_topk, unpack_topk
+    rng = np.random.default_rng(3)
+    dd = torch.from_numpy(rng.standard_normal((5, 7)).astype(np.float32))
+    ii = torch.from_numpy(rng.integers(-1, 1 << 40, (5, 7)))
+    b = pack_topk(dd, ii)
+    d2, i2 = unpack_topk(torch.stack([b, b]), 5, 7)
+    assert torch.equal(d2[1], dd) and torch.equal(i2[0], ii)
