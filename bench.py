@@ -240,6 +240,8 @@ def main():
                     help="pdx_search_params.batched: 0 auto, 1 per-query scan, 2 batched")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        args.no_extras = True  # the extras (BSA index, GPU build) are single-GPU measurements
     args.warps = tuple(int(v) for v in str(args.warps).split(",")) if "," in str(args.warps) else int(args.warps)
 
     ws, rank, local = dist_env()
@@ -273,18 +275,20 @@ def main():
     col = P.VectorCollection.from_array(XR)
     fx = load_fixture(XR)
     t0 = time.perf_counter()
-    if fx is not None:
-        cent, assign, same = fx
-        index = P.IvfIndex.from_assignment(col, cent, assign, nlist=NLIST, x_dev=x_dev)
-        config["index_data_fingerprint_match"] = same
-    else:  # other sizes: this repo's GPU k-means (same algorithm, index.py:27-64)
-        index = P.ivf_build(col, nlist=NLIST, seed=0, x_dev=x_dev)
+    if fx is None:  # other sizes: this repo's GPU k-means (same algorithm, index.py:27-64)
+        cent, assign = P.index.lloyd_kmeans_device(x_dev, NLIST, 0)
+        cent, assign = cent.cpu().numpy(), assign.cpu().numpy().astype(np.int64)
         config["index"] = "GPU lloyd_kmeans (no reference fixture for this n)"
+    else:
+        cent, assign, same = fx
+        config["index_data_fingerprint_match"] = same
+    if ws > 1:  # this rank packs only the buckets it owns (LPT by size)
+        from paper_2503_04422_b200.sharded import shard_from_assignment
+        index = shard_from_assignment(XR, cent, assign, rank, ws, x_dev=x_dev, nlist=NLIST)
+    else:
+        index = P.IvfIndex.from_assignment(col, cent, assign, nlist=NLIST, x_dev=x_dev)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
-    if ws > 1:
-        from paper_2503_04422_b200.sharded import shard_index
-        index = shard_index(index, col, rank, ws, x_dev=x_dev)
     del x_dev
     params = P.SearchParams(k=K, pruner="ads", ads=P.AdsPruner(d=D, epsilon0=EPS))
     searcher = P.IvfSearcher(index, params, args.nprobe, warps=args.warps, batched=args.batched)
