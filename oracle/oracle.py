@@ -242,7 +242,7 @@ def search(blocks, query, k, metric="l2", pruner="none", selection_fraction=0.2,
            initial_step=2, ads_d=None, eps0=2.1, orders=None, survivors_cap=1 << 20,
            bsa_coef=None):
     """search (search.py:177-205).  Returns (items, stats dict)."""
-    bl = blocks if isinstance(blocks, BlockList) else BlockList(blocks)
+    bl = blocks if isinstance(blocks, (BlockList, PackedBlocks)) else BlockList(blocks)
     q = np.ascontiguousarray(query, dtype=np.float32)
     p = _params(k, metric, pruner, selection_fraction, initial_step,
                 ads_d if ads_d is not None else bl.d, eps0, bsa_coef)
@@ -387,7 +387,7 @@ def exact_search_batch(blocks, global_means, queries, k, metric="l2", pruner="no
                        criteria="sequential", zone_width=None, selection_fraction=0.2,
                        initial_step=2, ads_d=None, eps0=2.1, nthreads=None, survivors_cap=0,
                        bsa_coef=None):
-    bl = blocks if isinstance(blocks, BlockList) else BlockList(blocks)
+    bl = blocks if isinstance(blocks, (BlockList, PackedBlocks)) else BlockList(blocks)
     Q = np.ascontiguousarray(queries, dtype=np.float32)
     mu = np.ascontiguousarray(global_means, dtype=np.float64)
     nq = Q.shape[0]

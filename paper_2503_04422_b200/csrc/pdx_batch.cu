@@ -1986,7 +1986,11 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   auto scan = [&](int mode) -> cudaError_t {
     // wide vectors: survivors of the head are many and long — the dense
     // continuation variant (all live queries of a tile advance together)
-    const bool dense = store->d > 256;
+    static const int dense_env = [] {
+      const char* e = getenv("PDX_BSCAN_DENSE");
+      return e ? atoi(e) : -1;
+    }();
+    const bool dense = dense_env >= 0 ? dense_env != 0 : store->d > 256;
     int nsm = 148, dv = 0;
     cudaGetDevice(&dv);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
