@@ -1039,72 +1039,88 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     uint32_t live = 0;  // DENSE: queries with live slots after the head
     int nlive = 0;      // DENSE: live (query, slot) pairs
 
-    // finish the queued deep items, one per lane (all belong to this tile)
+    // finish the queued deep items, one per lane (all belong to this tile and
+    // sit at the same schedule position: they were queued together after the
+    // head or the dense continuation).  Step by step: a pass over the queue
+    // accumulates the step's dims for 32 items per warp iteration and takes
+    // the step's decision; the survivors are compacted to the front of the
+    // queue for the next step, so dead items stop costing lanes.
     auto flush = [&]() {
       __syncwarp();
-      for (int b = 0; b < qn; b += 32) {
-        bool act = b + lane < qn;
-        const DeepItem di = act ? s_deep[w][b + lane] : DeepItem{0.f, 0, 0, 0.f, 0, 0};
-        const int j = di.j, slot = di.slot;
-        const int q = s_qid[j];
-        const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
-        const bool q4 = (P.d & 3) == 0;
-        float acc = di.acc;
-        int s = di.s, pos = di.pos;
-        int nend = s_ends[s];
-        while (act) {
-          const int g = pos >> 3;
-          float x[8], qv[8];
-          ldg8(tb + ((size_t)g * kTile + slot) * 8, x);
-          if (q4 && g * 8 + 8 <= P.d) {
-            const float4 a = ldg4(qg + g * 8), c = ldg4(qg + g * 8 + 4);
-            qv[0] = a.x; qv[1] = a.y; qv[2] = a.z; qv[3] = a.w;
-            qv[4] = c.x; qv[5] = c.y; qv[6] = c.z; qv[7] = c.w;
-          } else {
+      if (qn == 0) return;
+      int n = qn;
+      int s = s_deep[w][0].s, pos = s_deep[w][0].pos;
+      const bool q4 = (P.d & 3) == 0;
+      while (n > 0 && s < nsteps) {
+        const int a = pos, bend = s_ends[s];
+        int nn = 0;
+        for (int base = 0; base < n; base += 32) {
+          const bool act = base + lane < n;
+          const DeepItem di = act ? s_deep[w][base + lane] : DeepItem{0.f, 0, 0, 0.f, 0, 0};
+          const int j = di.j, slot = di.slot;
+          const int q = s_qid[j];
+          const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
+          float acc = di.acc;
+          if (act) {
+            for (int g = a >> 3; g * 8 < bend; ++g) {
+              float x[8], qv[8];
+              ldg8(tb + ((size_t)g * kTile + slot) * 8, x);
+              if (q4 && g * 8 + 8 <= P.d) {
+                const float4 u = ldg4(qg + g * 8), c = ldg4(qg + g * 8 + 4);
+                qv[0] = u.x; qv[1] = u.y; qv[2] = u.z; qv[3] = u.w;
+                qv[4] = c.x; qv[5] = c.y; qv[6] = c.z; qv[7] = c.w;
+              } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + g * 8 + e) : 0.f;
-          }
-          if (pos == g * 8 && g * 8 + 8 < nend) {  // no step ends in this group
+                for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + g * 8 + e) : 0.f;
+              }
+              if (g * 8 >= a && g * 8 + 8 <= bend) {  // a whole group inside the step
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc = l2upd(acc, qv[e], x[e]);
-            pos += 8;
-            continue;
-          }
+                for (int e = 0; e < 8; ++e) acc = l2upd(acc, qv[e], x[e]);
+              } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int dim = g * 8 + e;
-            if (act && dim >= pos) {
-              acc = l2upd(acc, qv[e], x[e]);
-              if (dim + 1 == nend) {
-                float v = acc;
-                if (BSA) {
-                  const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
-                  v = bsa_est2(acc, __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + slot),
-                               bq[s], bq[nsteps + s], s_coef[s]);
-                }
-                const float B = MODE == 0 ? s_bnd[j][s] : bound_at(P, di.that, s, s_ratio, s_band);
-                const bool ok = v < B;
-                if (ok) {
-                  atomicAdd(&s_dcnt[w][j][s], 1u);
-                  if (MODE == 0)
-                    atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
-                }
-                ++s;
-                nend = s < nsteps ? s_ends[s] : 0x7fffffff;
-                if (!ok) {
-                  act = false;
-                } else if (s == nsteps) {
-                  if (MODE == 0)
-                    record_survivor(P, A, q, s_base[j] + ti, acc, tile, slot);
-                  else
-                    confirm_survivor(P, A, q, s_base[j] + ti, slot);
-                  act = false;
+                for (int e = 0; e < 8; ++e) {
+                  const int dim = g * 8 + e;
+                  if (dim >= a && dim < bend) acc = l2upd(acc, qv[e], x[e]);
                 }
               }
             }
           }
-          pos = (g + 1) * 8;
+          bool ok = false;
+          if (act) {
+            float v = acc;
+            if (BSA) {
+              const float* bq = A.bsaq + (int64_t)q * 2 * nsteps;
+              v = bsa_est2(acc, __ldg(A.resid + ((size_t)tile * nsteps + s) * kTile + slot), bq[s],
+                           bq[nsteps + s], s_coef[s]);
+            }
+            const float B = MODE == 0 ? s_bnd[j][s] : bound_at(P, di.that, s, s_ratio, s_band);
+            ok = v < B;
+            if (ok) {
+              atomicAdd(&s_dcnt[w][j][s], 1u);
+              if (MODE == 0)
+                atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
+              if (s + 1 == nsteps) {
+                if (MODE == 0)
+                  record_survivor(P, A, q, s_base[j] + ti, acc, tile, slot);
+                else
+                  confirm_survivor(P, A, q, s_base[j] + ti, slot);
+                ok = false;
+              }
+            }
+          }
+          // compact the survivors to the front (positions < base + 32: this
+          // batch has been read by every lane, later batches are not touched)
+          const unsigned keep = __ballot_sync(kFull, ok);
+          __syncwarp();
+          if (ok)
+            s_deep[w][nn + __popc(keep & ((1u << lane) - 1u))] =
+                DeepItem{acc, (int16_t)j, (int16_t)slot, di.that, (int16_t)(s + 1), (int16_t)bend};
+          nn += __popc(keep);
+          __syncwarp();
         }
+        n = nn;
+        pos = bend;
+        ++s;
       }
       __syncwarp();
       qn = 0;
