@@ -1188,6 +1188,9 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
             acc0 = a.x;
             acc1 = a.y;
             step(s, s == 0 ? ib0 : s == 1 ? ib1 : s == 2 ? ib2 : ib3);
+            // every slot of the pair already pruned: the rest of the head
+            // would only add dead dims (its counts stay 0, no deep items)
+            if (s >= 1 && s + 1 < HS && !__any_sync(kFull, al0 || al1)) break;
           }
         }
       } else {
