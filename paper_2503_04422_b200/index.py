@@ -274,12 +274,80 @@ def ivf_build(collection: VectorCollection, nlist: int | None = None, seed: int 
 
 
 # --------------------------------------------------------------- selection
-def select_buckets_device(index: IvfIndex, Q, nprobe: int, metric=Metric.L2, scratch=None):
-    """Kernel K2 for a device batch: int32 [nq, nprobe] bucket ids."""
+# Bucket selection on the tensor cores pays once the centroid scan is a real
+# GEMM (C5: 10,000 queries x 65,536 centroids x 768 dims).
+TC_SELECT_MIN_WORK = 1 << 34  # nq * nlist * d
+
+
+def _select_tensor_cores(index: IvfIndex, Q, nprobe: int, metric: Metric):
+    """ivf_select_buckets (index.py:111-127) for a batch through K8: tcgen05
+    TF32 candidates of the nprobe nearest centroids (pdx_k8_candidates), then
+    the candidates' exact keys with the reference's arithmetic (the vertical
+    kernel over the centroid chain: per-op-rounded sequential float32) and the
+    nprobe smallest (key, bucket) — the stable argsort's order
+    (pdx_k8_rescore_rows).  Identical to K2.  None when a query's candidates
+    overflow (the caller runs K2)."""
+    import ctypes as C
+
+    import torch
+    L = _lib.lib()
+    d, nlist, nq = index.d, index.nlist, Q.shape[0]
+    ld = (d + 3) // 4 * 4
+    tc = getattr(index, "_tc_select", None)
+    if tc is None:
+        X = torch.zeros((nlist, ld), dtype=torch.float32, device=Q.device)
+        X[:, :d] = index.centroids_dev
+        xn2 = torch.empty(nlist, dtype=torch.float32, device=Q.device)
+        _lib.check(L.pdx_k8_norms_ld(_lib.ptr(X), nlist, d, ld, _lib.ptr(xn2),
+                                     _lib.stream_handle()))
+        tc = index._tc_select = {"X": X, "xn2": xn2,
+                                 "rowids": torch.arange(nlist, dtype=torch.int64,
+                                                        device=Q.device)}
+    Qp = Q if ld == d else torch.nn.functional.pad(Q, (0, ld - d))
+    Qp = Qp.contiguous()
+    cap = max(4096, 4 * nprobe)
+    met = _lib.METRIC[metric.value]
+    cand = torch.empty((nq, cap), dtype=torch.int64, device=Q.device)
+    cnt = torch.zeros(nq, dtype=torch.int32, device=Q.device)
+    wb = C.c_int64(0)
+    args = (_lib.ptr(tc["X"]), nlist, d, ld, _lib.ptr(tc["xn2"]), _lib.ptr(Qp), nq, met, nprobe,
+            _lib.ptr(cand), _lib.ptr(cnt), cap)
+    _lib.check(L.pdx_k8_candidates(*args, None, C.cast(C.pointer(wb), C.c_void_p),
+                                   _lib.stream_handle()))
+    work = tc.get("work")
+    if work is None or work.numel() < wb.value:
+        work = tc["work"] = torch.empty(max(1, wb.value), dtype=torch.uint8, device=Q.device)
+    _lib.check(L.pdx_k8_candidates(*args, _lib.ptr(work), C.cast(C.pointer(wb), C.c_void_p),
+                                   _lib.stream_handle()))
+    cmax = int(cnt.max().item())
+    if cmax > cap:
+        return None
+    dist = torch.empty((nq, nprobe), dtype=torch.float32, device=Q.device)
+    ids = torch.empty((nq, nprobe), dtype=torch.int64, device=Q.device)
+    _lib.check(L.pdx_k8_rescore_rows(_lib.ptr(tc["X"]), ld, d, _lib.ptr(tc["rowids"]),
+                                     _lib.ptr(Qp), nq, met, nprobe, _lib.ptr(cand), _lib.ptr(cnt),
+                                     cap, max(1, cmax), _lib.ptr(dist), _lib.ptr(ids),
+                                     _lib.stream_handle()))
+    return ids.to(torch.int32)
+
+
+def select_buckets_device(index: IvfIndex, Q, nprobe: int, metric=Metric.L2, scratch=None,
+                          tensor_cores=None):
+    """Bucket selection for a device batch: int32 [nq, nprobe] bucket ids —
+    K2 (pdx_select_buckets), or, for GEMM-sized batches (tensor_cores None:
+    nq * nlist * d >= TC_SELECT_MIN_WORK) over L2 / IP, the tensor-core path
+    with identical results (_select_tensor_cores)."""
     import torch
     if not 1 <= nprobe <= index.nlist:
         raise ValueError(f"nprobe must be in [1, {index.nlist}], got {nprobe}")
     nq = Q.shape[0]
+    metric = Metric(metric)
+    use_tc = tensor_cores if tensor_cores is not None else (
+        nq * index.nlist * index.d >= TC_SELECT_MIN_WORK)
+    if use_tc and metric in (Metric.L2, Metric.IP) and nq > 0 and index.nlist >= nprobe:
+        sel = _select_tensor_cores(index, Q.contiguous(), nprobe, metric)
+        if sel is not None:
+            return sel
     if scratch is None or scratch.numel() < nq * index.nlist:
         scratch = torch.empty((nq * index.nlist,), dtype=torch.float32, device=Q.device)
     sel = torch.empty((nq, nprobe), dtype=torch.int32, device=Q.device)

@@ -562,3 +562,29 @@ def test_vertical_accumulate_ops(P, metric):
         P.vertical_accumulate(blk, q, (5, 38), metric, P.new_accumulator(64))
     with pytest.raises(ValueError):
         P.vertical_accumulate_selected(blk, q, (0, 3), metric, P.new_accumulator(64), [50])
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_select_buckets_tensor_cores_equal_k2(P, oracle, metric):
+    """Bucket selection through K8 (tcgen05 candidates + the reference's
+    exact centroid keys) = K2 = the oracle's stable argsort, incl. nprobe 1,
+    d not a multiple of 4 and duplicated centroids (ties -> lower bucket)."""
+    import torch
+    rng = np.random.default_rng(8)
+    for nlist, d, nq in ((5000, 100, 300), (9000, 37, 140)):
+        cents = rng.standard_normal((nlist, d)).astype(np.float32)
+        cents[7] = cents[3]
+        x = np.repeat(cents, 2, 0) + 0.01 * rng.standard_normal((2 * nlist, d)).astype(np.float32)
+        index = P.IvfIndex.from_assignment(P.VectorCollection.from_array(x), cents,
+                                           np.repeat(np.arange(nlist), 2), nlist=nlist)
+        Q = torch.from_numpy(cents[rng.integers(0, nlist, nq)] +
+                             0.5 * rng.standard_normal((nq, d)).astype(np.float32)).cuda()
+        for nprobe in (1, 64, 256):
+            a = P.index.select_buckets_device(index, Q, nprobe, metric, tensor_cores=True)
+            b = P.index.select_buckets_device(index, Q, nprobe, metric, tensor_cores=False)
+            np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+        view = _oracle_ivf(oracle, index, x)
+        qh = Q.cpu().numpy()
+        for i in range(0, nq, 37):
+            ref = oracle.select_buckets(view.cent, nlist, qh[i], metric, 256)
+            np.testing.assert_array_equal(a[i].cpu().numpy(), ref)

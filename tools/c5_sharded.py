@@ -106,6 +106,15 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         t_ms = float(np.median(ts))
+        sel_ms = []
+        for _ in range(3):  # the bucket-selection part alone (K2)
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s.select(q)
+            e1.record()
+            torch.cuda.synchronize()
+            sel_ms.append(e0.elapsed_time(e1))
         if ws > 1:
             tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -116,6 +125,7 @@ def main():
                 "queries": a.nq, "k": K, "pruner": pruner, "world": world, "rank": rank,
                 "rows_this_rank": rows_here, "chunks": nchunks, "chunk_rows": ROWS,
                 "batch_ms": t_ms, "qps": a.nq / (t_ms / 1e3),
+                "selection_ms": float(np.median(sel_ms)),
                 "timing": ("whole job: scan + packed all_gather + K7, max over ranks"
                            if ws > 1 else "this rank's scan only (emulated rank; one GPU)"),
                 "local_recall_at_10": rec,
