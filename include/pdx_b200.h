@@ -449,6 +449,21 @@ int pdx_k8_candidates(const float* d_x, int64_t n, int32_t d, int64_t ld, const 
                       const float* d_q, int64_t nq, int32_t metric, int32_t k, int64_t* d_cand,
                       int32_t* d_ccount, int32_t C, void* d_work, int64_t* work_bytes,
                       void* stream);
+/* The same pass with bf16 MMA operands (tcgen05 kind::f16: twice the
+ * tensor-core rate and half the operand bytes of tf32) and the interval
+ * widened for their round-to-nearest error, (2 * 2^-8 + 2^-16) |q||x|:
+ * d_x16 / d_q16 bf16 [rows][ld16] (pdx_k8_to_bf16 of the float32 rows; ld16
+ * a multiple of 8), d_q float32 [nq][ld] (the norms and the L2 expansion
+ * are those of the float32 vectors).  More candidates per query than the
+ * tf32 pass; the same exactness argument. */
+int pdx_k8_candidates_bf16(const void* d_x16, int64_t n, int32_t d, int64_t ld16,
+                           const float* d_xn2, const void* d_q16, const float* d_q, int64_t ld,
+                           int64_t nq, int32_t metric, int32_t k, int64_t* d_cand,
+                           int32_t* d_ccount, int32_t C, void* d_work, int64_t* work_bytes,
+                           void* stream);
+/* float32 rows (ld apart) -> bf16 rows (ld16 apart, zero padded), round to nearest. */
+int pdx_k8_to_bf16(const float* d_x, int64_t n, int32_t d, int64_t ld, int64_t ld16, void* d_y,
+                   void* stream);
 float pdx_k8_margin(int32_t d, int32_t metric);
 int pdx_k8_filter(const float* d_S, int64_t ldS, int64_t nq, int32_t R, int64_t row0,
                   const float* d_xn2, const float* d_qn2, int32_t metric, int32_t d, int32_t k,

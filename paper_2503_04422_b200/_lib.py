@@ -31,7 +31,8 @@ EXPORTS = ("pdx_abi_version", "pdx_last_error", "pdx_device_info", "pdx_pack_til
            "pdx_vertical_accumulate", "pdx_batch_profile", "pdx_row_norms",
            "pdx_kmeans_assign", "pdx_bucket_layout", "pdx_kmeans_update", "pdx_kmeans_shift",
            "pdx_kmeans_farthest", "pdx_gather_rows", "pdx_pack_rows", "pdx_k8_norms_ld",
-           "pdx_k8_candidates", "pdx_k8_rescore_rows")
+           "pdx_k8_candidates", "pdx_k8_rescore_rows", "pdx_k8_candidates_bf16",
+           "pdx_k8_to_bf16")
 
 
 class PdxStore(C.Structure):
@@ -150,6 +151,9 @@ def lib():
         L.pdx_gather_rows.argtypes = [vp, i32, vp, i64, vp, vp]
         L.pdx_pack_rows.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         L.pdx_k8_norms_ld.argtypes = [vp, i64, i32, i64, vp, vp]
+        L.pdx_k8_candidates_bf16.argtypes = [vp, i64, i32, i64, vp, vp, vp, i64, i64, i32, i32,
+                                             vp, vp, i32, vp, vp, vp]
+        L.pdx_k8_to_bf16.argtypes = [vp, i64, i32, i64, i64, vp, vp]
         L.pdx_k8_rescore_rows.argtypes = [vp, i64, i32, vp, vp, i64, i32, i32, vp, vp, i32, i32,
                                            vp, vp, vp]
         L.pdx_k8_candidates.argtypes = [vp, i64, i32, i64, vp, vp, i64, i32, i32, vp, vp, i32,

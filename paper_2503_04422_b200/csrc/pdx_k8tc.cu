@@ -23,15 +23,18 @@
 // 256-vector slice run back to back and the slice is read from HBM once.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 
 #include "pdx_common.cuh"
 
 namespace pdx {
 namespace {
 
-constexpr int kTM = 128, kTN = 256, kTK = 32;  // tile M (queries), N (vectors), K (floats)
+// Tile M (queries) x N (vectors) x one 128-byte swizzle row of K per stage:
+// 32 tf32 or 64 bf16 elements.
+constexpr int kTM = 128, kTN = 256, kRowBytes = 128;
 constexpr int kStages = 4;
-constexpr int kABytes = kTM * kTK * 4, kBBytes = kTN * kTK * 4;
+constexpr int kABytes = kTM * kRowBytes, kBBytes = kTN * kRowBytes;
 constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, each half the columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 /*align*/ + 256 /*barriers*/;
@@ -79,13 +82,21 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                    bar)
                : "memory");
 }
-__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+template <bool BF16>
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  if (BF16)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
 // K-major operand tile in 128-byte swizzle (rows of 32 floats, 8-row groups
 // 1024 B apart): start address, LBO 16 B (unused for swizzled K-major), SBO
@@ -94,9 +105,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: D f32, A/B tf32, both K-major, N = 256, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTN >> 3) << 17) |
-                            ((uint32_t)(kTM >> 4) << 24);
+// instruction descriptor: D f32, A/B tf32 (format 2) or bf16 (format 1),
+// both K-major, N = 256, M = 128
+template <bool BF16>
+__host__ __device__ constexpr uint32_t idesc_of() {
+  return (1u << 4) | ((BF16 ? 1u : 2u) << 7) | ((BF16 ? 1u : 2u) << 10) |
+         ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+}
 
 #define PDX_TMEM_LD32(taddr, r)                                                                   \
   asm volatile(                                                                                   \
@@ -111,7 +126,7 @@ constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTN
 
 struct K8Args {
   int64_t nq, r0, r1;  // queries; vector rows [r0, r1) of X
-  int nk;              // K blocks of 32 floats
+  int nk;              // K blocks of one 128-byte row (32 tf32 / 64 bf16 elements)
   int metric;
   float c, e2;         // pdx_k8_margin and the L2 expansion's relative term
   const float* qn2;    // [nq]
@@ -126,7 +141,7 @@ struct K8Args {
   int64_t ldS;
 };
 
-template <int MODE>
+template <int MODE, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                             const __grid_constant__ CUtensorMap tx,
                                                             const K8Args a) {
@@ -181,8 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           mbar_expect_tx(fb, kABytes + kBBytes);
-          tma_load_2d(sA + stage * kABytes, &tq, kb * kTK, qrow, fb);
-          tma_load_2d(sB + stage * kBBytes, &tx, kb * kTK, xrow, fb);
+          const int kel = kb * (BF16 ? 64 : 32);  // element column of this K block
+          tma_load_2d(sA + stage * kABytes, &tq, kel, qrow, fb);
+          tma_load_2d(sB + stage * kBBytes, &tx, kel, xrow, fb);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -207,9 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
           const uint64_t ad = smem_desc(sA + stage * kABytes);
           const uint64_t bd = smem_desc(sB + stage * kBBytes);
 #pragma unroll
-          for (int k = 0; k < kTK / 8; ++k)  // K = 8 tf32 = 32 bytes per MMA
-            tc_mma_tf32(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), kIdesc,
-                        (kb | k) != 0);
+          for (int k = 0; k < 4; ++k)  // 32 bytes per MMA: K = 8 tf32 / 16 bf16
+            tc_mma<BF16>(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k),
+                         idesc_of<BF16>(), (kb | k) != 0);
           tc_commit(empty0 + 8 * stage);  // the stage is free once these MMAs finish
           if (++stage == kStages) {
             stage = 0;
@@ -331,40 +347,64 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// rows x ld float32, row-major; box = 32 floats (128 B, one swizzle row) x box_rows
-int make_map(CUtensorMap* m, const float* p, int64_t rows, int64_t ld, int box_rows) {
+// rows x ld elements (float32 or bf16), row-major; box = one 128-byte
+// swizzle row of elements x box_rows
+int make_map(CUtensorMap* m, const void* p, int64_t rows, int64_t ld, int box_rows, bool bf16) {
   auto fn = encode_fn();
   PDX_REQUIRE(fn, "cuTensorMapEncodeTiled is unavailable (driver too old)");
+  const int es_bytes = bf16 ? 2 : 4;
   const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kTK, (cuuint32_t)box_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * es_bytes};
+  const cuuint32_t box[2] = {(cuuint32_t)(kRowBytes / es_bytes), (cuuint32_t)box_rows};
   const cuuint32_t es[2] = {1, 1};
-  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides,
+  const CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        2, const_cast<void*>(p), dims, strides,
                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PDX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return PDX_OK;
 }
 
+// float32 rows (ld floats apart) -> bf16 rows (ld16 elements apart, zero padded), RN
+__global__ void __launch_bounds__(256) to_bf16_kernel(const float* __restrict__ x, int64_t n, int d,
+                                                      int64_t ld, int64_t ld16,
+                                                      __nv_bfloat16* __restrict__ y) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= n) return;
+  for (int j = threadIdx.x & 31; j < ld16; j += 32)
+    y[r * ld16 + j] = __float2bfloat16_rn(j < d ? x[r * ld + j] : 0.f);
+}
+
 }  // namespace
+
+int k8_to_bf16(const float* d_x, int64_t n, int d, int64_t ld, int64_t ld16, void* d_y,
+               cudaStream_t st) {
+  if (n == 0) return PDX_OK;
+  to_bf16_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(d_x, n, d, ld, ld16,
+                                                          static_cast<__nv_bfloat16*>(d_y));
+  PDX_LAUNCH_CHECK();
+  return PDX_OK;
+}
 
 // The tensor-core pass over X rows [r0, r1) (mode 0: dense S; mode 1: fused
 // candidate filter).  Shared by pdx_k8_candidates (pdx_k8.cu).
-int k8_tc_pass(int mode, const float* d_x, int64_t n, int64_t ld, const float* d_q, int64_t nq,
-               int64_t r0, int64_t r1, int d, int metric, float c, float e2, const float* qn2,
-               const float* xn2, const float* tau, int64_t* cand, float* cand_lb, float* cand_ub,
-               int32_t* ccount, int C, float* S, int64_t ldS, cudaStream_t st) {
-  PDX_REQUIRE(ld % 4 == 0 && ld >= d, "row stride must be a multiple of 4 floats >= d");
+int k8_tc_pass(int mode, bool bf16, const void* d_x, int64_t n, int64_t ld, const void* d_q,
+               int64_t nq, int64_t r0, int64_t r1, int d, int metric, float c, float e2,
+               const float* qn2, const float* xn2, const float* tau, int64_t* cand,
+               float* cand_lb, float* cand_ub, int32_t* ccount, int C, float* S, int64_t ldS,
+               cudaStream_t st) {
+  PDX_REQUIRE(ld % (bf16 ? 8 : 4) == 0 && ld >= d, "row stride must be 16-byte aligned and >= d");
   PDX_REQUIRE(((uintptr_t)d_x & 15) == 0 && ((uintptr_t)d_q & 15) == 0, "rows must be 16-B aligned");
   if (r1 <= r0 || nq == 0) return PDX_OK;
   CUtensorMap tq, tx;
-  PDX_TRY(make_map(&tq, d_q, nq, ld, kTM));
-  PDX_TRY(make_map(&tx, d_x, n, ld, kTN));
+  PDX_TRY(make_map(&tq, d_q, nq, ld, kTM, bf16));
+  PDX_TRY(make_map(&tx, d_x, n, ld, kTN, bf16));
   K8Args a;
   a.nq = nq;
   a.r0 = r0;
   a.r1 = r1;
-  a.nk = (int)((d + kTK - 1) / kTK);
+  const int kel = bf16 ? 64 : 32;
+  a.nk = (int)((d + kel - 1) / kel);
   a.metric = metric;
   a.c = c;
   a.e2 = e2;
@@ -383,15 +423,18 @@ int k8_tc_pass(int mode, const float* d_x, int64_t n, int64_t ld, const float* d
   PDX_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const int64_t tiles = ((nq + kTM - 1) / kTM) * ((r1 - r0 + kTN - 1) / kTN);
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, nsm);
+#define PDX_K8TC(M, B)                                                                      \
+  do {                                                                                      \
+    PDX_CUDA_CHECK(cudaFuncSetAttribute(k8_tc_kernel<M, B>,                                 \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)); \
+    k8_tc_kernel<M, B><<<grid, kThreads, kSmem, st>>>(tq, tx, a);                           \
+  } while (0)
   if (mode == 0) {
-    PDX_CUDA_CHECK(cudaFuncSetAttribute(k8_tc_kernel<0>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    k8_tc_kernel<0><<<grid, kThreads, kSmem, st>>>(tq, tx, a);
+    if (bf16) PDX_K8TC(0, true); else PDX_K8TC(0, false);
   } else {
-    PDX_CUDA_CHECK(cudaFuncSetAttribute(k8_tc_kernel<1>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    k8_tc_kernel<1><<<grid, kThreads, kSmem, st>>>(tq, tx, a);
+    if (bf16) PDX_K8TC(1, true); else PDX_K8TC(1, false);
   }
+#undef PDX_K8TC
   PDX_LAUNCH_CHECK();
   return PDX_OK;
 }

