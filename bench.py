@@ -259,10 +259,15 @@ def main():
 
     import torch
     if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()  # (ranks share a GPU only in a gloo smoke run)
         torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PDX_DIST_BACKEND", "nccl")  # gloo: a one-GPU smoke test
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2503_04422_b200 as P
     from paper_2503_04422_b200 import _lib
     _lib.lib()

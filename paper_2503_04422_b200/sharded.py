@@ -209,7 +209,10 @@ def gather_merge(dist, ids, k: int, group=None, merge=merge_device):
     world = dist_.get_world_size(group)
     nq = dist.shape[0]
     buf = pack_topk(dist.contiguous(), ids.contiguous())
+    dev = buf.device
+    if dev.type == "cuda" and dist_.get_backend(group) != "nccl":
+        buf = buf.cpu()  # gloo moves host tensors
     out = torch.empty(world * buf.numel(), dtype=torch.int32, device=buf.device)
     dist_.all_gather_into_tensor(out, buf, group=group)
-    d_all, i_all = unpack_topk(out.view(world, -1), nq, k)
+    d_all, i_all = unpack_topk(out.view(world, -1).to(dev), nq, k)
     return merge(d_all, i_all, k)
