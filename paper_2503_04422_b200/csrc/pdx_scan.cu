@@ -194,6 +194,12 @@ extern "C" int64_t pdx_search_workspace(const pdx_store* store, int64_t nq, int3
   return 512 + nq * (int64_t)sizeof(int32_t) + 256 + nq * maxvis * (int64_t)sizeof(TileEntry) + 256;
 }
 
+namespace pdx {
+int linear_split_scan(const pdx_store* store, int metric, int k, const float* d_queries,
+                      int64_t nq, int nsplit, float* tdist, int64_t* tids, int64_t* touched,
+                      int64_t* total, cudaStream_t st, bool* applied);
+}
+
 static int search_impl(const pdx_store* store, const pdx_search_params* prm,
                        const float* d_queries, int64_t nq, const int32_t* d_seg_bucket,
                        int32_t nseg, const uint16_t* d_orders, int64_t order_qstride,
@@ -361,11 +367,17 @@ static int search_impl(const pdx_store* store, const pdx_search_params* prm,
     pool_kept = true;
   }
 
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
   const bool ord = d_orders != nullptr;
   const int mt = prm->pruner == PDX_PRUNER_BSA ? kMetricL2Bsa : prm->metric;
   const int grid = (int)(nq * nsplit);
-  if (store->group == 8)
+  bool linear = false;  // an unpruned split scan streams (pdx_linear.cu)
+  if (nsplit > 1 && prm->pruner == PDX_PRUNER_NONE && !ord && !d_seg_bucket && !only &&
+      !out->d_debug && !getenv("PDX_NO_LINEAR"))
+    PDX_TRY(linear_split_scan(store, prm->metric, prm->k, d_queries, nq, nsplit, tdist, tids,
+                              A.out_touched, A.out_total, st, &linear));
+  if (linear) {
+  } else if (store->group == 8)
     e = ord ? launch_metric<8, true>(mt, A, L, grid, W, tpw, st)
             : launch_metric<8, false>(mt, A, L, grid, W, tpw, st);
   else

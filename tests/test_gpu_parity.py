@@ -589,3 +589,20 @@ def test_select_buckets_tensor_cores_equal_k2(P, oracle, metric):
         for i in range(0, nq, 37):
             ref = oracle.select_buckets(view.cent, nlist, qh[i], metric, 256)
             np.testing.assert_array_equal(a[i].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("metric,k,d,psize,splits", [("l1", 7, 37, 1000, 50), ("l2", 300, 24, 64, 37),
+                                                     ("ip", 1, 130, 333, 148)])
+def test_split_mode_streaming_exact(P, metric, k, d, psize, splits):
+    """Unpruned split scans take the streaming kernel (pdx_linear.cu): the
+    exact top-k of the single-chain scan with the same stats, incl. d not a
+    multiple of 8, wide partitions whose last tile is partly padding, k up to
+    300 and more splits than blocks in some ranges."""
+    x = recipes.data("normal", 30_000, d, 53)
+    Q = recipes.queries("near", x, 9, 54)
+    flat = P.flat_build(P.VectorCollection.from_array(x), psize, group=8)
+    params = P.SearchParams(k=k, metric=metric, pruner="none")
+    one = P.exact_search_batch(flat, Q, params, stats=True)
+    many = P.exact_search_batch(flat, Q, params, stats=True, splits=splits)
+    for key in ("ids", "dist", "count", "touched", "total"):
+        np.testing.assert_array_equal(many[key], one[key])
