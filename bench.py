@@ -323,11 +323,12 @@ def main():
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    # One GPU: the step as two CUDA graphs (fixed device buffers, inputs
-    # resident) — projection + bucket selection, then the search — so the
-    # ~30 launches of a step leave no host gaps; events between the replays
-    # time the search.  The replayed results are checked against the direct
-    # path.  (Multi-GPU steps end in an NCCL gather: launched directly.)
+    # One GPU: the step as one CUDA graph (fixed device buffers, inputs
+    # resident: projection + bucket selection + the search), so the ~30
+    # launches of a step leave no host gaps; the search alone is timed from a
+    # two-graph split (events between the replays).  The replayed results are
+    # checked against the direct path.  (Multi-GPU steps end in an NCCL
+    # gather: launched directly.)
     graphs = None
     if ws == 1:
         gs = torch.cuda.Stream()
@@ -342,20 +343,26 @@ def main():
         with torch.cuda.stream(gs):
             searcher.search(Qr_g, pre())  # warm on the capture stream
             torch.cuda.synchronize()
-            g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            g1, g2, gall = (torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(),
+                            torch.cuda.CUDAGraph())
             with torch.cuda.graph(g1, stream=gs):
                 sel_g = pre()
             with torch.cuda.graph(g2, stream=gs):
                 res_g = searcher.search(Qr_g, sel_g)
+            with torch.cuda.graph(gall, stream=gs):  # the whole step as one launch
+                res_all = searcher.search(Qr_g, pre())
         torch.cuda.synchronize()
         g1.replay()
         g2.replay()
+        gall.replay()
         torch.cuda.synchronize()
         d_ref, i_ref = step(Qd)
         torch.cuda.synchronize()
         assert torch.equal(res_g.ids, i_ref) and torch.equal(res_g.dist, d_ref), \
             "graph replay differs from the direct search"
-        graphs = (g1, g2)
+        assert torch.equal(res_all.ids, i_ref) and torch.equal(res_all.dist, d_ref), \
+            "graph replay differs from the direct search"
+        graphs = (g1, g2, gall)
     step_ms, scan_ms = [], []
     with Clocks(local) as clk:
         for _ in range(args.steps):
@@ -364,16 +371,25 @@ def main():
             torch.cuda.synchronize()
             ev[0].record()
             if graphs:
-                graphs[0].replay()
-                ev[1].record()
-                graphs[1].replay()
-                ev[2].record()
+                graphs[2].replay()
             else:
                 step(Qd, ev=ev)
             ev[3].record()
             torch.cuda.synchronize()
             step_ms.append(ev[0].elapsed_time(ev[3]))
-            scan_ms.append(ev[1].elapsed_time(ev[2]))
+            if not graphs:
+                scan_ms.append(ev[1].elapsed_time(ev[2]))
+    if graphs:  # the search part alone: the two-graph split, events between
+        for _ in range(max(5, args.steps // 2)):
+            flush.fill_(1)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda.synchronize()
+            graphs[0].replay()
+            ev[0].record()
+            graphs[1].replay()
+            ev[1].record()
+            torch.cuda.synchronize()
+            scan_ms.append(ev[0].elapsed_time(ev[1]))
     t_step = float(np.mean(step_ms))
     t_scan = float(np.mean(scan_ms))
     if ws > 1:

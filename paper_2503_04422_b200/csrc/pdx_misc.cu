@@ -66,50 +66,51 @@ __global__ void __launch_bounds__(256) pack_kernel(const float* __restrict__ x, 
 }
 
 // ------------------------------------------------------------------- K3
-// y = x @ M^T, float32 (FMA) — apply_transform (pruning.py:48-53).
-constexpr int kPT = 64, kPK = 16;
+// y = x @ M^T, float32 (FMA) — apply_transform (pruning.py:48-53).  A CTA
+// computes 16 rows x 64 columns (a thread: one row, four columns) over K
+// chunks of 32 staged in shared memory: small tiles, so a 1,000-query batch
+// still spreads over ~128 CTAs (the projection sits on the search's
+// critical path).
+constexpr int kPR = 16, kPC = 64, kPK = 32;
 
 __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ x, int64_t n, int d,
                                                       const float* __restrict__ M,
                                                       float* __restrict__ y) {
-  __shared__ float xs[kPK][kPT + 4];
-  __shared__ float ms[kPK][kPT + 4];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t r0 = (int64_t)blockIdx.y * kPT;
-  const int c0 = blockIdx.x * kPT;
-  float acc[4][4] = {};
+  __shared__ float xs[kPK][kPR + 1];
+  __shared__ float ms[kPK][kPC + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // cols tx*4..+3, row ty
+  const int64_t r0 = (int64_t)blockIdx.y * kPR;
+  const int c0 = blockIdx.x * kPC;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int j0 = 0; j0 < d; j0 += kPK) {
-#pragma unroll
-    for (int it = 0; it < (kPT * kPK) / 256; ++it) {
-      const int e = threadIdx.x + 256 * it;
+    for (int e = threadIdx.x; e < kPR * kPK; e += 256) {
       const int r = e / kPK, c = e % kPK;
       const int dj = j0 + c;
       xs[c][r] = (r0 + r < n && dj < d) ? x[(r0 + r) * d + dj] : 0.f;
+    }
+    for (int e = threadIdx.x; e < kPC * kPK; e += 256) {
+      const int r = e / kPK, c = e % kPK;
+      const int dj = j0 + c;
       ms[c][r] = (c0 + r < d && dj < d) ? M[(int64_t)(c0 + r) * d + dj] : 0.f;
     }
     __syncthreads();
-#pragma unroll
+#pragma unroll 8
     for (int jj = 0; jj < kPK; ++jj) {
-      float xv[4], mv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) xv[i] = xs[jj][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) mv[j] = ms[jj][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xv[i], mv[j], acc[i][j]);
+      const float xv = xs[jj][ty];
+      const float4 mv = *reinterpret_cast<const float4*>(&ms[jj][tx * 4]);
+      acc[0] = fmaf(xv, mv.x, acc[0]);
+      acc[1] = fmaf(xv, mv.y, acc[1]);
+      acc[2] = fmaf(xv, mv.z, acc[2]);
+      acc[3] = fmaf(xv, mv.w, acc[3]);
     }
     __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + ty * 4 + i;
-    if (r >= n) continue;
+  const int64_t r = r0 + ty;
+  if (r < n) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = c0 + tx * 4 + j;
-      if (c < d) y[r * d + c] = acc[i][j];
+      if (c < d) y[r * d + c] = acc[j];
     }
   }
 }
@@ -380,10 +381,13 @@ extern "C" int pdx_project(const float* d_x, int64_t n, int32_t d, const float* 
   PDX_REQUIRE(d >= 1 && n >= 0, "bad sizes");
   PDX_REQUIRE(d_x != d_y, "pdx_project: output must not alias input");
   if (n == 0) return PDX_OK;
-  PDX_REQUIRE((n + kPT - 1) / kPT <= 65535, "too many rows for one launch");
-  dim3 grid((d + kPT - 1) / kPT, (unsigned)((n + kPT - 1) / kPT));
-  project_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_x, n, d, d_matrix, d_y);
-  PDX_LAUNCH_CHECK();
+  const int64_t per = (int64_t)65535 * kPR;  // rows per launch (grid.y limit)
+  for (int64_t r = 0; r < n; r += per) {
+    const int64_t m = n - r < per ? n - r : per;
+    dim3 grid((d + kPC - 1) / kPC, (unsigned)((m + kPR - 1) / kPR));
+    project_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_x + r * d, m, d, d_matrix, d_y + r * d);
+    PDX_LAUNCH_CHECK();
+  }
   return PDX_OK;
 }
 

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) select_warp_kernel(const float* __restric
   for (int size = 2; size <= n2; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int t = lane; t < n2 / 2; t += 32) {
-        const int i = (t / stride) * stride * 2 + (t % stride), jn = i + stride;
+        const int i = 2 * t - (t & (stride - 1)), jn = i + stride;  // stride: a power of two
         const bool asc = (i & size) == 0;
         const uint64_t a = c[i], b = c[jn];
         if ((a > b) == asc) {
