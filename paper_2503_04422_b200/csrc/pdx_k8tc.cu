@@ -33,11 +33,11 @@ namespace {
 // Tile M (queries) x N (vectors) x one 128-byte swizzle row of K per stage:
 // 32 tf32 or 64 bf16 elements.
 constexpr int kTM = 128, kTN = 256, kRowBytes = 128;
-constexpr int kStages = 4;
+constexpr int kMaxStages = 6;
 constexpr int kABytes = kTM * kRowBytes, kBBytes = kTN * kRowBytes;
 constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, each half the columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kSmem = 4 * (kABytes + kBBytes) + 1024 /*align*/ + 16 * kMaxStages + 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -82,6 +82,59 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                    bar)
                : "memory");
 }
+// CTA-pair (cta_group::2) helpers: the cluster address of a CTA's variable,
+// remote arrives, the pair's TMA load (bytes counted on the leader's
+// barrier), the pair MMA and its multicast commit, the cluster barrier.
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0,
+                                                 int c1, uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+template <bool BF16>
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  if (BF16)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 template <bool BF16>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                        uint32_t idesc, uint32_t accumulate) {
@@ -107,10 +160,10 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
 }
 // instruction descriptor: D f32, A/B tf32 (format 2) or bf16 (format 1),
 // both K-major, N = 256, M = 128
-template <bool BF16>
+template <bool BF16, int M = kTM>
 __host__ __device__ constexpr uint32_t idesc_of() {
   return (1u << 4) | ((BF16 ? 1u : 2u) << 7) | ((BF16 ? 1u : 2u) << 10) |
-         ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+         ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 #define PDX_TMEM_LD32(taddr, r)                                                                   \
@@ -141,64 +194,94 @@ struct K8Args {
   int64_t ldS;
 };
 
-template <int MODE, bool BF16>
+// PAIR: a CTA pair (cluster of 2) shares each MMA (tcgen05.mma.cta_group::2,
+// M = 256): CTA r loads queries [m*256 + r*128, +128) and vectors
+// [n*256 + r*128, +128) of the tile, the leader (rank 0) issues the MMAs,
+// each CTA's TMEM holds its 128 query rows x 256 columns and its epilogue
+// filters them.  B operand bytes per CTA halve for the same FLOPs.
+template <int MODE, bool BF16, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                             const __grid_constant__ CUtensorMap tx,
                                                             const K8Args a) {
+  constexpr int BROWS = PAIR ? kTN / 2 : kTN;  // B rows this CTA stages
+  constexpr int BBYTES = BROWS * kRowBytes;
+  constexpr int MQ = PAIR ? 2 * kTM : kTM;  // queries per tile
+  constexpr int kStages = PAIR ? 6 : 4;     // (the same shared-memory budget)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   const uint32_t sA = base, sB = base + kStages * kABytes;
-  const uint32_t bars = sB + kStages * kBBytes;  // full[4] empty[4] tfull[2] tempty[2] tmem_ptr
+  const uint32_t bars = sB + kStages * BBYTES;  // full[S] empty[S] tfull[2] tempty[2] tmem_ptr
   const uint32_t full0 = bars, empty0 = bars + 8 * kStages, tfull0 = bars + 16 * kStages,
                  tempty0 = tfull0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 16 * kStages + 32 - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cta_rank() : 0u;
+  const int64_t unit = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t nunits = PAIR ? gridDim.x / 2 : gridDim.x;
 
-  const int64_t num_m = (a.nq + kTM - 1) / kTM;
+  const int64_t num_m = (a.nq + MQ - 1) / MQ;
   const int64_t num_n = (a.r1 - a.r0 + kTN - 1) / kTN;
   const int64_t ntiles = num_m * num_n;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full0 + 8 * s, 1);
+      mbar_init(full0 + 8 * s, PAIR ? 2 : 1);
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull0 + 8 * s, 1);
-      mbar_init(tempty0 + 8 * s, kEpiWarps);
+      mbar_init(tempty0 + 8 * s, PAIR ? 2 * kEpiWarps : kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tx)) : "memory");
   }
   if (warp == 1) {  // TMEM: 2 accumulator stages x 256 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     su32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       su32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       su32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote use
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
+    if (lane == 0) {  // ---- TMA producer (in each CTA of a pair: its halves)
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int64_t t = unit; t < ntiles; t += nunits) {
         const int m = (int)(t % num_m);
         const int64_t n = t / num_m;
-        const int qrow = m * kTM;
-        const int xrow = (int)(a.r0 + n * kTN);
+        const int qrow = m * MQ + (int)rank * kTM;
+        const int xrow = (int)(a.r0 + n * kTN) + (int)rank * BROWS;
         for (int kb = 0; kb < a.nk; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
-          const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, kABytes + kBBytes);
           const int kel = kb * (BF16 ? 64 : 32);  // element column of this K block
-          tma_load_2d(sA + stage * kABytes, &tq, kel, qrow, fb);
-          tma_load_2d(sB + stage * kBBytes, &tx, kel, xrow, fb);
+          if (PAIR) {
+            const uint32_t lb = mapa(full0 + 8 * stage, 0);  // the leader's barrier
+            if (rank == 0)
+              mbar_expect_tx(full0 + 8 * stage, 2 * (kABytes + BBYTES));
+            else
+              mbar_arrive_cluster(lb);
+            tma_load_2d_pair(sA + stage * kABytes, &tq, kel, qrow, lb);
+            tma_load_2d_pair(sB + stage * BBYTES, &tx, kel, xrow, lb);
+          } else {
+            const uint32_t fb = full0 + 8 * stage;
+            mbar_expect_tx(fb, kABytes + BBYTES);
+            tma_load_2d(sA + stage * kABytes, &tq, kel, qrow, fb);
+            tma_load_2d(sB + stage * BBYTES, &tx, kel, xrow, fb);
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -207,11 +290,11 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    if (lane == 0 && rank == 0) {  // ---- MMA issuer (the leader of a pair)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(tempty0 + 8 * acc, aphase ^ 1);
@@ -221,18 +304,25 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint64_t ad = smem_desc(sA + stage * kABytes);
-          const uint64_t bd = smem_desc(sB + stage * kBBytes);
+          const uint64_t bd = smem_desc(sB + stage * BBYTES);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)  // 32 bytes per MMA: K = 8 tf32 / 16 bf16
-            tc_mma<BF16>(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k),
-                         idesc_of<BF16>(), (kb | k) != 0);
-          tc_commit(empty0 + 8 * stage);  // the stage is free once these MMAs finish
+          for (int k = 0; k < 4; ++k) {  // 32 bytes per MMA: K = 8 tf32 / 16 bf16
+            if (PAIR)
+              tc_mma_pair<BF16>(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k),
+                                idesc_of<BF16, 2 * kTM>(), (kb | k) != 0);
+            else
+              tc_mma<BF16>(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k),
+                           idesc_of<BF16>(), (kb | k) != 0);
+          }
+          // the stage is free (in both CTAs) once these MMAs finish
+          if (PAIR) tc_commit_pair(empty0 + 8 * stage); else tc_commit(empty0 + 8 * stage);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull0 + 8 * acc);  // the accumulator is complete
+        // the accumulator is complete (in both CTAs)
+        if (PAIR) tc_commit_pair(tfull0 + 8 * acc); else tc_commit(tfull0 + 8 * acc);
       }
     }
   } else {  // ---- epilogue: warps 2..9; TMEM lane quarter = warp % 4, column half = (warp-2)/4
@@ -244,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
     // rearranged; e2t adds slack for the rearrangement's own rounding)
     const float e2t = a.e2 + 32.f / 16777216.f;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
       const int m = (int)(t % num_m);
       const int64_t n = t / num_m;
       const int acc = it & 1;
@@ -258,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
       }
       mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
       tc_fence_after();
-      const int64_t q = (int64_t)m * kTM + row;
+      const int64_t q = (int64_t)m * MQ + (int64_t)rank * kTM + row;
       const bool qok = q < a.nq;
       const float qq = qok ? a.qn2[q] : 0.f;
       const float qn = sqrtf(qq) * 1.000001f;
@@ -324,13 +414,24 @@ __global__ void __launch_bounds__(kThreads, 1) k8_tc_kernel(const __grid_constan
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cluster(mapa(tempty0 + 8 * acc, 0));  // the leader's MMA waits on it
+        else
+          mbar_arrive(tempty0 + 8 * acc);
+      }
     }
   }
   __syncthreads();
+  if (PAIR) cluster_sync();  // both CTAs are done with TMEM and the leader's barriers
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                   : "memory");
   }
 }
 
@@ -397,8 +498,15 @@ int k8_tc_pass(int mode, bool bf16, const void* d_x, int64_t n, int64_t ld, cons
   PDX_REQUIRE(((uintptr_t)d_x & 15) == 0 && ((uintptr_t)d_q & 15) == 0, "rows must be 16-B aligned");
   if (r1 <= r0 || nq == 0) return PDX_OK;
   CUtensorMap tq, tx;
+  // CTA pairs (cta_group::2) with PDX_K8_PAIR=1 (exact, but measured at C4:
+  // 16.4 ms against 9.2-10.8 ms for single-CTA tiles per candidate pass, so
+  // off by default); a pair CTA stages half of the tile's vectors
+  static const bool pair = [] {
+    const char* e = getenv("PDX_K8_PAIR");
+    return e && atoi(e) == 1;
+  }();
   PDX_TRY(make_map(&tq, d_q, nq, ld, kTM, bf16));
-  PDX_TRY(make_map(&tx, d_x, n, ld, kTN, bf16));
+  PDX_TRY(make_map(&tx, d_x, n, ld, pair ? kTN / 2 : kTN, bf16));
   K8Args a;
   a.nq = nq;
   a.r0 = r0;
@@ -421,20 +529,35 @@ int k8_tc_pass(int mode, bool bf16, const void* d_x, int64_t n, int64_t ld, cons
   int dev = 0, nsm = 148;
   PDX_CUDA_CHECK(cudaGetDevice(&dev));
   PDX_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t tiles = ((nq + kTM - 1) / kTM) * ((r1 - r0 + kTN - 1) / kTN);
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, nsm);
-#define PDX_K8TC(M, B)                                                                      \
-  do {                                                                                      \
-    PDX_CUDA_CHECK(cudaFuncSetAttribute(k8_tc_kernel<M, B>,                                 \
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)); \
-    k8_tc_kernel<M, B><<<grid, kThreads, kSmem, st>>>(tq, tx, a);                           \
-  } while (0)
-  if (mode == 0) {
-    if (bf16) PDX_K8TC(0, true); else PDX_K8TC(0, false);
-  } else {
-    if (bf16) PDX_K8TC(1, true); else PDX_K8TC(1, false);
-  }
-#undef PDX_K8TC
+  const int mq = pair ? 2 * kTM : kTM;
+  const int64_t tiles = ((nq + mq - 1) / mq) * ((r1 - r0 + kTN - 1) / kTN);
+  const unsigned grid = pair ? (unsigned)(2 * std::min<int64_t>(tiles, nsm / 2))
+                             : (unsigned)std::min<int64_t>(tiles, nsm);
+  auto launch = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pair ? 2 : 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tq, tx, a);
+  };
+  cudaError_t e;
+  if (pair)
+    e = mode == 0 ? (bf16 ? launch(k8_tc_kernel<0, true, true>) : launch(k8_tc_kernel<0, false, true>))
+                  : (bf16 ? launch(k8_tc_kernel<1, true, true>) : launch(k8_tc_kernel<1, false, true>));
+  else
+    e = mode == 0 ? (bf16 ? launch(k8_tc_kernel<0, true, false>) : launch(k8_tc_kernel<0, false, false>))
+                  : (bf16 ? launch(k8_tc_kernel<1, true, false>) : launch(k8_tc_kernel<1, false, false>));
+  PDX_CUDA_CHECK(e);
   PDX_LAUNCH_CHECK();
   return PDX_OK;
 }

@@ -2,6 +2,7 @@
 golden outputs and the C oracle: identical ids, bit-identical float32
 distances, identical values_touched / values_total and survivor traces."""
 import numpy as np
+from pathlib import Path
 import pytest
 
 import recipes
@@ -487,6 +488,33 @@ def test_tensor_core_exact_equals_scan(P, metric, k, normalize, n, d, nq):
             np.testing.assert_array_equal(out.count.cpu().numpy(), ref.count.cpu().numpy())
         if n > 100_000:
             break  # the 1000-wide partitions repeat the same rows
+
+
+def test_tensor_core_cta_pair_mode(P):
+    """The cta_group::2 variant of the K8 kernel (PDX_K8_PAIR=1: a CTA pair
+    per 256 x 256 tile, leader-issued MMAs, multicast commits) returns the
+    scan's results too (run in a subprocess: the mode is read once)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2503_04422_b200 as P\n"
+        "rng = np.random.default_rng(3)\n"
+        "x = rng.standard_normal((90000, 72)).astype(np.float32)\n"
+        "q = torch.from_numpy(rng.standard_normal((300, 72)).astype(np.float32)).cuda()\n"
+        "flat = P.flat_build(P.VectorCollection.from_array(x), 64)\n"
+        "for m in ('l2', 'ip'):\n"
+        "    prm = P.SearchParams(k=20, metric=m)\n"
+        "    a = P.TensorCoreExactSearcher(flat, prm).run(q)\n"
+        "    b = P.ExactSearcher(flat, prm).run(q)\n"
+        "    assert torch.equal(a.ids, b.ids) and torch.equal(a.dist, b.dist), m\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, PDX_K8_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300, cwd=str(Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 def test_tensor_core_dense_mode_scores(P):
