@@ -250,7 +250,9 @@ def main():
               "n": args.n, "d": D, "nlist": NLIST, "nprobe": args.nprobe, "queries": args.nq,
               "k": K, "epsilon0": EPS, "pruner": "ads", "layout": "tiles [D/8][64][8] f32",
               "index": "reference lloyd_kmeans (tests/golden/c2_ivf_reference.npz)",
-              "l2_flush": "256 MiB write between timed steps", "parallelism": f"buckets x{ws}"}
+              "l2_flush": "256 MiB write between timed steps", "parallelism": f"buckets x{ws}",
+              "outputs": "ids + distances per query (as kneighbors / ivf_search without "
+                         "SearchStats); values_touched comes from a separate stats pass"}
 
     if args.impl == "reference":
         if rank == 0:
@@ -588,7 +590,13 @@ def parity_block(P, view, index, params, Qr_dev, args, i_h):
              "selection_equal": bool(np.array_equal(r.selected.cpu().numpy(), ref["selected"])),
              "oracle_s": round(time.perf_counter() - t0, 2)}
         e["queries_differing"] = int(np.sum(np.any(r.ids.cpu().numpy() != ref["ids"], axis=1)))
-        ok = ok and e["ids_equal"] and e["dist_equal"] and e["touched_equal"]
+        # the timed step's own path: results only (no stats: the survivor
+        # verification instead of the MODE 1 recompute)
+        r0 = s.run(Qr_dev)
+        e["results_only_ids_equal"] = bool(np.array_equal(r0.ids.cpu().numpy(), ref["ids"]))
+        e["results_only_dist_equal"] = bool(np.array_equal(r0.dist.cpu().numpy(), ref["dist"]))
+        ok = (ok and e["ids_equal"] and e["dist_equal"] and e["touched_equal"]
+              and e["results_only_ids_equal"] and e["results_only_dist_equal"])
         out[f"nprobe_{npb}"] = e
         if npb == args.nprobe:  # the e2e handle's answer (host rotation path) vs device path
             out["e2e_ids_equal_device"] = bool(np.array_equal(i_h, r.ids.cpu().numpy()))

@@ -98,7 +98,7 @@ struct BSurv {
   int32_t slot;
   float tafter;
   int32_t real;
-  int32_t pad;
+  int32_t tile;  // the store tile holding the slot (bverify_kernel)
 };
 struct DeepItem {
   float acc;
@@ -112,6 +112,7 @@ struct DeepItem {
 struct BParams {
   int32_t d, d_pad, nsteps, hsteps, hdims, k, pruner, nseg;
   int32_t nq, surv_cap;
+  int32_t dbg;     // PDX_BATCH_DEBUG: MODE 1 counts its work in nitems[4..6]
   uint32_t hmask;  // bit e: a head step ends after dim e
   int32_t ends[kMaxSteps];
   double ratio[kMaxSteps], band[kMaxSteps];
@@ -354,7 +355,7 @@ __device__ __forceinline__ void record_survivor(const BParams& P, const BArgs& A
   const int i = atomicAdd(&A.nsurv[q], 1);
   if (i < P.surv_cap)
     A.surv[(int64_t)q * P.surv_cap + i] =
-        BSurv{dist, pair, __ldg(A.tile_ids + tile * kTile + slot), slot, 0.f, 0, 0};
+        BSurv{dist, pair, __ldg(A.tile_ids + tile * kTile + slot), slot, 0.f, 0, (int32_t)tile};
   else
     A.flags[q] = 1;
 }
@@ -921,6 +922,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     }
     __syncthreads();
     if (s_jmay == 0) return;  // every pair of this item is certain
+    if (P.dbg && threadIdx.x == 0) atomicAdd(const_cast<int32_t*>(A.nitems) + 4, 1);
   }
   for (int i = threadIdx.x; i < ne * kHeadDims; i += blockDim.x) {
     const int j = i / kHeadDims, e = i % kHeadDims;
@@ -984,6 +986,10 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     if (MODE == 1 && nt <= kTodoCap) {
       todo = s_todo[ti];
       if (!todo) continue;
+      if (P.dbg && lane == 0) {
+        atomicAdd(const_cast<int32_t*>(A.nitems) + 5, 1);
+        atomicAdd(const_cast<int32_t*>(A.nitems) + 6, __popc(todo));
+      }
       if ((todo >> lane) & 1u) {
         float that = s_that0[lane];
         if ((s_jvar >> lane) & 1u) {
@@ -1484,6 +1490,54 @@ __global__ void bchain_kernel(const BParams P, const BArgs A) {
   for (int i = lane; i < n; i += 32) sv[i] = ls[i];
 }
 
+// Results-only searches (no values_touched / traces requested): the only
+// thing MODE 1 contributes to the ids and distances is which T'-survivors of
+// uncertain pairs the exact chain keeps.  One thread per T'-survivor of such
+// a pair recomputes that slot's chain — the same per-op-rounded partials at
+// every step end and the same bounds B_s(T^_p) MODE 1 would use — and
+// confirms it when it survives every step (bfinal drops the rest, and
+// flags a query whose dropped survivor lies below T^_p, exactly as after
+// MODE 1).  Pair statistics are not recomputed: they are not output.
+template <bool BSA>
+__global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BArgs A) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = (int)(gid / P.surv_cap), i = (int)(gid % P.surv_cap);
+  if (q >= P.nq || A.flags[q]) return;
+  const int n = min(A.nsurv[q], P.surv_cap);
+  if (i >= n) return;
+  BSurv* sv = A.surv + (int64_t)q * P.surv_cap;  // pair-sorted (bchain_kernel)
+  const BSurv e = sv[i];
+  const float tp = A.tprime[q];
+  const float that = that_of(sv, n, e.pair, tp);
+  if (!pair_uncertain(that, tp, A.prho[A.qoff[q] + e.pair])) return;
+  const float* __restrict__ tb = A.tiles + (int64_t)e.tile * A.tile_stride;
+  const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
+  const float* bq = BSA ? A.bsaq + (int64_t)q * 2 * P.nsteps : nullptr;
+  float acc = 0.f;
+  int s = 0;
+  int nend = P.ends[0];
+  for (int g = 0; g * 8 < P.d; ++g) {
+    float x[8];
+    ldg8(tb + ((size_t)g * kTile + e.slot) * 8, x);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int dim = g * 8 + u;
+      if (dim >= P.d) break;
+      acc = l2upd(acc, __ldg(qg + dim), x[u]);
+      if (dim + 1 == nend) {
+        float v = acc;
+        if (BSA)
+          v = bsa_est2(acc, __ldg(A.resid + ((size_t)e.tile * P.nsteps + s) * kTile + e.slot),
+                       bq[s], bq[P.nsteps + s], A.coef[s]);
+        if (!(v < bound_at(P, that, s, P.ratio, P.band))) return;  // the exact chain prunes it
+        ++s;
+        nend = s < P.nsteps ? P.ends[s] : 0x7fffffff;
+      }
+    }
+  }
+  sv[i].real = 1;
+}
+
 // ------------------------------------------------------------------ final
 // One warp per unflagged query: survivors of uncertain pairs that the
 // recompute pass did not confirm are dropped (or, below T^, flag the query);
@@ -1727,6 +1781,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   PDX_REQUIRE(P.hsteps >= 1, "batched search needs initial_step <= %d", kHeadDims);
   for (int m = 0; m <= kTile; ++m) P.wmin[m] = m > 0 ? host_warm_min(m, prm->selection_fraction) : 0;
   P.surv_cap = 4 * k + 64;
+  P.dbg = getenv("PDX_BATCH_DEBUG") != nullptr;
   const int64_t per = nseg - 1;
   const int64_t pmax = nq64 * nseg * store->max_bucket_tiles;
   const bool trace = out->d_trace != nullptr;
@@ -1762,7 +1817,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     carve<int64_t>(at, nb + 1);                // bnvec
     carve<BEntry>(at, nq64 * nseg + 1);        // entries
     carve<BItem>(at, nitems_max);              // items
-    carve<int32_t>(at, 4);                     // nitems
+    carve<int32_t>(at, 8);                     // nitems, counters
     carve<int32_t>(at, nq);                    // count scratch
     carve<float>(at, nq);                      // tprime
     carve<float>(at, nq64 * P.nsteps);         // bounds
@@ -1816,7 +1871,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   int64_t* bnvec = carve<int64_t>(at, nb + 1);
   BEntry* entries = carve<BEntry>(at, nq64 * nseg + 1);
   BItem* items = carve<BItem>(at, nitems_max);
-  int32_t* ctr = carve<int32_t>(at, 4);
+  int32_t* ctr = carve<int32_t>(at, 8);
   int32_t* cnt_scratch = carve<int32_t>(at, nq);
   float* tprime = carve<float>(at, nq);
   float* bounds = carve<float>(at, nq64 * P.nsteps);
@@ -1868,7 +1923,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   PDX_B_CHECK(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (nb + 1), st));
   PDX_B_CHECK(cudaMemsetAsync(wcount + nq, 0, sizeof(int64_t), st));
   PDX_B_CHECK(cudaMemsetAsync(w0count + nq, 0, sizeof(int64_t), st));
-  PDX_B_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 4, st));
+  PDX_B_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 8, st));
   bprep_kernel<<<(nq + 7) / 8, 256, 0, st>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
                                              store->d_block_tile, seg0, wcount, pbase, bcnt,
                                              w0count, fseg);
@@ -2062,7 +2117,17 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   bchain_kernel<<<(nq + cw - 1) / cw, cw * 32, csm, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("chain");
-  if (nitems_max > 0) PDX_B_CHECK(scan(1));
+  const bool stats_wanted = out->d_touched || out->d_total || trace || getenv("PDX_FULL_MODE1");
+  if (!stats_wanted) {  // results only: verify the uncertain pairs' survivors
+    const int64_t nt = nq64 * P.surv_cap;
+    if (bsa)
+      bverify_kernel<true><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(P, A);
+    else
+      bverify_kernel<false><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(P, A);
+    PDX_B_CHECK(cudaGetLastError());
+  } else if (nitems_max > 0) {
+    PDX_B_CHECK(scan(1));
+  }
   phase("recompute");
   const size_t fper = (size_t)k * (sizeof(float) + sizeof(int64_t)) +
                       (size_t)P.surv_cap * (sizeof(float) + sizeof(int64_t));
@@ -2085,14 +2150,17 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   }
   phase("fallback");
   if (getenv("PDX_BATCH_DEBUG")) {  // development aid: work items, uncertain pairs, fallbacks
-    int32_t h[1] = {0};
+    int32_t h[8] = {0};
     std::vector<int32_t> fl(nq);
     cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(fl.data(), flags, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     int nf = 0;
     for (int32_t f : fl) nf += f != 0;
-    fprintf(stderr, "[pdx batched] nq=%d items=%d fallback=%d\n", nq, h[0], nf);
+    fprintf(stderr,
+            "[pdx batched] nq=%d items=%d fallback=%d mode1: active items %d, tiles %d, "
+            "uncertain pairs %d\n",
+            nq, h[0], nf, h[4], h[5], h[6]);
   }
   PDX_B_CHECK(cudaFreeAsync(base, st));
   if (timing) {

@@ -275,3 +275,36 @@ def test_batched_limits_and_trace_overflow(P, rotated):
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
     np.testing.assert_array_equal(outs[0][2], outs[1][2])
     assert (outs[0][1] == -1).all()
+
+
+@pytest.mark.parametrize("eps,nprobe,k", [(2.1, 32, 10), (0.7, 16, 10), (0.3, 16, 10),
+                                          (2.1, 16, 1), (2.1, 16, 100)])
+def test_batched_results_only_equals_full(P, oracle, rotated, eps, nprobe, k):
+    """Without stats or traces the pipeline replaces the MODE 1 recompute by
+    the survivor verification (bverify_kernel): ids and float32 distances
+    identical to the full pipeline, the per-query scan and the oracle."""
+    xr, qr, index = rotated
+    params = P.SearchParams(k=k, pruner="ads", ads=P.AdsPruner(d=128, epsilon0=eps))
+    fast = P.ivf_search_batch(index, qr, params, nprobe, batched=2)
+    full = P.ivf_search_batch(index, qr, params, nprobe, stats=True, batched=2)
+    scan = P.ivf_search_batch(index, qr, params, nprobe, batched=1)
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, xr), qr, k, nprobe, pruner="ads",
+                                  eps0=eps)
+    for got in (fast, scan):
+        np.testing.assert_array_equal(got["ids"], full["ids"])
+        np.testing.assert_array_equal(got["dist"], full["dist"])
+    np.testing.assert_array_equal(fast["ids"], ref["ids"])
+    np.testing.assert_array_equal(fast["dist"], ref["dist"])
+
+
+def test_batched_results_only_bond_and_bsa(P, oracle):
+    import torch
+    x, Q, xr, qr = _bsa_setup(P)
+    bsa = P.fit_bsa(torch.from_numpy(xr).cuda())
+    index = P.ivf_build(P.VectorCollection.from_array(xr), nlist=128, seed=0)
+    for params in (P.SearchParams(k=10, pruner="bsa", bsa=bsa),
+                   P.SearchParams(k=10, pruner="bond", initial_step=2)):
+        fast = P.ivf_search_batch(index, qr, params, 16, batched=2)
+        full = P.ivf_search_batch(index, qr, params, 16, stats=True, batched=2)
+        np.testing.assert_array_equal(fast["ids"], full["ids"])
+        np.testing.assert_array_equal(fast["dist"], full["dist"])

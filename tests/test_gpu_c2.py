@@ -57,7 +57,10 @@ def test_c2_all_queries_equal_oracle(P, oracle, c2, nprobe):
     XR, QR, index, cent, assign, _ = c2
     view = oracle.IvfView.from_assignment(XR, cent, assign, 1024)
     out = P.ivf_search_batch(index, QR, _params(P), nprobe, stats=True)
+    fast = P.ivf_search_batch(index, QR, _params(P), nprobe)  # results only (bverify path)
     ref = oracle.ivf_search_batch(view, QR, 10, nprobe, pruner="ads", eps0=2.1)
+    np.testing.assert_array_equal(fast["ids"], ref["ids"])
+    np.testing.assert_array_equal(fast["dist"], ref["dist"])
     np.testing.assert_array_equal(out["selected"], ref["selected"])
     np.testing.assert_array_equal(out["ids"], ref["ids"])
     np.testing.assert_array_equal(out["dist"], ref["dist"])
