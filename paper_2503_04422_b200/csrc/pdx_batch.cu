@@ -860,7 +860,10 @@ __device__ __forceinline__ void confirm_survivor(const BParams& P, const BArgs& 
 // together group by group (the group loaded once per warp, per-query
 // accumulators in shared memory) until few live slots remain; otherwise
 // the head's survivors go straight to the one-lane-per-survivor queue.
-template <int IS, bool BSA, int MODE, bool DENSE>
+// ST: the pairs' statistics (survivor counts per step, values_touched,
+// traces) are kept; a results-only search (MODE 0 before bverify_kernel)
+// needs only rho and the T'-survivors.
+template <int IS, bool BSA, int MODE, bool DENSE, bool ST = true>
 __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSCAN_MIN_BLOCKS)
     bscan_kernel(const BParams P, const BArgs A) {
   constexpr int BW = DENSE ? kBWD : kBW;  // warps per CTA
@@ -1102,7 +1105,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
             const float B = MODE == 0 ? s_bnd[j][s] : bound_at(P, di.that, s, s_ratio, s_band);
             ok = v < B;
             if (ok) {
-              atomicAdd(&s_dcnt[w][j][s], 1u);
+              if (ST) atomicAdd(&s_dcnt[w][j][s], 1u);
               if (MODE == 0)
                 atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
               if (s + 1 == nsteps) {
@@ -1134,7 +1137,8 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
 
     for (int j = lane; j < ne; j += 32)  // deep-step counters of this tile's pairs
       if ((todo >> j) & 1u)
-        for (int t = hs; t < nsteps; ++t) s_dcnt[w][j][t] = 0u;
+        if (ST)
+          for (int t = hs; t < nsteps; ++t) s_dcnt[w][j][t] = 0u;
     __syncwarp();
     for (uint32_t tm = todo; tm; tm &= tm - 1) {
       const int j = __ffs(tm) - 1;
@@ -1172,7 +1176,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
             if (al1) rho = fmaxf(rho, __fmul_rn(v1, ib));
           }
         }
-        cntl += (al0 ? 1u << (8 * s) : 0u) + (al1 ? 1u << (8 * s) : 0u);
+        if (ST) cntl += (al0 ? 1u << (8 * s) : 0u) + (al1 ? 1u << (8 * s) : 0u);
       };
       if (IS > 0) {
         float qv[HD > 0 ? HD : 1];
@@ -1215,8 +1219,10 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
           }
         }
       }
-      const uint32_t packed = __reduce_add_sync(kFull, cntl);  // counts <= 64: no carries
-      if (lane == 0) s_hcnt[w][j] = packed;
+      if (ST) {
+        const uint32_t packed = __reduce_add_sync(kFull, cntl);  // counts <= 64: no carries
+        if (lane == 0) s_hcnt[w][j] = packed;
+      }
       if (MODE == 0) {
         if (IS > 0) {  // max_s(max v_s * ib_s) = max over (slot, s) of v * ib: rounding is monotone
 #pragma unroll
@@ -1362,7 +1368,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
                     const uint32_t rm = __reduce_max_sync(kFull, __float_as_uint(r));
                     if (lane == 0 && rm > s_rho[w][j]) s_rho[w][j] = rm;
                   }
-                  if (lane == 0) s_dcnt[w][j][se] = (uint32_t)c;
+                  if (ST && lane == 0) s_dcnt[w][j][se] = (uint32_t)c;
                   if (se == nsteps - 1) {  // the last step: survivors
                     if (MODE == 0) {
                       if (l0) record_survivor(P, A, q, s_base[j] + ti, a0, tile, lane);
@@ -1401,6 +1407,10 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     for (int j = lane; j < ne; j += 32) {
       if (!((todo >> j) & 1u)) continue;
       const int64_t p = s_qo[j] + s_base[j] + ti;
+      if (!ST) {
+        A.prho[p] = __uint_as_float(s_rho[w][j]);
+        continue;
+      }
       const uint32_t hp = s_hcnt[w][j];
       int64_t touched = 0, prev = m;
       bool warm = true;
@@ -2057,6 +2067,9 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   // ---- phase 2: every (query, tile) pair of the other buckets under T';
   // chain; recompute of the uncertain pairs under T^ (same kernel, MODE 1)
   const int is = (store->d >= kHeadDims) ? prm->initial_step : 0;
+  // results only (no values_touched / traces requested): MODE 0 keeps no
+  // pair statistics and bverify_kernel replaces the MODE 1 recompute
+  const bool stats_wanted = out->d_touched || out->d_total || trace || getenv("PDX_FULL_MODE1");
   auto scan = [&](int mode) -> cudaError_t {
     // wide vectors: survivors of the head are many and long — the dense
     // continuation variant (all live queries of a tile advance together)
@@ -2074,25 +2087,31 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
                            : (unsigned)std::min<int64_t>(nitems_max, (int64_t)nsm * (dense ? 8 : 6)));
     const dim3 b(kBW * 32), bd(kBWD * 32);
     const int dsm = (int)(sizeof(float) * kBWD * kQC * kTile);
-#define PDX_B_DENSE(IS, B, M)                                                          \
+#define PDX_B_DENSE(IS, B, M, S)                                                       \
   {                                                                                    \
-    auto fn = bscan_kernel<IS, B, M, true>;                                            \
+    auto fn = bscan_kernel<IS, B, M, true, S>;                                         \
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);        \
     fn<<<g, bd, dsm, st>>>(P, A);                                                      \
   }
-#define PDX_B_LAUNCH(IS)                                                               \
-  if (dense) {                                                                         \
-    if (bsa) {                                                                         \
-      if (mode == 0) PDX_B_DENSE(IS, true, 0) else PDX_B_DENSE(IS, true, 1)            \
+#define PDX_B_MODE0(IS, B, D)                                                          \
+  {                                                                                    \
+    if (D) {                                                                           \
+      if (stats_wanted) PDX_B_DENSE(IS, B, 0, true) else PDX_B_DENSE(IS, B, 0, false)  \
+    } else if (stats_wanted) {                                                         \
+      bscan_kernel<IS, B, 0, false, true><<<g, b, 0, st>>>(P, A);                      \
     } else {                                                                           \
-      if (mode == 0) PDX_B_DENSE(IS, false, 0) else PDX_B_DENSE(IS, false, 1)          \
+      bscan_kernel<IS, B, 0, false, false><<<g, b, 0, st>>>(P, A);                     \
     }                                                                                  \
+  }
+#define PDX_B_LAUNCH(IS)                                                               \
+  if (mode == 0) {                                                                     \
+    if (bsa) PDX_B_MODE0(IS, true, dense) else PDX_B_MODE0(IS, false, dense)           \
+  } else if (dense) {                                                                  \
+    if (bsa) PDX_B_DENSE(IS, true, 1, true) else PDX_B_DENSE(IS, false, 1, true)       \
   } else if (bsa) {                                                                    \
-    if (mode == 0) bscan_kernel<IS, true, 0, false><<<g, b, 0, st>>>(P, A);            \
-    else bscan_kernel<IS, true, 1, false><<<g, b, 0, st>>>(P, A);                      \
+    bscan_kernel<IS, true, 1, false><<<g, b, 0, st>>>(P, A);                           \
   } else {                                                                             \
-    if (mode == 0) bscan_kernel<IS, false, 0, false><<<g, b, 0, st>>>(P, A);           \
-    else bscan_kernel<IS, false, 1, false><<<g, b, 0, st>>>(P, A);                     \
+    bscan_kernel<IS, false, 1, false><<<g, b, 0, st>>>(P, A);                          \
   }
     switch (is) {
       case 1: PDX_B_LAUNCH(1) break;
@@ -2102,6 +2121,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       default: PDX_B_LAUNCH(0) break;
     }
 #undef PDX_B_LAUNCH
+#undef PDX_B_MODE0
 #undef PDX_B_DENSE
     return cudaGetLastError();
   };
@@ -2117,7 +2137,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   bchain_kernel<<<(nq + cw - 1) / cw, cw * 32, csm, st>>>(P, A);
   PDX_B_CHECK(cudaGetLastError());
   phase("chain");
-  const bool stats_wanted = out->d_touched || out->d_total || trace || getenv("PDX_FULL_MODE1");
   if (!stats_wanted) {  // results only: verify the uncertain pairs' survivors
     const int64_t nt = nq64 * P.surv_cap;
     if (bsa)
