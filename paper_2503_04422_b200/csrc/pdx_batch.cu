@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
 
 // NSM >= nsteps: register arrays sized to the schedule.  RK (k <= 32): the
 // heap lives in registers, lane i holding the i-th smallest (dist, id).
-template <int NSM, bool RK>
+template <int NSM, bool RK, bool ST = true>
 __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
                                                       const int32_t* __restrict__ seg0,
                                                       const int64_t* __restrict__ p1off,
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
     const bool linear = ti == 0 || T == INFINITY;  // search.py:201
     bool c0 = lane < m, c1 = lane + 32 < m;
     if (linear) {
-      if (lane == 0) {
+      if (ST && lane == 0) {
         touched += (int64_t)m * P.d;
         if (tr) {
           if (tlen >= 0 && tlen + 2 <= A.trace_cap) {
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
       // (one byte per step, <= 64 per byte), summed over the warp per 4 steps
       int mycnt = 0;
 #pragma unroll
-      for (int g = 0; g < (NSM + 3) / 4; ++g) {
+      for (int g = 0; g < (ST ? (NSM + 3) / 4 : 0); ++g) {
         if (4 * g >= nsteps) break;
         auto unary = [&](int dd) -> unsigned {
           const int u = min(max(dd - 4 * g, 0), 4);
@@ -667,6 +667,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
       }
       c0 = d0 >= nsteps;
       c1 = d1 >= nsteps;
+      if (ST) {
       // values_touched (search.py:148-169): step s counts m * w_s while the
       // entering count stays >= the WARMUP minimum (counts only fall, so the
       // flag is just that test), entering * w_s after; one lane per step
@@ -692,8 +693,9 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
           }
         }
       }
+      }
     }
-    if (lane == 0) total += (int64_t)m * P.d;
+    if (ST && lane == 0) total += (int64_t)m * P.d;
     if (ti == 0 && k <= kTile) {
       // the linear first block into an empty heap: the k smallest (dist, id)
       // of its m vectors, by a warp bitonic sort of the 64 slots
@@ -1795,6 +1797,9 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   const int64_t per = nseg - 1;
   const int64_t pmax = nq64 * nseg * store->max_bucket_tiles;
   const bool trace = out->d_trace != nullptr;
+  // results only (no values_touched / traces requested): phase 1 and MODE 0
+  // keep no pair statistics and bverify_kernel replaces the MODE 1 recompute
+  const bool stats_wanted = out->d_touched || out->d_total || trace || getenv("PDX_FULL_MODE1");
   const int64_t nitems_max = (nb + (nq64 * nseg + kQC - 1) / kQC + 1) *
                              ((store->max_bucket_tiles + kTC - 1) / kTC);
 
@@ -2050,7 +2055,11 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       return cudaGetLastError();
     };
     const bool rk = k <= 32;  // the heap in registers
-    if (P.nsteps <= 8)
+    if (!stats_wanted && rk && P.nsteps <= 8)  // results only: no chain statistics
+      PDX_B_CHECK(chain1(bchain1_kernel<8, true, false>));
+    else if (!stats_wanted && rk && P.nsteps <= 12)
+      PDX_B_CHECK(chain1(bchain1_kernel<12, true, false>));
+    else if (P.nsteps <= 8)
       PDX_B_CHECK(rk ? chain1(bchain1_kernel<8, true>) : chain1(bchain1_kernel<8, false>));
     else if (P.nsteps <= 12)
       PDX_B_CHECK(rk ? chain1(bchain1_kernel<12, true>) : chain1(bchain1_kernel<12, false>));
@@ -2067,9 +2076,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   // ---- phase 2: every (query, tile) pair of the other buckets under T';
   // chain; recompute of the uncertain pairs under T^ (same kernel, MODE 1)
   const int is = (store->d >= kHeadDims) ? prm->initial_step : 0;
-  // results only (no values_touched / traces requested): MODE 0 keeps no
-  // pair statistics and bverify_kernel replaces the MODE 1 recompute
-  const bool stats_wanted = out->d_touched || out->d_total || trace || getenv("PDX_FULL_MODE1");
   auto scan = [&](int mode) -> cudaError_t {
     // wide vectors: survivors of the head are many and long — the dense
     // continuation variant (all live queries of a tile advance together)
