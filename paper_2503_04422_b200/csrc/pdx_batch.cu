@@ -1528,22 +1528,29 @@ __global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BAr
   float acc = 0.f;
   int s = 0;
   int nend = P.ends[0];
-  for (int g = 0; g * 8 < P.d; ++g) {
-    float x[8];
-    ldg8(tb + ((size_t)g * kTile + e.slot) * 8, x);
+  const int ng = (P.d + 7) >> 3;
+  for (int g0 = 0; g0 < ng; g0 += 4) {  // four 8-dim groups in flight at a time
+    float x[4][8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int dim = g * 8 + u;
-      if (dim >= P.d) break;
-      acc = l2upd(acc, __ldg(qg + dim), x[u]);
-      if (dim + 1 == nend) {
-        float v = acc;
-        if (BSA)
-          v = bsa_est2(acc, __ldg(A.resid + ((size_t)e.tile * P.nsteps + s) * kTile + e.slot),
-                       bq[s], bq[P.nsteps + s], A.coef[s]);
-        if (!(v < bound_at(P, that, s, P.ratio, P.band))) return;  // the exact chain prunes it
-        ++s;
-        nend = s < P.nsteps ? P.ends[s] : 0x7fffffff;
+    for (int u = 0; u < 4; ++u)
+      if (g0 + u < ng) ldg8(tb + ((size_t)(g0 + u) * kTile + e.slot) * 8, x[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (g0 + u >= ng) break;
+#pragma unroll
+      for (int v8 = 0; v8 < 8; ++v8) {
+        const int dim = (g0 + u) * 8 + v8;
+        if (dim >= P.d) break;
+        acc = l2upd(acc, __ldg(qg + dim), x[u][v8]);
+        if (dim + 1 == nend) {
+          float v = acc;
+          if (BSA)
+            v = bsa_est2(acc, __ldg(A.resid + ((size_t)e.tile * P.nsteps + s) * kTile + e.slot),
+                         bq[s], bq[P.nsteps + s], A.coef[s]);
+          if (!(v < bound_at(P, that, s, P.ratio, P.band))) return;  // the exact chain prunes it
+          ++s;
+          nend = s < P.nsteps ? P.ends[s] : 0x7fffffff;
+        }
       }
     }
   }
