@@ -113,6 +113,7 @@ struct BParams {
   int32_t d, d_pad, nsteps, hsteps, hdims, k, pruner, nseg;
   int32_t nq, surv_cap;
   int32_t dbg;     // PDX_BATCH_DEBUG: MODE 1 counts its work in nitems[4..6]
+  int32_t norho;   // results only: no rho; every pair with T^ < T' counts as uncertain
   uint32_t hmask;  // bit e: a head step ends after dim e
   int32_t ends[kMaxSteps];
   double ratio[kMaxSteps], band[kMaxSteps];
@@ -1108,7 +1109,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
             ok = v < B;
             if (ok) {
               if (ST) atomicAdd(&s_dcnt[w][j][s], 1u);
-              if (MODE == 0)
+              if (MODE == 0 && ST)
                 atomicMax(&s_rho[w][j], __float_as_uint(fmaxf(__fmul_rn(v, s_invb[s]), 0.f)));
               if (s + 1 == nsteps) {
                 if (MODE == 0)
@@ -1169,7 +1170,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
         const float B = bnd[s];
         al0 = al0 && v0 < B;
         al1 = al1 && v1 < B;
-        if (MODE == 0) {
+        if (MODE == 0 && ST) {
           if (IS > 0) {  // s is a compile-time constant here: v * ib is folded in once per pair
             if (al0) mx[s] = fmaxf(mx[s], v0);
             if (al1) mx[s] = fmaxf(mx[s], v1);
@@ -1225,7 +1226,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
         const uint32_t packed = __reduce_add_sync(kFull, cntl);  // counts <= 64: no carries
         if (lane == 0) s_hcnt[w][j] = packed;
       }
-      if (MODE == 0) {
+      if (MODE == 0 && ST) {
         if (IS > 0) {  // max_s(max v_s * ib_s) = max over (slot, s) of v * ib: rounding is monotone
 #pragma unroll
           for (int s = 0; s < HS; ++s)
@@ -1363,7 +1364,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
                   l0 = l0 && v0 < B;
                   l1 = l1 && v1 < B;
                   const int c = __popc(__ballot_sync(kFull, l0)) + __popc(__ballot_sync(kFull, l1));
-                  if (MODE == 0) {
+                  if (MODE == 0 && ST) {
                     float r = 0.f;
                     if (l0) r = fmaxf(r, __fmul_rn(v0, s_invb[se]));
                     if (l1) r = fmaxf(r, __fmul_rn(v1, s_invb[se]));
@@ -1409,10 +1410,7 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     for (int j = lane; j < ne; j += 32) {
       if (!((todo >> j) & 1u)) continue;
       const int64_t p = s_qo[j] + s_base[j] + ti;
-      if (!ST) {
-        A.prho[p] = __uint_as_float(s_rho[w][j]);
-        continue;
-      }
+      if (!ST) continue;  // (results only: every pair with T^ < T' is verified, no rho)
       const uint32_t hp = s_hcnt[w][j];
       int64_t touched = 0, prev = m;
       bool warm = true;
@@ -1521,7 +1519,7 @@ __global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BAr
   const BSurv e = sv[i];
   const float tp = A.tprime[q];
   const float that = that_of(sv, n, e.pair, tp);
-  if (!pair_uncertain(that, tp, A.prho[A.qoff[q] + e.pair])) return;
+  if (!(P.norho ? that < tp : pair_uncertain(that, tp, A.prho[A.qoff[q] + e.pair]))) return;
   const float* __restrict__ tb = A.tiles + (int64_t)e.tile * A.tile_stride;
   const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
   const float* bq = BSA ? A.bsaq + (int64_t)q * 2 * P.nsteps : nullptr;
@@ -1585,7 +1583,8 @@ __global__ void bfinal_kernel(const BParams P, const BArgs A) {
   bool bad = false;
   for (int i = lane; i < n; i += 32) {
     const float that = that_of(sv, n, sv[i].pair, tp);
-    if (pair_uncertain(that, tp, A.prho[p0 + sv[i].pair]) && !sv[i].real) {
+    const bool unc = P.norho ? that < tp : pair_uncertain(that, tp, A.prho[p0 + sv[i].pair]);
+    if (unc && !sv[i].real) {
       if (sv[i].dist < that) bad = true;
       sv[i].real = -1;
     }
@@ -1801,6 +1800,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   for (int m = 0; m <= kTile; ++m) P.wmin[m] = m > 0 ? host_warm_min(m, prm->selection_fraction) : 0;
   P.surv_cap = 4 * k + 64;
   P.dbg = getenv("PDX_BATCH_DEBUG") != nullptr;
+  P.norho = !(out->d_touched || out->d_total || out->d_trace || getenv("PDX_FULL_MODE1"));
   const int64_t per = nseg - 1;
   const int64_t pmax = nq64 * nseg * store->max_bucket_tiles;
   const bool trace = out->d_trace != nullptr;
