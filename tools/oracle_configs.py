@@ -46,11 +46,16 @@ def host_assign(index):
     return a
 
 
-def compare(name, path, got, ref, extra=None):
+def compare(name, path, got, ref, extra=None, fast=None):
+    """fast: the results-only run of the same searcher (no stats: the
+    batched pipeline's verification path), compared too."""
     line = {"config": name, "path": path, "prefix_queries": int(ref["ids"].shape[0]),
             "ids_equal": bool(np.array_equal(got["ids"], ref["ids"])),
             "dist_equal": bool(np.array_equal(got["dist"], ref["dist"])),
             "queries_differing": int(np.sum(np.any(got["ids"] != ref["ids"], axis=1)))}
+    if fast is not None:
+        line["results_only_ids_equal"] = bool(np.array_equal(fast["ids"], ref["ids"]))
+        line["results_only_dist_equal"] = bool(np.array_equal(fast["dist"], ref["dist"]))
     if "touched" in got and got["touched"] is not None:
         line["touched_equal"] = bool(np.array_equal(got["touched"], ref["touched"]))
     line.update(extra or {})
@@ -72,13 +77,16 @@ def c3():
     qh = q.cpu().numpy()[:PREFIX]
     for pruner in ("ads", "bond"):
         prm = P.SearchParams(k=k, pruner=pruner, ads=P.AdsPruner(d=d))
-        r = P.IvfSearcher(ix, prm, nprobe).run(q, stats=True)
+        sr = P.IvfSearcher(ix, prm, nprobe)
+        r = sr.run(q, stats=True)
         got = {"ids": r.ids.cpu().numpy()[:PREFIX], "dist": r.dist.cpu().numpy()[:PREFIX],
                "touched": r.touched.cpu().numpy()[:PREFIX]}
+        r0 = sr.run(q)
+        fast = {"ids": r0.ids.cpu().numpy()[:PREFIX], "dist": r0.dist.cpu().numpy()[:PREFIX]}
         t0 = time.perf_counter()
         ref = O.ivf_search_batch(view, qh, k, nprobe, pruner=pruner, nthreads=THREADS)
         compare("C3 1M x 960, nlist 2048, nprobe 64", f"batched pipeline, {pruner}", got, ref,
-                {"oracle_s": round(time.perf_counter() - t0, 1), "gpu_batch_queries": nq})
+                {"oracle_s": round(time.perf_counter() - t0, 1), "gpu_batch_queries": nq}, fast)
 
 
 def c4():
@@ -154,14 +162,17 @@ def c5():
     qh = q.cpu().numpy()[:PREFIX]
     for pruner in ("ads", "bond"):
         prm = P.SearchParams(k=10, pruner=pruner, ads=P.AdsPruner(d=D))
-        r = P.IvfSearcher(ix, prm, nprobe).run(q, stats=True)
+        sr = P.IvfSearcher(ix, prm, nprobe)
+        r = sr.run(q, stats=True)
         got = {"ids": r.ids.cpu().numpy()[:PREFIX], "dist": r.dist.cpu().numpy()[:PREFIX],
                "touched": r.touched.cpu().numpy()[:PREFIX]}
+        r0 = sr.run(q)
+        fast = {"ids": r0.ids.cpu().numpy()[:PREFIX], "dist": r0.dist.cpu().numpy()[:PREFIX]}
         t0 = time.perf_counter()
         ref = O.ivf_search_batch(view, qh, 10, nprobe, pruner=pruner, nthreads=THREADS)
         compare("C5 rank 0 of 8 (6.3M x 768 of 50M, nlist 65536, nprobe 256)",
                 f"batched pipeline, {pruner}", got, ref,
-                {"oracle_s": round(time.perf_counter() - t0, 1), "gpu_batch_queries": 2000})
+                {"oracle_s": round(time.perf_counter() - t0, 1), "gpu_batch_queries": 2000}, fast)
 
 
 if __name__ == "__main__":
