@@ -74,6 +74,7 @@ constexpr int kBWD = 4;         // warps per work-item CTA of the dense variant 
 constexpr int kQC = 32;         // queries per work item
 constexpr int kTC = 32;         // tiles per work item (long buckets are split: load balance)
 constexpr int kP1Cap = 64;      // phase 1 covers at most this many tiles of the first bucket
+__constant__ int c_p1cap = kP1Cap;  // (PDX_P1CAP lowers it, for measurements)
 constexpr int kHeadDims = 16;   // dims every pair evaluates for all 64 slots
 constexpr int kMaxHead = 5;     // steps inside the head (initial_step 1: 1,3,7,15)
 constexpr int kDeepCap = 64;    // deep items per warp queue
@@ -245,7 +246,7 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
   };
   while (f < nseg - 1 && ntiles(sq[f]) == 0) ++f;
   const int nt0 = ntiles(sq[f]);
-  const int p1 = min(nt0, kP1Cap);
+  const int p1 = min(nt0, c_p1cap);
   if (lane == 0) {
     seg0[q] = sq[f];
     fseg[q] = f;
@@ -304,7 +305,7 @@ __global__ void bfill_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
   const int c = sel[(int64_t)q * nseg + s];
   const int64_t ntc = block_tile[bucket_block[c + 1]] - block_tile[bucket_block[c]];
   const int f = fseg[q];
-  if (s < f || (s == f ? ntc <= kP1Cap : ntc == 0)) return;  // before / no tail of the first bucket
+  if (s < f || (s == f ? ntc <= c_p1cap : ntc == 0)) return;  // before / no tail of the first bucket
   const int pos = atomicAdd(&bcur[c], 1);
   entries[boff[c] + pos] = BEntry{q, pbase[(int64_t)q * nseg + s]};
 }
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
     if (threadIdx.x < P.nsteps) b0bnd[(int64_t)q * P.nsteps + threadIdx.x] = INFINITY;
     return;
   }
-  if (!FIRST && (int)blockIdx.y * 4 + 1 >= min(nt, kP1Cap)) return;
+  if (!FIRST && (int)blockIdx.y * 4 + 1 >= min(nt, c_p1cap)) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   if (FIRST && w > 0) return;
   {  // one tile per warp (latency-bound: many tiles in flight)
   const int ti = FIRST ? 0 : blockIdx.y * 4 + w + 1;
-  if (ti >= min(nt, kP1Cap)) return;
+  if (ti >= min(nt, c_p1cap)) return;
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
   const float bl = (!FIRST && lane < nsteps) ? b0bnd[(int64_t)q * nsteps + lane] : INFINITY;
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   auto rk_threshold = [&]() { return rn < k ? INFINITY : __shfl_sync(kFull, rd, k - 1); };
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
-  const int nt = min((int)(A.bucket_block[c + 1] - b0), kP1Cap);
+  const int nt = min((int)(A.bucket_block[c + 1] - b0), c_p1cap);
   const int64_t t0 = A.block_tile[b0];
   int32_t* tr = A.trace ? A.trace + (int64_t)q * A.trace_cap : nullptr;
   int64_t touched = 0, total = 0, tlen = 0;  // lane 0
@@ -1646,7 +1647,7 @@ __global__ void bfinal_kernel(const BParams P, const BArgs A) {
     for (int s = fs + 1 + lane; s < P.nseg; s += 32) v += A.bnvec[A.sel[(int64_t)q * P.nseg + s]];
     const int64_t f0 = A.bucket_block[A.sel[(int64_t)q * P.nseg + fs]];
     const int nt0 = (int)(A.bucket_block[A.sel[(int64_t)q * P.nseg + fs] + 1] - f0);
-    for (int ti = kP1Cap + lane; ti < nt0; ti += 32) v += A.block_m[f0 + ti];  // first-bucket tail
+    for (int ti = c_p1cap + lane; ti < nt0; ti += 32) v += A.block_m[f0 + ti];  // first-bucket tail
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     if (lane == 0) A.out_total[q] += v * P.d;
   }
@@ -1798,7 +1799,18 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   }
   PDX_REQUIRE(P.hsteps >= 1, "batched search needs initial_step <= %d", kHeadDims);
   for (int m = 0; m <= kTile; ++m) P.wmin[m] = m > 0 ? host_warm_min(m, prm->selection_fraction) : 0;
-  P.surv_cap = 4 * k + 64;
+  static const int p1cap = [] {
+    const char* e = getenv("PDX_P1CAP");
+    const int v = e ? atoi(e) : kP1Cap;
+    const int c = v < 1 ? 1 : (v > kP1Cap ? kP1Cap : v);
+    if (c != kP1Cap) cudaMemcpyToSymbol(c_p1cap, &c, sizeof(int));
+    return c;
+  }();
+  static const int surv_extra = [] {
+    const char* e = getenv("PDX_SURV_EXTRA");
+    return e ? atoi(e) : 64;
+  }();
+  P.surv_cap = 4 * k + surv_extra;
   P.dbg = getenv("PDX_BATCH_DEBUG") != nullptr;
   P.norho = !(out->d_touched || out->d_total || out->d_trace || getenv("PDX_FULL_MODE1"));
   const int64_t per = nseg - 1;
@@ -1828,7 +1840,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     carve<int64_t>(at, nq + 1);                // qoff
     carve<int64_t>(at, nq + 1);                // w0count
     carve<int64_t>(at, nq + 1);                // p1off
-    carve<float>(at, nq64 * std::min(store->max_bucket_tiles, kP1Cap) * P.nsteps * kTile);  // part1
+    carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);  // part1
     carve<float>(at, nq64 * P.nsteps);                                     // b0bnd
     carve<int32_t>(at, nq64 * nseg);           // pbase
     carve<int32_t>(at, nb + 1);                // bcnt
@@ -1882,7 +1894,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   int64_t* qoff = carve<int64_t>(at, nq + 1);
   int64_t* w0count = carve<int64_t>(at, nq + 1);
   int64_t* p1off = carve<int64_t>(at, nq + 1);
-  float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, kP1Cap) * P.nsteps * kTile);
+  float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);
   float* b0bnd = carve<float>(at, nq64 * P.nsteps);
   int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
   int32_t* bcnt = carve<int32_t>(at, nb + 1);
@@ -2023,7 +2035,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   const bool bsa = prm->pruner == PDX_PRUNER_BSA;
   // ---- phase 1: the first selected bucket of every query (exact chain)
   {
-    const int p1max = std::min(store->max_bucket_tiles, kP1Cap);
+    const int p1max = std::min(store->max_bucket_tiles, p1cap);
     const dim3 g((unsigned)nq, (unsigned)((p1max + 2) / 4));
     const size_t sm = sizeof(float) * (store->d_pad + 2 * kMaxSteps);
     if (sm > 48 * 1024) {
