@@ -217,6 +217,45 @@ __device__ __forceinline__ float2 unpack2(unsigned long long v) {
   return r;
 }
 
+// Plain f32x2 helpers of the results-only head filter (bscan0_kernel): no
+// per-op-rounding contract — its results only discard slots under a
+// certainty margin.
+__device__ __forceinline__ unsigned long long bcast2(float a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b,
+                                                   unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// position of the r-th (0-based) set bit of m (r < popc(m))
+__device__ __forceinline__ int nth_bit(uint32_t m, int r) {
+  int pos = 0;
+#pragma unroll
+  for (int wd = 16; wd >= 1; wd >>= 1) {
+    const int c = __popc(m & ((1u << wd) - 1u));
+    if (r >= c) {
+      r -= c;
+      pos += wd;
+      m >>= wd;
+    }
+  }
+  return pos;
+}
+
 // BSA estimate (bsa_est in pdx_scan_spec.cuh, same association).
 __device__ __forceinline__ float bsa_est2(float acc, float rx, float rq, float sq, float coef) {
   const float cx = __fmul_rn(coef, __fsqrt_rn(rx));
@@ -1450,6 +1489,342 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
   }
 }
 
+// ------------------------------------------- phase 2, results-only searches
+// bscan0_kernel: MODE 0 of bscan_kernel for searches that output only ids and
+// distances (ADS / BOND, compile-time head schedule, d <= 256): same work
+// items, same T'-survivors with the same float32 distances — no pair
+// statistics.  Two things differ from bscan_kernel's head:
+//
+// 1. The head is a FILTER.  Per (query, tile) pair it only discards slots
+//    that the reference prunes at some head step for certain; everything
+//    else is a candidate whose exact chain is evaluated later.  Slot x is
+//    pruned at step s iff v_s >= B_s (v_s the per-op-rounded partial,
+//    search.py:165).  In exact arithmetic V_s - B_s = XX_s + QQ_s - B_s -
+//    2 DOT_s, so with h = (1 - c) / 2, c = 2^-17 = 128 u (u = 2^-24):
+//        dot_s <= fl(h xx_s) + G_s,   G_s = fl(h (qq_s - B_s)) - (c |B_s| + floor)
+//    implies v_s - B_s >= c (W + |B_s|) - (72.5 W + 4.04 |B_s|) u + floor > 0
+//    (W = QQ_s + XX_s, n <= 16 head dims: |v - V| <= 2 (n + 2) u W; the dot
+//    product, the norms and the threshold sum contribute ((2n + 4) W + 4 |B|)
+//    u).  One FFMA2 per dim and slot pair (the dot products of two queries
+//    interleaved), one FADD2 and two compares per step; the slots' prefix
+//    norms are computed once per tile, G once per work item.  A tile or a
+//    query with a non-finite or huge (>= 1e30) norm or bound skips the
+//    filter: every slot is a candidate.
+// 2. The candidates of a tile are expanded from the per-query ballot masks
+//    (lane j keeps query j's masks) 32 at a time — one lane per candidate —
+//    and each lane runs the reference's chain for its (query, slot) from dim
+//    0 with __fsub_rn / __fmul_rn / __fadd_rn: the head dims and the rest of
+//    the first 16 dims from shared memory (the tile's two first groups and
+//    the queries' first 32 dims are staged there), every head decision and
+//    the first deep step exactly as bscan_kernel takes them.  Survivors go to
+//    the warp's queue and finish step by step with compaction, as there.
+// Every decision that reaches the output is therefore taken on the
+// per-op-rounded partials; the filter only saves evaluating slots whose
+// pruning is certain.
+constexpr float kFiltC = 7.62939453125e-06f;       // c = 2^-17
+constexpr float kFiltH = 0.49999618530273438f;     // (1 - c) / 2, exact in float32
+constexpr float kFiltFloor = 1e-30f;
+constexpr float kFiltHuge = 1e30f;
+constexpr int kQRow = 36;  // floats per staged query row: 32 dims + 4 (rows of distinct queries in distinct banks)
+constexpr int kXRow = 18;  // floats per staged slot row: 16 dims + 2 (9 8-byte words: consecutive slots in distinct banks)
+constexpr int kBscan0Smem = kBW * kTile * kXRow * (int)sizeof(float);
+
+template <int IS>
+__global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
+    bscan0_kernel(const BParams P, const BArgs A) {
+  constexpr int HS = HeadSched<IS>::n, HD = HeadSched<IS>::dims;
+  static_assert(HS >= 1 && HD <= 16, "compile-time head schedule");
+  __shared__ __align__(16) float s_q[kQC][kQRow];
+  __shared__ __align__(16) float s_bnd[kQC][kMaxSteps];
+  __shared__ __align__(16) float s_g[kQC][4];
+  __shared__ int32_t s_qid[kQC], s_base[kQC];
+  __shared__ uint32_t s_qex;
+  __shared__ unsigned long long s_hn[kBW][HS][32];
+  __shared__ uint16_t s_dkey[kBW][kDeepCap];
+  __shared__ float s_dacc[kBW][kDeepCap];
+  __shared__ int32_t s_ends[kMaxSteps];
+  extern __shared__ __align__(16) float s_xh[];  // [kBW][kTile][kXRow]
+
+  if ((int)blockIdx.x >= *A.nitems) return;
+  const BItem it = A.items[blockIdx.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ne = it.ne, nsteps = P.nsteps;
+  const int64_t bk0 = A.bucket_block[it.bucket];
+  const int tbeg = it.t0;
+  const int tend = min((int)(A.bucket_block[it.bucket + 1] - bk0), tbeg + kTC);
+  const int nt = tend - tbeg;
+  const int64_t b0 = bk0 + tbeg;
+  const int64_t t0 = A.block_tile[b0];
+
+  // ---- stage the item's queries: first 32 dims, bounds, filter thresholds
+  for (int i = threadIdx.x; i < ne * 32; i += blockDim.x) {
+    const int j = i >> 5, e = i & 31;
+    const int q = A.entries[it.e0 + j].q;
+    s_q[j][e] = e < P.d ? A.queries[(int64_t)q * P.d + e] : 0.f;
+  }
+  for (int i = threadIdx.x; i < ne * nsteps; i += blockDim.x) {
+    const int j = i / nsteps, s = i % nsteps;
+    s_bnd[j][s] = A.bounds[(int64_t)A.entries[it.e0 + j].q * nsteps + s];
+  }
+  for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) s_ends[i] = P.ends[i];
+  if (threadIdx.x < 32) {  // (ne <= kQC = 32: one lane per query)
+    bool ex = false;
+    if ((int)threadIdx.x < ne) {
+      const BEntry en = A.entries[it.e0 + threadIdx.x];
+      s_qid[threadIdx.x] = en.q;
+      s_base[threadIdx.x] = en.base + tbeg;  // pair index of local tile 0
+      const float* __restrict__ qg = A.queries + (int64_t)en.q * P.d;
+      float qq = 0.f;
+#pragma unroll
+      for (int e = 0; e < HD; ++e) {
+        const float qe = __ldg(qg + e);
+        qq = fmaf(qe, qe, qq);
+        const int s = HeadSched<IS>::step_at(e);
+        if (s >= 0) {
+          const float B = A.bounds[(int64_t)en.q * nsteps + s];
+          s_g[threadIdx.x][s] = kFiltH * (qq - B) - fmaf(kFiltC, fabsf(B), kFiltFloor);
+          if (!(fabsf(B) < kFiltHuge)) ex = true;
+        }
+      }
+      if (!(qq < kFiltHuge)) ex = true;
+    }
+    const unsigned mex = __ballot_sync(kFull, ex);
+    if (threadIdx.x == 0) s_qex = mex;
+  }
+  __syncthreads();
+  const uint32_t qex = s_qex;
+  const int hs = HS;
+  const int e1 = s_ends[hs];  // end of the first deep step: 16 <= e1 <= 32
+
+  for (int ti = w; ti < nt; ti += kBW) {
+    const int64_t tile = t0 + ti;
+    const uint32_t todo = __ballot_sync(kFull, lane < ne && s_base[lane] + ti >= 0);
+    if (!todo) continue;  // (tiles of a first bucket that phase 1 covered)
+    const int m = A.block_m[b0 + ti];
+    const float* __restrict__ tb = A.tiles + tile * A.tile_stride;
+    unsigned long long xx[HD];
+    bool tile_all = false;
+    {
+      float x0[16], x1[16];
+      ldg8(tb + lane * 8, *reinterpret_cast<float(*)[8]>(x0));
+      ldg8(tb + (32 + lane) * 8, *reinterpret_cast<float(*)[8]>(x1));
+      ldg8(tb + (kTile + lane) * 8, *reinterpret_cast<float(*)[8]>(x0 + 8));
+      ldg8(tb + (kTile + 32 + lane) * 8, *reinterpret_cast<float(*)[8]>(x1 + 8));
+      // the first 16 dims of both slots, for the exact chains
+      float* xa = s_xh + (size_t)(w * kTile + lane) * kXRow;
+      float* xb = s_xh + (size_t)(w * kTile + 32 + lane) * kXRow;
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {
+        *reinterpret_cast<float2*>(xa + e) = make_float2(x0[e], x0[e + 1]);
+        *reinterpret_cast<float2*>(xb + e) = make_float2(x1[e], x1[e + 1]);
+      }
+#pragma unroll
+      for (int e = 0; e < HD; ++e) xx[e] = pack2_hold(x0[e], x1[e]);
+      // h * (prefix norms at the head step ends) of the slot pair
+      unsigned long long n2 = pack2(0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < HD; ++e) {
+        n2 = fma2(xx[e], xx[e], n2);
+        const int s = HeadSched<IS>::step_at(e);
+        if (s >= 0) s_hn[w][s][lane] = mul2(n2, bcast2(kFiltH));
+      }
+      const float2 nl = unpack2(n2);
+      tile_all = __any_sync(kFull, !(nl.x < kFiltHuge) || !(nl.y < kFiltHuge));
+    }
+    const bool in0 = lane < m, in1 = lane + 32 < m;
+    __syncwarp();
+
+    // ---- the filter: two queries per iteration; lane j keeps query j's masks
+    // (a forced query — non-finite / huge norms — keeps every slot: mask | ~0)
+    const uint32_t inm0 = __ballot_sync(kFull, in0), inm1 = __ballot_sync(kFull, in1);
+    const uint32_t fex = tile_all ? 0xffffffffu : qex;
+    uint32_t mm0 = 0u, mm1 = 0u;
+    for (uint32_t tm = todo; tm;) {
+      const int ja = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const int jb = tm ? __ffs(tm) - 1 : ja;
+      tm &= tm - 1;
+      bool a0 = true, a1 = true, c0 = true, c1 = true;
+      unsigned long long da = pack2(0.f, 0.f), db = pack2(0.f, 0.f);
+      const float* __restrict__ qa = s_q[ja];
+      const float* __restrict__ qb = s_q[jb];
+      const float4 ga = *reinterpret_cast<const float4*>(s_g[ja]);
+      const float4 gb = *reinterpret_cast<const float4*>(s_g[jb]);
+#pragma unroll
+      for (int e = 0; e < HD; ++e) {
+        da = fma2(xx[e], bcast2(qa[e]), da);
+        db = fma2(xx[e], bcast2(qb[e]), db);
+        const int s = HeadSched<IS>::step_at(e);
+        if (s >= 0) {
+          const unsigned long long hn = s_hn[w][s][lane];
+          const float2 ta = unpack2(add2(hn, bcast2(s == 0 ? ga.x : s == 1 ? ga.y : s == 2 ? ga.z : ga.w)));
+          const float2 tb2 = unpack2(add2(hn, bcast2(s == 0 ? gb.x : s == 1 ? gb.y : s == 2 ? gb.z : gb.w)));
+          const float2 va = unpack2(da), vb = unpack2(db);
+          a0 = a0 && va.x > ta.x;
+          a1 = a1 && va.y > ta.y;
+          c0 = c0 && vb.x > tb2.x;
+          c1 = c1 && vb.y > tb2.y;
+        }
+      }
+      const uint32_t fa = ((fex >> ja) & 1u) ? 0xffffffffu : 0u;
+      const uint32_t fb = ((fex >> jb) & 1u) ? 0xffffffffu : 0u;
+      const uint32_t ma0 = (__ballot_sync(kFull, a0) | fa) & inm0;
+      const uint32_t ma1 = (__ballot_sync(kFull, a1) | fa) & inm1;
+      const uint32_t mb0 = (__ballot_sync(kFull, c0) | fb) & inm0;
+      const uint32_t mb1 = (__ballot_sync(kFull, c1) | fb) & inm1;
+      if (lane == ja) {
+        mm0 = ma0;
+        mm1 = ma1;
+      }
+      if (lane == jb) {  // (jb == ja for an odd last query: the same masks)
+        mm0 = mb0;
+        mm1 = mb1;
+      }
+    }
+
+    // ---- the candidates' exact chains
+    int qn = 0;  // survivors of the first deep step queued by this warp
+    const bool q4 = (P.d & 3) == 0;
+    // finish the queued survivors step by step (all sit after step hs)
+    auto drain = [&]() {
+      __syncwarp();
+      int n = qn, s = hs + 1, pos = e1;
+      while (n > 0 && s < nsteps) {
+        const int a = pos, bend = s_ends[s];
+        int nn = 0;
+        for (int base = 0; base < n; base += 32) {
+          const bool act = base + lane < n;
+          const uint32_t key = act ? s_dkey[w][base + lane] : 0u;
+          const int j = key >> 8, slot = key & 0xffu;
+          float acc = act ? s_dacc[w][base + lane] : 0.f;
+          const float* __restrict__ qg = A.queries + (int64_t)s_qid[j] * P.d;
+          if (act) {
+            for (int g0 = a >> 3; g0 * 8 < bend; g0 += 2) {  // two groups in flight
+              float x[2][8];
+              ldg8(tb + ((size_t)g0 * kTile + slot) * 8, x[0]);
+              const bool two = (g0 + 1) * 8 < bend;
+              if (two) ldg8(tb + ((size_t)(g0 + 1) * kTile + slot) * 8, x[1]);
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !two) break;
+                const int g = g0 + u;
+                float qv[8];
+                if (q4 && g * 8 + 8 <= P.d) {
+                  const float4 v0 = ldg4(qg + g * 8), v1 = ldg4(qg + g * 8 + 4);
+                  qv[0] = v0.x; qv[1] = v0.y; qv[2] = v0.z; qv[3] = v0.w;
+                  qv[4] = v1.x; qv[5] = v1.y; qv[6] = v1.z; qv[7] = v1.w;
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) qv[e] = g * 8 + e < P.d ? __ldg(qg + g * 8 + e) : 0.f;
+                }
+                if (g * 8 >= a && g * 8 + 8 <= bend) {  // a whole group inside the step
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) acc = l2upd(acc, qv[e], x[u][e]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    const int dim = g * 8 + e;
+                    if (dim >= a && dim < bend) acc = l2upd(acc, qv[e], x[u][e]);
+                  }
+                }
+              }
+            }
+          }
+          bool ok = act && acc < s_bnd[j][s];
+          if (ok && s + 1 == nsteps) {
+            record_survivor(P, A, s_qid[j], s_base[j] + ti, acc, tile, slot);
+            ok = false;
+          }
+          const unsigned keep = __ballot_sync(kFull, ok);
+          __syncwarp();
+          if (ok) {
+            const int at = nn + __popc(keep & ((1u << lane) - 1u));
+            s_dkey[w][at] = (uint16_t)key;
+            s_dacc[w][at] = acc;
+          }
+          nn += __popc(keep);
+          __syncwarp();
+        }
+        n = nn;
+        pos = bend;
+        ++s;
+      }
+      __syncwarp();
+      qn = 0;
+    };
+
+    const int cnt = __popc(mm0) + __popc(mm1);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int ntot = __shfl_sync(kFull, incl, 31);
+    for (int base = 0; base < ntot; base += 32) {
+      const int idx = base + lane;
+      const bool act = idx < ntot;
+      int j = 0;  // the first query whose inclusive count exceeds idx
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int v = __shfl_sync(kFull, incl, j + st - 1);
+        if (v <= idx) j += st;
+      }
+      const int excl = __shfl_sync(kFull, incl - cnt, j);
+      const uint32_t m0 = __shfl_sync(kFull, mm0, j), m1 = __shfl_sync(kFull, mm1, j);
+      int slot = 0;
+      if (act) {
+        const int r = idx - excl, p0 = __popc(m0);
+        slot = r < p0 ? nth_bit(m0, r) : 32 + nth_bit(m1, r - p0);
+      } else {
+        j = 0;
+      }
+      // dims 16 .. e1 of the slot come from HBM / L2: issue the loads first
+      float xg[2][8];
+      if (act && e1 > 16) ldg8(tb + ((size_t)2 * kTile + slot) * 8, xg[0]);
+      if (act && e1 > 24) ldg8(tb + ((size_t)3 * kTile + slot) * 8, xg[1]);
+      const float* __restrict__ xr = s_xh + (size_t)(w * kTile + slot) * kXRow;
+      const float* __restrict__ qr = s_q[j];
+      float acc = 0.f;
+      bool ok = act;
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {  // the reference's chain, per-op rounded; every head decision
+        const float2 xv = *reinterpret_cast<const float2*>(xr + e);
+        const float2 qv = *reinterpret_cast<const float2*>(qr + e);
+        acc = l2upd(acc, qv.x, xv.x);
+        if (HeadSched<IS>::step_at(e) >= 0) ok = ok && acc < s_bnd[j][HeadSched<IS>::step_at(e)];
+        acc = l2upd(acc, qv.y, xv.y);
+        if (HeadSched<IS>::step_at(e + 1) >= 0) ok = ok && acc < s_bnd[j][HeadSched<IS>::step_at(e + 1)];
+      }
+      if (e1 > 16) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (16 + u * 8 >= e1) break;
+          if (ok) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (16 + u * 8 + e < e1) acc = l2upd(acc, qr[16 + u * 8 + e], xg[u][e]);
+          }
+        }
+      }
+      ok = ok && acc < s_bnd[j][hs];
+      if (ok && hs + 1 == nsteps) {
+        record_survivor(P, A, s_qid[j], s_base[j] + ti, acc, tile, slot);
+        ok = false;
+      }
+      const unsigned keep = __ballot_sync(kFull, ok);
+      if (ok) {
+        const int at = qn + __popc(keep & ((1u << lane) - 1u));
+        s_dkey[w][at] = (uint16_t)((j << 8) | slot);
+        s_dacc[w][at] = acc;
+      }
+      qn += __popc(keep);
+      if (qn > kDeepCap - 32) drain();
+    }
+    drain();
+  }
+}
+
 // ------------------------------------------------------------------ chain
 // One warp per query: sort its T'-survivors by pair and record, per entry,
 // T^ after the pushes of its pair (the k-th smallest of H and the survivors
@@ -2103,6 +2478,11 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       return e ? atoi(e) : -1;
     }();
     const bool dense = dense_env >= 0 ? dense_env != 0 : store->d > 256;
+    // results-only MODE 0 through the filtered head (PDX_BSCAN_FILTER=0: bscan_kernel)
+    static const bool filt_env = [] {
+      const char* e = getenv("PDX_BSCAN_FILTER");
+      return e ? atoi(e) != 0 : true;
+    }();
     int nsm = 148, dv = 0;
     cudaGetDevice(&dv);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
@@ -2124,6 +2504,10 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       if (stats_wanted) PDX_B_DENSE(IS, B, 0, true) else PDX_B_DENSE(IS, B, 0, false)  \
     } else if (stats_wanted) {                                                         \
       bscan_kernel<IS, B, 0, false, true><<<g, b, 0, st>>>(P, A);                      \
+    } else if (!B && IS > 0 && filt_env) {                                             \
+      auto fn = bscan0_kernel<(IS > 0 ? IS : 1)>;                                      \
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kBscan0Smem); \
+      fn<<<g, b, kBscan0Smem, st>>>(P, A);                                             \
     } else {                                                                           \
       bscan_kernel<IS, B, 0, false, false><<<g, b, 0, st>>>(P, A);                     \
     }                                                                                  \
