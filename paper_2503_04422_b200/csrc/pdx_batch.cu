@@ -241,6 +241,13 @@ __device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigne
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+// (asm volatile: the load stays where it is written — ptxas otherwise hoists
+// these out of the pair loop and spills them)
+__device__ __forceinline__ unsigned long long lds64(const unsigned long long* p) {
+  unsigned long long r;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return r;
+}
 // position of the r-th (0-based) set bit of m (r < popc(m))
 __device__ __forceinline__ int nth_bit(uint32_t m, int r) {
   int pos = 0;
@@ -1540,6 +1547,7 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
   __shared__ int32_t s_qid[kQC], s_base[kQC];
   __shared__ uint32_t s_qex;
   __shared__ unsigned long long s_hn[kBW][HS][32];
+  __shared__ uint2 s_mm[kBW][kQC];  // candidate masks (slots l, l + 32) per query of the warp's tile
   __shared__ uint16_t s_dkey[kBW][kDeepCap];
   __shared__ float s_dacc[kBW][kDeepCap];
   __shared__ int32_t s_ends[kMaxSteps];
@@ -1626,39 +1634,33 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
       for (int e = 0; e < HD; ++e) {
         n2 = fma2(xx[e], xx[e], n2);
         const int s = HeadSched<IS>::step_at(e);
-        if (s >= 0) s_hn[w][s][lane] = mul2(n2, bcast2(kFiltH));
+        if (s >= 0) {
+          const float2 hn = unpack2(mul2(n2, bcast2(kFiltH)));
+          s_hn[w][s][lane] = pack2(lane < m ? hn.x : INFINITY, lane + 32 < m ? hn.y : INFINITY);
+        }
       }
       const float2 nl = unpack2(n2);
       tile_all = __any_sync(kFull, !(nl.x < kFiltHuge) || !(nl.y < kFiltHuge));
     }
-    const bool in0 = lane < m, in1 = lane + 32 < m;
+    const uint32_t fex = tile_all ? 0xffffffffu : qex;
     __syncwarp();
 
     // ---- the filter: two queries per iteration; lane j keeps query j's masks
-    // (a forced query — non-finite / huge norms — keeps every slot: mask | ~0)
-    const uint32_t inm0 = __ballot_sync(kFull, in0), inm1 = __ballot_sync(kFull, in1);
-    const uint32_t fex = tile_all ? 0xffffffffu : qex;
-    uint32_t mm0 = 0u, mm1 = 0u;
-    for (uint32_t tm = todo; tm;) {
-      const int ja = __ffs(tm) - 1;
-      tm &= tm - 1;
-      const int jb = tm ? __ffs(tm) - 1 : ja;
-      tm &= tm - 1;
+    // (slots past the block's m vectors carry a +inf norm: never candidates)
+    auto filter2 = [&](const int ja, const int jb) {
       bool a0 = true, a1 = true, c0 = true, c1 = true;
       unsigned long long da = pack2(0.f, 0.f), db = pack2(0.f, 0.f);
       const float* __restrict__ qa = s_q[ja];
       const float* __restrict__ qb = s_q[jb];
-      const float4 ga = *reinterpret_cast<const float4*>(s_g[ja]);
-      const float4 gb = *reinterpret_cast<const float4*>(s_g[jb]);
 #pragma unroll
       for (int e = 0; e < HD; ++e) {
         da = fma2(xx[e], bcast2(qa[e]), da);
         db = fma2(xx[e], bcast2(qb[e]), db);
         const int s = HeadSched<IS>::step_at(e);
         if (s >= 0) {
-          const unsigned long long hn = s_hn[w][s][lane];
-          const float2 ta = unpack2(add2(hn, bcast2(s == 0 ? ga.x : s == 1 ? ga.y : s == 2 ? ga.z : ga.w)));
-          const float2 tb2 = unpack2(add2(hn, bcast2(s == 0 ? gb.x : s == 1 ? gb.y : s == 2 ? gb.z : gb.w)));
+          const unsigned long long hn = lds64(&s_hn[w][s][lane]);
+          const float2 ta = unpack2(add2(hn, bcast2(s_g[ja][s])));
+          const float2 tb2 = unpack2(add2(hn, bcast2(s_g[jb][s])));
           const float2 va = unpack2(da), vb = unpack2(db);
           a0 = a0 && va.x > ta.x;
           a1 = a1 && va.y > ta.y;
@@ -1666,20 +1668,42 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
           c1 = c1 && vb.y > tb2.y;
         }
       }
-      const uint32_t fa = ((fex >> ja) & 1u) ? 0xffffffffu : 0u;
-      const uint32_t fb = ((fex >> jb) & 1u) ? 0xffffffffu : 0u;
-      const uint32_t ma0 = (__ballot_sync(kFull, a0) | fa) & inm0;
-      const uint32_t ma1 = (__ballot_sync(kFull, a1) | fa) & inm1;
-      const uint32_t mb0 = (__ballot_sync(kFull, c0) | fb) & inm0;
-      const uint32_t mb1 = (__ballot_sync(kFull, c1) | fb) & inm1;
-      if (lane == ja) {
-        mm0 = ma0;
-        mm1 = ma1;
+      uint32_t ma0 = __ballot_sync(kFull, a0), ma1 = __ballot_sync(kFull, a1);
+      uint32_t mb0 = __ballot_sync(kFull, c0), mb1 = __ballot_sync(kFull, c1);
+      if (fex) {  // a forced query (non-finite / huge norms) keeps every slot of the block
+        const uint32_t inm0 = m >= 32 ? 0xffffffffu : (1u << m) - 1u;
+        const uint32_t inm1 = m >= 64 ? 0xffffffffu : m > 32 ? (1u << (m - 32)) - 1u : 0u;
+        if ((fex >> ja) & 1u) {
+          ma0 = inm0;
+          ma1 = inm1;
+        }
+        if ((fex >> jb) & 1u) {
+          mb0 = inm0;
+          mb1 = inm1;
+        }
       }
-      if (lane == jb) {  // (jb == ja for an odd last query: the same masks)
-        mm0 = mb0;
-        mm1 = mb1;
+      // (every lane stores the same words: no divergence; jb == ja for an odd
+      // last query: the same masks)
+      s_mm[w][ja] = make_uint2(ma0, ma1);
+      s_mm[w][jb] = make_uint2(mb0, mb1);
+    };
+    if (todo == (ne >= 32 ? 0xffffffffu : (1u << ne) - 1u)) {  // every query of the item: a counted loop
+      for (int j = 0; j < ne; j += 2) filter2(j, min(j + 1, ne - 1));
+    } else {
+      for (uint32_t tm = todo; tm;) {
+        const int ja = __ffs(tm) - 1;
+        tm &= tm - 1;
+        const int jb = tm ? __ffs(tm) - 1 : ja;
+        tm &= tm - 1;
+        filter2(ja, jb);
       }
+    }
+    __syncwarp();
+    uint32_t mm0 = 0u, mm1 = 0u;  // lane j: query j's candidate masks
+    if ((todo >> lane) & 1u) {
+      const uint2 mm = s_mm[w][lane];
+      mm0 = mm.x;
+      mm1 = mm.y;
     }
 
     // ---- the candidates' exact chains
