@@ -429,17 +429,31 @@ __device__ __forceinline__ float bound_at(const BParams& P, float T, int s, cons
 // block (b0bnd, +inf while the heap is not full): T_0 >= every later T_b of
 // the chain, so a slot pruned under it is pruned by the chain too — its
 // partials past that step are recorded as +inf and never read from HBM.
+// st.release / ld.acquire at gpu scope: the per-tile ready flags between the
+// dense kernel and the chain kernel running next to it.
+__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One CTA of the dense pass: query q, warp w takes tile tile0 + w of the
+// query's first bucket.  ready (overlapped phase 1): flag per phase-1 tile,
+// set once the tile's partials are written.
 template <bool BSA, bool FIRST>
-__global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArgs A,
-                                                     const int32_t* __restrict__ seg0,
-                                                     const int64_t* __restrict__ p1off,
-                                                     float* __restrict__ part1,
-                                                     float* __restrict__ b0bnd) {
+__device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
+                                           const int32_t* __restrict__ seg0,
+                                           const int64_t* __restrict__ p1off,
+                                           float* __restrict__ part1, float* __restrict__ b0bnd,
+                                           const int q, const int tile0, int32_t* ready) {
   extern __shared__ __align__(16) float s_q[];  // [d_pad] query, then [2][nsteps] BSA rq, sqrt
   __shared__ int32_t s_ends[kMaxSteps];
   __shared__ float s_coef[kMaxSteps];
   __shared__ double s_ratio[FIRST ? kMaxSteps : 1], s_band[FIRST ? kMaxSteps : 1];
-  const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
@@ -447,7 +461,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
     if (threadIdx.x < P.nsteps) b0bnd[(int64_t)q * P.nsteps + threadIdx.x] = INFINITY;
     return;
   }
-  if (!FIRST && (int)blockIdx.y * 4 + 1 >= min(nt, c_p1cap)) return;
+  if (!FIRST && tile0 >= min(nt, c_p1cap)) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
@@ -472,7 +486,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   }
   if (FIRST && w > 0) return;
   {  // one tile per warp (latency-bound: many tiles in flight)
-  const int ti = FIRST ? 0 : blockIdx.y * 4 + w + 1;
+  const int ti = FIRST ? 0 : tile0 + w;
   if (ti >= min(nt, c_p1cap)) return;
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
@@ -483,7 +497,7 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
   float acc0 = 0.f, acc1 = 0.f;
   bool al0 = lane < m, al1 = lane + 32 < m;
   int nend = s_ends[0];  // end of the current step
-  float n0[8], n1[8];
+  float n0[8], n1[8];  // the next group loads while the current one is evaluated
 #pragma unroll
   for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
   if (FIRST || al0) ldg8(tb + lane * 8, n0);
@@ -570,17 +584,37 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
       b0bnd[(int64_t)q * nsteps + lane] =
           T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
   }
+  if (!FIRST && ready) {  // the tile's partials are complete: publish
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(ready + p1off[q] + ti, 1);
   }
+  }
+}
+
+template <bool BSA, bool FIRST>
+__global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArgs A,
+                                                     const int32_t* __restrict__ seg0,
+                                                     const int64_t* __restrict__ p1off,
+                                                     float* __restrict__ part1,
+                                                     float* __restrict__ b0bnd,
+                                                     int32_t* __restrict__ ready) {
+  bdense_cta<BSA, FIRST>(P, A, seg0, p1off, part1, b0bnd, blockIdx.x,
+                         FIRST ? 0 : (int)blockIdx.y * 4 + 1, ready);
 }
 
 
 // NSM >= nsteps: register arrays sized to the schedule.  RK (k <= 32): the
 // heap lives in registers, lane i holding the i-th smallest (dist, id).
-template <int NSM, bool RK, bool ST = true>
-__global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
-                                                      const int32_t* __restrict__ seg0,
-                                                      const int64_t* __restrict__ p1off,
-                                                      const float* __restrict__ part1) {
+// A chain CTA: 8 warps, warp wq walks query oct * 8 + wq for oct = oct0, oct0 +
+// oct_stride, ...  ready (overlapped phase 1): the dense CTAs' per-tile flags —
+// a tile's partials are read (at L2) only after its flag has been observed.
+template <int NSM, bool RK, bool ST>
+__device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
+                                            const int32_t* __restrict__ seg0,
+                                            const int64_t* __restrict__ p1off,
+                                            const float* __restrict__ part1, const int oct0,
+                                            const int oct_stride, const int32_t* ready) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   __shared__ Control s_ctl[8];
   __shared__ int32_t s_cnt[8][kMaxSteps];
@@ -594,7 +628,8 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   for (int i = threadIdx.x; i <= kTile; i += blockDim.x) s_wmin[i] = P.wmin[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const int q = blockIdx.x * 8 + wq;
+  for (int oct = oct0; oct * 8 < P.nq; oct += oct_stride) {
+  const int q = oct * 8 + wq;
   if (q >= P.nq) return;
   const int k = P.k, nsteps = P.nsteps;
   float* tkd = reinterpret_cast<float*>(s_raw) + (size_t)wq * k;
@@ -643,21 +678,51 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   int64_t id0 = 0, id1 = 0, nid0 = 0, nid1 = 0;
   int m = 0, nm = 0;
   const float* __restrict__ pq = part1 + p1off[q] * nsteps * kTile;
+  const int32_t* rdy = ready ? ready + p1off[q] : nullptr;
   auto fetch = [&](int ti) {
     if (ti >= nt) return;
     const float* __restrict__ pp = pq + (int64_t)ti * nsteps * kTile;
 #pragma unroll
-    for (int s = 0; s < NSM; ++s) {
-      n0[s] = s < nsteps ? __ldg(pp + s * kTile + lane) : 0.f;
-      n1[s] = s < nsteps ? __ldg(pp + s * kTile + 32 + lane) : 0.f;
+    for (int s = 0; s < NSM; ++s) {  // (L2 reads: the partials may come from a concurrent CTA)
+      n0[s] = s < nsteps ? __ldcg(pp + s * kTile + lane) : 0.f;
+      n1[s] = s < nsteps ? __ldcg(pp + s * kTile + 32 + lane) : 0.f;
     }
     const int64_t* gid = A.tile_ids + (t0 + ti) * kTile;
     nid0 = __ldg(gid + lane);
     nid1 = __ldg(gid + lane + 32);
     nm = A.block_m[b0 + ti];
   };
-  fetch(0);
+  // nready: tiles [0, nready) are known to be published (tile 0 comes from
+  // the kernel before).  A refresh reads the flags of the next 32 tiles in one
+  // go (flags only ever go up), so the chain pays an L2 round trip for flags
+  // only while it runs ahead of the dense pass.
+  int nready = rdy ? 1 : nt;
+  auto refresh = [&]() {
+    const int t = nready + lane;
+    const int f = t < nt ? ld_acquire(rdy + t) : 0;
+    const unsigned mk = __ballot_sync(kFull, f != 0);
+    __syncwarp();
+    nready += mk == 0xffffffffu ? 32 : __ffs(~mk) - 1;  // consecutive published tiles
+  };
+  bool have = false;  // n0 / n1 hold tile ti's partials
+  bool dead = false;  // a tile never arrived (cannot happen while the dense CTAs run): give up
   for (int ti = 0; ti < nt; ++ti) {
+    if (!have) {
+      if (ti >= nready) {
+        const long long t_start = clock64();
+        for (;;) {
+          refresh();
+          if (ti < nready) break;
+          __nanosleep(64);
+          if (clock64() - t_start > (1ll << 24)) {  // ~10 ms: no heap -> T' = +inf -> the per-query scan
+            dead = true;
+            break;
+          }
+        }
+        if (dead) break;
+      }
+      fetch(ti);
+    }
 #pragma unroll
     for (int s = 0; s < NSM; ++s) {
       u0[s] = n0[s];
@@ -666,7 +731,9 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
     id0 = nid0;
     id1 = nid1;
     m = nm;
-    fetch(ti + 1);
+    if (ti + 1 >= nready && ti + 1 < nt) refresh();  // (one poll; the wait is at the top)
+    have = ti + 1 < nready || ti + 1 >= nt;
+    if (have) fetch(ti + 1);
     const bool linear = ti == 0 || T == INFINITY;  // search.py:201
     bool c0 = lane < m, c1 = lane + 32 < m;
     if (linear) {
@@ -817,6 +884,7 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
   }
   __syncwarp();
   if (RK) {
+    if (dead) rn = 0;
     if (lane < k) {
       A.out_dist[(int64_t)q * k + lane] = lane < rn ? rd : INFINITY;
       A.out_ids[(int64_t)q * k + lane] = lane < rn ? ri : -1;
@@ -827,9 +895,9 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
       if (A.out_total) A.out_total[q] = total;
       if (A.trace_len) A.trace_len[q] = tlen;
     }
-    return;
+    continue;
   }
-  const int n = ctl.n;
+  const int n = dead ? 0 : ctl.n;
   for (int i = lane; i < k; i += 32) {
     A.out_dist[(int64_t)q * k + i] = i < n ? tkd[i] : INFINITY;
     A.out_ids[(int64_t)q * k + i] = i < n ? tki[i] : -1;
@@ -840,6 +908,17 @@ __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BAr
     if (A.out_total) A.out_total[q] = total;
     if (A.trace_len) A.trace_len[q] = tlen;
   }
+  __syncwarp();
+  }  // queries of this warp
+}
+
+template <int NSM, bool RK, bool ST = true>
+__global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
+                                                      const int32_t* __restrict__ seg0,
+                                                      const int64_t* __restrict__ p1off,
+                                                      const float* __restrict__ part1,
+                                                      const int32_t* __restrict__ ready) {
+  bchain1_cta<NSM, RK, ST>(P, A, seg0, p1off, part1, blockIdx.x, gridDim.x, ready);
 }
 
 // ------------------------------------------------------------ phase 2 scan
@@ -2093,12 +2172,13 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 // slot 0..3: the work-list stream of one pipeline instance; slots 4..7: the
-// streams the query chunks of an overlapped batch run on
+// streams the query chunks of an overlapped batch run on; slots 8..11: the
+// phase-1 chain stream of one pipeline instance
 SideStream& side_stream(int slot = 0) {
-  thread_local SideStream per_dev[16][8];
+  thread_local SideStream per_dev[16][16];
   int dev = 0;
   cudaGetDevice(&dev);
-  SideStream& ss = per_dev[dev & 15][slot & 7];
+  SideStream& ss = per_dev[dev & 15][slot & 15];
   if (!ss.s) {
     cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
@@ -2241,6 +2321,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     carve<int64_t>(at, nq + 1);                // p1off
     carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);  // part1
     carve<float>(at, nq64 * P.nsteps);                                     // b0bnd
+    carve<int32_t>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) + 1);  // p1ready
     carve<int32_t>(at, nq64 * nseg);           // pbase
     carve<int32_t>(at, nb + 1);                // bcnt
     carve<int32_t>(at, nb + 1);                // boff
@@ -2295,6 +2376,8 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   int64_t* p1off = carve<int64_t>(at, nq + 1);
   float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);
   float* b0bnd = carve<float>(at, nq64 * P.nsteps);
+  const int64_t p1ready_n = nq64 * std::min(store->max_bucket_tiles, p1cap) + 1;
+  int32_t* p1ready = carve<int32_t>(at, p1ready_n);
   int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
   int32_t* bcnt = carve<int32_t>(at, nb + 1);
   int32_t* boff = carve<int32_t>(at, nb + 1);
@@ -2336,9 +2419,12 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   // after the fork the side stream may still write into base: join it
   // before the free
   SideStream* forked = nullptr;
+  SideStream* forked2 = nullptr;  // the phase-1 chain stream
   auto fail = [&](int r) {
     if (forked && cudaEventRecord(forked->join, forked->s) == cudaSuccess)
       cudaStreamWaitEvent(st, forked->join, 0);
+    if (forked2 && cudaEventRecord(forked2->join, forked2->s) == cudaSuccess)
+      cudaStreamWaitEvent(st, forked2->join, 0);
     cudaFreeAsync(base, st);
     return r;
   };
@@ -2447,43 +2533,84 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
-    if (p1max > 0) {
-      const dim3 g1((unsigned)nq, 1);
-      if (bsa)
-        bdense_kernel<true, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
-      else
-        bdense_kernel<false, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
-      PDX_B_CHECK(cudaGetLastError());
-      if (p1max > 1) {
-        if (bsa)
-          bdense_kernel<true, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
-        else
-          bdense_kernel<false, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd);
-        PDX_B_CHECK(cudaGetLastError());
-      }
-    }
+    // results only, k <= 32: the threshold chain (latency-bound, one warp per
+    // query) runs underneath the dense pass — its kernel goes first, on a
+    // second stream, with at most one persistent CTA per SM, and consumes a
+    // tile as soon as the dense kernel has raised the tile's ready flag.  The
+    // dense CTAs never wait, so there is no circular wait; a chain warp that
+    // still waits after ~10 ms gives its query up to the per-query scan.
+    // (PDX_P1_OVERLAP=0: the two kernels one after the other.)
+    static const bool overlap_env = [] {
+      const char* e = getenv("PDX_P1_OVERLAP");
+      return e ? atoi(e) != 0 : true;
+    }();
+    int nsm = 148, dv = 0;
+    cudaGetDevice(&dv);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
+    // (larger batches: the chain CTAs would have to take turns — the chain
+    // kernel after the dense one, all its CTAs at once, is faster there)
+    const bool overlap = overlap_env && !stats_wanted && k <= 32 && P.nsteps <= 12 && p1max > 1 &&
+                         (nq + 7) / 8 <= nsm;
+    const int nchain = (nq + 7) / 8;  // at most one chain CTA per SM
+    if (overlap) PDX_B_CHECK(cudaMemsetAsync(p1ready, 0, sizeof(int32_t) * p1ready_n, st));
     const size_t hsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t));
-    auto chain1 = [&](auto kern) -> cudaError_t {
+    auto chain1 = [&](auto kern, cudaStream_t cs, int nblk, const int32_t* rdy) -> cudaError_t {
       if (hsm > 48 * 1024) {
         const cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
         if (e != cudaSuccess) return e;
       }
-      kern<<<(nq + 7) / 8, 256, hsm, st>>>(P, A, seg0, p1off, part1);
+      kern<<<nblk, 256, hsm, cs>>>(P, A, seg0, p1off, part1, rdy);
       return cudaGetLastError();
     };
+    SideStream& cside = side_stream(8 + side_slot);
+    if (p1max > 0) {
+      const dim3 g1((unsigned)nq, 1);
+      if (bsa)
+        bdense_kernel<true, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
+      else
+        bdense_kernel<false, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
+      PDX_B_CHECK(cudaGetLastError());
+      if (overlap) {  // the chain first (its CTAs become resident), then the dense pass
+        PDX_B_CHECK(cudaEventRecord(cside.fork, st));
+        PDX_B_CHECK(cudaStreamWaitEvent(cside.s, cside.fork, 0));
+        forked2 = &cside;
+        if (P.nsteps <= 8)
+          PDX_B_CHECK(chain1(bchain1_kernel<8, true, false>, cside.s, nchain, p1ready));
+        else
+          PDX_B_CHECK(chain1(bchain1_kernel<12, true, false>, cside.s, nchain, p1ready));
+        PDX_B_CHECK(cudaEventRecord(cside.join, cside.s));
+      }
+      if (p1max > 1) {
+        int32_t* rdy = overlap ? p1ready : nullptr;
+        if (bsa)
+          bdense_kernel<true, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, rdy);
+        else
+          bdense_kernel<false, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, rdy);
+        PDX_B_CHECK(cudaGetLastError());
+      }
+      if (overlap) {
+        PDX_B_CHECK(cudaStreamWaitEvent(st, cside.join, 0));
+        forked2 = nullptr;
+      }
+    }
     const bool rk = k <= 32;  // the heap in registers
-    if (!stats_wanted && rk && P.nsteps <= 8)  // results only: no chain statistics
-      PDX_B_CHECK(chain1(bchain1_kernel<8, true, false>));
+    const int nq8 = (nq + 7) / 8;
+    if (overlap && p1max > 0) {
+      // (the chain ran underneath the dense pass)
+    } else if (!stats_wanted && rk && P.nsteps <= 8)  // results only: no chain statistics
+      PDX_B_CHECK(chain1(bchain1_kernel<8, true, false>, st, nq8, nullptr));
     else if (!stats_wanted && rk && P.nsteps <= 12)
-      PDX_B_CHECK(chain1(bchain1_kernel<12, true, false>));
+      PDX_B_CHECK(chain1(bchain1_kernel<12, true, false>, st, nq8, nullptr));
     else if (P.nsteps <= 8)
-      PDX_B_CHECK(rk ? chain1(bchain1_kernel<8, true>) : chain1(bchain1_kernel<8, false>));
+      PDX_B_CHECK(rk ? chain1(bchain1_kernel<8, true>, st, nq8, nullptr)
+                     : chain1(bchain1_kernel<8, false>, st, nq8, nullptr));
     else if (P.nsteps <= 12)
-      PDX_B_CHECK(rk ? chain1(bchain1_kernel<12, true>) : chain1(bchain1_kernel<12, false>));
+      PDX_B_CHECK(rk ? chain1(bchain1_kernel<12, true>, st, nq8, nullptr)
+                     : chain1(bchain1_kernel<12, false>, st, nq8, nullptr));
     else
-      PDX_B_CHECK(rk ? chain1(bchain1_kernel<kMaxSteps, true>)
-                     : chain1(bchain1_kernel<kMaxSteps, false>));
+      PDX_B_CHECK(rk ? chain1(bchain1_kernel<kMaxSteps, true>, st, nq8, nullptr)
+                     : chain1(bchain1_kernel<kMaxSteps, false>, st, nq8, nullptr));
   }
   phase("phase1");
   PDX_B_CHECK(cudaStreamWaitEvent(st, side.join, 0));  // the work lists are ready

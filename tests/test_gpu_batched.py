@@ -308,3 +308,82 @@ def test_batched_results_only_bond_and_bsa(P, oracle):
         full = P.ivf_search_batch(index, qr, params, 16, stats=True, batched=2)
         np.testing.assert_array_equal(fast["ids"], full["ids"])
         np.testing.assert_array_equal(fast["dist"], full["dist"])
+
+
+def _results_only_vs_oracle(P, oracle, x, q, nlist, nprobe, params, from_rows=False, **okw):
+    if from_rows:  # buckets around sampled rows (float64 assignment): no k-means on wild data
+        rng = np.random.default_rng(nlist)
+        ok = np.flatnonzero(np.abs(x).max(1) < 100.0)
+        cent = x[rng.choice(ok, nlist, replace=False)]
+        with np.errstate(over="ignore"):
+            x64, c64 = x.astype(np.float64), cent.astype(np.float64)
+            d2 = (x64 * x64).sum(1)[:, None] + (c64 * c64).sum(1)[None, :] - 2.0 * (x64 @ c64.T)
+        index = P.IvfIndex.from_assignment(P.VectorCollection.from_array(x), cent,
+                                           np.argmin(d2, axis=1), nlist=nlist)
+    else:
+        index = P.ivf_build(P.VectorCollection.from_array(x), nlist=nlist, seed=0)
+    fast = P.ivf_search_batch(index, q, params, nprobe, batched=2)
+    scan = P.ivf_search_batch(index, q, params, nprobe, batched=1)
+    ref = oracle.ivf_search_batch(_oracle_ivf(oracle, index, x), q, params.k, nprobe, **okw)
+    np.testing.assert_array_equal(fast["ids"], scan["ids"])
+    np.testing.assert_array_equal(fast["dist"], scan["dist"])
+    np.testing.assert_array_equal(fast["ids"], ref["ids"])
+    np.testing.assert_array_equal(fast["dist"], ref["dist"])
+
+
+@pytest.mark.parametrize("initial_step", [1, 2, 4, 8])
+@pytest.mark.parametrize("pruner", ["ads", "bond"])
+def test_filtered_head_schedules(P, oracle, pruner, initial_step):
+    """bscan0_kernel (results-only MODE 0: the head as a certainty-margin
+    filter, the candidates' exact chains from shared memory) for every
+    compile-time head schedule, d not a multiple of 8 included."""
+    for d, seed in [(128, 3), (44, 4), (16, 5)]:
+        x = recipes.data("mixture", 40_000, d, seed)
+        q = recipes.queries("near", x, 70, seed + 1)
+        params = P.SearchParams(k=10, pruner=pruner, initial_step=initial_step)
+        _results_only_vs_oracle(P, oracle, x, q, 64, 12, params, pruner=pruner,
+                                initial_step=initial_step)
+
+
+def test_filtered_head_offset_data_every_slot_a_candidate(P, oracle):
+    """A large common offset: norms dwarf the distances, the filter's margin
+    exceeds every partial and keeps (nearly) every slot — all decisions come
+    from the exact chains, the warp queues overflow and drain mid-tile."""
+    rng = np.random.default_rng(21)
+    x = (rng.standard_normal((30_000, 64)) + 3000.0).astype(np.float32)
+    q = (x[rng.choice(30_000, 48, replace=False)] +
+         0.05 * rng.standard_normal((48, 64))).astype(np.float32)
+    for pruner in ("ads", "bond"):
+        _results_only_vs_oracle(P, oracle, x, q, 32, 8, P.SearchParams(k=10, pruner=pruner),
+                                pruner=pruner)
+
+
+def test_filtered_head_huge_and_nonfinite_norms(P, oracle):
+    """Tiles and queries whose head norms are huge (>= 1e30, squares still
+    finite) or overflow to +inf skip the filter; the exact chains reproduce
+    the reference's float32 arithmetic (inf distances included)."""
+    rng = np.random.default_rng(22)
+    x = rng.standard_normal((20_000, 32)).astype(np.float32)
+    x[::997, 3] = 2e15          # square 4e30: huge, finite
+    x[5::1501, 1] = 3e19        # square overflows float32: +inf partials
+    q = (x[rng.choice(20_000, 40, replace=False)] +
+         0.1 * rng.standard_normal((40, 32))).astype(np.float32)
+    q[7, 2] = 1.5e15            # a query with a huge head norm
+    q[11] = x[997]              # a query equal to a huge vector
+    with np.errstate(over="ignore", invalid="ignore"):
+        for pruner in ("ads", "bond"):
+            _results_only_vs_oracle(P, oracle, x, q, 40, 10, P.SearchParams(k=10, pruner=pruner),
+                                    from_rows=True, pruner=pruner)
+
+
+def test_phase1_chain_sequential_equals_overlapped(P, rotated):
+    """Phase 1 with the chain kernel after the dense kernel (k > 32 takes it;
+    so does PDX_P1_OVERLAP=0) and with the chain running underneath the
+    dense pass (k <= 32, results only): both equal the per-query scan."""
+    _, qr, index = rotated
+    for k in (10, 32, 33):
+        params = P.SearchParams(k=k, pruner="ads", ads=P.AdsPruner(d=128, epsilon0=2.1))
+        fast = P.ivf_search_batch(index, qr, params, 16, batched=2)
+        scan = P.ivf_search_batch(index, qr, params, 16, batched=1)
+        np.testing.assert_array_equal(fast["ids"], scan["ids"])
+        np.testing.assert_array_equal(fast["dist"], scan["dist"])
