@@ -276,8 +276,8 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
                              const int64_t* __restrict__ bucket_block,
                              const int64_t* __restrict__ block_tile, int32_t* __restrict__ seg0,
                              int64_t* __restrict__ wcount, int32_t* __restrict__ pbase,
-                             int32_t* __restrict__ bcnt, int64_t* __restrict__ w0count,
-                             int32_t* __restrict__ fseg) {
+                             int32_t* __restrict__ bcnt, int64_t* __restrict__ p1off,
+                             int p1max, int32_t* __restrict__ fseg) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -296,7 +296,8 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
   if (lane == 0) {
     seg0[q] = sq[f];
     fseg[q] = f;
-    w0count[q] = p1;
+    p1off[q] = (int64_t)q * p1max;  // phase-1 tiles of query q: a fixed stride, no scan needed
+    if (q == 0) wcount[nq] = 0;
     pbase[(int64_t)q * nseg + f] = -p1;
     if (nt0 > p1) atomicAdd(&bcnt[sq[f]], 1);
   }
@@ -370,26 +371,25 @@ __global__ void bitems_kernel(const int32_t* __restrict__ bcnt, int nb,
     for (int i = 0; i < n; i += kQC) items[j++] = BItem{c, boff[c] + i, min(kQC, n - i), t};
 }
 
-// T' per query (the phase-1 heap's k-th distance), the bounds B_s(T'), and
-// the BSA query residual energies (the scan kernel's prologue order).
-__global__ void btprime_kernel(const BParams P, BArgs A) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= P.nq) return;
-  const int cnt = A.out_count[q];
-  const float T = cnt >= P.k ? A.out_dist[(int64_t)q * P.k + P.k - 1] : INFINITY;
-  float* tp = const_cast<float*>(A.tprime);
-  float* bd = const_cast<float*>(A.bounds);
-  tp[q] = T;
-  A.flags[q] = T == INFINITY ? 1 : 0;
-  A.nsurv[q] = 0;
-  for (int s = 0; s < P.nsteps; ++s)
-    bd[(int64_t)q * P.nsteps + s] =
+// T' of a query (the phase-1 heap's k-th distance, +inf while the heap is not
+// full: the query is flagged for the per-query scan), the bounds B_s(T'), and
+// the BSA query residual energies (the scan kernel's prologue order); called
+// by the query's chain warp once its heap is final.
+__device__ __forceinline__ void btprime_query(const BParams& P, const BArgs& A, const int q,
+                                              const float T, const int lane) {
+  if (lane == 0) {
+    const_cast<float*>(A.tprime)[q] = T;
+    A.flags[q] = T == INFINITY ? 1 : 0;
+    A.nsurv[q] = 0;
+  }
+  if (lane < P.nsteps) {
+    const int s = lane;
+    const_cast<float*>(A.bounds)[(int64_t)q * P.nsteps + s] =
         T == INFINITY ? -INFINITY
                       : (P.pruner == PDX_PRUNER_BSA ? T : ads_or_bond_bound(T, P.ratio[s], P.band[s]));
-  if (P.pruner == PDX_PRUNER_BSA) {
-    const float* qg = A.queries + (int64_t)q * P.d;
-    float* bq = const_cast<float*>(A.bsaq) + (int64_t)q * 2 * P.nsteps;
-    for (int s = 0; s < P.nsteps; ++s) {
+    if (P.pruner == PDX_PRUNER_BSA) {
+      const float* qg = A.queries + (int64_t)q * P.d;
+      float* bq = const_cast<float*>(A.bsaq) + (int64_t)q * 2 * P.nsteps;
       float r = 0.f;
       for (int j = P.ends[s]; j < P.d; ++j) r = __fadd_rn(r, __fmul_rn(qg[j], qg[j]));
       bq[s] = r;
@@ -895,6 +895,7 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
       if (A.out_total) A.out_total[q] = total;
       if (A.trace_len) A.trace_len[q] = tlen;
     }
+    btprime_query(P, A, q, rk_threshold(), lane);
     continue;
   }
   const int n = dead ? 0 : ctl.n;
@@ -908,6 +909,7 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
     if (A.out_total) A.out_total[q] = total;
     if (A.trace_len) A.trace_len[q] = tlen;
   }
+  btprime_query(P, A, q, n >= k ? tkd[k - 1] : INFINITY, lane);
   __syncwarp();
   }  // queries of this warp
 }
@@ -2317,21 +2319,20 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     carve<int32_t>(at, nq);                    // fseg
     carve<int64_t>(at, nq + 1);                // wcount
     carve<int64_t>(at, nq + 1);                // qoff
-    carve<int64_t>(at, nq + 1);                // w0count
     carve<int64_t>(at, nq + 1);                // p1off
     carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);  // part1
     carve<float>(at, nq64 * P.nsteps);                                     // b0bnd
-    carve<int32_t>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) + 1);  // p1ready
     carve<int32_t>(at, nq64 * nseg);           // pbase
-    carve<int32_t>(at, nb + 1);                // bcnt
+    carve<int32_t>(at, nb + 1);                // bcnt     } zeroed by one memset
+    carve<int32_t>(at, nb + 1);                // bcur     }
+    carve<int32_t>(at, 8);                     // counters }
+    carve<int32_t>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) + 1);  // p1ready }
     carve<int32_t>(at, nb + 1);                // boff
-    carve<int32_t>(at, nb + 1);                // bcur
     carve<int32_t>(at, nb + 1);                // nch
     carve<int32_t>(at, nb + 1);                // choff
     carve<int64_t>(at, nb + 1);                // bnvec
     carve<BEntry>(at, nq64 * nseg + 1);        // entries
     carve<BItem>(at, nitems_max);              // items
-    carve<int32_t>(at, 8);                     // nitems, counters
     carve<int32_t>(at, nq);                    // count scratch
     carve<float>(at, nq);                      // tprime
     carve<float>(at, nq64 * P.nsteps);         // bounds
@@ -2372,22 +2373,22 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   int32_t* fseg = carve<int32_t>(at, nq);
   int64_t* wcount = carve<int64_t>(at, nq + 1);
   int64_t* qoff = carve<int64_t>(at, nq + 1);
-  int64_t* w0count = carve<int64_t>(at, nq + 1);
   int64_t* p1off = carve<int64_t>(at, nq + 1);
   float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);
   float* b0bnd = carve<float>(at, nq64 * P.nsteps);
+  int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
+  int32_t* bcnt = carve<int32_t>(at, nb + 1);  // bcnt .. p1ready: zeroed by one memset
+  int32_t* bcur = carve<int32_t>(at, nb + 1);
+  int32_t* ctr = carve<int32_t>(at, 8);
   const int64_t p1ready_n = nq64 * std::min(store->max_bucket_tiles, p1cap) + 1;
   int32_t* p1ready = carve<int32_t>(at, p1ready_n);
-  int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
-  int32_t* bcnt = carve<int32_t>(at, nb + 1);
+  const unsigned char* zero_end = at;
   int32_t* boff = carve<int32_t>(at, nb + 1);
-  int32_t* bcur = carve<int32_t>(at, nb + 1);
   int32_t* nch = carve<int32_t>(at, nb + 1);
   int32_t* choff = carve<int32_t>(at, nb + 1);
   int64_t* bnvec = carve<int64_t>(at, nb + 1);
   BEntry* entries = carve<BEntry>(at, nq64 * nseg + 1);
   BItem* items = carve<BItem>(at, nitems_max);
-  int32_t* ctr = carve<int32_t>(at, 8);
   int32_t* cnt_scratch = carve<int32_t>(at, nq);
   float* tprime = carve<float>(at, nq);
   float* bounds = carve<float>(at, nq64 * P.nsteps);
@@ -2438,17 +2439,12 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   } while (0)
 
   // ---- plan: per-query windows, bucket-major entries, work items
-  PDX_B_CHECK(cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), st));
-  PDX_B_CHECK(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (nb + 1), st));
-  PDX_B_CHECK(cudaMemsetAsync(wcount + nq, 0, sizeof(int64_t), st));
-  PDX_B_CHECK(cudaMemsetAsync(w0count + nq, 0, sizeof(int64_t), st));
-  PDX_B_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 8, st));
+  PDX_B_CHECK(cudaMemsetAsync(bcnt, 0, zero_end - reinterpret_cast<unsigned char*>(bcnt), st));
   bprep_kernel<<<(nq + 7) / 8, 256, 0, st>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
                                              store->d_block_tile, seg0, wcount, pbase, bcnt,
-                                             w0count, fseg);
+                                             p1off, std::min(store->max_bucket_tiles, p1cap), fseg);
   PDX_B_CHECK(cudaGetLastError());
   size_t cb = cubb;
-  PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, w0count, p1off, nq + 1, st));
   // The work lists (below) and phase 1 (after them) only share bprep's
   // outputs: build the lists on a side stream while phase 1 runs; the main
   // stream joins before phase 2.
@@ -2552,7 +2548,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     const bool overlap = overlap_env && !stats_wanted && k <= 32 && P.nsteps <= 12 && p1max > 1 &&
                          (nq + 7) / 8 <= nsm;
     const int nchain = (nq + 7) / 8;  // at most one chain CTA per SM
-    if (overlap) PDX_B_CHECK(cudaMemsetAsync(p1ready, 0, sizeof(int32_t) * p1ready_n, st));
     const size_t hsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t));
     auto chain1 = [&](auto kern, cudaStream_t cs, int nblk, const int32_t* rdy) -> cudaError_t {
       if (hsm > 48 * 1024) {
@@ -2615,8 +2610,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   phase("phase1");
   PDX_B_CHECK(cudaStreamWaitEvent(st, side.join, 0));  // the work lists are ready
   forked = nullptr;
-  btprime_kernel<<<(nq + 127) / 128, 128, 0, st>>>(P, A);
-  PDX_B_CHECK(cudaGetLastError());
   phase("tprime");
   // ---- phase 2: every (query, tile) pair of the other buckets under T';
   // chain; recompute of the uncertain pairs under T^ (same kernel, MODE 1)
