@@ -1936,16 +1936,11 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
 // of pairs up to it).  Pushing a T'-survivor the exact chain prunes leaves
 // the k-th distance unchanged when its distance is >= T^ (bfinal_kernel
 // checks that every such survivor is), so this is the reference's chain.
-__global__ void bchain_kernel(const BParams P, const BArgs A) {
-  extern __shared__ float s_top[];  // [warps][k] then [warps][surv_cap] BSurv
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int q = blockIdx.x * nw + wq;
-  if (q >= P.nq || A.flags[q]) return;
+__device__ __forceinline__ void bchain_query(const BParams& P, const BArgs& A, const int q,
+                                             const int lane, float* top, BSurv* ls) {
   const int n = min(A.nsurv[q], P.surv_cap);
   if (n == 0) return;
   const int k = P.k;
-  float* top = s_top + (size_t)wq * k;
-  BSurv* ls = reinterpret_cast<BSurv*>(s_top + (size_t)nw * k + 4) + (size_t)wq * P.surv_cap;
   BSurv* sv = A.surv + (int64_t)q * P.surv_cap;
   for (int i = lane; i < k; i += 32) top[i] = A.out_dist[(int64_t)q * k + i];
   // rank sort by (pair, list position), lane-parallel: O(n^2 / 32)
@@ -1981,6 +1976,15 @@ __global__ void bchain_kernel(const BParams P, const BArgs A) {
   for (int i = lane; i < n; i += 32) sv[i] = ls[i];
 }
 
+__global__ void bchain_kernel(const BParams P, const BArgs A) {
+  extern __shared__ float s_top[];  // [warps][k] then [warps][surv_cap] BSurv
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q = blockIdx.x * nw + wq;
+  if (q >= P.nq || A.flags[q]) return;
+  bchain_query(P, A, q, lane, s_top + (size_t)wq * P.k,
+               reinterpret_cast<BSurv*>(s_top + (size_t)nw * P.k + 4) + (size_t)wq * P.surv_cap);
+}
+
 // Results-only searches (no values_touched / traces requested): the only
 // thing MODE 1 contributes to the ids and distances is which T'-survivors of
 // uncertain pairs the exact chain keeps.  One thread per T'-survivor of such
@@ -1990,12 +1994,8 @@ __global__ void bchain_kernel(const BParams P, const BArgs A) {
 // flags a query whose dropped survivor lies below T^_p, exactly as after
 // MODE 1).  Pair statistics are not recomputed: they are not output.
 template <bool BSA>
-__global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BArgs A) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int q = (int)(gid / P.surv_cap), i = (int)(gid % P.surv_cap);
-  if (q >= P.nq || A.flags[q]) return;
-  const int n = min(A.nsurv[q], P.surv_cap);
-  if (i >= n) return;
+__device__ __forceinline__ void bverify_entry(const BParams& P, const BArgs& A, const int q,
+                                              const int i, const int n) {
   BSurv* sv = A.surv + (int64_t)q * P.surv_cap;  // pair-sorted (bchain_kernel)
   const BSurv e = sv[i];
   const float tp = A.tprime[q];
@@ -2036,15 +2036,22 @@ __global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BAr
   sv[i].real = 1;
 }
 
+template <bool BSA>
+__global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BArgs A) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = (int)(gid / P.surv_cap), i = (int)(gid % P.surv_cap);
+  if (q >= P.nq || A.flags[q]) return;
+  const int n = min(A.nsurv[q], P.surv_cap);
+  if (i >= n) return;
+  bverify_entry<BSA>(P, A, q, i, n);
+}
+
 // ------------------------------------------------------------------ final
 // One warp per unflagged query: survivors of uncertain pairs that the
 // recompute pass did not confirm are dropped (or, below T^, flag the query);
 // top-k of H and the real survivors; the stats.
-__global__ void bfinal_kernel(const BParams P, const BArgs A) {
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const int q = blockIdx.x * (blockDim.x >> 5) + wq;
-  if (q >= P.nq || A.flags[q]) return;
+__device__ __forceinline__ void bfinal_query(const BParams& P, const BArgs& A, const int q,
+                                             const int lane, const int wq, unsigned char* s_raw) {
   const int k = P.k;
   const int nwb = blockDim.x >> 5;  // smem: td | ti | tsi | ts, each 16-byte aligned
   const size_t o_ti = ((size_t)nwb * k * 4 + 15) & ~(size_t)15;
@@ -2144,6 +2151,14 @@ __global__ void bfinal_kernel(const BParams P, const BArgs A) {
     }
     if (lane == 0) A.trace_len[q] = fits ? tl + np * rec : -1;
   }
+}
+
+__global__ void bfinal_kernel(const BParams P, const BArgs A) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int q = blockIdx.x * (blockDim.x >> 5) + wq;
+  if (q >= P.nq || A.flags[q]) return;
+  bfinal_query(P, A, q, lane, wq, s_raw);
 }
 
 int schedule(int d, int initial_step, int32_t* ends) {
@@ -2680,6 +2695,8 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   };
   if (nitems_max > 0) PDX_B_CHECK(scan(0));
   phase("scan");
+  const size_t fper = (size_t)k * (sizeof(float) + sizeof(int64_t)) +
+                      (size_t)P.surv_cap * (sizeof(float) + sizeof(int64_t));
   // one warp per query; its heap threshold and survivor list live in shared memory
   const size_t cper = (size_t)k * sizeof(float) + (size_t)P.surv_cap * sizeof(BSurv);
   const int cw = (int)std::max<size_t>(1, std::min<size_t>(8, (160u << 10) / cper));
@@ -2701,8 +2718,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     PDX_B_CHECK(scan(1));
   }
   phase("recompute");
-  const size_t fper = (size_t)k * (sizeof(float) + sizeof(int64_t)) +
-                      (size_t)P.surv_cap * (sizeof(float) + sizeof(int64_t));
   const int fw = (int)std::max<size_t>(1, std::min<size_t>(8, (160u << 10) / fper));
   const size_t fsm = fw * fper + 32;
   if (fsm > 48 * 1024)
