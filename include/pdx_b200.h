@@ -317,6 +317,10 @@ int pdx_vertical_accumulate(const float* d_block, int32_t d, int32_t mp, const f
  * [6] final, [7] fallback.  Copies up to cap accumulated values (ms) to
  * out_ms and the call count to out_calls (either may be NULL); enable >= 0
  * then resets the accumulators and sets the mode, enable < 0 only reads.
+ * A call captured into a CUDA graph while enabled records its phase events as
+ * external event nodes; after a replay (and a synchronize) enable = 2 adds
+ * that replay's phase times to the accumulators (the output arguments are
+ * filled first, as always).
  */
 int pdx_batch_profile(int32_t enable, double* out_ms, int32_t cap, int64_t* out_calls);
 

@@ -434,6 +434,11 @@ __device__ __forceinline__ float bound_at(const BParams& P, float T, int s, cons
 __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -587,7 +592,7 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
   if (!FIRST && ready) {  // the tile's partials are complete: publish
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release(ready + p1off[q] + ti, 1);
+    if (lane == 0) st_release(ready + p1off[q] + ti, P.dbg ? (int32_t)(gtimer_ns() >> 7) | 1 : 1);
   }
   }
 }
@@ -679,6 +684,7 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
   int m = 0, nm = 0;
   const float* __restrict__ pq = part1 + p1off[q] * nsteps * kTile;
   const int32_t* rdy = ready ? ready + p1off[q] : nullptr;
+  if (P.dbg && ready && lane == 0) A.ptouched[2 * q] = (uint32_t)(gtimer_ns() >> 7);
   auto fetch = [&](int ti) {
     if (ti >= nt) return;
     const float* __restrict__ pp = pq + (int64_t)ti * nsteps * kTile;
@@ -896,6 +902,7 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
       if (A.trace_len) A.trace_len[q] = tlen;
     }
     btprime_query(P, A, q, rk_threshold(), lane);
+    if (P.dbg && ready && lane == 0) A.ptouched[2 * q + 1] = (uint32_t)(gtimer_ns() >> 7);
     continue;
   }
   const int n = dead ? 0 : ctl.n;
@@ -2197,6 +2204,8 @@ SideStream& side_stream(int slot = 0) {
   cudaGetDevice(&dev);
   SideStream& ss = per_dev[dev & 15][slot & 15];
   if (!ss.s) {
+    // (a high-priority chain stream was measured: the overlap becomes
+    // reliable for direct launches, but the replayed graph loses 17 us)
     cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
@@ -2423,11 +2432,21 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   BatchProfile& prof = batch_profile();
   cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap_st);
-  const bool timing = prof.enabled && cap_st == cudaStreamCaptureStatusNone && !flags_out;
+  // (while the stream is being captured the phase events become external
+  // event-record nodes of the graph: pdx_batch_profile(2) reads them after a
+  // replay)
+  const bool capturing = cap_st != cudaStreamCaptureStatusNone;
+  const bool timing = prof.enabled && !flags_out;
   int nev = 0;
-  if (timing) cudaEventRecord(prof.ev[nev++], st);
+  auto mark = [&]() {
+    if (capturing)
+      cudaEventRecordWithFlags(prof.ev[nev++], st, cudaEventRecordExternal);
+    else
+      cudaEventRecord(prof.ev[nev++], st);
+  };
+  if (timing) mark();
   auto phase = [&](const char* name) {
-    if (timing && nev < BatchProfile::kEv) cudaEventRecord(prof.ev[nev++], st);
+    if (timing && nev < BatchProfile::kEv) mark();
     if (!dbg_sync) return;
     const cudaError_t e = cudaStreamSynchronize(st);
     fprintf(stderr, "[pdx batched] %s done: %s\n", name, cudaGetErrorString(e));
@@ -2622,6 +2641,27 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       PDX_B_CHECK(rk ? chain1(bchain1_kernel<kMaxSteps, true>, st, nq8, nullptr)
                      : chain1(bchain1_kernel<kMaxSteps, false>, st, nq8, nullptr));
   }
+  if (P.dbg && getenv("PDX_P1_TIMING")) {  // development aid: the overlapped phase 1's timeline
+    cudaStreamSynchronize(st);
+    const int p1m = std::min(store->max_bucket_tiles, p1cap);
+    std::vector<int32_t> fl((size_t)nq * p1m);
+    std::vector<uint32_t> cs(2 * (size_t)nq);
+    cudaMemcpy(fl.data(), p1ready, fl.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(cs.data(), ptouched, cs.size() * 4, cudaMemcpyDeviceToHost);
+    uint32_t t0 = 0xffffffffu, dend = 0, cend = 0;
+    for (int q = 0; q < nq; ++q) t0 = std::min(t0, cs[2 * q]);
+    double lag = 0;
+    for (int q = 0; q < nq; ++q) {
+      uint32_t last = 0;
+      for (int t = 0; t < p1m; ++t)
+        if (fl[(size_t)q * p1m + t]) last = std::max(last, (uint32_t)fl[(size_t)q * p1m + t] - t0);
+      dend = std::max(dend, last);
+      cend = std::max(cend, cs[2 * q + 1] - t0);
+      lag += (double)(cs[2 * q + 1] - t0) - last;
+    }
+    fprintf(stderr, "[pdx p1] dense end %.1f us, chain end %.1f us, mean chain lag after its last tile %.1f us\n",
+            dend * 0.128, cend * 0.128, lag / nq * 0.128);
+  }
   phase("phase1");
   PDX_B_CHECK(cudaStreamWaitEvent(st, side.join, 0));  // the work lists are ready
   forked = nullptr;
@@ -2750,7 +2790,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
             nq, h[0], nf, h[4], h[5], h[6]);
   }
   PDX_B_CHECK(cudaFreeAsync(base, st));
-  if (timing) {
+  if (timing && !capturing) {
     PDX_CUDA_CHECK(cudaEventSynchronize(prof.ev[nev - 1]));
     for (int i = 1; i < nev; ++i) {
       float ms = 0.f;
@@ -2823,6 +2863,15 @@ extern "C" int pdx_batch_profile(int32_t enable, double* out_ms, int32_t cap, in
   if (out_ms)
     for (int i = 0; i < cap && i < pdx::BatchProfile::kEv - 1; ++i) out_ms[i] = p.ms[i];
   if (out_calls) *out_calls = p.calls;
+  if (enable == 2) {  // a replayed graph's phase events (the caller has synchronised)
+    for (int i = 1; i < pdx::BatchProfile::kEv; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p.ev[i - 1], p.ev[i]) == cudaSuccess) p.ms[i - 1] += ms;
+    }
+    cudaGetLastError();
+    p.calls += 1;
+    return PDX_OK;
+  }
   if (enable >= 0) {
     if (enable && !p.ev[0])
       for (auto& e : p.ev) PDX_CUDA_CHECK(cudaEventCreate(&e));
