@@ -8,11 +8,14 @@ every product entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import subprocess
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libpdx_b200.so"
+if os.environ.get("PDX_B200_LIB"):  # development: an alternative build of the same ABI (A/B runs)
+    LIB_PATH = Path(os.environ["PDX_B200_LIB"])
 CSRC = PKG / "csrc"
 
 PDX_OK, PDX_EINVAL, PDX_ECUDA, PDX_ENOSUPPORT, PDX_EFORMAT, PDX_EIO = 0, 1, 2, 3, 4, 5

@@ -502,30 +502,10 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
   float acc0 = 0.f, acc1 = 0.f;
   bool al0 = lane < m, al1 = lane + 32 < m;
   int nend = s_ends[0];  // end of the current step
-  float n0[8], n1[8];  // the next group loads while the current one is evaluated
-#pragma unroll
-  for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
-  if (FIRST || al0) ldg8(tb + lane * 8, n0);
-  if (FIRST || al1) ldg8(tb + (32 + lane) * 8, n1);
   int s = 0;
-  for (int g = 0; g < ng && s < nsteps; ++g) {
-    if (!FIRST && !__any_sync(kFull, al0 || al1)) {  // every slot pruned under T_0
-      for (; s < nsteps; ++s) {
-        out[s * kTile + lane] = INFINITY;
-        out[s * kTile + 32 + lane] = INFINITY;
-      }
-      break;
-    }
-    float x0[8], x1[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      x0[e] = n0[e];
-      x1[e] = n1[e];
-    }
-    if (g + 1 < ng) {
-      if (FIRST || al0) ldg8(tb + ((size_t)(g + 1) * kTile + lane) * 8, n0);
-      if (FIRST || al1) ldg8(tb + ((size_t)(g + 1) * kTile + 32 + lane) * 8, n1);
-    }
+  // one 8-dim group of both slots: the partial sums, and at a step end the
+  // decision under B_s(T_0) and the recorded partials
+  auto group = [&](const int g, const float (&x0)[8], const float (&x1)[8]) {
     const float4 qa = *reinterpret_cast<const float4*>(s_q + g * 8);
     const float4 qb = *reinterpret_cast<const float4*>(s_q + g * 8 + 4);
     const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
@@ -535,7 +515,7 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
         acc0 = l2upd(acc0, qv[e], x0[e]);
         acc1 = l2upd(acc1, qv[e], x1[e]);
       }
-      continue;
+      return;
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -562,6 +542,58 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
           nend = s < nsteps ? s_ends[s] : 0x7fffffff;
         }
       }
+    }
+  };
+  if constexpr (FIRST) {
+    // the linear first block of every query: one warp per query and nothing
+    // else to hide the loads behind — four groups per batch, the next batch
+    // in flight while this one is evaluated
+    float a0[4][8], b0x[4][8], a1[4][8], b1x[4][8];
+    auto load4 = [&](const int g0, float (&xa)[4][8], float (&xb)[4][8]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (g0 + u < ng) {
+          ldg8(tb + ((size_t)(g0 + u) * kTile + lane) * 8, xa[u]);
+          ldg8(tb + ((size_t)(g0 + u) * kTile + 32 + lane) * 8, xb[u]);
+        }
+    };
+    auto proc4 = [&](const int g0, const float (&xa)[4][8], const float (&xb)[4][8]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (g0 + u < ng && s < nsteps) group(g0 + u, xa[u], xb[u]);
+    };
+    load4(0, a0, b0x);
+    for (int g0 = 0; g0 < ng; g0 += 8) {
+      load4(g0 + 4, a1, b1x);
+      proc4(g0, a0, b0x);
+      load4(g0 + 8, a0, b0x);
+      proc4(g0 + 4, a1, b1x);
+    }
+  } else {
+    float n0[8], n1[8];  // the next group loads while the current one is evaluated
+#pragma unroll
+    for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
+    if (al0) ldg8(tb + lane * 8, n0);
+    if (al1) ldg8(tb + (32 + lane) * 8, n1);
+    for (int g = 0; g < ng && s < nsteps; ++g) {
+      if (!__any_sync(kFull, al0 || al1)) {  // every slot pruned under T_0
+        for (; s < nsteps; ++s) {
+          out[s * kTile + lane] = INFINITY;
+          out[s * kTile + 32 + lane] = INFINITY;
+        }
+        break;
+      }
+      float x0[8], x1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        x0[e] = n0[e];
+        x1[e] = n1[e];
+      }
+      if (g + 1 < ng) {
+        if (al0) ldg8(tb + ((size_t)(g + 1) * kTile + lane) * 8, n0);
+        if (al1) ldg8(tb + ((size_t)(g + 1) * kTile + 32 + lane) * 8, n1);
+      }
+      group(g, x0, x1);
     }
   }
   if (FIRST) {
@@ -2596,9 +2628,9 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     if (p1max > 0) {
       const dim3 g1((unsigned)nq, 1);
       if (bsa)
-        bdense_kernel<true, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
+        bdense_kernel<true, true><<<g1, 32, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
       else
-        bdense_kernel<false, true><<<g1, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
+        bdense_kernel<false, true><<<g1, 32, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
       PDX_B_CHECK(cudaGetLastError());
       if (overlap) {  // the chain first (its CTAs become resident), then the dense pass
         PDX_B_CHECK(cudaEventRecord(cside.fork, st));
