@@ -1993,7 +1993,27 @@ __device__ __forceinline__ void bchain_query(const BParams& P, const BArgs& A, c
     ls[r] = sv[i];
   }
   __syncwarp();
-  if (lane == 0) {
+  if (k <= 32) {
+    // the heap's distances in registers (lane l: the l-th smallest); a push
+    // lands after the elements <= it, the rest shift up by one lane
+    float t = lane < k ? top[lane] : INFINITY;
+    for (int i = 0; i < n;) {
+      const int pi = ls[i].pair;
+      int e = i;
+      for (; e < n && ls[e].pair == pi; ++e) {
+        const float dv = ls[e].dist;
+        if (dv < __shfl_sync(kFull, t, k - 1)) {  // TopK.push, threshold value only
+          const int pos = __popc(__ballot_sync(kFull, lane < k && t <= dv));
+          const float up = __shfl_up_sync(kFull, t, 1);
+          if (lane == pos) t = dv;
+          else if (lane > pos && lane < k) t = up;
+        }
+      }
+      const float T = __shfl_sync(kFull, t, k - 1);
+      for (int j = i + lane; j < e; j += 32) ls[j].tafter = T;
+      i = e;
+    }
+  } else if (lane == 0) {
     for (int i = 0; i < n;) {
       int e = i;
       for (; e < n && ls[e].pair == ls[i].pair; ++e) {
@@ -2048,10 +2068,22 @@ __device__ __forceinline__ void bverify_entry(const BParams& P, const BArgs& A, 
   int nend = P.ends[0];
   const int ng = (P.d + 7) >> 3;
   for (int g0 = 0; g0 < ng; g0 += 4) {  // four 8-dim groups in flight at a time
-    float x[4][8];
+    float x[4][8], qv[4][8];
+    const bool q4 = (P.d & 3) == 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (g0 + u < ng) ldg8(tb + ((size_t)(g0 + u) * kTile + e.slot) * 8, x[u]);
+      if (g0 + u < ng) {
+        ldg8(tb + ((size_t)(g0 + u) * kTile + e.slot) * 8, x[u]);
+        const int g = g0 + u;
+        if (q4 && g * 8 + 8 <= P.d) {  // the query's group with the slot's: all loads in flight together
+          const float4 a = ldg4(qg + g * 8), b = ldg4(qg + g * 8 + 4);
+          qv[u][0] = a.x; qv[u][1] = a.y; qv[u][2] = a.z; qv[u][3] = a.w;
+          qv[u][4] = b.x; qv[u][5] = b.y; qv[u][6] = b.z; qv[u][7] = b.w;
+        } else {
+#pragma unroll
+          for (int v8 = 0; v8 < 8; ++v8) qv[u][v8] = g * 8 + v8 < P.d ? __ldg(qg + g * 8 + v8) : 0.f;
+        }
+      }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (g0 + u >= ng) break;
@@ -2059,7 +2091,7 @@ __device__ __forceinline__ void bverify_entry(const BParams& P, const BArgs& A, 
       for (int v8 = 0; v8 < 8; ++v8) {
         const int dim = (g0 + u) * 8 + v8;
         if (dim >= P.d) break;
-        acc = l2upd(acc, __ldg(qg + dim), x[u][v8]);
+        acc = l2upd(acc, qv[u][v8], x[u][v8]);
         if (dim + 1 == nend) {
           float v = acc;
           if (BSA)
@@ -2092,12 +2124,15 @@ __global__ void __launch_bounds__(256) bverify_kernel(const BParams P, const BAr
 __device__ __forceinline__ void bfinal_query(const BParams& P, const BArgs& A, const int q,
                                              const int lane, const int wq, unsigned char* s_raw) {
   const int k = P.k;
-  const int nwb = blockDim.x >> 5;  // smem: td | ti | tsi | ts, each 16-byte aligned
-  const size_t o_ti = ((size_t)nwb * k * 4 + 15) & ~(size_t)15;
-  const size_t o_tsi = o_ti + (size_t)nwb * k * 8;
+  const int nwb = blockDim.x >> 5;  // smem: td, hd | ti | hi | tsi | ts, each 16-byte aligned
+  const size_t o_ti = ((size_t)nwb * 2 * k * 4 + 15) & ~(size_t)15;
+  const size_t o_hi = o_ti + (size_t)nwb * k * 8;
+  const size_t o_tsi = o_hi + (size_t)nwb * k * 8;
   const size_t o_ts = o_tsi + (size_t)nwb * P.surv_cap * 8;
-  float* td = reinterpret_cast<float*>(s_raw) + (size_t)wq * k;
+  float* td = reinterpret_cast<float*>(s_raw) + (size_t)wq * 2 * k;
+  float* hd = td + k;  // the heap (H) staged for the merge
   int64_t* ti = reinterpret_cast<int64_t*>(s_raw + o_ti) + (size_t)wq * k;
+  int64_t* hid = reinterpret_cast<int64_t*>(s_raw + o_hi) + (size_t)wq * k;
   int64_t* tsi = reinterpret_cast<int64_t*>(s_raw + o_tsi) + (size_t)wq * P.surv_cap;
   float* ts = reinterpret_cast<float*>(s_raw + o_ts) + (size_t)wq * P.surv_cap;
   const int n = min(A.nsurv[q], P.surv_cap);
@@ -2138,19 +2173,39 @@ __device__ __forceinline__ void bfinal_query(const BParams& P, const BArgs& A, c
     for (int i = lane; i < n; i += 32) nr += sv[i].real >= 0;
     nr = __reduce_add_sync(kFull, nr);
     __syncwarp();
-    if (lane == 0) {
-      int a = 0, b = 0;
-      for (int r = 0; r < k; ++r) {
-        const bool takeh = b >= nr || (a < k && pair_less(od[a], oi[a], ts[b], tsi[b]));
-        if (takeh) {
-          td[r] = od[a];
-          ti[r] = oi[a];
-          ++a;
-        } else {
-          td[r] = ts[b];
-          ti[r] = tsi[b];
-          ++b;
-        }
+    // merge of the heap (k entries, ascending) and the nr real survivors by
+    // rank: the ids of the two lists are distinct (the heap holds vectors of
+    // the first bucket), so an entry's output position is its own index plus
+    // the number of entries of the other list below it
+    for (int a = lane; a < k; a += 32) {
+      hd[a] = od[a];
+      hid[a] = oi[a];
+    }
+    __syncwarp();
+    for (int a = lane; a < k; a += 32) {
+      const float da = hd[a];
+      const int64_t ia = hid[a];
+      int lo = 0, hi = nr;  // survivors below (da, ia)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pair_less(ts[mid], tsi[mid], da, ia)) lo = mid + 1; else hi = mid;
+      }
+      if (a + lo < k) {
+        td[a + lo] = da;
+        ti[a + lo] = ia;
+      }
+    }
+    for (int b = lane; b < nr && b < k; b += 32) {
+      const float db = ts[b];
+      const int64_t ib = tsi[b];
+      int lo = 0, hi = k;  // heap entries below (db, ib)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pair_less(hd[mid], hid[mid], db, ib)) lo = mid + 1; else hi = mid;
+      }
+      if (b + lo < k) {
+        td[b + lo] = db;
+        ti[b + lo] = ib;
       }
     }
     __syncwarp();
@@ -2767,7 +2822,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   };
   if (nitems_max > 0) PDX_B_CHECK(scan(0));
   phase("scan");
-  const size_t fper = (size_t)k * (sizeof(float) + sizeof(int64_t)) +
+  const size_t fper = (size_t)2 * k * (sizeof(float) + sizeof(int64_t)) +
                       (size_t)P.surv_cap * (sizeof(float) + sizeof(int64_t));
   // one warp per query; its heap threshold and survivor list live in shared memory
   const size_t cper = (size_t)k * sizeof(float) + (size_t)P.surv_cap * sizeof(BSurv);
