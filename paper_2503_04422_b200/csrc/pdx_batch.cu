@@ -1652,6 +1652,15 @@ constexpr float kFiltC = 7.62939453125e-06f;       // c = 2^-17
 constexpr float kFiltH = 0.49999618530273438f;     // (1 - c) / 2, exact in float32
 constexpr float kFiltFloor = 1e-30f;
 constexpr float kFiltHuge = 1e30f;
+#ifndef PDX_FILT_LAST_ONLY
+#define PDX_FILT_LAST_ONLY 1
+#endif
+// The filter tests only the LAST head step: a slot pruned at an earlier head
+// step almost always fails the last one too (the bounds tighten relative to
+// the partials as dims accumulate), and the few that do not are discarded by
+// their exact chains' head decisions — fewer filter instructions per pair
+// for a few more candidates.
+constexpr bool kFiltLastOnly = PDX_FILT_LAST_ONLY != 0;
 constexpr int kQRow = 36;  // floats per staged query row: 32 dims + 4 (rows of distinct queries in distinct banks)
 constexpr int kXRow = 18;  // floats per staged slot row: 16 dims + 2 (9 8-byte words: consecutive slots in distinct banks)
 constexpr int kBscan0Smem = kBW * kTile * kXRow * (int)sizeof(float);
@@ -1776,7 +1785,7 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
       for (int e = 0; e < HD; ++e) {
         da = fma2(xx[e], bcast2(qa[e]), da);
         db = fma2(xx[e], bcast2(qb[e]), db);
-        const int s = HeadSched<IS>::step_at(e);
+        const int s = HeadSched<IS>::step_at(e) == HS - 1 || !kFiltLastOnly ? HeadSched<IS>::step_at(e) : -1;
         if (s >= 0) {
           const unsigned long long hn = lds64(&s_hn[w][s][lane]);
           const float2 ta = unpack2(add2(hn, bcast2(s_g[ja][s])));
