@@ -56,6 +56,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "pdx_batch.cuh"
@@ -1661,6 +1662,10 @@ constexpr float kFiltHuge = 1e30f;
 // their exact chains' head decisions — fewer filter instructions per pair
 // for a few more candidates.
 constexpr bool kFiltLastOnly = PDX_FILT_LAST_ONLY != 0;
+#ifndef PDX_FILT_NQ
+#define PDX_FILT_NQ 2  // (4 measured: +5 us, register pressure)
+#endif
+constexpr int kFiltNQ = PDX_FILT_NQ;  // queries per filter call of the counted loop (2 or 4)
 constexpr int kQRow = 36;  // floats per staged query row: 32 dims + 4 (rows of distinct queries in distinct banks)
 constexpr int kXRow = 18;  // floats per staged slot row: 16 dims + 2 (9 8-byte words: consecutive slots in distinct banks)
 constexpr int kBscan0Smem = kBW * kTile * kXRow * (int)sizeof(float);
@@ -1731,6 +1736,8 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
   __syncthreads();
   const uint32_t qex = s_qex;
   const int hs = HS;
+  constexpr int E1C = IS * ((2 << HS) - 1);  // the first deep step's end when d reaches it
+  static_assert(E1C > 16 && E1C <= 32, "first deep step inside the staged 32 dims");
   const int e1 = s_ends[hs];  // end of the first deep step: 16 <= e1 <= 32
 
   for (int ti = w; ti < nt; ti += kBW) {
@@ -1776,55 +1783,70 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
 
     // ---- the filter: two queries per iteration; lane j keeps query j's masks
     // (slots past the block's m vectors carry a +inf norm: never candidates)
-    auto filter2 = [&](const int ja, const int jb) {
-      bool a0 = true, a1 = true, c0 = true, c1 = true;
-      unsigned long long da = pack2(0.f, 0.f), db = pack2(0.f, 0.f);
-      const float* __restrict__ qa = s_q[ja];
-      const float* __restrict__ qb = s_q[jb];
+    // NQ queries per call: their dot-product chains are independent (ILP), the
+    // tile's norms are read once
+    auto filter = [&](auto nqc, const int (&jj)[4]) {
+      constexpr int NQ = decltype(nqc)::value;
+      unsigned long long dt[NQ];
+      const float* __restrict__ qp[NQ];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        dt[u] = pack2(0.f, 0.f);
+        qp[u] = s_q[jj[u]];
+      }
+      bool a0[NQ], a1[NQ];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) a0[u] = a1[u] = true;
 #pragma unroll
       for (int e = 0; e < HD; ++e) {
-        da = fma2(xx[e], bcast2(qa[e]), da);
-        db = fma2(xx[e], bcast2(qb[e]), db);
+#pragma unroll
+        for (int u = 0; u < NQ; ++u) dt[u] = fma2(xx[e], bcast2(qp[u][e]), dt[u]);
         const int s = HeadSched<IS>::step_at(e) == HS - 1 || !kFiltLastOnly ? HeadSched<IS>::step_at(e) : -1;
         if (s >= 0) {
           const unsigned long long hn = lds64(&s_hn[w][s][lane]);
-          const float2 ta = unpack2(add2(hn, bcast2(s_g[ja][s])));
-          const float2 tb2 = unpack2(add2(hn, bcast2(s_g[jb][s])));
-          const float2 va = unpack2(da), vb = unpack2(db);
-          a0 = a0 && va.x > ta.x;
-          a1 = a1 && va.y > ta.y;
-          c0 = c0 && vb.x > tb2.x;
-          c1 = c1 && vb.y > tb2.y;
+#pragma unroll
+          for (int u = 0; u < NQ; ++u) {
+            const float2 th = unpack2(add2(hn, bcast2(s_g[jj[u]][s])));
+            const float2 v = unpack2(dt[u]);
+            a0[u] = a0[u] && v.x > th.x;
+            a1[u] = a1[u] && v.y > th.y;
+          }
         }
       }
-      uint32_t ma0 = __ballot_sync(kFull, a0), ma1 = __ballot_sync(kFull, a1);
-      uint32_t mb0 = __ballot_sync(kFull, c0), mb1 = __ballot_sync(kFull, c1);
+      uint32_t m0[NQ], m1[NQ];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        m0[u] = __ballot_sync(kFull, a0[u]);
+        m1[u] = __ballot_sync(kFull, a1[u]);
+      }
       if (fex) {  // a forced query (non-finite / huge norms) keeps every slot of the block
         const uint32_t inm0 = m >= 32 ? 0xffffffffu : (1u << m) - 1u;
         const uint32_t inm1 = m >= 64 ? 0xffffffffu : m > 32 ? (1u << (m - 32)) - 1u : 0u;
-        if ((fex >> ja) & 1u) {
-          ma0 = inm0;
-          ma1 = inm1;
-        }
-        if ((fex >> jb) & 1u) {
-          mb0 = inm0;
-          mb1 = inm1;
-        }
+#pragma unroll
+        for (int u = 0; u < NQ; ++u)
+          if ((fex >> jj[u]) & 1u) {
+            m0[u] = inm0;
+            m1[u] = inm1;
+          }
       }
-      // (every lane stores the same words: no divergence; jb == ja for an odd
-      // last query: the same masks)
-      s_mm[w][ja] = make_uint2(ma0, ma1);
-      s_mm[w][jb] = make_uint2(mb0, mb1);
+      // (every lane stores the same words: no divergence; repeated queries of
+      // a ragged last group store the same masks)
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) s_mm[w][jj[u]] = make_uint2(m0[u], m1[u]);
     };
     if (todo == (ne >= 32 ? 0xffffffffu : (1u << ne) - 1u)) {  // every query of the item: a counted loop
-      for (int j = 0; j < ne; j += 2) filter2(j, min(j + 1, ne - 1));
+      for (int j = 0; j < ne; j += kFiltNQ) {
+        const int jj[4] = {j, min(j + 1, ne - 1), min(j + 2, ne - 1), min(j + 3, ne - 1)};
+        filter(std::integral_constant<int, kFiltNQ>{}, jj);
+      }
     } else {
       for (uint32_t tm = todo; tm;) {
         const int ja = __ffs(tm) - 1;
         tm &= tm - 1;
         const int jb = tm ? __ffs(tm) - 1 : ja;
         tm &= tm - 1;
-        filter2(ja, jb);
+        const int jj[4] = {ja, jb, jb, jb};
+        filter(std::integral_constant<int, 2>{}, jj);
       }
     }
     __syncwarp();
@@ -1941,15 +1963,29 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
       float acc = 0.f;
       bool ok = act;
 #pragma unroll
-      for (int e = 0; e < 16; e += 2) {  // the reference's chain, per-op rounded; every head decision
-        const float2 xv = *reinterpret_cast<const float2*>(xr + e);
-        const float2 qv = *reinterpret_cast<const float2*>(qr + e);
-        acc = l2upd(acc, qv.x, xv.x);
-        if (HeadSched<IS>::step_at(e) >= 0) ok = ok && acc < s_bnd[j][HeadSched<IS>::step_at(e)];
-        acc = l2upd(acc, qv.y, xv.y);
-        if (HeadSched<IS>::step_at(e + 1) >= 0) ok = ok && acc < s_bnd[j][HeadSched<IS>::step_at(e + 1)];
+      for (int e = 0; e < 16; e += 4) {  // the reference's chain, per-op rounded; every head decision
+        const float2 xa = *reinterpret_cast<const float2*>(xr + e);
+        const float2 xb = *reinterpret_cast<const float2*>(xr + e + 2);
+        const float4 qv = *reinterpret_cast<const float4*>(qr + e);
+        const float xs[4] = {xa.x, xa.y, xb.x, xb.y}, qs[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc = l2upd(acc, qs[u], xs[u]);
+          if (HeadSched<IS>::step_at(e + u) >= 0) ok = ok && acc < s_bnd[j][HeadSched<IS>::step_at(e + u)];
+        }
       }
-      if (e1 > 16) {
+      if (e1 == E1C) {  // (d >= the schedule's step end: compile-time bounds, no per-dim tests)
+        if (ok) {
+#pragma unroll
+          for (int e = 16; e < E1C; e += 4) {
+            const float4 qv = *reinterpret_cast<const float4*>(qr + e);
+            const float qs[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (e + u < E1C) acc = l2upd(acc, qs[u], xg[(e + u - 16) >> 3][(e + u) & 7]);
+          }
+        }
+      } else if (e1 > 16) {
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (16 + u * 8 >= e1) break;
