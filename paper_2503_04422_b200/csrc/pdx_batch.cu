@@ -1662,6 +1662,9 @@ constexpr float kFiltHuge = 1e30f;
 // their exact chains' head decisions — fewer filter instructions per pair
 // for a few more candidates.
 constexpr bool kFiltLastOnly = PDX_FILT_LAST_ONLY != 0;
+#ifndef PDX_BSCAN0_MIN_BLOCKS
+#define PDX_BSCAN0_MIN_BLOCKS 3
+#endif
 #ifndef PDX_FILT_NQ
 #define PDX_FILT_NQ 2  // (4 measured: +5 us, register pressure)
 #endif
@@ -1671,7 +1674,7 @@ constexpr int kXRow = 18;  // floats per staged slot row: 16 dims + 2 (9 8-byte 
 constexpr int kBscan0Smem = kBW * kTile * kXRow * (int)sizeof(float);
 
 template <int IS>
-__global__ void __launch_bounds__(kBW * 32, PDX_BSCAN_MIN_BLOCKS)
+__global__ void __launch_bounds__(kBW * 32, PDX_BSCAN0_MIN_BLOCKS)
     bscan0_kernel(const BParams P, const BArgs A) {
   constexpr int HS = HeadSched<IS>::n, HD = HeadSched<IS>::dims;
   static_assert(HS >= 1 && HD <= 16, "compile-time head schedule");
