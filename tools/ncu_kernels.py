@@ -18,7 +18,9 @@ def role(name):
     m = re.search(r"bscan_kernel<(\d+), (\w+), (\d+)", name)
     if m:
         return f"bscan_mode{m.group(3)}"
-    for key in ("bdense", "bchain1", "bchain_kernel", "bfinal", "btprime", "bprep", "bfill",
+    if "bscan0_kernel" in name:  # results-only MODE 0 (filtered head)
+        return "bscan_mode0"
+    for key in ("bdense", "bchain1", "bchain_kernel", "bverify", "bfinal", "btprime", "bprep", "bfill",
                 "bitems", "bchunks", "select", "centroid_dist", "project", "DeviceScan"):
         if key in name:
             return key.replace("_kernel", "")
