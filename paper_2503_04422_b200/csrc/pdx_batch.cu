@@ -1619,9 +1619,9 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
 
 // ------------------------------------------- phase 2, results-only searches
 // bscan0_kernel: MODE 0 of bscan_kernel for searches that output only ids and
-// distances (ADS / BOND, compile-time head schedule, d <= 256): same work
-// items, same T'-survivors with the same float32 distances — no pair
-// statistics.  Two things differ from bscan_kernel's head:
+// distances (ADS / BOND with a compile-time head schedule; d <= 256, and
+// wider vectors under ADS): same work items, same T'-survivors with the same
+// float32 distances — no pair statistics.  Two things differ from bscan_kernel's head:
 //
 // 1. The head is a FILTER.  Per (query, tile) pair it only discards slots
 //    that the reference prunes at some head step for certain; everything
@@ -2817,6 +2817,16 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       const char* e = getenv("PDX_BSCAN_FILTER");
       return e ? atoi(e) != 0 : true;
     }();
+    // ... also for wide vectors (d > 256) under ADS, whose head leaves few
+    // survivors (C3, d = 960: 620K -> 774K q/s); BOND on unrotated-energy data
+    // prunes late, and the dense continuation stays faster there (C3: 151K
+    // vs 131K q/s).  PDX_BSCAN_FILTER_WIDE=0/1 forces either.
+    static const int filt_wide_env = [] {
+      const char* e = getenv("PDX_BSCAN_FILTER_WIDE");
+      return e ? atoi(e) : -1;
+    }();
+    const bool filt_wide =
+        filt_wide_env >= 0 ? filt_wide_env != 0 : prm->pruner == PDX_PRUNER_ADS;
     int nsm = 148, dv = 0;
     cudaGetDevice(&dv);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
@@ -2834,7 +2844,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   }
 #define PDX_B_MODE0(IS, B, D)                                                          \
   {                                                                                    \
-    if (D) {                                                                           \
+    if (D && !(filt_wide && !stats_wanted && !B && IS > 0 && filt_env)) {              \
       if (stats_wanted) PDX_B_DENSE(IS, B, 0, true) else PDX_B_DENSE(IS, B, 0, false)  \
     } else if (stats_wanted) {                                                         \
       bscan_kernel<IS, B, 0, false, true><<<g, b, 0, st>>>(P, A);                      \
