@@ -2422,7 +2422,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   PDX_REQUIRE(P.nsteps > 0, "step schedule too long");
   for (int s = P.nsteps; s < kMaxSteps; ++s) P.ends[s] = 0x7fffffff;
   const int ads_d = (prm->ads_d >= 1 && prm->pruner != PDX_PRUNER_BSA) ? prm->ads_d : store->d;
-  for (int s = 0; s < P.nsteps; ++s) {  // bound_factors_kernel (pdx_scan.cu)
+  for (int s = 0; s < P.nsteps; ++s) {  // bound_factors (pdx_scan.cu)
     double ratio = 1.0, band = 1.0;
     if (prm->pruner == PDX_PRUNER_ADS && P.ends[s] < ads_d) {
       ratio = (double)P.ends[s] / (double)ads_d;

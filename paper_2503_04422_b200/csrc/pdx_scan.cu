@@ -120,16 +120,19 @@ __global__ void __launch_bounds__(256) build_visits_kernel(
 // ADS ratio = d'/D and band = 1 + eps0/sqrt(d') in float64 (pruning.py:80-88);
 // ratio = band = 1 wherever the comparison is against T itself (BOND, none,
 // BSA — whose per-vector estimate is compared with T — and ADS at d' >= D).
-__global__ void bound_factors_kernel(int pruner, int d, int initial_step, int nsteps, int ads_d,
-                                     double eps0, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+// The ADS bound's per-step factors (pruning.py:68-88) in float64, on the
+// host: IEEE division, square root and addition, the same values the device
+// intrinsics (__ddiv_rn, __dsqrt_rn, __dadd_rn) give.
+static void bound_factors(int pruner, int d, int initial_step, int nsteps, int ads_d, double eps0,
+                          double* out) {
   int64_t e = 0, width = initial_step;  // step_schedule (search.py:106-117)
+  for (int s = 0; s < 2 * kMaxSteps; ++s) out[s] = 1.0;
   for (int s = 0; s < nsteps; ++s, width *= 2) {
     e = e + width < d ? e + width : d;
     double ratio = 1.0, band = 1.0;
     if (pruner == PDX_PRUNER_ADS && e < ads_d) {
-      ratio = __ddiv_rn((double)e, (double)ads_d);
-      band = __dadd_rn(1.0, __ddiv_rn(eps0, __dsqrt_rn((double)e)));
+      ratio = (double)e / (double)ads_d;
+      band = 1.0 + eps0 / sqrt((double)e);
     }
     out[s] = ratio;
     out[kMaxSteps + s] = band;
@@ -270,15 +273,13 @@ static int search_impl(const pdx_store* store, const pdx_search_params* prm,
               (long long)work_bytes, (long long)need);
   unsigned char* w = reinterpret_cast<unsigned char*>(d_work);
   int32_t* d_overflow = reinterpret_cast<int32_t*>(w);
-  double* d_factors = reinterpret_cast<double*>(w + 64);  // [2][kMaxSteps], header < 512 B
   int32_t* d_counts = reinterpret_cast<int32_t*>(w + 512);
   TileEntry* d_vis = reinterpret_cast<TileEntry*>(
       w + 512 + ((nlists * sizeof(int32_t) + 255) / 256) * 256);
   cudaStream_t st = as_stream(stream);
-  PDX_CUDA_CHECK(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), st));
-  bound_factors_kernel<<<1, 32, 0, st>>>(prm->pruner, store->d, prm->initial_step, nsteps,
-                                         prm->ads_d >= 1 ? prm->ads_d : store->d,
-                                         prm->ads_epsilon0, d_factors);
+  // (the overflow word is write-only diagnostics: the fallback of a batched
+  // search, `only`, skips its reset and saves a graph node)
+  if (!only) PDX_CUDA_CHECK(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), st));
   if (nseg > 0 && maxvis > 0) {
     build_visits_kernel<<<(unsigned)nlists, 256, 0, st>>>(
         d_seg_bucket, nseg, store->d_bucket_block, store->d_block_tile, store->d_block_m,
@@ -310,7 +311,8 @@ static int search_impl(const pdx_store* store, const pdx_search_params* prm,
   A.nsteps = nsteps;
   A.sf = prm->selection_fraction;
   A.ads_d = (prm->ads_d >= 1 && prm->pruner != PDX_PRUNER_BSA) ? prm->ads_d : store->d;
-  A.factors = d_factors;
+  bound_factors(prm->pruner, store->d, prm->initial_step, nsteps,
+                prm->ads_d >= 1 ? prm->ads_d : store->d, prm->ads_epsilon0, A.factors);
   A.resid = store->d_resid;
   A.bsa_coef = prm->bsa_coef;
   A.eps0 = prm->ads_epsilon0;

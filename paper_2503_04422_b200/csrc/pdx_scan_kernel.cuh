@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(288, PDX_SCAN_MIN_BLOCKS) pdx_scan_kernel(cons
     ctl.cyc[0] = ctl.cyc[1] = ctl.cyc[2] = ctl.cyc[3] = 0;
   }
   __syncthreads();
-  if (threadIdx.x < nsteps) {  // bound factors (bound_factors_kernel, pdx_scan.cu)
+  if (threadIdx.x < nsteps) {  // bound factors (bound_factors, pdx_scan.cu: kernel parameters)
     s_ratio[threadIdx.x] = A.factors[threadIdx.x];
     s_band[threadIdx.x] = A.factors[kMaxSteps + threadIdx.x];
     if (METRIC == kMetricL2Bsa) {  // the query's residual energy after this step

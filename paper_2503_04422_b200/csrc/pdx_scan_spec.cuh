@@ -97,7 +97,7 @@ struct ScanArgs {
   int64_t* trace_len;
   int64_t* debug;  // optional [nq][8] counters (see pdx_search_out)
   int32_t sparse_max;  // a tile goes sparse once at most this many slots survive
-  const double* factors;  // [2][kMaxSteps]: per-step bound ratio, band
+  double factors[2 * kMaxSteps];  // per-step bound ratio, then band (bound_factors, pdx_scan.cu)
   int32_t nq, nsplit;     // split mode: CTA b scans range b / nq of query b % nq
   const float* resid;     // BSA: [ntiles][nsteps][64] residual energy per slot and step
   const float* bsa_coef;  // BSA: [nsteps]
@@ -134,7 +134,7 @@ struct QueryRefs {
 // against T itself (BOND, none, ADS once dims_seen >= d): T * 1 * 1 * 1
 // rounds back to T exactly, so one branch-free formula serves every pruner.
 __device__ __forceinline__ float ads_or_bond_bound(float T, double ratio, double band) {
-  // bound_factors_kernel never pairs ratio 1 with band != 1: same value as the
+  // bound_factors never pairs ratio 1 with band != 1: same value as the
   // formula, fewer live registers
   if (ratio == 1.0) return T;
   const double t = __dmul_rn(__dmul_rn(__dmul_rn((double)T, ratio), band), band);

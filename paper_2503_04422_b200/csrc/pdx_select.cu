@@ -34,21 +34,40 @@ __device__ __forceinline__ float2 sqdiff_pair(float q, float c0, float c1) {
   return r;
 }
 
+// acc + (q - c)^2 for a centroid pair, all three steps f32x2: FADD2 (q
+// broadcast), the square as FFMA2 with a +0 addend — the exact square rounded
+// once, bit-identical to mul.rn (a square is never -0) — and FADD2; ptxas does
+// not contract FFMA2 + FADD2, so each op stays separately rounded (the
+// vertical kernel's arithmetic) at 3 instructions per dim and pair.
+__device__ __forceinline__ unsigned long long sqacc_pair(unsigned long long acc, float q,
+                                                         unsigned long long cc) {
+  unsigned long long qq, z, t, p, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(z) : "f"(0.0f));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(qq), "l"(cc));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(p) : "l"(t), "l"(z));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(acc), "l"(p));
+  return r;
+}
+
 template <int METRIC>
 __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restrict__ Q, int64_t nq,
                                                             const float* __restrict__ Cm, int nlist,
                                                             int d, float* __restrict__ out) {
-  __shared__ float qs[kDC][kQT + 4];
-  __shared__ float cs[kDC][kCT + 4];
+  __shared__ __align__(16) float qs[kDC][kQT + 4];
+  __shared__ __align__(16) float cs[kDC][kCT + 4];
   constexpr int RI = kQT / 16;  // query rows per thread
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t q0 = (int64_t)blockIdx.y * kQT;
   const int c0 = blockIdx.x * kCT;
   float acc[RI][4];
+  unsigned long long acc2[RI][2];  // L2: the accumulators as centroid pairs
 #pragma unroll
-  for (int i = 0; i < RI; ++i)
+  for (int i = 0; i < RI; ++i) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    acc2[i][0] = acc2[i][1] = 0ull;  // (+0, +0)
+  }
   for (int j0 = 0; j0 < d; j0 += kDC) {
 #pragma unroll
     for (int it = 0; it < (kQT * kDC) / 256; ++it) {
@@ -70,19 +89,21 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
     const int jn = min(kDC, d - j0);
     for (int jj = 0; jj < jn; ++jj) {
       float qv[RI], cv[4];
-#pragma unroll
-      for (int i = 0; i < RI; ++i) qv[i] = qs[jj][ty * RI + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) cv[j] = cs[jj][tx * 4 + j];
+      static_assert(RI == 2, "the query pair is one 64-bit shared-memory load");
+      const float2 q2 = *reinterpret_cast<const float2*>(&qs[jj][ty * RI]);
+      qv[0] = q2.x;
+      qv[1] = q2.y;
+      const float4 c4 = *reinterpret_cast<const float4*>(&cs[jj][tx * 4]);
+      cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
       if (METRIC == PDX_METRIC_L2) {
+        unsigned long long c01, c23;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(c01) : "f"(cv[0]), "f"(cv[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(c23) : "f"(cv[2]), "f"(cv[3]));
 #pragma unroll
-        for (int i = 0; i < RI; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; j += 2) {
-            const float2 p = sqdiff_pair(qv[i], cv[j], cv[j + 1]);
-            acc[i][j] = __fadd_rn(acc[i][j], p.x);
-            acc[i][j + 1] = __fadd_rn(acc[i][j + 1], p.y);
-          }
+        for (int i = 0; i < RI; ++i) {
+          acc2[i][0] = sqacc_pair(acc2[i][0], qv[i], c01);
+          acc2[i][1] = sqacc_pair(acc2[i][1], qv[i], c23);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < RI; ++i)
@@ -91,6 +112,13 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
       }
     }
     __syncthreads();
+  }
+  if (METRIC == PDX_METRIC_L2) {
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i][2 * h]), "=f"(acc[i][2 * h + 1]) : "l"(acc2[i][h]));
   }
 #pragma unroll
   for (int i = 0; i < RI; ++i) {
