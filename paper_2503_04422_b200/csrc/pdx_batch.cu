@@ -1953,7 +1953,8 @@ __global__ void __launch_bounds__(kBW * 32, PDX_BSCAN0_MIN_BLOCKS)
       int slot = 0;
       if (act) {
         const int r = idx - excl, p0 = __popc(m0);
-        slot = r < p0 ? nth_bit(m0, r) : 32 + nth_bit(m1, r - p0);
+        const bool hi = r >= p0;  // (one n-th-bit search, over the half that holds it)
+        slot = nth_bit(hi ? m1 : m0, hi ? r - p0 : r) + (hi ? 32 : 0);
       } else {
         j = 0;
       }
