@@ -337,7 +337,7 @@ def test_filtered_head_schedules(P, oracle, pruner, initial_step):
     """bscan0_kernel (results-only MODE 0: the head as a certainty-margin
     filter, the candidates' exact chains from shared memory) for every
     compile-time head schedule, d not a multiple of 8 included."""
-    for d, seed in [(128, 3), (44, 4), (16, 5)]:
+    for d, seed in [(128, 3), (44, 4), (27, 6), (20, 7), (16, 5)]:  # (d < the first deep step's end too)
         x = recipes.data("mixture", 40_000, d, seed)
         q = recipes.queries("near", x, 70, seed + 1)
         params = P.SearchParams(k=10, pruner=pruner, initial_step=initial_step)
@@ -387,3 +387,17 @@ def test_phase1_chain_sequential_equals_overlapped(P, rotated):
         scan = P.ivf_search_batch(index, qr, params, 16, batched=1)
         np.testing.assert_array_equal(fast["ids"], scan["ids"])
         np.testing.assert_array_equal(fast["dist"], scan["dist"])
+
+
+def test_large_batch_takes_the_sequential_phase1(P, rotated):
+    """More than 8 queries per SM: the chain kernel runs after the dense one
+    (all its CTAs at once) instead of underneath it."""
+    _, qr, index = rotated
+    rng = np.random.default_rng(3)
+    q = np.concatenate([qr + 0.01 * rng.standard_normal(qr.shape).astype(np.float32)
+                        for _ in range(14)])  # 1,344 queries
+    params = P.SearchParams(k=10, pruner="ads", ads=P.AdsPruner(d=128, epsilon0=2.1))
+    fast = P.ivf_search_batch(index, q, params, 16, batched=2)
+    scan = P.ivf_search_batch(index, q, params, 16, batched=1)
+    np.testing.assert_array_equal(fast["ids"], scan["ids"])
+    np.testing.assert_array_equal(fast["dist"], scan["dist"])
