@@ -1601,19 +1601,19 @@ __global__ void __launch_bounds__((DENSE ? kBWD : kBW) * 32, DENSE ? 4 : PDX_BSC
     __syncwarp();
   }
   };
-  if (MODE == 0) {  // one item per CTA: CTAs retire independently (no item barrier)
+  if constexpr (MODE == 0) {  // one item per CTA: CTAs retire independently (no item barrier)
     if ((int)blockIdx.x < *A.nitems) run_item(blockIdx.x);
-    return;
-  }
-  // MODE 1 (most items need little work): persistent CTAs pull work items
-  // from a counter instead of launching the item-count upper bound
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_itx = atomicAdd(A.wctr + MODE, 1);
-    __syncthreads();
-    const int itx = s_itx;
-    if (itx >= *A.nitems) return;
-    run_item(itx);
+  } else {
+    // MODE 1 (most items need little work): persistent CTAs pull work items
+    // from a counter instead of launching the item-count upper bound
+    for (;;) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_itx = atomicAdd(A.wctr + MODE, 1);
+      __syncthreads();
+      const int itx = s_itx;
+      if (itx >= *A.nitems) return;
+      run_item(itx);
+    }
   }
 }
 
@@ -2454,7 +2454,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   P.surv_cap = 4 * k + surv_extra;
   P.dbg = getenv("PDX_BATCH_DEBUG") != nullptr;
   P.norho = !(out->d_touched || out->d_total || out->d_trace || getenv("PDX_FULL_MODE1"));
-  const int64_t per = nseg - 1;
   const int64_t pmax = nq64 * nseg * store->max_bucket_tiles;
   const bool trace = out->d_trace != nullptr;
   // results only (no values_touched / traces requested): phase 1 and MODE 0
