@@ -101,6 +101,7 @@ struct BSurv {
   float tafter;
   int32_t real;
   int32_t tile;  // the store tile holding the slot (bverify_kernel)
+  float tbefore;  // T^ before the pushes of its pair (= that_of(pair)): no search in verify / final
 };
 struct DeepItem {
   float acc;
@@ -404,7 +405,7 @@ __device__ __forceinline__ void record_survivor(const BParams& P, const BArgs& A
   const int i = atomicAdd(&A.nsurv[q], 1);
   if (i < P.surv_cap)
     A.surv[(int64_t)q * P.surv_cap + i] =
-        BSurv{dist, pair, __ldg(A.tile_ids + tile * kTile + slot), slot, 0.f, 0, (int32_t)tile};
+        BSurv{dist, pair, __ldg(A.tile_ids + tile * kTile + slot), slot, 0.f, 0, (int32_t)tile, 0.f};
   else
     A.flags[q] = 1;
 }
@@ -2048,6 +2049,7 @@ __device__ __forceinline__ void bchain_query(const BParams& P, const BArgs& A, c
     float t = lane < k ? top[lane] : INFINITY;
     for (int i = 0; i < n;) {
       const int pi = ls[i].pair;
+      const float Tb = __shfl_sync(kFull, t, k - 1);
       int e = i;
       for (; e < n && ls[e].pair == pi; ++e) {
         const float dv = ls[e].dist;
@@ -2059,12 +2061,16 @@ __device__ __forceinline__ void bchain_query(const BParams& P, const BArgs& A, c
         }
       }
       const float T = __shfl_sync(kFull, t, k - 1);
-      for (int j = i + lane; j < e; j += 32) ls[j].tafter = T;
+      for (int j = i + lane; j < e; j += 32) {
+        ls[j].tafter = T;
+        ls[j].tbefore = Tb;
+      }
       i = e;
     }
   } else if (lane == 0) {
     for (int i = 0; i < n;) {
       int e = i;
+      const float Tb = top[k - 1];
       for (; e < n && ls[e].pair == ls[i].pair; ++e) {
         const float dv = ls[e].dist;
         if (dv < top[k - 1]) {  // TopK.push, threshold value only
@@ -2076,7 +2082,10 @@ __device__ __forceinline__ void bchain_query(const BParams& P, const BArgs& A, c
           top[j] = dv;
         }
       }
-      for (int j = i; j < e; ++j) ls[j].tafter = top[k - 1];
+      for (int j = i; j < e; ++j) {
+        ls[j].tafter = top[k - 1];
+        ls[j].tbefore = Tb;
+      }
       i = e;
     }
   }
@@ -2107,7 +2116,8 @@ __device__ __forceinline__ void bverify_entry(const BParams& P, const BArgs& A, 
   BSurv* sv = A.surv + (int64_t)q * P.surv_cap;  // pair-sorted (bchain_kernel)
   const BSurv e = sv[i];
   const float tp = A.tprime[q];
-  const float that = that_of(sv, n, e.pair, tp);
+  const float that = e.tbefore;  // (= that_of(sv, n, e.pair, tp))
+  (void)n;
   if (!(P.norho ? that < tp : pair_uncertain(that, tp, A.prho[A.qoff[q] + e.pair]))) return;
   const float* __restrict__ tb = A.tiles + (int64_t)e.tile * A.tile_stride;
   const float* __restrict__ qg = A.queries + (int64_t)q * P.d;
@@ -2193,7 +2203,7 @@ __device__ __forceinline__ void bfinal_query(const BParams& P, const BArgs& A, c
   // drop unconfirmed survivors of uncertain pairs (the list is pair-sorted)
   bool bad = false;
   for (int i = lane; i < n; i += 32) {
-    const float that = that_of(sv, n, sv[i].pair, tp);
+    const float that = sv[i].tbefore;  // (= that_of(sv, n, sv[i].pair, tp))
     const bool unc = P.norho ? that < tp : pair_uncertain(that, tp, A.prho[p0 + sv[i].pair]);
     if (unc && !sv[i].real) {
       if (sv[i].dist < that) bad = true;
