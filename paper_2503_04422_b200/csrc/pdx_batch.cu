@@ -16,10 +16,10 @@
 //
 //  Phase 1  each query's first selected bucket that has blocks (at most its
 //           first kP1Cap tiles), exactly: bdense_kernel records every
-//           slot's partial at every step end (the linear first block dense,
-//           the rest pruned under T_0, the threshold after that block, which
-//           bounds every later T_b), then bchain1_kernel (one warp per query)
-//           replays the reference chain over those partials.  Heap H, T' =
+//           slot's partial at every step end (prune-free), and
+//           bchain1_kernel (one warp per query; for results-only searches
+//           running underneath the dense pass, tile by tile) replays the
+//           reference chain over those partials.  Heap H, T' =
 //           its k-th distance; every later block has T_b <= T'.  The rest of
 //           the selected blocks (the bucket's tail first) form the window.
 //  Phase 2  (bscan_kernel MODE 0) every (query, tile) pair of the window,
@@ -426,11 +426,11 @@ __device__ __forceinline__ float bound_at(const BParams& P, float T, int s, cons
 // and the survivor traces.  (A query's first bucket is where its threshold
 // moves at almost every block, so pruned speculation would be replayed
 // anyway after chasing long survivor tails one L2 round trip at a time.)
-// FIRST: tile 0 of each query's first bucket (its linear block), no pruning.
-// Otherwise tiles 1.. under the bounds B_s(T_0), T_0 the threshold after that
-// block (b0bnd, +inf while the heap is not full): T_0 >= every later T_b of
-// the chain, so a slot pruned under it is pruned by the chain too — its
-// partials past that step are recorded as +inf and never read from HBM.
+// (Pruning the dense pass under T_0, the threshold after the first block, was
+// measured and removed: in a query's own bucket T_0 prunes little, the
+// conditional loads and the extra first-block kernel cost more than the
+// bytes they save — dense pass 85 -> 79 us, and 14 us of first-block kernel
+// gone from the critical path.)
 // st.release / ld.acquire at gpu scope: the per-tile ready flags between the
 // dense kernel and the chain kernel running next to it.
 __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
@@ -450,35 +450,26 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
 // One CTA of the dense pass: query q, warp w takes tile tile0 + w of the
 // query's first bucket.  ready (overlapped phase 1): flag per phase-1 tile,
 // set once the tile's partials are written.
-template <bool BSA, bool FIRST>
+template <bool BSA>
 __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
                                            const int32_t* __restrict__ seg0,
                                            const int64_t* __restrict__ p1off,
-                                           float* __restrict__ part1, float* __restrict__ b0bnd,
-                                           const int q, const int tile0, int32_t* ready) {
+                                           float* __restrict__ part1, const int q, const int tile0,
+                                           int32_t* ready) {
   extern __shared__ __align__(16) float s_q[];  // [d_pad] query, then [2][nsteps] BSA rq, sqrt
   __shared__ int32_t s_ends[kMaxSteps];
   __shared__ float s_coef[kMaxSteps];
-  __shared__ double s_ratio[FIRST ? kMaxSteps : 1], s_band[FIRST ? kMaxSteps : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = seg0[q];
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
-  if (FIRST && nt == 0) {  // no first block: T_0 = +inf
-    if (threadIdx.x < P.nsteps) b0bnd[(int64_t)q * P.nsteps + threadIdx.x] = INFINITY;
-    return;
-  }
-  if (!FIRST && tile0 >= min(nt, c_p1cap)) return;
+  if (tile0 >= min(nt, c_p1cap)) return;
   const int nsteps = P.nsteps;
   const float* qg = A.queries + (int64_t)q * P.d;
   for (int j = threadIdx.x; j < P.d_pad; j += blockDim.x) s_q[j] = j < P.d ? qg[j] : 0.f;
   for (int i = threadIdx.x; i < kMaxSteps; i += blockDim.x) {
     s_ends[i] = P.ends[i];
     s_coef[i] = (BSA && i < nsteps) ? A.coef[i] : 0.f;
-    if (FIRST) {
-      s_ratio[i] = P.ratio[i];
-      s_band[i] = P.band[i];
-    }
   }
   __syncthreads();
   float* s_bq = s_q + P.d_pad;
@@ -491,23 +482,32 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
     }
     __syncthreads();
   }
-  if (FIRST && w > 0) return;
-  {  // one tile per warp (latency-bound: many tiles in flight)
-  const int ti = FIRST ? 0 : tile0 + w;
+  // one tile per warp (latency-bound: many tiles in flight)
+  const int ti = tile0 + w;
   if (ti >= min(nt, c_p1cap)) return;
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
-  const float bl = (!FIRST && lane < nsteps) ? b0bnd[(int64_t)q * nsteps + lane] : INFINITY;
   const float* __restrict__ tb = A.tiles + tile * A.tile_stride;
   float* __restrict__ out = part1 + (p1off[q] + ti) * nsteps * kTile;
   const int ng = P.d_pad >> 3;
   float acc0 = 0.f, acc1 = 0.f;
-  bool al0 = lane < m, al1 = lane + 32 < m;
+  const bool in0 = lane < m, in1 = lane + 32 < m;
   int nend = s_ends[0];  // end of the current step
   int s = 0;
-  // one 8-dim group of both slots: the partial sums, and at a step end the
-  // decision under B_s(T_0) and the recorded partials
-  auto group = [&](const int g, const float (&x0)[8], const float (&x1)[8]) {
+  float n0[8], n1[8];  // the next group loads while the current one is evaluated
+  ldg8(tb + lane * 8, n0);
+  ldg8(tb + (32 + lane) * 8, n1);
+  for (int g = 0; g < ng && s < nsteps; ++g) {
+    float x0[8], x1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      x0[e] = n0[e];
+      x1[e] = n1[e];
+    }
+    if (g + 1 < ng) {
+      ldg8(tb + ((size_t)(g + 1) * kTile + lane) * 8, n0);
+      ldg8(tb + ((size_t)(g + 1) * kTile + 32 + lane) * 8, n1);
+    }
     const float4 qa = *reinterpret_cast<const float4*>(s_q + g * 8);
     const float4 qb = *reinterpret_cast<const float4*>(s_q + g * 8 + 4);
     const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
@@ -517,7 +517,7 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
         acc0 = l2upd(acc0, qv[e], x0[e]);
         acc1 = l2upd(acc1, qv[e], x1[e]);
       }
-      return;
+      continue;
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -533,113 +533,28 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
             v0 = bsa_est2(acc0, __ldg(rs + lane), s_bq[s], s_bq[nsteps + s], s_coef[s]);
             v1 = bsa_est2(acc1, __ldg(rs + lane + 32), s_bq[s], s_bq[nsteps + s], s_coef[s]);
           }
-          if (!FIRST) {
-            const float B = __shfl_sync(kFull, bl, s);
-            al0 = al0 && v0 < B;
-            al1 = al1 && v1 < B;
-          }
-          out[s * kTile + lane] = (FIRST || al0) ? v0 : INFINITY;
-          out[s * kTile + 32 + lane] = (FIRST || al1) ? v1 : INFINITY;
+          out[s * kTile + lane] = in0 ? v0 : INFINITY;  // (slots past the block's m vectors)
+          out[s * kTile + 32 + lane] = in1 ? v1 : INFINITY;
           ++s;
           nend = s < nsteps ? s_ends[s] : 0x7fffffff;
         }
       }
     }
-  };
-  if constexpr (FIRST) {
-    // the linear first block of every query: one warp per query and nothing
-    // else to hide the loads behind — four groups per batch, the next batch
-    // in flight while this one is evaluated
-    float a0[4][8], b0x[4][8], a1[4][8], b1x[4][8];
-    auto load4 = [&](const int g0, float (&xa)[4][8], float (&xb)[4][8]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (g0 + u < ng) {
-          ldg8(tb + ((size_t)(g0 + u) * kTile + lane) * 8, xa[u]);
-          ldg8(tb + ((size_t)(g0 + u) * kTile + 32 + lane) * 8, xb[u]);
-        }
-    };
-    auto proc4 = [&](const int g0, const float (&xa)[4][8], const float (&xb)[4][8]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (g0 + u < ng && s < nsteps) group(g0 + u, xa[u], xb[u]);
-    };
-    load4(0, a0, b0x);
-    for (int g0 = 0; g0 < ng; g0 += 8) {
-      load4(g0 + 4, a1, b1x);
-      proc4(g0, a0, b0x);
-      load4(g0 + 8, a0, b0x);
-      proc4(g0 + 4, a1, b1x);
-    }
-  } else {
-    float n0[8], n1[8];  // the next group loads while the current one is evaluated
-#pragma unroll
-    for (int e = 0; e < 8; ++e) n0[e] = n1[e] = 0.f;
-    if (al0) ldg8(tb + lane * 8, n0);
-    if (al1) ldg8(tb + (32 + lane) * 8, n1);
-    for (int g = 0; g < ng && s < nsteps; ++g) {
-      if (!__any_sync(kFull, al0 || al1)) {  // every slot pruned under T_0
-        for (; s < nsteps; ++s) {
-          out[s * kTile + lane] = INFINITY;
-          out[s * kTile + 32 + lane] = INFINITY;
-        }
-        break;
-      }
-      float x0[8], x1[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        x0[e] = n0[e];
-        x1[e] = n1[e];
-      }
-      if (g + 1 < ng) {
-        if (al0) ldg8(tb + ((size_t)(g + 1) * kTile + lane) * 8, n0);
-        if (al1) ldg8(tb + ((size_t)(g + 1) * kTile + 32 + lane) * 8, n1);
-      }
-      group(g, x0, x1);
-    }
   }
-  if (FIRST) {
-    // T_0: the k-th smallest distance of the first block (the heap after the
-    // linear block, search.py:125-135), +inf below k vectors; b0bnd = B_s(T_0)
-    float T = INFINITY;
-    const int k = P.k;
-    if (m >= k) {
-      const float* fin = out + (nsteps - 1) * kTile;  // this lane's own writes
-      const float v0 = lane < m ? fin[lane] : INFINITY, v1 = lane + 32 < m ? fin[lane + 32] : INFINITY;
-      int l0 = 0, e0 = 0, l1 = 0, e1 = 0;  // values below / equal to mine
-      for (int j = 0; j < 32; ++j) {
-        const float a = __shfl_sync(kFull, v0, j), b = __shfl_sync(kFull, v1, j);
-        l0 += (a < v0) + (b < v0);
-        e0 += (a == v0) + (b == v0);
-        l1 += (a < v1) + (b < v1);
-        e1 += (a == v1) + (b == v1);
-      }
-      const bool h0 = l0 <= k - 1 && l0 + e0 >= k, h1 = l1 <= k - 1 && l1 + e1 >= k;
-      const unsigned hm = __ballot_sync(kFull, h0 || h1);
-      const int src = __ffs(hm) - 1;
-      T = __shfl_sync(kFull, h0 ? v0 : v1, src);
-    }
-    if (lane < nsteps)
-      b0bnd[(int64_t)q * nsteps + lane] =
-          T == INFINITY ? INFINITY : bound_at(P, T, lane, s_ratio, s_band);
-  }
-  if (!FIRST && ready) {  // the tile's partials are complete: publish
+  if (ready) {  // the tile's partials are complete: publish
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(ready + p1off[q] + ti, P.dbg ? (int32_t)(gtimer_ns() >> 7) | 1 : 1);
   }
-  }
 }
 
-template <bool BSA, bool FIRST>
+template <bool BSA>
 __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArgs A,
                                                      const int32_t* __restrict__ seg0,
                                                      const int64_t* __restrict__ p1off,
                                                      float* __restrict__ part1,
-                                                     float* __restrict__ b0bnd,
                                                      int32_t* __restrict__ ready) {
-  bdense_cta<BSA, FIRST>(P, A, seg0, p1off, part1, b0bnd, blockIdx.x,
-                         FIRST ? 0 : (int)blockIdx.y * 4 + 1, ready);
+  bdense_cta<BSA>(P, A, seg0, p1off, part1, blockIdx.x, (int)blockIdx.y * 4, ready);
 }
 
 
@@ -732,11 +647,10 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
     nid1 = __ldg(gid + lane + 32);
     nm = A.block_m[b0 + ti];
   };
-  // nready: tiles [0, nready) are known to be published (tile 0 comes from
-  // the kernel before).  A refresh reads the flags of the next 32 tiles in one
+  // nready: tiles [0, nready) are known to be published.  A refresh reads the flags of the next 32 tiles in one
   // go (flags only ever go up), so the chain pays an L2 round trip for flags
   // only while it runs ahead of the dense pass.
-  int nready = rdy ? 1 : nt;
+  int nready = rdy ? 0 : nt;
   auto refresh = [&]() {
     const int t = nready + lane;
     const int f = t < nt ? ld_acquire(rdy + t) : 0;
@@ -2490,7 +2404,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     carve<int64_t>(at, nq + 1);                // qoff
     carve<int64_t>(at, nq + 1);                // p1off
     carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);  // part1
-    carve<float>(at, nq64 * P.nsteps);                                     // b0bnd
     carve<int32_t>(at, nq64 * nseg);           // pbase
     carve<int32_t>(at, nb + 1);                // bcnt     } zeroed by one memset
     carve<int32_t>(at, nb + 1);                // bcur     }
@@ -2544,7 +2457,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   int64_t* qoff = carve<int64_t>(at, nq + 1);
   int64_t* p1off = carve<int64_t>(at, nq + 1);
   float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);
-  float* b0bnd = carve<float>(at, nq64 * P.nsteps);
   int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
   int32_t* bcnt = carve<int32_t>(at, nb + 1);  // bcnt .. p1ready: zeroed by one memset
   int32_t* bcur = carve<int32_t>(at, nb + 1);
@@ -2696,16 +2608,12 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   // ---- phase 1: the first selected bucket of every query (exact chain)
   {
     const int p1max = std::min(store->max_bucket_tiles, p1cap);
-    const dim3 g((unsigned)nq, (unsigned)((p1max + 2) / 4));
+    const dim3 g((unsigned)nq, (unsigned)((p1max + 3) / 4));
     const size_t sm = sizeof(float) * (store->d_pad + 2 * kMaxSteps);
     if (sm > 48 * 1024) {
-      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, true>,
+      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<true, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false, false>,
+      PDX_B_CHECK(cudaFuncSetAttribute(bdense_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
     // results only, k <= 32: the threshold chain (latency-bound, one warp per
@@ -2724,7 +2632,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
     // (larger batches: the chain CTAs would have to take turns — the chain
     // kernel after the dense one, all its CTAs at once, is faster there)
-    const bool overlap = overlap_env && !stats_wanted && k <= 32 && P.nsteps <= 12 && p1max > 1 &&
+    const bool overlap = overlap_env && !stats_wanted && k <= 32 && P.nsteps <= 12 && p1max > 0 &&
                          (nq + 7) / 8 <= nsm;
     const int nchain = (nq + 7) / 8;  // at most one chain CTA per SM
     const size_t hsm = (size_t)8 * k * (sizeof(float) + sizeof(int64_t));
@@ -2739,12 +2647,6 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     };
     SideStream& cside = side_stream(8 + side_slot);
     if (p1max > 0) {
-      const dim3 g1((unsigned)nq, 1);
-      if (bsa)
-        bdense_kernel<true, true><<<g1, 32, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
-      else
-        bdense_kernel<false, true><<<g1, 32, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, nullptr);
-      PDX_B_CHECK(cudaGetLastError());
       if (overlap) {  // the chain first (its CTAs become resident), then the dense pass
         PDX_B_CHECK(cudaEventRecord(cside.fork, st));
         PDX_B_CHECK(cudaStreamWaitEvent(cside.s, cside.fork, 0));
@@ -2755,12 +2657,12 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
           PDX_B_CHECK(chain1(bchain1_kernel<12, true, false>, cside.s, nchain, p1ready));
         PDX_B_CHECK(cudaEventRecord(cside.join, cside.s));
       }
-      if (p1max > 1) {
+      {
         int32_t* rdy = overlap ? p1ready : nullptr;
         if (bsa)
-          bdense_kernel<true, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, rdy);
+          bdense_kernel<true><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, rdy);
         else
-          bdense_kernel<false, false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, b0bnd, rdy);
+          bdense_kernel<false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, rdy);
         PDX_B_CHECK(cudaGetLastError());
       }
       if (overlap) {
