@@ -668,7 +668,7 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
           refresh();
           if (ti < nready) break;
           __nanosleep(64);
-          if (clock64() - t_start > (1ll << 24)) {  // ~10 ms: no heap -> T' = +inf -> the per-query scan
+          if (clock64() - t_start > (1ll << 22)) {  // ~2 ms: no heap -> T' = +inf -> the per-query scan
             dead = true;
             break;
           }
@@ -2621,7 +2621,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     // second stream, with at most one persistent CTA per SM, and consumes a
     // tile as soon as the dense kernel has raised the tile's ready flag.  The
     // dense CTAs never wait, so there is no circular wait; a chain warp that
-    // still waits after ~10 ms gives its query up to the per-query scan.
+    // still waits after ~2 ms gives its query up to the per-query scan.
     // (PDX_P1_OVERLAP=0: the two kernels one after the other.)
     static const bool overlap_env = [] {
       const char* e = getenv("PDX_P1_OVERLAP");
