@@ -401,3 +401,18 @@ def test_large_batch_takes_the_sequential_phase1(P, rotated):
     scan = P.ivf_search_batch(index, q, params, 16, batched=1)
     np.testing.assert_array_equal(fast["ids"], scan["ids"])
     np.testing.assert_array_equal(fast["dist"], scan["dist"])
+
+
+def test_fuzz_batched_equals_per_query_scan(P):
+    """A seeded sample of tools/fuzz_batched.py: random shapes, schedules,
+    pruners, k, nprobe and data distributions (offsets, denormal-scale values,
+    duplicates, integer grids) — the batched pipeline, results only and with
+    statistics, equals the per-query scan."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "tools" / "fuzz_batched.py"), "14", "7"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "14 / 14 identical" in r.stdout

@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for c in 64 48 32 24; do
+for c in 64 48 40 32 64 48; do
 PDX_P1CAP=$c timeout 600 python bench.py --steps 20 --warmup 5 --no-extras > gpurun_out/bench_cap$c.json 2> gpurun_out/bench_cap$c.err
 python -c "
 import json
