@@ -115,6 +115,7 @@ struct DeepItem {
 struct BParams {
   int32_t d, d_pad, nsteps, hsteps, hdims, k, pruner, nseg;
   int32_t nq, surv_cap;
+  int32_t p1max;   // phase-1 tiles per query (stride of part1 and of the ready flags)
   int32_t dbg;     // PDX_BATCH_DEBUG: MODE 1 counts its work in nitems[4..6]
   int32_t norho;   // results only: no rho; every pair with T^ < T' counts as uncertain
   uint32_t hmask;  // bit e: a head step ends after dim e
@@ -276,10 +277,9 @@ __device__ __forceinline__ float bsa_est2(float acc, float rx, float rq, float s
 // selected buckets, the window's pair count, and the bucket histogram.
 __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
                              const int64_t* __restrict__ bucket_block,
-                             const int64_t* __restrict__ block_tile, int32_t* __restrict__ seg0,
+                             const int64_t* __restrict__ block_tile,
                              int64_t* __restrict__ wcount, int32_t* __restrict__ pbase,
-                             int32_t* __restrict__ bcnt, int64_t* __restrict__ p1off,
-                             int p1max, int32_t* __restrict__ fseg) {
+                             int32_t* __restrict__ bcnt, int32_t* __restrict__ fseg) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -296,9 +296,7 @@ __global__ void bprep_kernel(const int32_t* __restrict__ sel, int nq, int nseg,
   const int nt0 = ntiles(sq[f]);
   const int p1 = min(nt0, c_p1cap);
   if (lane == 0) {
-    seg0[q] = sq[f];
     fseg[q] = f;
-    p1off[q] = (int64_t)q * p1max;  // phase-1 tiles of query q: a fixed stride, no scan needed
     if (q == 0) wcount[nq] = 0;
     pbase[(int64_t)q * nseg + f] = -p1;
     if (nt0 > p1) atomicAdd(&bcnt[sq[f]], 1);
@@ -415,6 +413,21 @@ __device__ __forceinline__ float bound_at(const BParams& P, float T, int s, cons
   return P.pruner == PDX_PRUNER_BSA ? T : ads_or_bond_bound(T, ratio[s], band[s]);
 }
 
+// Phase 1's bucket of query q: the first selected bucket that has tiles (the
+// last selected one if none has) — bprep_kernel's fseg, recomputed here so
+// that phase 1 does not wait for the planning kernels.  Its partials and
+// ready flags live at a fixed stride: tile ti of query q is entry q * p1max + ti.
+__device__ __forceinline__ int first_bucket(const BParams& P, const BArgs& A, const int q) {
+  const int32_t* sq = A.sel + (int64_t)q * P.nseg;
+  int f = 0;
+  for (;;) {
+    const int c = sq[f];
+    const int64_t nt = A.block_tile[A.bucket_block[c + 1]] - A.block_tile[A.bucket_block[c]];
+    if (nt > 0 || f >= P.nseg - 1) return c;
+    ++f;
+  }
+}
+
 // ---------------------------------------------------------------- phase 1
 // The reference chain over each query's first selected bucket, in two
 // kernels.  bdense_kernel: every slot's partial (the BSA estimate for bsa)
@@ -452,15 +465,13 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
 // set once the tile's partials are written.
 template <bool BSA>
 __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
-                                           const int32_t* __restrict__ seg0,
-                                           const int64_t* __restrict__ p1off,
                                            float* __restrict__ part1, const int q, const int tile0,
                                            int32_t* ready) {
   extern __shared__ __align__(16) float s_q[];  // [d_pad] query, then [2][nsteps] BSA rq, sqrt
   __shared__ int32_t s_ends[kMaxSteps];
   __shared__ float s_coef[kMaxSteps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = seg0[q];
+  const int c = first_bucket(P, A, q);
   const int64_t b0 = A.bucket_block[c];
   const int nt = (int)(A.bucket_block[c + 1] - b0);
   if (tile0 >= min(nt, c_p1cap)) return;
@@ -488,7 +499,7 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
   const int64_t tile = A.block_tile[b0] + ti;
   const int m = A.block_m[b0 + ti];
   const float* __restrict__ tb = A.tiles + tile * A.tile_stride;
-  float* __restrict__ out = part1 + (p1off[q] + ti) * nsteps * kTile;
+  float* __restrict__ out = part1 + ((int64_t)q * P.p1max + ti) * nsteps * kTile;
   const int ng = P.d_pad >> 3;
   float acc0 = 0.f, acc1 = 0.f;
   const bool in0 = lane < m, in1 = lane + 32 < m;
@@ -544,17 +555,16 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
   if (ready) {  // the tile's partials are complete: publish
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release(ready + p1off[q] + ti, P.dbg ? (int32_t)(gtimer_ns() >> 7) | 1 : 1);
+    if (lane == 0)
+      st_release(ready + (int64_t)q * P.p1max + ti, P.dbg ? (int32_t)(gtimer_ns() >> 7) | 1 : 1);
   }
 }
 
 template <bool BSA>
 __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArgs A,
-                                                     const int32_t* __restrict__ seg0,
-                                                     const int64_t* __restrict__ p1off,
                                                      float* __restrict__ part1,
                                                      int32_t* __restrict__ ready) {
-  bdense_cta<BSA>(P, A, seg0, p1off, part1, blockIdx.x, (int)blockIdx.y * 4, ready);
+  bdense_cta<BSA>(P, A, part1, blockIdx.x, (int)blockIdx.y * 4, ready);
 }
 
 
@@ -565,8 +575,6 @@ __global__ void __launch_bounds__(128) bdense_kernel(const BParams P, const BArg
 // a tile's partials are read (at L2) only after its flag has been observed.
 template <int NSM, bool RK, bool ST>
 __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
-                                            const int32_t* __restrict__ seg0,
-                                            const int64_t* __restrict__ p1off,
                                             const float* __restrict__ part1, const int oct0,
                                             const int oct_stride, const int32_t* ready) {
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -618,7 +626,7 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
     }
   };
   auto rk_threshold = [&]() { return rn < k ? INFINITY : __shfl_sync(kFull, rd, k - 1); };
-  const int c = seg0[q];
+  const int c = first_bucket(P, A, q);
   const int64_t b0 = A.bucket_block[c];
   const int nt = min((int)(A.bucket_block[c + 1] - b0), c_p1cap);
   const int64_t t0 = A.block_tile[b0];
@@ -631,8 +639,8 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
   float u0[NSM], u1[NSM], n0[NSM], n1[NSM];
   int64_t id0 = 0, id1 = 0, nid0 = 0, nid1 = 0;
   int m = 0, nm = 0;
-  const float* __restrict__ pq = part1 + p1off[q] * nsteps * kTile;
-  const int32_t* rdy = ready ? ready + p1off[q] : nullptr;
+  const float* __restrict__ pq = part1 + (int64_t)q * P.p1max * nsteps * kTile;
+  const int32_t* rdy = ready ? ready + (int64_t)q * P.p1max : nullptr;
   if (P.dbg && ready && lane == 0) A.ptouched[2 * q] = (uint32_t)(gtimer_ns() >> 7);
   auto fetch = [&](int ti) {
     if (ti >= nt) return;
@@ -871,11 +879,9 @@ __device__ __forceinline__ void bchain1_cta(const BParams& P, const BArgs& A,
 
 template <int NSM, bool RK, bool ST = true>
 __global__ void __launch_bounds__(256) bchain1_kernel(const BParams P, const BArgs A,
-                                                      const int32_t* __restrict__ seg0,
-                                                      const int64_t* __restrict__ p1off,
                                                       const float* __restrict__ part1,
                                                       const int32_t* __restrict__ ready) {
-  bchain1_cta<NSM, RK, ST>(P, A, seg0, p1off, part1, blockIdx.x, gridDim.x, ready);
+  bchain1_cta<NSM, RK, ST>(P, A, part1, blockIdx.x, gridDim.x, ready);
 }
 
 // ------------------------------------------------------------ phase 2 scan
@@ -2376,6 +2382,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     return e ? atoi(e) : 64;
   }();
   P.surv_cap = 4 * k + surv_extra;
+  P.p1max = std::min(store->max_bucket_tiles, p1cap);
   P.dbg = getenv("PDX_BATCH_DEBUG") != nullptr;
   P.norho = !(out->d_touched || out->d_total || out->d_trace || getenv("PDX_FULL_MODE1"));
   const int64_t pmax = nq64 * nseg * store->max_bucket_tiles;
@@ -2398,11 +2405,9 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   {
     unsigned char* z = nullptr;
     unsigned char* at = z;
-    carve<int32_t>(at, nq);                    // seg0
     carve<int32_t>(at, nq);                    // fseg
     carve<int64_t>(at, nq + 1);                // wcount
     carve<int64_t>(at, nq + 1);                // qoff
-    carve<int64_t>(at, nq + 1);                // p1off
     carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);  // part1
     carve<int32_t>(at, nq64 * nseg);           // pbase
     carve<int32_t>(at, nb + 1);                // bcnt     } zeroed by one memset
@@ -2451,11 +2456,9 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
   unsigned char* base = nullptr;
   PDX_CUDA_CHECK(cudaMallocAsync(&base, bytes, st));
   unsigned char* at = base;
-  int32_t* seg0 = carve<int32_t>(at, nq);
   int32_t* fseg = carve<int32_t>(at, nq);
   int64_t* wcount = carve<int64_t>(at, nq + 1);
   int64_t* qoff = carve<int64_t>(at, nq + 1);
-  int64_t* p1off = carve<int64_t>(at, nq + 1);
   float* part1 = carve<float>(at, nq64 * std::min(store->max_bucket_tiles, p1cap) * P.nsteps * kTile);
   int32_t* pbase = carve<int32_t>(at, nq64 * nseg);
   int32_t* bcnt = carve<int32_t>(at, nb + 1);  // bcnt .. p1ready: zeroed by one memset
@@ -2529,22 +2532,23 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
     }                                                                                        \
   } while (0)
 
-  // ---- plan: per-query windows, bucket-major entries, work items
-  PDX_B_CHECK(cudaMemsetAsync(bcnt, 0, zero_end - reinterpret_cast<unsigned char*>(bcnt), st));
-  bprep_kernel<<<(nq + 7) / 8, 256, 0, st>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
-                                             store->d_block_tile, seg0, wcount, pbase, bcnt,
-                                             p1off, std::min(store->max_bucket_tiles, p1cap), fseg);
-  PDX_B_CHECK(cudaGetLastError());
-  size_t cb = cubb;
-  // The work lists (below) and phase 1 (after them) only share bprep's
-  // outputs: build the lists on a side stream while phase 1 runs; the main
-  // stream joins before phase 2.
+  // ---- plan: per-query windows, bucket-major entries, work items.  Phase 1
+  // needs none of it (its kernels find each query's first bucket themselves,
+  // its buffers have a fixed stride): the whole plan runs on a side stream
+  // while phase 1 runs; the main stream only clears phase 1's ready flags and
+  // joins before phase 2.
   SideStream& side = side_stream(side_slot);
   cudaStream_t st2 = side.s;
   PDX_B_CHECK(cudaEventRecord(side.fork, st));
   PDX_B_CHECK(cudaStreamWaitEvent(st2, side.fork, 0));
   forked = &side;
-  cb = cubb;
+  PDX_B_CHECK(cudaMemsetAsync(bcnt, 0, reinterpret_cast<unsigned char*>(p1ready) -
+                                           reinterpret_cast<unsigned char*>(bcnt), st2));
+  PDX_B_CHECK(cudaMemsetAsync(p1ready, 0, zero_end - reinterpret_cast<unsigned char*>(p1ready), st));
+  bprep_kernel<<<(nq + 7) / 8, 256, 0, st2>>>(d_seg_bucket, nq, nseg, store->d_bucket_block,
+                                              store->d_block_tile, wcount, pbase, bcnt, fseg);
+  PDX_B_CHECK(cudaGetLastError());
+  size_t cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, wcount, qoff, nq + 1, st2));
   cb = cubb;
   PDX_B_CHECK(cub::DeviceScan::ExclusiveSum(cubtmp, cb, bcnt, boff, nb + 1, st2));
@@ -2642,7 +2646,7 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
         if (e != cudaSuccess) return e;
       }
-      kern<<<nblk, 256, hsm, cs>>>(P, A, seg0, p1off, part1, rdy);
+      kern<<<nblk, 256, hsm, cs>>>(P, A, part1, rdy);
       return cudaGetLastError();
     };
     SideStream& cside = side_stream(8 + side_slot);
@@ -2660,9 +2664,9 @@ int search_batched_core(const pdx_store* store, const pdx_search_params* prm,
       {
         int32_t* rdy = overlap ? p1ready : nullptr;
         if (bsa)
-          bdense_kernel<true><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, rdy);
+          bdense_kernel<true><<<g, 128, sm, st>>>(P, A, part1, rdy);
         else
-          bdense_kernel<false><<<g, 128, sm, st>>>(P, A, seg0, p1off, part1, rdy);
+          bdense_kernel<false><<<g, 128, sm, st>>>(P, A, part1, rdy);
         PDX_B_CHECK(cudaGetLastError());
       }
       if (overlap) {
