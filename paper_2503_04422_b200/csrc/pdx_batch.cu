@@ -563,7 +563,7 @@ __device__ __forceinline__ void bdense_cta(const BParams& P, const BArgs& A,
 // (9 CTAs per SM: 56 registers — the pass is occupancy bound: -6 us per step
 // against 64 registers / 8 CTAs; 10 CTAs / 48 registers spill in the loop)
 template <bool BSA>
-__global__ void __launch_bounds__(128, 9) bdense_kernel(const BParams P, const BArgs A,
+__global__ void __launch_bounds__(128, BSA ? 7 : 9) bdense_kernel(const BParams P, const BArgs A,
                                                      float* __restrict__ part1,
                                                      int32_t* __restrict__ ready) {
   bdense_cta<BSA>(P, A, part1, blockIdx.x, (int)blockIdx.y * 4, ready);
