@@ -22,6 +22,7 @@ class PdxIndex:
         self.d = int(d)
         self.nlist = int(nlist)
         self._keep = keep  # objects whose device memory the handle borrows
+        self._pcache = {}  # PdxQueryParams of repeated calls (search)
 
     # ------------------------------------------------------------ creation
     @classmethod
@@ -104,11 +105,22 @@ class PdxIndex:
         if pruner == "bsa":
             coef = np.ascontiguousarray(bsa.coef, np.float32)
         rot = bool(rotate) if rotate is not None else False
-        p = _lib.PdxQueryParams(int(k), _lib.METRIC[Metric(metric).value], _lib.PRUNER[pruner],
-                                _lib.CRITERIA[OrderCriteria(criteria).value], 0,
-                                int(nprobe) if self.nlist else 0, float(selection_fraction),
-                                int(initial_step), int(rot), float(epsilon0), _lib.ptr(coef),
-                                int(on_dev), int(on_dev), int(bool(tensor_cores)))
+        # (the parameter struct of a repeated call is reused: building it is a
+        # measurable part of a 0.5 ms call)
+        pkey = (k, metric, pruner, criteria, nprobe, selection_fraction, initial_step, rot,
+                epsilon0, on_dev, tensor_cores) if coef is None else None
+        p = self._pcache.get(pkey) if pkey is not None else None
+        if p is None:
+            p = _lib.PdxQueryParams(int(k), _lib.METRIC[Metric(metric).value],
+                                    _lib.PRUNER[pruner],
+                                    _lib.CRITERIA[OrderCriteria(criteria).value], 0,
+                                    int(nprobe) if self.nlist else 0, float(selection_fraction),
+                                    int(initial_step), int(rot), float(epsilon0), _lib.ptr(coef),
+                                    int(on_dev), int(on_dev), int(bool(tensor_cores)))
+            if pkey is not None:
+                if len(self._pcache) > 64:
+                    self._pcache.clear()
+                self._pcache[pkey] = p
         _lib.check(_lib.lib().pdx_index_search(
             self._h, C.byref(p), _lib.ptr(Q), nq, _lib.ptr(out["dist"]), _lib.ptr(out["ids"]),
             _lib.ptr(out.get("touched")), _lib.ptr(out.get("total")),
