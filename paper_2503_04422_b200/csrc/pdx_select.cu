@@ -68,26 +68,45 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
     acc2[i][0] = acc2[i][1] = 0ull;  // (+0, +0)
   }
-  for (int j0 = 0; j0 < d; j0 += kDC) {
+  // the next chunk's operands are loaded into registers while this chunk is
+  // evaluated (every CTA is resident at once: the kernel's time is one CTA's
+  // chain of load - store - evaluate rounds)
+  constexpr int NQL = (kQT * kDC) / 256, NCL = (kCT * kDC) / 256;
+  float rq[NQL], rc[NCL];
+  auto load_chunk = [&](const int j0) {
 #pragma unroll
-    for (int it = 0; it < (kQT * kDC) / 256; ++it) {
+    for (int it = 0; it < NQL; ++it) {
       const int e = threadIdx.x + 256 * it;
       const int r = e / kDC, c = e % kDC;
       const int64_t qr = q0 + r;
       const int dj = j0 + c;
-      qs[c][r] = (qr < nq && dj < d) ? Q[qr * d + dj] : 0.f;
+      rq[it] = (qr < nq && dj < d) ? Q[qr * d + dj] : 0.f;
     }
 #pragma unroll
-    for (int it = 0; it < (kCT * kDC) / 256; ++it) {
+    for (int it = 0; it < NCL; ++it) {
       const int e = threadIdx.x + 256 * it;
       const int r = e / kDC, c = e % kDC;
       const int dj = j0 + c;
       const int cr = c0 + r;
-      cs[c][r] = (cr < nlist && dj < d) ? Cm[(int64_t)cr * d + dj] : 0.f;
+      rc[it] = (cr < nlist && dj < d) ? Cm[(int64_t)cr * d + dj] : 0.f;
+    }
+  };
+  load_chunk(0);
+  for (int j0 = 0; j0 < d; j0 += kDC) {
+#pragma unroll
+    for (int it = 0; it < NQL; ++it) {
+      const int e = threadIdx.x + 256 * it;
+      qs[e % kDC][e / kDC] = rq[it];
+    }
+#pragma unroll
+    for (int it = 0; it < NCL; ++it) {
+      const int e = threadIdx.x + 256 * it;
+      cs[e % kDC][e / kDC] = rc[it];
     }
     __syncthreads();
+    if (j0 + kDC < d) load_chunk(j0 + kDC);
     const int jn = min(kDC, d - j0);
-    for (int jj = 0; jj < jn; ++jj) {
+    auto dim_step = [&](const int jj) {
       float qv[RI], cv[4];
       static_assert(RI == 2, "the query pair is one 64-bit shared-memory load");
       const float2 q2 = *reinterpret_cast<const float2*>(&qs[jj][ty * RI]);
@@ -110,6 +129,12 @@ __global__ void __launch_bounds__(256) centroid_dist_kernel(const float* __restr
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = upd<METRIC>(acc[i][j], qv[i], cv[j]);
       }
+    };
+    if (jn == kDC) {  // a full chunk: straight-line code (the loop was ~30% of the instructions)
+#pragma unroll
+      for (int jj = 0; jj < kDC; ++jj) dim_step(jj);
+    } else {
+      for (int jj = 0; jj < jn; ++jj) dim_step(jj);
     }
     __syncthreads();
   }
